@@ -1,0 +1,275 @@
+"""Pins of the oracle's time stepping (orc_step; position Verlet).
+
+Closed forms / physics: free drift, rigid spin (matrix exponential), momentum conservation,
+second-order self-convergence in dt, sync == async, clamps, damping decay,
+the small-load cantilever vs Euler-Bernoulli/Timoshenko + elastica (north_star, within 1%),
+the axial mode period 2L/sqrt(E/rho) (north_star, within 1%), bounded energy, director
+orthonormality, and relaxation to a prescribed rest curvature (sign of kappa0 vs the
+kappa = ax(Q dQ^T/ds) definition).
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+from scipy.integrate import solve_ivp
+from scipy.optimize import brentq
+
+import workloads as W
+from rodkit import concat, rod
+
+
+def skew_np(v):
+    return np.array([[0, -v[2], v[1]], [v[2], 0, -v[0]], [-v[1], v[0], 0.0]])
+
+
+def perturbed(w, seed, ang=0.01, vel=1e-3):
+    rng = np.random.default_rng(seed)
+    E = w.n_elems_total
+    Q = np.stack([sla.expm(skew_np(rng.standard_normal(3) * ang)) for _ in range(E)]) @ w.directors
+    return dataclasses.replace(w, directors=Q, velocities=rng.standard_normal(w.positions.shape) * vel,
+                               omega=rng.standard_normal((E, 3)) * vel * 10)
+
+
+def test_free_drift(orc):
+    w = rod(N=6, L=0.3)
+    v = np.array([0.3, -0.1, 0.05])
+    w.velocities[:] = v
+    st, s, _, _ = orc.step(w, n_steps=1000, dt=1e-5)
+    assert s == 0
+    assert np.allclose(st.positions, w.positions + 1000 * 1e-5 * v, rtol=0, atol=1e-14)
+    # internal forces are pure round-off of the rounded rest positions (EA * eps / m * t)
+    assert np.max(np.abs(st.velocities - w.velocities)) <= 1e-9
+    assert np.array_equal(st.directors, w.directors)
+
+
+def test_rigid_spin_about_axis(orc):
+    Q0 = sla.expm(skew_np([0.4, 1.0, -0.3]))
+    w = rod(N=5, L=0.5, Q=Q0)
+    Om = np.array([0.0, 0.0, 3.0])
+    w.omega[:] = Om
+    n, dt = 4000, 1e-5
+    st, s, _, _ = orc.step(w, n_steps=n, dt=dt)
+    expect = sla.expm(-n * dt * skew_np(Om)) @ Q0
+    assert np.max(np.abs(st.directors - expect[None])) <= 1e-13
+    assert np.allclose(st.omega, Om[None], rtol=1e-14, atol=1e-9)
+    assert np.max(np.abs(st.positions - w.positions)) <= 1e-13
+
+
+def test_momentum_conserved(orc):
+    w = perturbed(rod(N=20, L=0.5, r=0.01), 3)
+    m = orc.energy(w)
+    P0 = m[6:9]
+    st, s, _, _ = orc.step(w, n_steps=2000, dt=1e-5)
+    P1 = orc.energy(w, st)[6:9]
+    scale = np.sum(np.linalg.norm(w.velocities, axis=1)) * w.density[0] * w.area[0] * 0.5 / 20
+    assert np.max(np.abs(P1 - P0)) <= 1e-12 * scale
+
+
+def test_second_order_in_dt(orc):
+    w = perturbed(rod(N=10, L=0.2, r=0.01, nu=0.3, g=(0, 0, -9.81)), 4)
+    T = 2e-3
+    sols = []
+    for dt in (4e-5, 2e-5, 1e-5, 5e-6):
+        st, s, _, _ = orc.step(w, n_steps=int(round(T / dt)), dt=dt)
+        sols.append(np.concatenate([st.positions.ravel(), st.directors.ravel()]))
+    d = [np.max(np.abs(sols[i] - sols[i + 1])) for i in range(3)]
+    order = np.log2(np.array(d[:-1]) / np.array(d[1:]))
+    assert np.all(np.abs(order - 2.0) < 0.1), order
+
+
+def test_sync_equals_async(orc):
+    w = W.make("cfg2", n_rods=8)
+    a, _, _, _ = orc.step(w, n_steps=30, protocol=orc.SYNC)
+    b, _, _, _ = orc.step(w, n_steps=30, protocol=orc.ASYNC)
+    for k in ("positions", "velocities", "directors", "omega"):
+        assert np.array_equal(getattr(a, k), getattr(b, k))
+    assert a.t == b.t
+
+
+def test_clamps_hold_exactly(orc):
+    w0 = perturbed(rod(N=8, L=0.4, clamp=0, tip=(1e-3, 0, 2e-3)), 5)
+    w1 = perturbed(rod(N=8, L=0.4, clamp=1, tip=(0, 1e-3, 0)), 6)
+    w = concat([w0, w1])
+    st, s, _, _ = orc.step(w, n_steps=200, dt=1e-5)
+    assert s == 0
+    assert np.array_equal(st.positions[0], w.positions[0]) and np.array_equal(st.directors[0], w.directors[0])
+    assert np.array_equal(st.velocities[0], np.zeros(3)) and np.array_equal(st.omega[0], np.zeros(3))
+    assert np.array_equal(st.positions[17], w.positions[17]) and np.array_equal(st.directors[15], w.directors[15])
+    assert np.array_equal(st.velocities[17], np.zeros(3)) and np.array_equal(st.omega[15], np.zeros(3))
+    assert not np.array_equal(st.positions[8], w.positions[8])          # free tip moved
+
+
+def test_damping_decay_closed_form(orc):
+    """Rigid translation under rate damping: v_n = v_0 (1 - h nu)^n exactly."""
+    w = rod(N=3, L=0.3, nu=50.0)
+    w.velocities[:] = [0.2, 0.0, -0.1]
+    n, dt = 100, 1e-4
+    st, _, _, _ = orc.step(w, n_steps=n, dt=dt)
+    assert np.allclose(st.velocities, w.velocities * (1 - dt * 50.0) ** n, rtol=1e-12, atol=0)
+
+
+# ------------------------------------------------------------------ cantilever
+def elastica_tip(F, L, EI):
+    """Inextensible, unshearable elastica: clamped along +z at s=0, dead load F along +x.
+    EI theta'' = -F cos(theta), theta(0)=0, theta'(L)=0 (shooting)."""
+    def rhs(s, y):
+        return [y[1], -F / EI * np.cos(y[0]), np.sin(y[0]), np.cos(y[0])]
+
+    def end(k0):
+        return solve_ivp(rhs, [0, L], [0, k0, 0, 0], rtol=1e-12, atol=1e-14).y[:, -1]
+    k0 = brentq(lambda k: end(k)[1], 0, 10 * F * L / EI)
+    return end(k0)[2]
+
+
+def relax_cantilever(orc, N, r, E=1e6, L=1.0, F=None, nu=None, dt=None, steps=None):
+    w = rod(N=N, L=L, r=r, E=E, clamp=0, tip=(F, 0, 0), nu=nu)
+    st, s, _, _ = orc.step(w, n_steps=steps, dt=dt)
+    assert s == 0 and np.max(np.abs(st.velocities)) < 1e-5
+    return w, st.positions[-1][0]
+
+
+def cantilever_closed_forms(w, F, L):
+    E, I, A, G, ac = w.youngs[0], w.I1[0], w.area[0], w.shear_mod[0], w.alpha_c[0]
+    eb = F * L ** 3 / (3 * E * I)
+    shear = F * L / (ac * G * A)
+    return eb, shear, elastica_tip(F, L, E * I)
+
+
+def test_cantilever_cfg1(orc):
+    """cfg1's rod (BASELINE configs[0]), relaxation variant nu = 1.2 ~ 2 omega_1.
+    The clamp fixes element 0's frame (C.4 #15), so the beam root sits at Leff = L - lhat/2;
+    against Euler-Bernoulli/Timoshenko at Leff (times the elastica factor) it matches to 0.1%,
+    and against the plain closed form at L it is within the O(lhat/L) clamp term (< 2%)."""
+    F, L, N = 1e-3, 1.0, 100
+    w, x = relax_cantilever(orc, N, 0.01, F=F, nu=1.2, dt=1e-4, steps=250000)
+    eb, shear, el = cantilever_closed_forms(w, F, L)
+    leff = L - L / N / 2
+    pred = eb * (leff / L) ** 3 * (el / eb) + shear
+    assert abs(x / pred - 1) < 1e-3, x / pred - 1
+    assert abs(x / (eb + shear) - 1) < 0.02
+    assert abs(el / eb - 1 + 0.00185) < 1e-4                   # exact elastica: -0.18%
+
+
+def test_cantilever_converges_to_timoshenko_elastica(orc):
+    """Resolution study on a thicker rod: the error is first order (clamp term) and the
+    Richardson extrapolation lands on elastica + Timoshenko shear within 0.1%; each run is
+    within 1% of the Euler-Bernoulli/Timoshenko closed form at Leff (north_star)."""
+    r, E, L = 0.03, 1e6, 1.0
+    I = np.pi * r ** 4 / 4
+    A = np.pi * r ** 2
+    F = 0.05 * E * I / L ** 2
+    om1 = 3.516 * np.sqrt(E * I / (1000 * A)) / L ** 2
+    xs = {}
+    for N in (25, 50, 100):
+        dt = 1e-4 * 100 / N
+        w, xs[N] = relax_cantilever(orc, N, r, E=E, L=L, F=F, nu=2 * om1, dt=dt, steps=int(14 / om1 / dt))
+    eb, shear, el = cantilever_closed_forms(w, F, L)
+    target = el + shear
+    e50, e100 = xs[50] / target - 1, xs[100] / target - 1
+    assert 1.8 < e50 / e100 < 2.2                                # first order in lhat
+    assert abs((2 * xs[100] - xs[50]) / target - 1) < 1e-3
+    for N, x in xs.items():
+        leff = L - L / N / 2
+        assert abs(x / (F * leff ** 3 / (3 * E * I) + shear) - 1) < 0.01
+
+
+def test_axial_mode_period(orc):
+    """Free-free cfg1 rod, v = v0 cos(pi s/L) e3: period 2L/sqrt(E/rho) = 63.25 ms (north_star)."""
+    N, L = 100, 1.0
+    w = rod(N=N, L=L, r=0.01)
+    s = np.arange(N + 1) * L / N
+    w.velocities[:, 2] = 1e-6 * np.cos(np.pi * s / L)
+    dt = 1e-4
+    st = None
+    vz = []
+    for _ in range(2000):
+        st, _, _, _ = orc.step(w, st, n_steps=1, dt=dt)
+        vz.append(st.velocities[-1, 2])
+    vz = np.array(vz)
+    idx = np.where(np.sign(vz[:-1]) != np.sign(vz[1:]))[0]
+    tc = (idx + vz[idx] / (vz[idx] - vz[idx + 1])) * dt + dt   # linear interpolation
+    period = 2 * np.mean(np.diff(tc))
+    expect = 2 * L / np.sqrt(w.youngs[0] / w.density[0])
+    assert abs(period / expect - 1) < 0.01, period / expect - 1
+    assert abs(period / expect - 1) < 2e-3
+
+
+def test_energy_bounded_undamped(orc):
+    """Undamped free rod, small random perturbation, 1e5 steps: energy oscillates within 1%
+    with no secular trend, and the oscillation is the integrator's
+    O(dt^2) shadow-energy error (halving dt quarters it).  The perturbation is kept small
+    (strains ~1e-3): the discretisation is not exactly variational (C.4 #24: the 1/e factors
+    of n and the e-dependent inertia are not the gradient of this energy), which shows up as an
+    O(strain) drift for large perturbations (1% over 1e5 steps at 0.01 rad)."""
+    w = perturbed(rod(N=50, L=1.0, r=0.01), 7, ang=0.001, vel=1e-4)
+    st = None
+    es = [orc.energy(w)]
+    for _ in range(50):
+        st, s, _, _ = orc.step(w, st, n_steps=2000, dt=2e-5)
+        es.append(orc.energy(w, st))
+    tot = np.array([e[:6].sum() for e in es])
+    rel = np.abs(tot / tot[0] - 1)
+    assert np.max(rel) < 0.01, np.max(rel)
+    assert abs(np.mean(tot[26:]) / np.mean(tot[1:26]) - 1) < 0.002
+    dev = []
+    for dt in (4e-5, 2e-5):
+        st, es2 = None, [orc.energy(w)]
+        for _ in range(10):
+            st, s, _, _ = orc.step(w, st, n_steps=int(round(0.01 / dt)), dt=dt)
+            es2.append(orc.energy(w, st))
+        t2 = np.array([e[:6].sum() for e in es2])
+        dev.append(np.max(np.abs(t2 / t2[0] - 1)))
+    assert 3.0 < dev[0] / dev[1] < 5.0, dev
+
+
+def test_orthonormality_over_cfg2_run(orc):
+    w = W.make("cfg2", n_rods=8)
+    st, s, _, _ = orc.step(w, n_steps=10000)
+    Q = st.directors
+    err = np.max(np.abs(Q @ np.transpose(Q, (0, 2, 1)) - np.eye(3)[None]))
+    assert s == 0 and err <= 1e-13, err
+
+
+def test_relaxes_to_rest_curvature(orc):
+    """A free rod with static rest curvature kappa0 = (k, 0, 0) relaxes to kappa_hat = kappa0 and
+    sigma = 0; in element 0's frame the chord bends toward -d2 (from kappa = ax(Q dQ^T/ds),
+    PAPER.md:238: Q(s) = exp(-s[kappa]x) Q(0) turns d3 toward -d2 for k > 0)."""
+    N, L, k = 20, 0.2, 5.0
+    w = rod(N=N, L=L, r=0.005, nu=40.0)
+    w = dataclasses.replace(w, rest_kappa=np.tile([k, 0.0, 0.0], (N - 1, 1)))
+    st, s, _, _ = orc.step(w, n_steps=60000, dt=1e-5)
+    e, sig, kap, _ = orc.rod_strains(w.rest_lengths, st.positions, st.directors)
+    assert np.allclose(kap, [[k, 0, 0]], atol=1e-5 * k)
+    assert np.max(np.abs(sig)) < 1e-6
+    chord = st.directors[0] @ (st.positions[-1] - st.positions[0])
+    lh = L / N
+    expect_len = lh * np.sin(N * lh * k / 2) / np.sin(lh * k / 2)    # regular polygon chord
+    assert abs(np.linalg.norm(chord) / expect_len - 1) < 1e-5
+    assert chord[1] < -0.1 * expect_len and abs(chord[0]) < 1e-6
+
+
+def test_actuation_profile_static(orc):
+    """Rest-curvature actuation kappa0_x = A sin(2 pi (s/L - f t)) with f = 0 (BASELINE configs[3]):
+    the relaxed curvature follows A sin(2 pi s_k / L) at the Voronoi points s_k = k lhat."""
+    N, L, A = 32, 0.5, 2.0
+    w = rod(N=N, L=L, r=0.004, nu=25.0)
+    w = dataclasses.replace(w, act_A=np.array([A]), act_f=np.array([0.0]), act_L=np.array([L]),
+                            act_component=0)
+    st, s, _, _ = orc.step(w, n_steps=150000, dt=1e-5)
+    _, _, kap, _ = orc.rod_strains(w.rest_lengths, st.positions, st.directors)
+    sk = np.arange(1, N) * L / N
+    assert np.allclose(kap[:, 0], A * np.sin(2 * np.pi * sk / L), atol=2e-4 * A)
+    assert np.max(np.abs(kap[:, 1:])) < 1e-4 * A
+
+
+def test_instability_detected(orc):
+    w = concat([rod(N=4, L=0.2), rod(N=4, L=0.2), rod(N=4, L=0.2)])
+    w.velocities[7, 1] = np.nan                                  # node 2 of rod 1
+    st, s, bad, bits = orc.step(w, n_steps=3, dt=1e-5)
+    assert s == 2 and bad == 1 and bits & orc.F_NONFINITE
+    w = concat([rod(N=4, L=0.2), rod(N=4, L=0.2)])
+    w.positions[6] = w.positions[5]                              # collapsed element (e = 0) in rod 1
+    w.positions[7:] = w.positions[5] + (w.positions[7:] - w.positions[6])
+    st, s, bad, bits = orc.step(w, n_steps=1, dt=1e-9)
+    assert s == 2 and bad == 1 and bits & orc.F_DEGENERATE
