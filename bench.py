@@ -1,0 +1,331 @@
+"""Benchmark: rod element-updates/s (fp64) of the batched Cosserat rod step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg3] [--steps-per-launch S] [--scaling strong|weak]
+
+One bench "step" = one position-Verlet time step (all SURVEY §8(a) rows A1-A10) over the
+whole batch.  Default workload: BASELINE.json configs[2] ("cfg3": 1,048,576 rods x 16
+elements, the paper's 1024^2-filament strong-scaling size), synthetic and seeded
+(workloads/).  Multi-GPU: one process per GPU (torchrun), rods sharded across ranks with no
+data-path collective; NCCL all-reduces only the scalar diagnostics once after the timed
+region.  Rank 0 prints one JSON line.
+
+`--impl reference`: there is no reference implementation to install (the paper ships no
+code); the reference arm is the CPU oracle (oracle/, plain C fp64), timed on
+the host on a bounded rod sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg3", choices=list(W.CONFIG_NAMES))
+    ap.add_argument("--steps-per-launch", type=int, default=1,
+                    help="1 = every step streams the state through HBM (the B_min design); "
+                         ">1 = temporal blocking (SURVEY NEXT-1)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-rods", type=int, default=8192)
+    ap.add_argument("--cpu-sample-steps", type=int, default=300)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        p = json.load(open(PEAKS_PATH))
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def b_min_per_el_step(w) -> float:
+    """16 [6(N+1) + 12 N] + P + 24 (N-1) chi_kappa0 bytes per rod-step, / N."""
+    N = w.n_elems.astype(np.float64)
+    per_rod = 16.0 * (6.0 * (N + 1) + 12.0 * N) + 128.0 + (24.0 * (N - 1) if w.rest_kappa is not None else 0.0)
+    return float(per_rod.sum() / N.sum())
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for k, nm in enumerate(names):
+                    if r[5 + k].lower() == "active":
+                        reasons.add(nm)
+            except Exception:
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def shard(w, rank, world, scaling):
+    """Strong: contiguous rod ranges balanced by slot count (N_r + 1).  Weak: every rank a full
+    copy-size batch (rank-seeded sample order is irrelevant: rods are independent)."""
+    if world == 1 or scaling == "weak":
+        return w
+    slots = np.cumsum(w.n_elems.astype(np.int64) + 1)
+    total = slots[-1]
+    cuts = [0] + [int(np.searchsorted(slots, total * k / world, side="left")) + 1 for k in range(1, world)] + [w.n_rods]
+    cuts = np.clip(cuts, 0, w.n_rods)
+    return w.subset(np.arange(cuts[rank], cuts[rank + 1]))
+
+
+def oracle_rate(w, n_rods, n_steps, seed=3):
+    """The oracle as it stands (single-threaded C), on a seeded rod sample."""
+    import oracle
+    rods = W.sample_rods(w, n_rods, seed=seed)
+    ws = w.subset(rods)
+    t0 = time.perf_counter()
+    st, s, _, _ = oracle.step(ws, n_steps=n_steps)
+    dt = time.perf_counter() - t0
+    return ws.n_elems_total * n_steps / dt, dt, ws
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w = W.make(a.config)
+    import oracle
+    rods = W.sample_rods(w, min(4096, w.n_rods), seed=4)
+    ws = w.subset(rods)
+    st = oracle.State.of(ws)
+    for _ in range(max(a.warmup, 0)):
+        oracle.step(ws, st, n_steps=1)
+    steps = max(1, min(a.steps, 20))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        oracle.step(ws, st, n_steps=1)
+    dt = time.perf_counter() - t0
+    value = ws.n_elems_total * steps / dt
+    sample = f"{len(rods)} seeded rods of {a.config} ({ws.n_elems_total} elements) x {steps} steps per run"
+    print(json.dumps({
+        "impl": "reference", "metric": "rod element-updates/sec (fp64)", "value": value,
+        "unit": "element-steps/s", "n_gpus": a.gpus, "steps": steps, "warmup": a.warmup,
+        "ms_per_step": dt / steps * 1e3, "higher_is_better": True, "scaling": a.scaling,
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, workloads/)",
+        "config": {"workload": f"{a.config}: {w.n_rods} rods (sample of {len(rods)})", "sample_rods": len(rods)},
+        "cpu_baseline": {"value": value, "unit": "element-steps/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "element-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "no reference code exists (SURVEY §0); the reference arm is the CPU oracle on the host",
+    }), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+        return
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    import paper_2605_13766_b200 as er
+
+    wfull = W.make(a.config)
+    w = shard(wfull, rank, world, a.scaling)
+    stream = torch.cuda.Stream(device=local)
+    b = er.RodBatch(w, device=local, stream=stream)
+    if a.steps_per_launch > 1:
+        b.set_option(er.ER_OPT_STEPS_PER_LAUNCH, a.steps_per_launch)
+    dt = w.dt
+
+    # warm-up (untimed)
+    b.step(a.warmup, dt)
+    torch.cuda.synchronize()
+    launches0 = b.info().launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)                     # let the sampler start
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        b.step(a.steps, dt)                 # K launches of the fused step on `stream`
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = b.info().launches - launches0
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    el_local = w.n_elems_total
+    el_total = torch.tensor([float(el_local)], dtype=torch.float64, device=f"cuda:{local}")
+    # scalar diagnostics: the only cross-GPU exchange (NCCL all-reduce of ~12 fp64)
+    diag = torch.tensor(b.diagnostics(), dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        vmax = diag[9].clone()
+        dist.all_reduce(el_total)
+        dist.all_reduce(diag)
+        dist.all_reduce(vmax, op=dist.ReduceOp.MAX)
+        diag[9] = vmax
+    value = float(el_total.item()) * a.steps / (ms_max * 1e-3)
+
+    # roofline of the dominant (only) kernel: one launch = one step (steps_per_launch=1)
+    bmin = b_min_per_el_step(w)
+    per_launch_bytes = bmin * el_local * max(1, a.steps_per_launch)
+    launch_ms = ms / max(launches, 1)
+    achieved = per_launch_bytes / (launch_ms * 1e-3) / 1e9
+    peak, peak_src = peaks()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            tj = json.load(open(tp))
+            key = f"{a.config}_spl{a.steps_per_launch}"
+            if key in tj:
+                traffic = tj[key]["dram_bytes_per_launch"]
+        except Exception:
+            traffic = None
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "peak_source": peak_src, "bytes_per_el_step": bmin,
+            "kernel": "er::step_kernel<256,2,0> (fused single-pass step)"}
+    if a.steps_per_launch > 1:
+        roof["note"] = ("temporal blocking: the state crosses HBM once per launch of "
+                        f"{a.steps_per_launch} steps, so 'achieved' counts B_min per step and can exceed the "
+                        "HBM peak; the binding resource is the FP64 pipe")
+
+    # end-to-end through the public API with HOST buffers (pinned): create from host, K steps,
+    # state back to host; the H2D/D2H bytes are amortised over the K steps of the job
+    e2e = None
+    if not a.no_e2e:
+        e2e = e2e_run(er, w, a.steps, dt, local, world)
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not a.no_cpu_baseline:
+            rate, secs, ws = oracle_rate(wfull, a.cpu_sample_rods, a.cpu_sample_steps)
+            cpu = {"value": rate, "unit": "element-steps/s", "cores": 1, "kind": "oracle",
+                   "sample": f"{ws.n_rods} seeded rods of {a.config} x {a.cpu_sample_steps} steps "
+                             f"({ws.n_elems_total * a.cpu_sample_steps:.3g} element-steps, {secs:.1f} s, 1 thread)"}
+        out = {
+            "metric": "rod element-updates/sec (fp64)", "value": value, "unit": "element-steps/s",
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_max / a.steps,
+            "higher_is_better": True, "scaling": a.scaling if world > 1 else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, workloads/)",
+            "config": {"workload": f"{a.config}: {wfull.n_rods} rods x "
+                                   f"{int(wfull.n_elems.min())}-{int(wfull.n_elems.max())} elements "
+                                   f"({wfull.n_elems_total} elements), dt={wfull.dt}",
+                       "rods_per_gpu": w.n_rods, "elements_per_gpu": w.n_elems_total,
+                       "steps_per_launch": a.steps_per_launch,
+                       "l2": "inputs larger than L2 (state %.2f GB per GPU vs 126 MB L2)" % (
+                           b.info().device_bytes / 1e9),
+                       "parallelism": f"rod shards over {world} GPU(s), NCCL for scalar diagnostics only"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "diagnostics": {k: float(v) for k, v in zip(er.DIAG_NAMES, diag.cpu().numpy())},
+        }
+        print(json.dumps(out), flush=True)
+    b.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_run(er, w, steps, dt, local, world):
+    import torch
+    import dataclasses
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    hp, hv, hd, ho = pin(w.positions), pin(w.velocities), pin(w.directors), pin(w.omega)
+    wp = dataclasses.replace(w, positions=hp.numpy(), velocities=hv.numpy(), directors=hd.numpy(), omega=ho.numpy())
+    outp, outv = torch.empty_like(hp).pin_memory(), torch.empty_like(hv).pin_memory()
+    outd, outo = torch.empty_like(hd).pin_memory(), torch.empty_like(ho).pin_memory()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    t0 = time.perf_counter()
+    b = er.RodBatch(wp, device=local)                  # H2D of the inputs (pinned host)
+    b.step(steps, dt)
+    b.get_state_into(outp.numpy(), outv.numpy(), outd.numpy(), outo.numpy())  # D2H of the result
+    secs = time.perf_counter() - t0
+    b.close()
+    tt = torch.tensor([secs], dtype=torch.float64, device=f"cuda:{local}")
+    el = torch.tensor([float(w.n_elems_total)], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dist.all_reduce(el)
+    state_bytes = 8 * (w.positions.size + w.velocities.size + w.directors.size + w.omega.size)
+    param_bytes = 8 * (w.rest_lengths.size + 7 * w.n_rods) + 4 * w.n_rods
+    return {"value": float(el.item()) * steps / float(tt.item()), "unit": "element-steps/s",
+            "h2d_bytes_per_step": (state_bytes + param_bytes) / steps, "d2h_bytes_per_step": state_bytes / steps,
+            "seconds": float(tt.item()),
+            "what": f"er_create_batch from pinned host arrays + er_step({steps}) + er_get_state to pinned host, "
+                    "wall clock (max over ranks); transfer bytes are per job / steps"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,233 @@
+/*
+ * er.h -- C-ABI of libelasticarod: batched discrete Cosserat rod stepping on B200 (sm_100a).
+ *
+ * The operation (PAPER.md "Methods / Cosserat rod dynamics", lines 231-258):
+ *   Eq. (1a)  rho A d2r/dt2 = d/ds( Q^T S sigma / e ) + f
+ *   Eq. (1b)  (rho I / e) dw/dt = d/ds( B kappa / e^3 ) + kappa x B kappa / e^3 + Q t x S sigma
+ *                                + (rho I w / e) x w + (rho I w / e^2) de/dt + c
+ *   sigma = Q(r' - d3), kappa = ax(Q dQ^T/ds), w = ax(Q dQ^T/dt), e = |r'|
+ *   B = diag{E I1, E I2, G(I1+I2)}, S = diag{alpha_c G A, alpha_c G A, E A},
+ *   I = diag{I1, I2, I1+I2}
+ * discretised on N+1 nodes / N elements / N-1 Voronoi domains per rod and advanced by
+ * position Verlet, drift(h/2) - kick(h) - drift(h/2), with kinematic constraints after
+ * every stage.  The discrete readings are DESIGN.md §3 (= SURVEY.md §8 C.3-C.4).
+ * Rods do not interact: every rod of a batch is advanced independently.
+ *
+ * Conventions shared by every call
+ *  - fp64 throughout.  Lab-frame vectors: positions, velocities, tip forces, gravity, b(t).
+ *    Local-frame vectors (components on d1, d2, d3): omega, rest_sigma, rest_kappa,
+ *    magnetization.
+ *  - Rod r owns n_elems[r] >= 1 elements, n_elems[r]+1 nodes and n_elems[r]-1 Voronoi
+ *    domains; rods are stored back to back in the order given ("canonical order").
+ *    elem_offset(r) = sum_{q<r} n_elems[q], node_offset(r) = elem_offset(r) + r,
+ *    voronoi_offset(r) = elem_offset(r) - r.
+ *  - Canonical array layouts (AoS per quantity, C order):
+ *      positions, velocities [n_nodes_total][3];  directors [n_elems_total][3][3], row a is
+ *      the director d_{a+1} in lab coordinates (Q maps lab -> local);
+ *      omega [n_elems_total][3];  rest_sigma [n_elems_total][3];  rest_kappa [n_voronoi_total][3].
+ *  - Ownership: the library copies every input at create/set time; the caller keeps its
+ *    arrays.  The handle owns all device memory until er_destroy.  Output pointers are
+ *    caller-owned buffers of the canonical size.
+ *  - Errors: every call returns er_status and never aborts.  ER_EINVAL messages list every
+ *    validation error found (not only the first).  er_last_error() returns the message of the
+ *    last failing call on that handle (or, for a NULL handle, of the last failed
+ *    er_create_batch on the calling thread).
+ *  - Threading / streams: one handle per host thread at a time.  All device work of a handle
+ *    is issued on its stream (the caller's, or one the library creates); calls that return
+ *    data to the caller synchronise that stream.
+ */
+#ifndef ELASTICAROD_ER_H
+#define ELASTICAROD_ER_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ER_ABI_VERSION 1
+
+typedef struct er_batch er_batch; /* opaque handle; owns device memory */
+
+typedef enum {
+  ER_OK = 0,
+  ER_EINVAL = 1,     /* invalid argument / input data (all problems listed in er_last_error) */
+  ER_EUNSTABLE = 2,  /* a fault was detected while stepping (er_fault gives rod and bits)   */
+  ER_EIO = 3,        /* reserved (no file I/O in the library)                               */
+  ER_ENOMEM = 4,     /* device allocation failed                                            */
+  ER_ECUDA = 5       /* any other CUDA error (message has the CUDA error string)            */
+} er_status;
+
+typedef enum { ER_HOST = 0, ER_DEVICE = 1 } er_mem;
+
+/* fault bits reported by er_fault after ER_EUNSTABLE */
+#define ER_F_NONFINITE 1   /* a state component became NaN/Inf                                  */
+#define ER_F_DEGENERATE 2  /* dilatation e = |edge|/lhat < 1e-12                               */
+#define ER_F_ANTIPODAL 4   /* adjacent-element relative rotation angle >= pi - 1e-6            */
+#define ER_F_OVERSPEED 8   /* |v| > 1e6 sqrt(E/rho)                                           */
+
+/* ------------------------------------------------------------------------- er_create_batch
+ * A ragged batch of rods with per-rod element counts (north_star "er_create_batch").
+ *  n_elems            HOST  [n_rods], each 1 <= n <= ER_MAX_ELEMS_PER_ROD.
+ *  material_per_rod   1: the seven material arrays have n_rods entries (one value per rod);
+ *                     0: they have n_elems_total entries (one value per element).
+ *  density            HOST  rho, volumetric mass density (kg/m^3) (reading DESIGN §3 #6).
+ *  area, I1, I2       HOST  cross-section area A and second moments of area I1, I2.
+ *  youngs, shear_mod  HOST  E and G.   alpha_c  HOST  shear correction factor.
+ *  rest_lengths       HOST  [n_elems_total] reference element lengths lhat > 0.
+ *  rest_sigma         HOST  [n_elems_total*3] intrinsic shear/stretch strain, or NULL (= 0).
+ *  rest_kappa         HOST  [n_voronoi_total*3] static intrinsic curvature, or NULL (= 0).
+ *  positions          src_mem [n_nodes_total*3]   (required)
+ *  velocities         src_mem [n_nodes_total*3]   or NULL (= 0)
+ *  directors          src_mem [n_elems_total*9]   (required; orthonormal, det +1 within 1e-10)
+ *  omega              src_mem [n_elems_total*3]   or NULL (= 0)
+ *  t0                 initial time (rest-curvature actuation and b(t) depend on t).
+ *  src_mem            memory space of positions/velocities/directors/omega.
+ *  device             CUDA device ordinal.
+ *  stream             cudaStream_t to use, or NULL to let the library create its own.
+ * Errors: ER_EINVAL (all problems listed), ER_ENOMEM, ER_ECUDA.  *out is NULL on error.
+ */
+#define ER_MAX_ELEMS_PER_ROD 511
+
+typedef struct {
+  int32_t n_rods;
+  const int32_t *n_elems;
+  int32_t material_per_rod;
+  const double *density, *area, *I1, *I2, *youngs, *shear_mod, *alpha_c;
+  const double *rest_lengths;
+  const double *rest_sigma;
+  const double *rest_kappa;
+  const double *positions;
+  const double *velocities;
+  const double *directors;
+  const double *omega;
+  double t0;
+  int32_t src_mem; /* er_mem */
+  int32_t device;
+  void *stream;
+} er_batch_desc;
+
+er_status er_create_batch(const er_batch_desc *desc, er_batch **out);
+
+/* ------------------------------------------------------------------------- er_set_bc
+ * Kinematic boundary conditions (reading DESIGN §3 #15).
+ *  clamp_end  HOST [n_rods]: -1 free-free; 0 clamp the s = 0 end (node 0 position and
+ *             element 0 frame); 1 clamp the s = L end (node N and element N-1).  NULL = all free.
+ * The clamped pose is the state at the time of this call; clamped node/element rates are
+ * zeroed after every kick.  Default after create: all free.   Errors: ER_EINVAL.
+ */
+er_status er_set_bc(er_batch *b, const int8_t *clamp_end);
+
+/* ------------------------------------------------------------------------- er_set_forcing
+ * External loads and actuation (PAPER.md:252 f and c; :263-268 magnetic couple;
+ * BASELINE configs[3] rest-curvature actuation).  All pointers HOST.
+ *  gravity         lab acceleration g; node i receives m_i g.
+ *  damping         [n_rods] linear damping rate nu (1/s): a -= nu v, alpha -= nu w
+ *                  (reading DESIGN §3 #11), or NULL to use damping_all for every rod.
+ *  tip_force       [n_rods*3] constant lab force on the free-end node (node N, or node 0 for
+ *                  rods clamped at s = L), or NULL.
+ *  act_A, act_f, act_L  [n_rods] each, or all NULL: time-varying rest curvature
+ *                  kappa0_k[act_component] += A sin(2 pi (s_k/L - f t)), s_k = arc length of
+ *                  interior node k, evaluated at t_n + h/2 (DESIGN §3 #13, #14).
+ *  magnetization   [n_elems_total*3] local magnetic moment per unit rest length m, or NULL;
+ *                  element couple c_j = lhat_j m_j x (Q_j b(t)) with
+ *                  b(t) = Rz(b_omega t) b_field (a field rotating in the lab x-y plane).
+ * Replaces all previous forcing.  Default after create: none.   Errors: ER_EINVAL.
+ */
+typedef struct {
+  double gravity[3];
+  const double *damping;
+  double damping_all;
+  const double *tip_force;
+  const double *act_A, *act_f, *act_L;
+  int32_t act_component;
+  const double *magnetization;
+  double b_field[3];
+  double b_omega;
+} er_forcing;
+
+er_status er_set_forcing(er_batch *b, const er_forcing *f);
+
+/* ------------------------------------------------------------------------- er_step
+ * Advance every rod by n_steps >= 0 position-Verlet steps of size dt > 0 (north_star
+ * "er_step(n_steps, dt)").  Stream-ordered; returns after the work completed and one 16-byte
+ * fault-word read.  ER_EUNSTABLE if any rod faulted during these steps (state is then
+ * undefined for the faulted rods; other rods are unaffected).  Errors: ER_EINVAL, ER_ECUDA.
+ */
+er_status er_step(er_batch *b, int64_t n_steps, double dt);
+
+/* ------------------------------------------------------------------------- er_get_state
+ * Copy the current state out in canonical order.  dst_mem says where the (caller-owned)
+ * buffers live.  Any pointer may be NULL to skip that quantity.  *t receives the time.
+ */
+er_status er_get_state(er_batch *b, int32_t dst_mem, double *positions, double *velocities,
+                       double *directors, double *omega, double *t);
+
+/* ------------------------------------------------------------------------- er_set_state
+ * Overwrite the state (resume from a snapshot taken with er_get_state, or inject a state).
+ * src_mem says where the arrays live; any pointer may be NULL to keep that quantity; t may be
+ * NULL to keep the time.  Deliberately NOT validated (no orthonormality / finiteness check):
+ * a bad state surfaces as ER_EUNSTABLE at the next er_step.  Clamped poses are unchanged
+ * (call er_set_bc again to re-pose).   Errors: ER_EINVAL (bad src_mem), ER_ECUDA.
+ */
+er_status er_set_state(er_batch *b, int32_t src_mem, const double *positions, const double *velocities,
+                       const double *directors, const double *omega, const double *t);
+
+/* ------------------------------------------------------------------------- er_diagnostics
+ * Batch-local scalar diagnostics at the current state:
+ *  out[ER_D_*] below.  Sums over this batch only (a multi-GPU caller all-reduces them:
+ *  ER_D_VMAX with max, the rest with sum).  Deterministic (fixed-order reduction).
+ */
+enum {
+  ER_D_KE_TRANS = 0, /* 1/2 sum m |v|^2                               */
+  ER_D_KE_ROT,       /* 1/2 sum w . (J/e) w                           */
+  ER_D_PE_SHEAR,     /* 1/2 sum (s - s0) . S (s - s0) lhat            */
+  ER_D_PE_BEND,      /* 1/2 sum (k - k0(t)) . Bv (k - k0(t)) Dh       */
+  ER_D_PE_GRAV,      /* - sum m g . r                                 */
+  ER_D_PE_TIP,       /* - F_tip . r_tip                               */
+  ER_D_PX, ER_D_PY, ER_D_PZ, /* sum m v                               */
+  ER_D_VMAX,         /* max |v|                                       */
+  ER_D_MASS,         /* sum m                                         */
+  ER_D_NELEM,        /* number of elements                            */
+  ER_NDIAG
+};
+er_status er_diagnostics(er_batch *b, double out[ER_NDIAG]);
+
+/* ------------------------------------------------------------------------- er_fault
+ * After ER_EUNSTABLE: lowest faulted rod id (canonical order) and the OR of fault bits.
+ */
+er_status er_fault(const er_batch *b, int64_t *rod, int32_t *bits);
+
+/* ------------------------------------------------------------------------- options / info */
+typedef enum {
+  ER_OPT_STEPS_PER_LAUNCH = 1, /* 1 (default): every step streams the state through HBM
+                                  (SURVEY §8 D.3 B_min design).  k > 1: each launch keeps a
+                                  rod tile on chip for k steps (temporal blocking, SURVEY §8(f)
+                                  NEXT-1); identical results. */
+  ER_OPT_KERNEL = 2            /* 0 (default): fused single-pass step kernel.
+                                  1: staged three-kernel path (drift / dynamics+kick / drift),
+                                  kept for ablation and debugging; identical results. */
+} er_option;
+er_status er_set_option(er_batch *b, int32_t option, int64_t value);
+
+typedef struct {
+  int64_t n_rods, n_elems_total, n_nodes_total, n_voronoi_total;
+  int64_t n_tiles;         /* CTAs per fused-step launch                       */
+  int32_t tile_slots;      /* threads per CTA (slots per tile)                 */
+  int32_t device;
+  void *stream;            /* the cudaStream_t all work is issued on            */
+  int64_t launches;        /* kernels launched by er_step so far               */
+  int64_t device_bytes;    /* device memory owned by the handle                */
+  double t;                /* current time                                     */
+  double bytes_per_step;   /* algorithmic HBM bytes of one step    */
+} er_info;
+er_status er_query(const er_batch *b, er_info *info);
+
+const char *er_last_error(const er_batch *b);
+int32_t er_abi_version(void);
+void er_destroy(er_batch *b);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ELASTICAROD_ER_H */

@@ -1,0 +1,639 @@
+// er_api.cu -- host implementation of the C-ABI (L3) declared in include/er.h.
+//
+// Validation (collect-all), the rod-layout builder (offsets, derived per-rod
+// constants, rod-aligned tiles), device allocation, stream-ordered stepping with one fault
+// word read per er_step, state read-back and the diagnostics reduction.  Nothing here does
+// per-element physics on the host: every step of the path runs in er_kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "er.h"
+#include "er_layout.h"
+
+extern "C" {
+cudaError_t er_launch_step(const ErStepParams *p, int64_t n_tiles, int block, int mode, cudaStream_t st);
+cudaError_t er_launch_diag(const ErStepParams *p, int64_t n_tiles, int block, double *out, cudaStream_t st);
+cudaError_t er_launch_aos_to_soa(const double *src, double *dst, int64_t n, int k, int64_t stride, cudaStream_t st);
+cudaError_t er_launch_soa_to_aos(const double *src, double *dst, int64_t n, int k, int64_t stride, cudaStream_t st);
+cudaError_t er_launch_fill(double *dst, int64_t n, int k, int64_t stride, double value, cudaStream_t st);
+cudaError_t er_launch_validate(const double *node, int64_t nn, int64_t n_nodes, const double *elem, int64_t ne,
+                               int64_t n_elems, double *out, cudaStream_t st);
+}
+
+namespace {
+
+thread_local std::string g_create_error;
+
+int64_t pad_to(int64_t n, int64_t q) { return ((n + q - 1) / q) * q + q; }
+
+struct Errors {
+  std::string msg;
+  int count = 0;
+  void add(const char *fmt, ...) {
+    if (count < 64) {
+      char buf[512];
+      va_list ap;
+      va_start(ap, fmt);
+      vsnprintf(buf, sizeof buf, fmt, ap);
+      va_end(ap);
+      if (!msg.empty()) msg += "; ";
+      msg += buf;
+    } else if (count == 64) {
+      msg += "; ...";
+    }
+    ++count;
+  }
+};
+
+}  // namespace
+
+struct er_batch {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int64_t n_rods = 0, n_elems = 0, n_nodes = 0, n_vor = 0;
+  int32_t max_n = 0;
+  int block = 256;
+  int64_t n_tiles = 0;
+  double t = 0.0;
+  int64_t steps_per_launch = 1;
+  int kernel_mode = 0;
+  int64_t launches = 0;
+  int64_t device_bytes = 0;
+  // device buffers
+  double *d_node = nullptr, *d_elem = nullptr;
+  int64_t nn = 0, ne = 0, nv = 0, ng = 0;
+  double *d_rec = nullptr, *d_rec2 = nullptr;
+  int32_t *d_flags = nullptr;
+  int64_t *d_eoff = nullptr;
+  int32_t *d_tiles = nullptr;
+  double *d_gpar = nullptr, *d_sigma0 = nullptr, *d_kappa0 = nullptr, *d_mag = nullptr;
+  unsigned long long *d_fault = nullptr;
+  double *d_diag_partial = nullptr, *d_diag_out = nullptr, *d_valid = nullptr;
+  // host mirrors
+  std::vector<int32_t> n_elems_h;
+  std::vector<int64_t> eoff;
+  std::vector<double> rec, rec2;
+  std::vector<int32_t> flags;
+  std::vector<double> rho_rod, E_rod;  // for vmax
+  double g[3] = {0, 0, 0};
+  double b0[3] = {0, 0, 0};
+  double b_omega = 0.0;
+  int act_comp = 0;
+  int64_t fault_rod = -1;
+  int32_t fault_bits = 0;
+  std::string last_error;
+};
+
+namespace {
+
+er_status cuda_fail(er_batch *b, cudaError_t e, const char *what) {
+  std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+  if (b) b->last_error = m; else g_create_error = m;
+  return e == cudaErrorMemoryAllocation ? ER_ENOMEM : ER_ECUDA;
+}
+
+#define CK(call, what)                                   \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return cuda_fail(b, e_, what); \
+  } while (0)
+
+template <class T>
+cudaError_t dalloc(er_batch *b, T **p, int64_t count) {
+  *p = nullptr;
+  if (count <= 0) count = 1;
+  cudaError_t e = cudaMalloc((void **)p, sizeof(T) * (size_t)count);
+  if (e == cudaSuccess) b->device_bytes += (int64_t)(sizeof(T) * (size_t)count);
+  return e;
+}
+
+void free_all(er_batch *b) {
+  void *ptrs[] = {b->d_node, b->d_elem, b->d_rec, b->d_rec2, b->d_flags, b->d_eoff, b->d_tiles, b->d_gpar,
+                  b->d_sigma0, b->d_kappa0, b->d_mag, b->d_fault, b->d_diag_partial, b->d_diag_out, b->d_valid};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+  if (b->own_stream && b->stream) cudaStreamDestroy(b->stream);
+}
+
+bool pos_finite(double x) { return std::isfinite(x) && x > 0.0; }
+
+ErStepParams params_of(const er_batch *b) {
+  ErStepParams p;
+  std::memset(&p, 0, sizeof p);
+  p.node = b->d_node; p.elem = b->d_elem; p.nn = b->nn; p.ne = b->ne;
+  p.rec = b->d_rec; p.rec2 = b->d_rec2; p.flags = b->d_flags; p.eoff = b->d_eoff; p.tiles = b->d_tiles;
+  p.gpar = b->d_gpar; p.ng = b->ng; p.sigma0 = b->d_sigma0; p.kappa0 = b->d_kappa0; p.nv = b->nv;
+  p.mag = b->d_mag;
+  for (int c = 0; c < 3; ++c) { p.g[c] = b->g[c]; p.b0[c] = b->b0[c]; }
+  p.b_omega = b->b_omega; p.act_comp = b->act_comp;
+  p.fault = b->d_fault; p.diag_partial = b->d_diag_partial;
+  return p;
+}
+
+// Upload a canonical AoS array [n][k] from src (host or device) into k SoA planes.
+er_status upload_planes(er_batch *b, const double *src, int src_mem, double *planes, int64_t n, int k,
+                        int64_t stride) {
+  if (n <= 0) return ER_OK;
+  if (src == nullptr) {
+    CK(er_launch_fill(planes, n, k, stride, 0.0, b->stream), "fill");
+    return ER_OK;
+  }
+  if (src_mem == ER_DEVICE) {
+    CK(er_launch_aos_to_soa(src, planes, n, k, stride, b->stream), "aos_to_soa");
+    return ER_OK;
+  }
+  double *stage = nullptr;
+  CK(cudaMallocAsync((void **)&stage, sizeof(double) * (size_t)(n * k), b->stream), "cudaMallocAsync(stage)");
+  CK(cudaMemcpyAsync(stage, src, sizeof(double) * (size_t)(n * k), cudaMemcpyHostToDevice, b->stream), "H2D");
+  CK(er_launch_aos_to_soa(stage, planes, n, k, stride, b->stream), "aos_to_soa");
+  CK(cudaFreeAsync(stage, b->stream), "cudaFreeAsync");
+  return ER_OK;
+}
+
+er_status download_planes(er_batch *b, const double *planes, double *dst, int dst_mem, int64_t n, int k,
+                          int64_t stride) {
+  if (dst == nullptr || n <= 0) return ER_OK;
+  if (dst_mem == ER_DEVICE) {
+    CK(er_launch_soa_to_aos(planes, dst, n, k, stride, b->stream), "soa_to_aos");
+    return ER_OK;
+  }
+  double *stage = nullptr;
+  CK(cudaMallocAsync((void **)&stage, sizeof(double) * (size_t)(n * k), b->stream), "cudaMallocAsync(stage)");
+  CK(er_launch_soa_to_aos(planes, stage, n, k, stride, b->stream), "soa_to_aos");
+  CK(cudaMemcpyAsync(dst, stage, sizeof(double) * (size_t)(n * k), cudaMemcpyDeviceToHost, b->stream), "D2H");
+  CK(cudaFreeAsync(stage, b->stream), "cudaFreeAsync");
+  return ER_OK;
+}
+
+// Derived constants (DESIGN §3 #5, #9, #10): S = diag(ac G A, ac G A, E A),
+// B = diag(E I1, E I2, G (I1+I2)), J = rho lhat diag(I1, I2, I1+I2), m_node = half element masses.
+struct ElemMat { double rho, A, I1, I2, E, G, ac, lh; };
+
+void fill_record(double *rec, const ElemMat &m, double nu) {
+  const double J1 = m.rho * m.lh * m.I1, J2 = m.rho * m.lh * m.I2, J3 = m.rho * m.lh * (m.I1 + m.I2);
+  rec[REC_LHAT] = m.lh;
+  rec[REC_ILHAT] = 1.0 / m.lh;
+  rec[REC_S1] = m.ac * m.G * m.A;
+  rec[REC_S3] = m.E * m.A;
+  rec[REC_B1] = m.E * m.I1;
+  rec[REC_B2] = m.E * m.I2;
+  rec[REC_B3] = m.G * (m.I1 + m.I2);
+  rec[REC_IJ1] = 1.0 / J1;
+  rec[REC_IJ2] = 1.0 / J2;
+  rec[REC_IJ3] = 1.0 / J3;
+  rec[REC_KJ1] = (J2 - J3) / J1;
+  rec[REC_KJ2] = (J3 - J1) / J2;
+  rec[REC_KJ3] = (J1 - J2) / J3;
+  rec[REC_IM] = 1.0 / (m.rho * m.A * m.lh);
+  rec[REC_NU] = nu;
+  const double vmax = 1e6 * std::sqrt(m.E / m.rho);
+  rec[REC_VMAX2] = vmax * vmax;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t er_abi_version(void) { return ER_ABI_VERSION; }
+
+const char *er_last_error(const er_batch *b) { return b ? b->last_error.c_str() : g_create_error.c_str(); }
+
+er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
+  g_create_error.clear();
+  if (out) *out = nullptr;
+  if (!d || !out) { g_create_error = "desc and out must be non-NULL"; return ER_EINVAL; }
+  Errors err;
+  const int64_t R = d->n_rods;
+  if (R < 0) err.add("n_rods = %lld < 0", (long long)R);
+  if (R > 0 && !d->n_elems) err.add("n_elems is NULL");
+  if (d->src_mem != ER_HOST && d->src_mem != ER_DEVICE) err.add("src_mem = %d is not ER_HOST/ER_DEVICE", d->src_mem);
+  if (err.count) { g_create_error = err.msg; return ER_EINVAL; }
+
+  std::vector<int64_t> eoff((size_t)R + 1, 0);
+  int32_t max_n = 0;
+  for (int64_t r = 0; r < R; ++r) {
+    const int32_t n = d->n_elems[r];
+    if (n < 1 || n > ER_MAX_ELEMS_PER_ROD) err.add("rod %lld: n_elems = %d outside [1, %d]", (long long)r, n, ER_MAX_ELEMS_PER_ROD);
+    eoff[r + 1] = eoff[r] + std::max(n, 0);
+    max_n = std::max(max_n, n);
+  }
+  const int64_t E = eoff[R];
+  const int64_t NN = E + R, NV = E - R;
+  const int64_t nmat = d->material_per_rod ? R : E;
+  const char *mnames[7] = {"density", "area", "I1", "I2", "youngs", "shear_mod", "alpha_c"};
+  const double *marr[7] = {d->density, d->area, d->I1, d->I2, d->youngs, d->shear_mod, d->alpha_c};
+  if (R > 0) {
+    for (int q = 0; q < 7; ++q) {
+      if (!marr[q]) { err.add("%s is NULL", mnames[q]); continue; }
+      for (int64_t k = 0; k < nmat; ++k)
+        if (!pos_finite(marr[q][k])) { err.add("%s[%lld] = %g is not positive and finite", mnames[q], (long long)k, marr[q][k]); break; }
+    }
+    if (!d->rest_lengths) err.add("rest_lengths is NULL");
+    else
+      for (int64_t k = 0; k < E; ++k)
+        if (!pos_finite(d->rest_lengths[k])) { err.add("rest_lengths[%lld] = %g is not positive and finite", (long long)k, d->rest_lengths[k]); break; }
+    if (!d->positions) err.add("positions is NULL");
+    if (!d->directors) err.add("directors is NULL");
+    if (d->rest_sigma)
+      for (int64_t k = 0; k < 3 * E; ++k)
+        if (!std::isfinite(d->rest_sigma[k])) { err.add("rest_sigma[%lld] is not finite", (long long)k); break; }
+    if (d->rest_kappa)
+      for (int64_t k = 0; k < 3 * NV; ++k)
+        if (!std::isfinite(d->rest_kappa[k])) { err.add("rest_kappa[%lld] is not finite", (long long)k); break; }
+  }
+  if (!std::isfinite(d->t0)) err.add("t0 is not finite");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) err.add("no CUDA device available");
+  else if (d->device < 0 || d->device >= ndev) err.add("device %d outside [0, %d)", d->device, ndev);
+  if (err.count) { g_create_error = err.msg; return ER_EINVAL; }
+
+  er_batch *b = new er_batch();
+  b->device = d->device;
+  b->n_rods = R; b->n_elems = E; b->n_nodes = NN; b->n_vor = NV; b->max_n = max_n;
+  b->t = d->t0;
+  b->n_elems_h.assign(d->n_elems, d->n_elems + R);
+  b->eoff = eoff;
+  auto fail = [&](er_status s) { g_create_error = b->last_error; free_all(b); delete b; return s; };
+#undef CK
+#define CK(call, what)                                                 \
+  do {                                                                 \
+    cudaError_t e_ = (call);                                           \
+    if (e_ != cudaSuccess) { cuda_fail(b, e_, what); return fail(e_ == cudaErrorMemoryAllocation ? ER_ENOMEM : ER_ECUDA); } \
+  } while (0)
+  CK(cudaSetDevice(d->device), "cudaSetDevice");
+  if (d->stream) b->stream = (cudaStream_t)d->stream;
+  else { CK(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking), "cudaStreamCreate"); b->own_stream = true; }
+
+  // ---- per-rod records; general rods get per-slot parameter planes
+  b->rec.assign((size_t)std::max<int64_t>(R, 1) * ER_REC, 0.0);
+  b->rec2.assign((size_t)std::max<int64_t>(R, 1) * ER_REC2, 0.0);
+  b->flags.assign((size_t)std::max<int64_t>(R, 1), 0);
+  auto mat_at = [&](int64_t r, int64_t j) {
+    const int64_t k = d->material_per_rod ? r : j;
+    ElemMat m{d->density[k], d->area[k], d->I1[k], d->I2[k], d->youngs[k], d->shear_mod[k], d->alpha_c[k], d->rest_lengths[j]};
+    return m;
+  };
+  bool any_general = false;
+  for (int64_t r = 0; r < R; ++r) {
+    const ElemMat m0 = mat_at(r, eoff[r]);
+    bool uniform = true;
+    for (int64_t j = eoff[r] + 1; j < eoff[r + 1] && uniform; ++j) {
+      const ElemMat m = mat_at(r, j);
+      uniform = m.rho == m0.rho && m.A == m0.A && m.I1 == m0.I1 && m.I2 == m0.I2 && m.E == m0.E && m.G == m0.G &&
+                m.ac == m0.ac && m.lh == m0.lh;
+    }
+    fill_record(&b->rec[(size_t)r * ER_REC], m0, 0.0);
+    if (!uniform) { b->flags[r] |= FL_GENERAL; any_general = true; }
+  }
+  b->nn = pad_to(NN, 32); b->ne = pad_to(E, 32); b->nv = pad_to(NV, 32); b->ng = b->nn;
+  std::vector<double> gpar;
+  if (any_general) {
+    gpar.assign((size_t)ER_GP * b->ng, 0.0);
+    for (int64_t r = 0; r < R; ++r) {
+      if (!(b->flags[r] & FL_GENERAL)) continue;
+      const int32_t N = b->n_elems_h[r];
+      const int64_t n0 = eoff[r] + r;
+      double sk = 0.0;
+      for (int32_t i = 0; i <= N; ++i) {
+        auto G = [&](int q) -> double & { return gpar[(size_t)q * b->ng + n0 + i]; };
+        double mass = 0.0;
+        if (i < N) {
+          const ElemMat m = mat_at(r, eoff[r] + i);
+          double tmp[ER_REC];
+          fill_record(tmp, m, 0.0);
+          G(GP_LHAT) = tmp[REC_LHAT]; G(GP_ILHAT) = tmp[REC_ILHAT]; G(GP_S1) = tmp[REC_S1]; G(GP_S3) = tmp[REC_S3];
+          for (int c = 0; c < 3; ++c) { G(GP_IJ1 + c) = tmp[REC_IJ1 + c]; G(GP_KJ1 + c) = tmp[REC_KJ1 + c]; }
+          mass += 0.5 * m.rho * m.A * m.lh;
+        }
+        if (i > 0) {
+          const ElemMat m = mat_at(r, eoff[r] + i - 1);
+          mass += 0.5 * m.rho * m.A * m.lh;
+        }
+        G(GP_IM) = 1.0 / mass;
+        G(GP_SK) = sk;
+        if (i >= 1 && i < N) {
+          const ElemMat ml = mat_at(r, eoff[r] + i - 1), mr = mat_at(r, eoff[r] + i);
+          const double Dh = 0.5 * (ml.lh + mr.lh);
+          const double Bl[3] = {ml.E * ml.I1, ml.E * ml.I2, ml.G * (ml.I1 + ml.I2)};
+          const double Br[3] = {mr.E * mr.I1, mr.E * mr.I2, mr.G * (mr.I1 + mr.I2)};
+          G(GP_DH) = Dh;
+          for (int c = 0; c < 3; ++c) G(GP_BV1 + c) = (Bl[c] * ml.lh + Br[c] * mr.lh) / (2.0 * Dh);
+        }
+        if (i < N) sk += d->rest_lengths[eoff[r] + i];
+      }
+    }
+  }
+
+  // ---- rod-aligned tiles (greedy contiguous packing, <= block slots per tile)
+  b->block = (max_n + 1 <= 256) ? 256 : 512;
+  std::vector<int32_t> tiles;
+  tiles.push_back(0);
+  {
+    int64_t used = 0;
+    for (int64_t r = 0; r < R; ++r) {
+      const int64_t sl = b->n_elems_h[r] + 1;
+      if (used + sl > b->block) { tiles.push_back((int32_t)r); used = 0; }
+      used += sl;
+    }
+    if (R > 0) tiles.push_back((int32_t)R);
+  }
+  b->n_tiles = (int64_t)tiles.size() - 1;
+
+  // ---- device allocation and upload
+  CK(dalloc(b, &b->d_node, 6 * b->nn), "cudaMalloc(node)");
+  CK(dalloc(b, &b->d_elem, 12 * b->ne), "cudaMalloc(elem)");
+  CK(dalloc(b, &b->d_rec, (int64_t)b->rec.size()), "cudaMalloc(rec)");
+  CK(dalloc(b, &b->d_rec2, (int64_t)b->rec2.size()), "cudaMalloc(rec2)");
+  CK(dalloc(b, &b->d_flags, (int64_t)b->flags.size()), "cudaMalloc(flags)");
+  CK(dalloc(b, &b->d_eoff, R + 1), "cudaMalloc(eoff)");
+  CK(dalloc(b, &b->d_tiles, (int64_t)tiles.size()), "cudaMalloc(tiles)");
+  CK(dalloc(b, &b->d_fault, 2), "cudaMalloc(fault)");
+  CK(dalloc(b, &b->d_diag_partial, std::max<int64_t>(b->n_tiles, 1) * 16), "cudaMalloc(diag)");
+  CK(dalloc(b, &b->d_diag_out, 16), "cudaMalloc(diag_out)");
+  CK(dalloc(b, &b->d_valid, 4), "cudaMalloc(valid)");
+  CK(cudaMemsetAsync(b->d_node, 0, sizeof(double) * 6 * b->nn, b->stream), "memset");
+  CK(cudaMemsetAsync(b->d_elem, 0, sizeof(double) * 12 * b->ne, b->stream), "memset");
+  CK(cudaMemcpyAsync(b->d_rec, b->rec.data(), sizeof(double) * b->rec.size(), cudaMemcpyHostToDevice, b->stream), "H2D rec");
+  CK(cudaMemcpyAsync(b->d_rec2, b->rec2.data(), sizeof(double) * b->rec2.size(), cudaMemcpyHostToDevice, b->stream), "H2D rec2");
+  CK(cudaMemcpyAsync(b->d_flags, b->flags.data(), sizeof(int32_t) * b->flags.size(), cudaMemcpyHostToDevice, b->stream), "H2D flags");
+  CK(cudaMemcpyAsync(b->d_eoff, eoff.data(), sizeof(int64_t) * (R + 1), cudaMemcpyHostToDevice, b->stream), "H2D eoff");
+  CK(cudaMemcpyAsync(b->d_tiles, tiles.data(), sizeof(int32_t) * tiles.size(), cudaMemcpyHostToDevice, b->stream), "H2D tiles");
+  if (any_general) {
+    CK(dalloc(b, &b->d_gpar, (int64_t)gpar.size()), "cudaMalloc(gpar)");
+    CK(cudaMemcpyAsync(b->d_gpar, gpar.data(), sizeof(double) * gpar.size(), cudaMemcpyHostToDevice, b->stream), "H2D gpar");
+  }
+  er_status st;
+  if ((st = upload_planes(b, d->positions, d->src_mem, b->d_node, NN, 3, b->nn)) != ER_OK) return fail(st);
+  if ((st = upload_planes(b, d->velocities, d->src_mem, b->d_node + 3 * b->nn, NN, 3, b->nn)) != ER_OK) return fail(st);
+  if ((st = upload_planes(b, d->directors, d->src_mem, b->d_elem, E, 9, b->ne)) != ER_OK) return fail(st);
+  if ((st = upload_planes(b, d->omega, d->src_mem, b->d_elem + 9 * b->ne, E, 3, b->ne)) != ER_OK) return fail(st);
+  if (d->rest_sigma) {
+    CK(dalloc(b, &b->d_sigma0, 3 * b->ne), "cudaMalloc(sigma0)");
+    if ((st = upload_planes(b, d->rest_sigma, ER_HOST, b->d_sigma0, E, 3, b->ne)) != ER_OK) return fail(st);
+  }
+  if (d->rest_kappa && NV > 0) {
+    CK(dalloc(b, &b->d_kappa0, 3 * b->nv), "cudaMalloc(kappa0)");
+    if ((st = upload_planes(b, d->rest_kappa, ER_HOST, b->d_kappa0, NV, 3, b->nv)) != ER_OK) return fail(st);
+  }
+  // ---- validate the uploaded state on the device (directors orthonormal within 1e-10)
+  double vres[4] = {0, 0, 0, 0};
+  CK(cudaMemsetAsync(b->d_valid, 0, sizeof(double) * 4, b->stream), "memset");
+  if (R > 0) CK(er_launch_validate(b->d_node, b->nn, NN, b->d_elem, b->ne, E, b->d_valid, b->stream), "validate");
+  CK(cudaMemcpyAsync(vres, b->d_valid, sizeof vres, cudaMemcpyDeviceToHost, b->stream), "D2H valid");
+  CK(cudaStreamSynchronize(b->stream), "cudaStreamSynchronize");
+  if (vres[2] > 0) err.add("%g state entries (positions/velocities/directors/omega) are not finite", vres[2]);
+  if (vres[0] > 1e-10) err.add("directors not orthonormal: max |Q Q^T - I| = %.3g > 1e-10", vres[0]);
+  if (vres[1] > 1e-10) err.add("directors not proper rotations: max |det Q - 1| = %.3g", vres[1]);
+  if (err.count) { b->last_error = err.msg; return fail(ER_EINVAL); }
+#undef CK
+  *out = b;
+  return ER_OK;
+}
+
+#define CK(call, what)                                    \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) return cuda_fail(b, e_, what); \
+  } while (0)
+
+er_status er_set_bc(er_batch *b, const int8_t *clamp_end) {
+  if (!b) return ER_EINVAL;
+  Errors err;
+  if (clamp_end)
+    for (int64_t r = 0; r < b->n_rods; ++r)
+      if (clamp_end[r] < -1 || clamp_end[r] > 1) err.add("clamp_end[%lld] = %d not in {-1, 0, 1}", (long long)r, clamp_end[r]);
+  if (err.count) { b->last_error = err.msg; return ER_EINVAL; }
+  for (int64_t r = 0; r < b->n_rods; ++r) {
+    b->flags[r] &= ~FL_CLAMP_MASK;
+    if (clamp_end && clamp_end[r] == 0) b->flags[r] |= 1;
+    if (clamp_end && clamp_end[r] == 1) b->flags[r] |= 2;
+  }
+  CK(cudaSetDevice(b->device), "cudaSetDevice");
+  CK(cudaMemcpyAsync(b->d_flags, b->flags.data(), sizeof(int32_t) * b->flags.size(), cudaMemcpyHostToDevice, b->stream), "H2D flags");
+  CK(cudaStreamSynchronize(b->stream), "sync");
+  return ER_OK;
+}
+
+er_status er_set_forcing(er_batch *b, const er_forcing *f) {
+  if (!b || !f) { if (b) b->last_error = "forcing is NULL"; return ER_EINVAL; }
+  Errors err;
+  const int64_t R = b->n_rods;
+  for (int c = 0; c < 3; ++c) {
+    if (!std::isfinite(f->gravity[c])) err.add("gravity[%d] not finite", c);
+    if (!std::isfinite(f->b_field[c])) err.add("b_field[%d] not finite", c);
+  }
+  if (!std::isfinite(f->b_omega)) err.add("b_omega not finite");
+  if (f->damping) {
+    for (int64_t r = 0; r < R; ++r)
+      if (!(std::isfinite(f->damping[r]) && f->damping[r] >= 0)) { err.add("damping[%lld] = %g must be finite and >= 0", (long long)r, f->damping[r]); break; }
+  } else if (!(std::isfinite(f->damping_all) && f->damping_all >= 0)) err.add("damping_all = %g must be finite and >= 0", f->damping_all);
+  if (f->tip_force)
+    for (int64_t k = 0; k < 3 * R; ++k)
+      if (!std::isfinite(f->tip_force[k])) { err.add("tip_force[%lld] not finite", (long long)k); break; }
+  const bool act = f->act_A || f->act_f || f->act_L;
+  if (act) {
+    if (!(f->act_A && f->act_f && f->act_L)) err.add("act_A, act_f and act_L must be all set or all NULL");
+    else
+      for (int64_t r = 0; r < R; ++r) {
+        if (!std::isfinite(f->act_A[r]) || !std::isfinite(f->act_f[r])) { err.add("act_A/act_f[%lld] not finite", (long long)r); break; }
+        if (!pos_finite(f->act_L[r])) { err.add("act_L[%lld] = %g must be positive", (long long)r, f->act_L[r]); break; }
+      }
+    if (f->act_component < 0 || f->act_component > 2) err.add("act_component = %d not in {0,1,2}", f->act_component);
+  }
+  if (f->magnetization)
+    for (int64_t k = 0; k < 3 * b->n_elems; ++k)
+      if (!std::isfinite(f->magnetization[k])) { err.add("magnetization[%lld] not finite", (long long)k); break; }
+  if (err.count) { b->last_error = err.msg; return ER_EINVAL; }
+
+  for (int c = 0; c < 3; ++c) { b->g[c] = f->gravity[c]; b->b0[c] = f->b_field[c]; }
+  b->b_omega = f->b_omega;
+  b->act_comp = act ? f->act_component : 0;
+  for (int64_t r = 0; r < R; ++r) {
+    double *rec = &b->rec[(size_t)r * ER_REC];
+    double *r2 = &b->rec2[(size_t)r * ER_REC2];
+    rec[REC_NU] = f->damping ? f->damping[r] : f->damping_all;
+    b->flags[r] &= ~(FL_TIP | FL_ACT);
+    for (int c = 0; c < 3; ++c) r2[REC2_TIPX + c] = f->tip_force ? f->tip_force[3 * r + c] : 0.0;
+    if (f->tip_force) b->flags[r] |= FL_TIP;
+    r2[REC2_ACTA] = act ? f->act_A[r] : 0.0;
+    r2[REC2_ACTF] = act ? f->act_f[r] : 0.0;
+    r2[REC2_ACTIL] = act ? 1.0 / f->act_L[r] : 0.0;
+    if (act) b->flags[r] |= FL_ACT;
+  }
+  CK(cudaSetDevice(b->device), "cudaSetDevice");
+  if (R > 0) {
+    CK(cudaMemcpyAsync(b->d_rec, b->rec.data(), sizeof(double) * b->rec.size(), cudaMemcpyHostToDevice, b->stream), "H2D rec");
+    CK(cudaMemcpyAsync(b->d_rec2, b->rec2.data(), sizeof(double) * b->rec2.size(), cudaMemcpyHostToDevice, b->stream), "H2D rec2");
+    CK(cudaMemcpyAsync(b->d_flags, b->flags.data(), sizeof(int32_t) * b->flags.size(), cudaMemcpyHostToDevice, b->stream), "H2D flags");
+  }
+  if (f->magnetization && b->n_elems > 0) {
+    if (!b->d_mag) CK(dalloc(b, &b->d_mag, 3 * b->ne), "cudaMalloc(mag)");
+    er_status st = upload_planes(b, f->magnetization, ER_HOST, b->d_mag, b->n_elems, 3, b->ne);
+    if (st != ER_OK) return st;
+  } else if (b->d_mag) {
+    cudaFree(b->d_mag);
+    b->device_bytes -= (int64_t)sizeof(double) * 3 * b->ne;
+    b->d_mag = nullptr;
+  }
+  CK(cudaStreamSynchronize(b->stream), "sync");
+  return ER_OK;
+}
+
+er_status er_set_option(er_batch *b, int32_t option, int64_t value) {
+  if (!b) return ER_EINVAL;
+  if (option == ER_OPT_STEPS_PER_LAUNCH) {
+    if (value < 1 || value > (1 << 30)) { b->last_error = "steps_per_launch must be in [1, 2^30]"; return ER_EINVAL; }
+    b->steps_per_launch = value;
+    return ER_OK;
+  }
+  if (option == ER_OPT_KERNEL) {
+    if (value != 0 && value != 1) { b->last_error = "kernel must be 0 (fused) or 1 (staged)"; return ER_EINVAL; }
+    b->kernel_mode = (int)value;
+    return ER_OK;
+  }
+  b->last_error = "unknown option";
+  return ER_EINVAL;
+}
+
+er_status er_step(er_batch *b, int64_t n_steps, double dt) {
+  if (!b) return ER_EINVAL;
+  Errors err;
+  if (n_steps < 0) err.add("n_steps = %lld < 0", (long long)n_steps);
+  if (!(std::isfinite(dt) && dt > 0.0)) err.add("dt = %g must be positive and finite", dt);
+  if (err.count) { b->last_error = err.msg; return ER_EINVAL; }
+  b->fault_rod = -1;
+  b->fault_bits = 0;
+  if (n_steps == 0 || b->n_rods == 0) return ER_OK;
+  CK(cudaSetDevice(b->device), "cudaSetDevice");
+  const unsigned long long init[2] = {0ull, ~0ull};
+  CK(cudaMemcpyAsync(b->d_fault, init, sizeof init, cudaMemcpyHostToDevice, b->stream), "H2D fault");
+  ErStepParams p = params_of(b);
+  p.h = dt;
+  int64_t done = 0;
+  double t = b->t;
+  while (done < n_steps) {
+    if (b->kernel_mode == 0) {
+      const int64_t k = std::min<int64_t>(b->steps_per_launch, n_steps - done);
+      p.n_steps = (int32_t)k;
+      p.t = t;
+      CK(er_launch_step(&p, b->n_tiles, b->block, 0, b->stream), "step kernel");
+      b->launches += 1;
+      for (int64_t q = 0; q < k; ++q) { const double th = t + 0.5 * dt; t = th + 0.5 * dt; }
+      done += k;
+    } else {  // staged ablation: drift | dynamics + kick | drift, state through HBM between stages
+      p.n_steps = 1;
+      p.t = t;
+      CK(er_launch_step(&p, b->n_tiles, b->block, 1, b->stream), "drift kernel");
+      CK(er_launch_step(&p, b->n_tiles, b->block, 2, b->stream), "dyn kernel");
+      CK(er_launch_step(&p, b->n_tiles, b->block, 1, b->stream), "drift kernel");
+      b->launches += 3;
+      const double th = t + 0.5 * dt;
+      t = th + 0.5 * dt;
+      done += 1;
+    }
+  }
+  b->t = t;
+  unsigned long long fw[2];
+  CK(cudaMemcpyAsync(fw, b->d_fault, sizeof fw, cudaMemcpyDeviceToHost, b->stream), "D2H fault");
+  CK(cudaStreamSynchronize(b->stream), "cudaStreamSynchronize");
+  if (fw[0]) {
+    b->fault_bits = (int32_t)fw[0];
+    b->fault_rod = (int64_t)fw[1];
+    char buf[256];
+    snprintf(buf, sizeof buf, "unstable: rod %lld faulted (bits 0x%x:%s%s%s%s) during er_step(%lld, %g)",
+             (long long)b->fault_rod, b->fault_bits, (fw[0] & ER_F_NONFINITE) ? " nonfinite" : "",
+             (fw[0] & ER_F_DEGENERATE) ? " degenerate" : "", (fw[0] & ER_F_ANTIPODAL) ? " antipodal" : "",
+             (fw[0] & ER_F_OVERSPEED) ? " overspeed" : "", (long long)n_steps, dt);
+    b->last_error = buf;
+    return ER_EUNSTABLE;
+  }
+  return ER_OK;
+}
+
+er_status er_get_state(er_batch *b, int32_t dst_mem, double *positions, double *velocities, double *directors,
+                       double *omega, double *t) {
+  if (!b) return ER_EINVAL;
+  if (dst_mem != ER_HOST && dst_mem != ER_DEVICE) { b->last_error = "dst_mem must be ER_HOST or ER_DEVICE"; return ER_EINVAL; }
+  CK(cudaSetDevice(b->device), "cudaSetDevice");
+  er_status st;
+  if ((st = download_planes(b, b->d_node, positions, dst_mem, b->n_nodes, 3, b->nn)) != ER_OK) return st;
+  if ((st = download_planes(b, b->d_node + 3 * b->nn, velocities, dst_mem, b->n_nodes, 3, b->nn)) != ER_OK) return st;
+  if ((st = download_planes(b, b->d_elem, directors, dst_mem, b->n_elems, 9, b->ne)) != ER_OK) return st;
+  if ((st = download_planes(b, b->d_elem + 9 * b->ne, omega, dst_mem, b->n_elems, 3, b->ne)) != ER_OK) return st;
+  CK(cudaStreamSynchronize(b->stream), "cudaStreamSynchronize");
+  if (t) *t = b->t;
+  return ER_OK;
+}
+
+er_status er_set_state(er_batch *b, int32_t src_mem, const double *positions, const double *velocities,
+                       const double *directors, const double *omega, const double *t) {
+  if (!b) return ER_EINVAL;
+  if (src_mem != ER_HOST && src_mem != ER_DEVICE) { b->last_error = "src_mem must be ER_HOST or ER_DEVICE"; return ER_EINVAL; }
+  if (t && !std::isfinite(*t)) { b->last_error = "t is not finite"; return ER_EINVAL; }
+  CK(cudaSetDevice(b->device), "cudaSetDevice");
+  er_status st;
+  if (positions && (st = upload_planes(b, positions, src_mem, b->d_node, b->n_nodes, 3, b->nn)) != ER_OK) return st;
+  if (velocities && (st = upload_planes(b, velocities, src_mem, b->d_node + 3 * b->nn, b->n_nodes, 3, b->nn)) != ER_OK) return st;
+  if (directors && (st = upload_planes(b, directors, src_mem, b->d_elem, b->n_elems, 9, b->ne)) != ER_OK) return st;
+  if (omega && (st = upload_planes(b, omega, src_mem, b->d_elem + 9 * b->ne, b->n_elems, 3, b->ne)) != ER_OK) return st;
+  CK(cudaStreamSynchronize(b->stream), "cudaStreamSynchronize");
+  if (t) b->t = *t;
+  return ER_OK;
+}
+
+er_status er_diagnostics(er_batch *b, double out[ER_NDIAG]) {
+  if (!b || !out) return ER_EINVAL;
+  CK(cudaSetDevice(b->device), "cudaSetDevice");
+  ErStepParams p = params_of(b);
+  p.t = b->t;
+  CK(er_launch_diag(&p, b->n_tiles, b->block, b->d_diag_out, b->stream), "diag kernel");
+  CK(cudaMemcpyAsync(out, b->d_diag_out, sizeof(double) * ER_NDIAG, cudaMemcpyDeviceToHost, b->stream), "D2H diag");
+  CK(cudaStreamSynchronize(b->stream), "cudaStreamSynchronize");
+  return ER_OK;
+}
+
+er_status er_fault(const er_batch *b, int64_t *rod, int32_t *bits) {
+  if (!b) return ER_EINVAL;
+  if (rod) *rod = b->fault_rod;
+  if (bits) *bits = b->fault_bits;
+  return ER_OK;
+}
+
+er_status er_query(const er_batch *b, er_info *info) {
+  if (!b || !info) return ER_EINVAL;
+  info->n_rods = b->n_rods;
+  info->n_elems_total = b->n_elems;
+  info->n_nodes_total = b->n_nodes;
+  info->n_voronoi_total = b->n_vor;
+  info->n_tiles = b->n_tiles;
+  info->tile_slots = b->block;
+  info->device = b->device;
+  info->stream = (void *)b->stream;
+  info->launches = b->launches;
+  info->device_bytes = b->device_bytes;
+  info->t = b->t;
+  // state read + written once per step (r, v: 6 per node; Q, w: 12 per element) + rod records
+  double bytes = 16.0 * (6.0 * b->n_nodes + 12.0 * b->n_elems) + 8.0 * ER_REC * b->n_rods;
+  if (b->d_kappa0) bytes += 24.0 * b->n_vor;
+  info->bytes_per_step = bytes;
+  return ER_OK;
+}
+
+void er_destroy(er_batch *b) {
+  if (!b) return;
+  cudaSetDevice(b->device);
+  if (b->stream) cudaStreamSynchronize(b->stream);
+  free_all(b);
+  delete b;
+}
+
+}  // extern "C"

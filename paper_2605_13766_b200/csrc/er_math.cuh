@@ -1,0 +1,105 @@
+// er_math.cuh -- device math (L1) of the rod step: the SO(3) exponential and log maps in
+// registers.  Independent of oracle/ (no shared code); both follow PAPER.md:238-239 and the
+// sign-locked readings of SURVEY §8 C.2 / DESIGN.md §3 #2.
+#pragma once
+
+namespace er {
+
+// sin(t)/t and (1 - cos t)/t^2 as series in x = t^2, valid (to < 1 ulp of truncation) for x < 0.25.
+__device__ __forceinline__ double sinc_x(double x) {
+  double p = 1.0 / 355687428096000.0;
+  p = fma(p, x, -1.0 / 1307674368000.0);
+  p = fma(p, x, 1.0 / 6227020800.0);
+  p = fma(p, x, -1.0 / 39916800.0);
+  p = fma(p, x, 1.0 / 362880.0);
+  p = fma(p, x, -1.0 / 5040.0);
+  p = fma(p, x, 1.0 / 120.0);
+  p = fma(p, x, -1.0 / 6.0);
+  return fma(p, x, 1.0);
+}
+__device__ __forceinline__ double cosc_x(double x) {
+  double p = 1.0 / 6402373705728000.0;
+  p = fma(p, x, -1.0 / 20922789888000.0);
+  p = fma(p, x, 1.0 / 87178291200.0);
+  p = fma(p, x, -1.0 / 479001600.0);
+  p = fma(p, x, 1.0 / 3628800.0);
+  p = fma(p, x, -1.0 / 40320.0);
+  p = fma(p, x, 1.0 / 720.0);
+  p = fma(p, x, -1.0 / 24.0);
+  return fma(p, x, 0.5);
+}
+// asin(s)/s as a series in x = s^2, for x < 0.04 (truncation < 1e-17).
+__device__ __forceinline__ double asinc_x(double x) {
+  double p = 88179.0 / 12058624.0;
+  p = fma(p, x, 46189.0 / 5505024.0);
+  p = fma(p, x, 12155.0 / 1245184.0);
+  p = fma(p, x, 6435.0 / 557056.0);
+  p = fma(p, x, 143.0 / 10240.0);
+  p = fma(p, x, 231.0 / 13312.0);
+  p = fma(p, x, 63.0 / 2816.0);
+  p = fma(p, x, 35.0 / 1152.0);
+  p = fma(p, x, 5.0 / 112.0);
+  p = fma(p, x, 3.0 / 40.0);
+  p = fma(p, x, 1.0 / 6.0);
+  return fma(p, x, 1.0);
+}
+
+// Q <- rot(v) Q with rot(v) = exp(-[v]x) = I - a [v]x + b [v]x^2 (Rodrigues; the in-place SO(3)
+// rotation of PAPER.md:30).  Rows of Q are the directors.  v = 0 leaves Q bit-identical.
+__device__ __forceinline__ void rotate_inplace(double Q[9], double vx, double vy, double vz) {
+  const double x = fma(vx, vx, fma(vy, vy, vz * vz));
+  double a, b;
+  if (x < 0.25) {
+    a = sinc_x(x);
+    b = cosc_x(x);
+  } else {
+    const double th = sqrt(x);
+    double s, c;
+    sincos(th, &s, &c);
+    a = s / th;
+    b = (1.0 - c) / x;
+  }
+  const double c1 = fma(-b, x, 1.0);
+  const double bx = b * vx, by = b * vy, bz = b * vz;
+  const double ax = a * vx, ay = a * vy, az = a * vz;
+  const double s01 = bx * vy, s02 = bx * vz, s12 = by * vz;
+  const double R00 = fma(bx, vx, c1), R11 = fma(by, vy, c1), R22 = fma(bz, vz, c1);
+  const double R01 = s01 + az, R10 = s01 - az;
+  const double R02 = s02 - ay, R20 = s02 + ay;
+  const double R12 = s12 + ax, R21 = s12 - ax;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double q0 = Q[c], q1 = Q[3 + c], q2 = Q[6 + c];
+    Q[c] = fma(R00, q0, fma(R01, q1, R02 * q2));
+    Q[3 + c] = fma(R10, q0, fma(R11, q1, R12 * q2));
+    Q[6 + c] = fma(R20, q0, fma(R21, q1, R22 * q2));
+  }
+}
+
+__device__ __forceinline__ double dot3(const double *a, const double *b) {
+  return fma(a[0], b[0], fma(a[1], b[1], a[2] * b[2]));
+}
+
+// v = logrot(Q Qp^T) (inverse Rodrigues): the discrete kappa_k * Dh_k with
+// Q = Q_k, Qp = Q_{k-1}.  Returns c = cos(theta) and s2 = sin^2(theta) for the antipodal check.
+__device__ __forceinline__ void logrot_pair(const double Q[9], const double Qp[9], double v[3],
+                                            double &c, double &s2) {
+  const double tr = dot3(Q, Qp) + dot3(Q + 3, Qp + 3) + dot3(Q + 6, Qp + 6);
+  const double w0 = dot3(Q + 6, Qp + 3) - dot3(Q + 3, Qp + 6);  // R21 - R12
+  const double w1 = dot3(Q, Qp + 6) - dot3(Q + 6, Qp);          // R02 - R20
+  const double w2 = dot3(Q + 3, Qp) - dot3(Q, Qp + 3);          // R10 - R01
+  s2 = 0.25 * fma(w0, w0, fma(w1, w1, w2 * w2));
+  c = 0.5 * (tr - 1.0);
+  double f;
+  if (c > 0.0 && s2 < 0.04) {
+    f = 0.5 * asinc_x(s2);  // theta/(2 sin theta) with sin theta = s
+  } else {
+    const double s = sqrt(s2);
+    f = atan2(s, c) / (2.0 * s);
+  }
+  v[0] = -f * w0;
+  v[1] = -f * w1;
+  v[2] = -f * w2;
+}
+
+}  // namespace er

@@ -18,3 +18,9 @@ def orc():
     import oracle
     oracle.lib()
     return oracle
+
+
+def pytest_sessionstart(session):
+    """Build the in-tree CUDA library before any test imports the package."""
+    import __graft_entry__
+    __graft_entry__._builder().build()

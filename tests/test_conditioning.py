@@ -1,0 +1,30 @@
+"""How close can two correct fp64 implementations be?  The oracle against itself with the
+input perturbed by half an ulp: this bounds the achievable GPU/oracle parity
+and justifies gating the raw (unfloored) rate ratios only where they are well conditioned."""
+import dataclasses
+
+import numpy as np
+
+import workloads as W
+from parity import TOL_1000, TOL_1STEP, errors
+
+
+def perturbed_run(orc, w, n, seed=0):
+    rng = np.random.default_rng(seed)
+    a, _, _, _ = orc.step(w, n_steps=n)
+    w2 = dataclasses.replace(w, positions=w.positions * (1 + rng.choice([-1, 1], w.positions.shape) * 2.0 ** -53))
+    b, _, _, _ = orc.step(w2, n_steps=n)
+    return errors(w, (a.positions, a.velocities, a.directors, a.omega), (b.positions, b.velocities, b.directors, b.omega))
+
+
+def test_oracle_self_conditioning_cfg4(orc):
+    w = W.make("cfg4", n_rods=24)
+    e1 = perturbed_run(orc, w, 1)
+    # cfg4's 100 m box coordinates: one ulp of r is ~1e-12 of an edge, so even one step moves
+    # the floored rates by ~1e-12 -- the 1-step gate is as tight as the inputs allow there
+    assert e1["r"] < TOL_1STEP and e1["Q"] < TOL_1STEP and max(e1["v"], e1["w"]) < 5 * TOL_1STEP, e1
+    e = perturbed_run(orc, w, 1000)
+    # floored metric stays well inside the 1e-8 gate ...
+    assert all(e[k] < TOL_1000 / 5 for k in ("r", "v", "Q", "w")), e
+    # ... while the raw rate ratios are at/above it: an ulp of input moves them by ~1e-8
+    assert max(e["v_raw"], e["w_raw"]) > 2e-9, e

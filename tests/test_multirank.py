@@ -1,0 +1,73 @@
+"""Multi-rank host logic on CPU (gloo, world size 2): the rod sharding bench.py uses and the
+scalar-diagnostics all-reduce (the only cross-GPU exchange).  The per-rank
+compute here is the oracle (a CPU stand-in for the GPU shard); the point is the host logic:
+every rod in exactly one shard, slot-balanced cuts, and all-reduced diagnostics equal to the
+single-process ones."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+import bench
+import workloads as W
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_shard_partition(world):
+    w = W.make("cfg5", n_rods=997)
+    shards = [bench.shard(w, r, world, "strong") for r in range(world)]
+    assert sum(s.n_rods for s in shards) == w.n_rods
+    assert np.array_equal(np.concatenate([s.n_elems for s in shards]), w.n_elems)
+    slots = [int((s.n_elems + 1).sum()) for s in shards]
+    assert max(slots) - min(slots) <= 2 * (int(w.n_elems.max()) + 1)
+    assert np.array_equal(np.concatenate([s.positions for s in shards]), w.positions)
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    w = W.make("cfg2", n_rods=10)
+    ws = bench.shard(w, rank, world, "strong")
+    st, s, _, _ = oracle.step(ws, n_steps=5)
+    d = torch.tensor(oracle.energy(ws, st), dtype=torch.float64)
+    vmax = d[9].clone()
+    dist.all_reduce(d)
+    dist.all_reduce(vmax, op=dist.ReduceOp.MAX)
+    d[9] = vmax
+    if rank == 0:
+        q.put(d.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_diagnostics_allreduce(orc):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    w = W.make("cfg2", n_rods=10)
+    st, _, _, _ = orc.step(w, n_steps=5)
+    ref = orc.energy(w, st)
+    assert np.allclose(got, ref, rtol=1e-12, atol=1e-300)
+    assert got[9] == ref[9] and got[11] == ref[11]
