@@ -204,9 +204,12 @@ typedef enum {
                                   (SURVEY §8 D.3 B_min design).  k > 1: each launch keeps a
                                   rod tile on chip for k steps (temporal blocking, SURVEY §8(f)
                                   NEXT-1); identical results. */
-  ER_OPT_KERNEL = 2            /* 0 (default): fused single-pass step kernel.
+  ER_OPT_KERNEL = 2            /* 0 (default): fused single-pass step, persistent CTAs with
+                                  TMA bulk prefetch of the next rod tile.
                                   1: staged three-kernel path (drift / dynamics+kick / drift),
-                                  kept for ablation and debugging; identical results. */
+                                  state through HBM between stages (ablation, debugging).
+                                  2: fused step, one tile per CTA, plain loads (ablation).
+                                  All three give identical results. */
 } er_option;
 er_status er_set_option(er_batch *b, int32_t option, int64_t value);
 

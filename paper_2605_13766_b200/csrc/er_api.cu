@@ -19,8 +19,8 @@
 #include "er_layout.h"
 
 extern "C" {
-cudaError_t er_launch_step(const ErStepParams *p, int64_t n_tiles, int block, int mode, cudaStream_t st);
-cudaError_t er_launch_diag(const ErStepParams *p, int64_t n_tiles, int block, double *out, cudaStream_t st);
+cudaError_t er_launch_step(const ErStepParams *p, int block, int kind, int feat, cudaStream_t st);
+cudaError_t er_launch_diag(const ErStepParams *p, int block, double *out, cudaStream_t st);
 cudaError_t er_launch_aos_to_soa(const double *src, double *dst, int64_t n, int k, int64_t stride, cudaStream_t st);
 cudaError_t er_launch_soa_to_aos(const double *src, double *dst, int64_t n, int k, int64_t stride, cudaStream_t st);
 cudaError_t er_launch_fill(double *dst, int64_t n, int k, int64_t stride, double value, cudaStream_t st);
@@ -71,18 +71,19 @@ struct er_batch {
   // device buffers
   double *d_node = nullptr, *d_elem = nullptr;
   int64_t nn = 0, ne = 0, nv = 0, ng = 0;
-  double *d_rec = nullptr, *d_rec2 = nullptr;
-  int32_t *d_flags = nullptr;
+  double *d_rec = nullptr;
   int64_t *d_eoff = nullptr;
-  int32_t *d_tiles = nullptr;
+  ErTile *d_tiles = nullptr;
+  int feat = 0;  // FEAT_* bits of this batch
   double *d_gpar = nullptr, *d_sigma0 = nullptr, *d_kappa0 = nullptr, *d_mag = nullptr;
   unsigned long long *d_fault = nullptr;
   double *d_diag_partial = nullptr, *d_diag_out = nullptr, *d_valid = nullptr;
   // host mirrors
   std::vector<int32_t> n_elems_h;
   std::vector<int64_t> eoff;
-  std::vector<double> rec, rec2;
+  std::vector<double> rec;
   std::vector<int32_t> flags;
+  bool any_general = false, has_sigma0 = false, has_act = false;
   std::vector<double> rho_rod, E_rod;  // for vmax
   double g[3] = {0, 0, 0};
   double b0[3] = {0, 0, 0};
@@ -117,7 +118,7 @@ cudaError_t dalloc(er_batch *b, T **p, int64_t count) {
 }
 
 void free_all(er_batch *b) {
-  void *ptrs[] = {b->d_node, b->d_elem, b->d_rec, b->d_rec2, b->d_flags, b->d_eoff, b->d_tiles, b->d_gpar,
+  void *ptrs[] = {b->d_node, b->d_elem, b->d_rec, b->d_eoff, b->d_tiles, b->d_gpar,
                   b->d_sigma0, b->d_kappa0, b->d_mag, b->d_fault, b->d_diag_partial, b->d_diag_out, b->d_valid};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -130,7 +131,7 @@ ErStepParams params_of(const er_batch *b) {
   ErStepParams p;
   std::memset(&p, 0, sizeof p);
   p.node = b->d_node; p.elem = b->d_elem; p.nn = b->nn; p.ne = b->ne;
-  p.rec = b->d_rec; p.rec2 = b->d_rec2; p.flags = b->d_flags; p.eoff = b->d_eoff; p.tiles = b->d_tiles;
+  p.rec = b->d_rec; p.eoff = b->d_eoff; p.tiles = b->d_tiles; p.n_tiles = b->n_tiles;
   p.gpar = b->d_gpar; p.ng = b->ng; p.sigma0 = b->d_sigma0; p.kappa0 = b->d_kappa0; p.nv = b->nv;
   p.mag = b->d_mag;
   for (int c = 0; c < 3; ++c) { p.g[c] = b->g[c]; p.b0[c] = b->b0[c]; }
@@ -197,6 +198,23 @@ void fill_record(double *rec, const ElemMat &m, double nu) {
   rec[REC_NU] = nu;
   const double vmax = 1e6 * std::sqrt(m.E / m.rho);
   rec[REC_VMAX2] = vmax * vmax;
+}
+
+// The flag word lives inside each rod record (REC_FLAGS), so one bulk copy brings it along.
+void sync_flags(er_batch *b) {
+  for (int64_t r = 0; r < b->n_rods; ++r)
+  {
+    const int64_t bits = (int64_t)b->flags[r];
+    std::memcpy(&b->rec[(size_t)r * ER_REC + REC_FLAGS], &bits, sizeof bits);
+  }
+}
+
+int feat_of(const er_batch *b) {
+  int f = 0;
+  if (b->any_general) f |= FEAT_GENERAL;
+  if (b->d_kappa0) f |= FEAT_KAPPA0;
+  if (b->has_sigma0 || b->d_mag || b->has_act) f |= FEAT_EXTRA;
+  return f;
 }
 
 }  // namespace
@@ -275,7 +293,6 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
 
   // ---- per-rod records; general rods get per-slot parameter planes
   b->rec.assign((size_t)std::max<int64_t>(R, 1) * ER_REC, 0.0);
-  b->rec2.assign((size_t)std::max<int64_t>(R, 1) * ER_REC2, 0.0);
   b->flags.assign((size_t)std::max<int64_t>(R, 1), 0);
   auto mat_at = [&](int64_t r, int64_t j) {
     const int64_t k = d->material_per_rod ? r : j;
@@ -294,6 +311,9 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
     fill_record(&b->rec[(size_t)r * ER_REC], m0, 0.0);
     if (!uniform) { b->flags[r] |= FL_GENERAL; any_general = true; }
   }
+  b->any_general = any_general;
+  b->has_sigma0 = d->rest_sigma != nullptr;
+  sync_flags(b);
   b->nn = pad_to(NN, 32); b->ne = pad_to(E, 32); b->nv = pad_to(NV, 32); b->ng = b->nn;
   std::vector<double> gpar;
   if (any_general) {
@@ -333,29 +353,37 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
     }
   }
 
-  // ---- rod-aligned tiles (greedy contiguous packing, <= block slots per tile)
+  // ---- rod-aligned tiles (greedy contiguous packing, <= block slots and <= block/8 rods per tile)
   b->block = (max_n + 1 <= 256) ? 256 : 512;
-  std::vector<int32_t> tiles;
-  tiles.push_back(0);
+  std::vector<ErTile> tiles;
   {
-    int64_t used = 0;
-    for (int64_t r = 0; r < R; ++r) {
-      const int64_t sl = b->n_elems_h[r] + 1;
-      if (used + sl > b->block) { tiles.push_back((int32_t)r); used = 0; }
-      used += sl;
+    int64_t r = 0;
+    while (r < R) {
+      ErTile T;
+      T.r0 = (int32_t)r;
+      T.nbase = eoff[r] + r;
+      T.ebase = eoff[r];
+      int64_t used = 0;
+      int32_t nr = 0;
+      while (r < R && nr < b->block / 8 && used + b->n_elems_h[r] + 1 <= b->block) {
+        used += b->n_elems_h[r] + 1;
+        ++nr;
+        ++r;
+      }
+      T.nr = nr;
+      T.nslots = (int32_t)used;
+      T.nel = (int32_t)(eoff[r] - eoff[T.r0]);
+      tiles.push_back(T);
     }
-    if (R > 0) tiles.push_back((int32_t)R);
   }
-  b->n_tiles = (int64_t)tiles.size() - 1;
+  b->n_tiles = (int64_t)tiles.size();
 
   // ---- device allocation and upload
   CK(dalloc(b, &b->d_node, 6 * b->nn), "cudaMalloc(node)");
   CK(dalloc(b, &b->d_elem, 12 * b->ne), "cudaMalloc(elem)");
   CK(dalloc(b, &b->d_rec, (int64_t)b->rec.size()), "cudaMalloc(rec)");
-  CK(dalloc(b, &b->d_rec2, (int64_t)b->rec2.size()), "cudaMalloc(rec2)");
-  CK(dalloc(b, &b->d_flags, (int64_t)b->flags.size()), "cudaMalloc(flags)");
-  CK(dalloc(b, &b->d_eoff, R + 1), "cudaMalloc(eoff)");
-  CK(dalloc(b, &b->d_tiles, (int64_t)tiles.size()), "cudaMalloc(tiles)");
+  CK(dalloc(b, &b->d_eoff, R + 4), "cudaMalloc(eoff)");
+  CK(dalloc(b, &b->d_tiles, std::max<int64_t>((int64_t)tiles.size(), 1)), "cudaMalloc(tiles)");
   CK(dalloc(b, &b->d_fault, 2), "cudaMalloc(fault)");
   CK(dalloc(b, &b->d_diag_partial, std::max<int64_t>(b->n_tiles, 1) * 16), "cudaMalloc(diag)");
   CK(dalloc(b, &b->d_diag_out, 16), "cudaMalloc(diag_out)");
@@ -363,10 +391,14 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   CK(cudaMemsetAsync(b->d_node, 0, sizeof(double) * 6 * b->nn, b->stream), "memset");
   CK(cudaMemsetAsync(b->d_elem, 0, sizeof(double) * 12 * b->ne, b->stream), "memset");
   CK(cudaMemcpyAsync(b->d_rec, b->rec.data(), sizeof(double) * b->rec.size(), cudaMemcpyHostToDevice, b->stream), "H2D rec");
-  CK(cudaMemcpyAsync(b->d_rec2, b->rec2.data(), sizeof(double) * b->rec2.size(), cudaMemcpyHostToDevice, b->stream), "H2D rec2");
-  CK(cudaMemcpyAsync(b->d_flags, b->flags.data(), sizeof(int32_t) * b->flags.size(), cudaMemcpyHostToDevice, b->stream), "H2D flags");
-  CK(cudaMemcpyAsync(b->d_eoff, eoff.data(), sizeof(int64_t) * (R + 1), cudaMemcpyHostToDevice, b->stream), "H2D eoff");
-  CK(cudaMemcpyAsync(b->d_tiles, tiles.data(), sizeof(int32_t) * tiles.size(), cudaMemcpyHostToDevice, b->stream), "H2D tiles");
+  {
+    std::vector<int64_t> ep(eoff);
+    ep.resize((size_t)R + 4, eoff[R]);
+    CK(cudaMemcpyAsync(b->d_eoff, ep.data(), sizeof(int64_t) * ep.size(), cudaMemcpyHostToDevice, b->stream), "H2D eoff");
+    CK(cudaStreamSynchronize(b->stream), "sync");
+  }
+  if (!tiles.empty())
+    CK(cudaMemcpyAsync(b->d_tiles, tiles.data(), sizeof(ErTile) * tiles.size(), cudaMemcpyHostToDevice, b->stream), "H2D tiles");
   if (any_general) {
     CK(dalloc(b, &b->d_gpar, (int64_t)gpar.size()), "cudaMalloc(gpar)");
     CK(cudaMemcpyAsync(b->d_gpar, gpar.data(), sizeof(double) * gpar.size(), cudaMemcpyHostToDevice, b->stream), "H2D gpar");
@@ -417,8 +449,10 @@ er_status er_set_bc(er_batch *b, const int8_t *clamp_end) {
     if (clamp_end && clamp_end[r] == 0) b->flags[r] |= 1;
     if (clamp_end && clamp_end[r] == 1) b->flags[r] |= 2;
   }
+  sync_flags(b);
   CK(cudaSetDevice(b->device), "cudaSetDevice");
-  CK(cudaMemcpyAsync(b->d_flags, b->flags.data(), sizeof(int32_t) * b->flags.size(), cudaMemcpyHostToDevice, b->stream), "H2D flags");
+  if (b->n_rods > 0)
+    CK(cudaMemcpyAsync(b->d_rec, b->rec.data(), sizeof(double) * b->rec.size(), cudaMemcpyHostToDevice, b->stream), "H2D rec");
   CK(cudaStreamSynchronize(b->stream), "sync");
   return ER_OK;
 }
@@ -457,24 +491,22 @@ er_status er_set_forcing(er_batch *b, const er_forcing *f) {
   for (int c = 0; c < 3; ++c) { b->g[c] = f->gravity[c]; b->b0[c] = f->b_field[c]; }
   b->b_omega = f->b_omega;
   b->act_comp = act ? f->act_component : 0;
+  b->has_act = act;
   for (int64_t r = 0; r < R; ++r) {
     double *rec = &b->rec[(size_t)r * ER_REC];
-    double *r2 = &b->rec2[(size_t)r * ER_REC2];
     rec[REC_NU] = f->damping ? f->damping[r] : f->damping_all;
     b->flags[r] &= ~(FL_TIP | FL_ACT);
-    for (int c = 0; c < 3; ++c) r2[REC2_TIPX + c] = f->tip_force ? f->tip_force[3 * r + c] : 0.0;
+    for (int c = 0; c < 3; ++c) rec[REC_TIPX + c] = f->tip_force ? f->tip_force[3 * r + c] : 0.0;
     if (f->tip_force) b->flags[r] |= FL_TIP;
-    r2[REC2_ACTA] = act ? f->act_A[r] : 0.0;
-    r2[REC2_ACTF] = act ? f->act_f[r] : 0.0;
-    r2[REC2_ACTIL] = act ? 1.0 / f->act_L[r] : 0.0;
+    rec[REC_ACTA] = act ? f->act_A[r] : 0.0;
+    rec[REC_ACTF] = act ? f->act_f[r] : 0.0;
+    rec[REC_ACTIL] = act ? 1.0 / f->act_L[r] : 0.0;
     if (act) b->flags[r] |= FL_ACT;
   }
+  sync_flags(b);
   CK(cudaSetDevice(b->device), "cudaSetDevice");
-  if (R > 0) {
+  if (R > 0)
     CK(cudaMemcpyAsync(b->d_rec, b->rec.data(), sizeof(double) * b->rec.size(), cudaMemcpyHostToDevice, b->stream), "H2D rec");
-    CK(cudaMemcpyAsync(b->d_rec2, b->rec2.data(), sizeof(double) * b->rec2.size(), cudaMemcpyHostToDevice, b->stream), "H2D rec2");
-    CK(cudaMemcpyAsync(b->d_flags, b->flags.data(), sizeof(int32_t) * b->flags.size(), cudaMemcpyHostToDevice, b->stream), "H2D flags");
-  }
   if (f->magnetization && b->n_elems > 0) {
     if (!b->d_mag) CK(dalloc(b, &b->d_mag, 3 * b->ne), "cudaMalloc(mag)");
     er_status st = upload_planes(b, f->magnetization, ER_HOST, b->d_mag, b->n_elems, 3, b->ne);
@@ -496,7 +528,7 @@ er_status er_set_option(er_batch *b, int32_t option, int64_t value) {
     return ER_OK;
   }
   if (option == ER_OPT_KERNEL) {
-    if (value != 0 && value != 1) { b->last_error = "kernel must be 0 (fused) or 1 (staged)"; return ER_EINVAL; }
+    if (value < 0 || value > 2) { b->last_error = "kernel must be 0 (fused persistent), 1 (staged) or 2 (fused, one tile per CTA)"; return ER_EINVAL; }
     b->kernel_mode = (int)value;
     return ER_OK;
   }
@@ -521,20 +553,20 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
   int64_t done = 0;
   double t = b->t;
   while (done < n_steps) {
-    if (b->kernel_mode == 0) {
+    if (b->kernel_mode == 0 || b->kernel_mode == 2) {
       const int64_t k = std::min<int64_t>(b->steps_per_launch, n_steps - done);
       p.n_steps = (int32_t)k;
       p.t = t;
-      CK(er_launch_step(&p, b->n_tiles, b->block, 0, b->stream), "step kernel");
+      CK(er_launch_step(&p, b->block, b->kernel_mode == 0 ? 0 : 3, feat_of(b), b->stream), "step kernel");
       b->launches += 1;
       for (int64_t q = 0; q < k; ++q) { const double th = t + 0.5 * dt; t = th + 0.5 * dt; }
       done += k;
     } else {  // staged ablation: drift | dynamics + kick | drift, state through HBM between stages
       p.n_steps = 1;
       p.t = t;
-      CK(er_launch_step(&p, b->n_tiles, b->block, 1, b->stream), "drift kernel");
-      CK(er_launch_step(&p, b->n_tiles, b->block, 2, b->stream), "dyn kernel");
-      CK(er_launch_step(&p, b->n_tiles, b->block, 1, b->stream), "drift kernel");
+      CK(er_launch_step(&p, b->block, 1, 7, b->stream), "drift kernel");
+      CK(er_launch_step(&p, b->block, 2, 7, b->stream), "dyn kernel");
+      CK(er_launch_step(&p, b->block, 1, 7, b->stream), "drift kernel");
       b->launches += 3;
       const double th = t + 0.5 * dt;
       t = th + 0.5 * dt;
@@ -595,7 +627,7 @@ er_status er_diagnostics(er_batch *b, double out[ER_NDIAG]) {
   CK(cudaSetDevice(b->device), "cudaSetDevice");
   ErStepParams p = params_of(b);
   p.t = b->t;
-  CK(er_launch_diag(&p, b->n_tiles, b->block, b->d_diag_out, b->stream), "diag kernel");
+  CK(er_launch_diag(&p, b->block, b->d_diag_out, b->stream), "diag kernel");
   CK(cudaMemcpyAsync(out, b->d_diag_out, sizeof(double) * ER_NDIAG, cudaMemcpyDeviceToHost, b->stream), "D2H diag");
   CK(cudaStreamSynchronize(b->stream), "cudaStreamSynchronize");
   return ER_OK;
@@ -624,6 +656,7 @@ er_status er_query(const er_batch *b, er_info *info) {
   // state read + written once per step (r, v: 6 per node; Q, w: 12 per element) + rod records
   double bytes = 16.0 * (6.0 * b->n_nodes + 12.0 * b->n_elems) + 8.0 * ER_REC * b->n_rods;
   if (b->d_kappa0) bytes += 24.0 * b->n_vor;
+  bytes += 8.0 * (ER_REC - 16) * b->n_rods;  // the record is 24 doubles (192 B), B_min counts 128 B
   info->bytes_per_step = bytes;
   return ER_OK;
 }

@@ -1,15 +1,13 @@
-// er_kernels.cu -- the hot path (L2): one fused single-pass Cosserat rod step per launch
-// (or k steps per launch with the rod tile kept on chip), plus the staged ablation kernels,
-// the diagnostics reduction and layout/validation helpers.  sm_100a, fp64, no tensor cores
-// (nothing here is a dense contraction).
+// er_kernels.cu -- the hot path (L2) of the batched Cosserat rod step on sm_100a, fp64.
+// No tensor cores: nothing here is a dense contraction.
 //
-// Mapping: one CTA per rod-aligned tile of <= BLOCK "slots"; slot s of a rod is
-// node i, element i (i < N) and Voronoi domain i (1 <= i < N) of that rod, one thread per slot.
-// Neighbour data (node i+1, element i-1, n_{i-1}, mbar_{i+1}, beta_{i+1}) are exchanged through
-// shared memory; rods never straddle tiles, so there are no halos in HBM and no grid barrier:
-// the paper's asynchronous protocol is free here.
+// Mapping: a rod-aligned tile of <= BLOCK "slots" per CTA; slot s of a rod is
+// node i, element i (i < N) and Voronoi domain i (1 <= i < N) of that rod, one thread per
+// slot.  Neighbour data (node i+1, element i-1, n_{i-1}, mbar_{i+1}, beta_{i+1}) move through
+// shared memory; rods never straddle tiles, so there are no halos in HBM and no grid-wide
+// barrier -- the paper's asynchronous protocol is free here.
 //
-// One step of one slot:
+// One step of one slot, `step_body` below:
 //   A1-A3  r += h/2 v; Q <- rot(h/2 w) Q; clamped entries are not moved
 //   A4-A5  l = r_{i+1} - r_i, e, de/dt, sigma = Q l / lhat - e3, nbar = S (sigma - sigma0)/e, n = Q^T nbar
 //   A6     kappa = logrot(Q_k Q_{k-1}^T)/Dh, mbar = Bv (kappa - kappa0(t+h/2))/eps^3, beta = (kappa x mbar) Dh
@@ -17,8 +15,18 @@
 //   A8,A9  C = mbar_{i+1} - mbar_i + (beta_{i+1} + beta_i)/2 + (Q l) x nbar + c_mag
 //          alpha = e J^-1 C + Euler((J w) x w) / J + w de/dt / e - nu w;   w += h alpha
 //   A10    r += h/2 v; Q <- rot(h/2 w) Q
-// (Q l) x nbar == lhat (Q t) x S(sigma - sigma0) and the two rate terms are Eq. (1b)'s
-// (J w / e) x w and (J w / e^2) de/dt multiplied by e/J; see DESIGN.md §4 for the algebra.
+// (Q l) x nbar == lhat (Q t) x S(sigma - sigma0); the two rate terms are Eq. (1b)'s
+// (J w / e) x w and (J w / e^2) de/dt multiplied by e/J.
+//
+// Kernels:
+//  fused_persistent : production.  148 x k persistent CTAs walk the tile list; while a tile is
+//                     computed, the next tile's state, records and offsets stream into the
+//                     other half of a double-buffered smem stage with TMA 1-D bulk copies
+//                     (cp.async.bulk + mbarrier).  n_steps steps per tile (1 = the B_min
+//                     design; k > 1 = temporal blocking).
+//  simple_kernel    : one tile per CTA, plain loads; MODE_FUSED (ablation), MODE_DRIFT /
+//                     MODE_DYN (the staged three-launch path).
+//  diag_kernel      : per-tile partial sums of the energy functional, deterministic.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -29,377 +37,555 @@ namespace er {
 
 enum { MODE_FUSED = 0, MODE_DRIFT = 1, MODE_DYN = 2 };
 
-// per-slot index bookkeeping shared by all kernels
-struct Slot {
-  int64_t node, elem, vor;
-  int32_t rod, i, N, fl;
-  bool active, has_e, has_v;
+// exchange planes (stride BLOCK): A = r(0-2) v(3-5) Q(6-14); B = l(15) n(16-18); C aliases A:
+// mbar(0-2) beta(3-5).  19 planes.
+enum { XR = 0, XV = 3, XQ = 6, XL = 15, XN = 16, XM = 0, XB = 3, XPLANES = 19 };
+
+struct SlotInfo {
+  int s;            // slot (thread) index in the tile
+  int i, N, q;      // node index in the rod, rod length, rod index in the tile
+  int rod;          // global rod id
+  int64_t node, elem, vor;  // global indices
+  int fl;
+  bool active, has_e, has_v, cl_node, cl_elem;
 };
 
-// Decode this thread's slot from the tile table.  rstart must hold BLOCK/2 + 2 ints.
-template <int BLOCK>
-__device__ __forceinline__ Slot decode_slot(const ErStepParams &p, int tile, int *rstart) {
-  const int r0 = p.tiles[tile], r1 = p.tiles[tile + 1];
-  const int nr = r1 - r0;
-  const int64_t nbase = p.eoff[r0] + r0;
-  for (int q = threadIdx.x; q <= nr; q += BLOCK) rstart[q] = (int)(p.eoff[r0 + q] + (r0 + q) - nbase);
-  __syncthreads();
-  Slot sl;
-  const int s = threadIdx.x;
-  const int nslots = rstart[nr];
-  sl.active = s < nslots;
-  int lo = 0, hi = nr - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (rstart[mid] <= s) lo = mid; else hi = mid - 1;
+__device__ __forceinline__ void finish_slot(SlotInfo &si) {
+  const int clamp = si.fl & FL_CLAMP_MASK;
+  si.has_e = si.active && si.i < si.N;
+  si.has_v = si.active && si.i >= 1 && si.i < si.N;
+  si.cl_node = si.active && ((clamp == 1 && si.i == 0) || (clamp == 2 && si.i == si.N));
+  si.cl_elem = si.has_e && ((clamp == 1 && si.i == 0) || (clamp == 2 && si.i == si.N - 1));
+}
+
+__device__ __forceinline__ int rec_flags(const double *rec) {
+  return (int)__double_as_longlong(rec[REC_FLAGS]);
+}
+
+// ------------------------------------------------------------------------------------------
+// One position-Verlet step (or one stage of it) of one slot.  State in registers; X is the
+// smem exchange area (XPLANES planes of stride BLOCK); rec points at the rod record (smem in
+// the persistent kernel, global in the simple one).  k0s: static rest curvature of the slot's
+// Voronoi domain (FEAT_KAPPA0).
+template <int BLOCK, int FEAT, bool DRIFT1, bool DYN, bool DRIFT2>
+__device__ __forceinline__ void step_body(const ErStepParams &p, double *__restrict__ X,
+                                          const double *__restrict__ rec, const SlotInfo &si,
+                                          double r[3], double v[3], double Q[9], double w[3],
+                                          const double k0s[3], double &t, unsigned &fbits) {
+  constexpr bool GEN = (FEAT & FEAT_GENERAL) != 0;
+  constexpr bool EXTRA = (FEAT & FEAT_EXTRA) != 0;
+  const int s = si.s, i = si.i, N = si.N;
+  const double h = p.h, hh = 0.5 * p.h;
+  const bool general = GEN && (si.fl & FL_GENERAL);
+  const double t_half = t + hh;
+  auto gp = [&](int plane) { return __ldg(p.gpar + plane * p.ng + si.node); };
+
+  if (DRIFT1) {
+    if (!si.cl_node) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) r[c] = fma(hh, v[c], r[c]);
+    }
+    if (si.has_e && !si.cl_elem) rotate_inplace(Q, hh * w[0], hh * w[1], hh * w[2]);
   }
-  sl.rod = r0 + lo;
-  sl.i = s - rstart[lo];
-  sl.N = rstart[lo + 1] - rstart[lo] - 1;
-  sl.node = nbase + s;
-  sl.elem = sl.node - sl.rod;
-  sl.vor = sl.elem - sl.rod - 1;
-  sl.has_e = sl.active && sl.i < sl.N;
-  sl.has_v = sl.active && sl.i >= 1 && sl.i < sl.N;
-  sl.fl = sl.active ? __ldg(p.flags + sl.rod) : 0;
-  return sl;
+  if (DYN) {
+    // ---- exchange A
+    if (si.active) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) { X[(XR + c) * BLOCK + s] = r[c]; X[(XV + c) * BLOCK + s] = v[c]; }
+#pragma unroll
+      for (int c = 0; c < 9; ++c) X[(XQ + c) * BLOCK + s] = Q[c];
+    }
+    __syncthreads();
+
+    // ---- A4-A5 edge i: kinematics, shear/stretch strain, stress
+    double Ql[3] = {0.0, 0.0, 0.0}, nb[3] = {0.0, 0.0, 0.0}, n[3] = {0.0, 0.0, 0.0};
+    double l = 0.0, inv_e = 0.0, e = 1.0, edot = 0.0;
+    if (si.has_e) {
+      const double lh = general ? gp(GP_LHAT) : rec[REC_LHAT];
+      const double ilh = general ? gp(GP_ILHAT) : rec[REC_ILHAT];
+      double ell[3], dv[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        ell[c] = X[(XR + c) * BLOCK + s + 1] - r[c];
+        dv[c] = X[(XV + c) * BLOCK + s + 1] - v[c];
+      }
+      const double l2 = dot3(ell, ell);
+      const double il = rsqrt(l2);
+      l = l2 * il;
+      e = l * ilh;
+      inv_e = lh * il;
+      edot = dot3(ell, dv) * il * ilh;
+      if (!(e >= 1e-12)) fbits |= 2u;  // ER_F_DEGENERATE
+      Ql[0] = dot3(Q, ell);
+      Ql[1] = dot3(Q + 3, ell);
+      Ql[2] = dot3(Q + 6, ell);
+      double sg[3] = {Ql[0] * ilh, Ql[1] * ilh, fma(Ql[2], ilh, -1.0)};  // sigma = Q l/lhat - e3
+      if (EXTRA && p.sigma0) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) sg[c] -= __ldg(p.sigma0 + c * p.ne + si.elem);
+      }
+      const double S1 = general ? gp(GP_S1) : rec[REC_S1];
+      const double S3 = general ? gp(GP_S3) : rec[REC_S3];
+      nb[0] = S1 * sg[0] * inv_e;
+      nb[1] = S1 * sg[1] * inv_e;
+      nb[2] = S3 * sg[2] * inv_e;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) n[c] = fma(Q[c], nb[0], fma(Q[3 + c], nb[1], Q[6 + c] * nb[2]));  // Q^T nbar
+    }
+    // ---- A6 Voronoi i: curvature via inverse Rodrigues
+    double kap[3] = {0.0, 0.0, 0.0};
+    if (si.has_v) {
+      double Qp[9], cth, s2;
+#pragma unroll
+      for (int c = 0; c < 9; ++c) Qp[c] = X[(XQ + c) * BLOCK + s - 1];
+      logrot_pair(Q, Qp, kap, cth, s2);
+      if (cth < 0.0 && s2 <= 1e-12 * cth * cth) fbits |= 4u;  // ER_F_ANTIPODAL: theta >= pi - 1e-6
+    }
+    // ---- exchange B
+    if (si.has_e) {
+      X[XL * BLOCK + s] = l;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) X[(XN + c) * BLOCK + s] = n[c];
+    }
+    __syncthreads();
+
+    // ---- A6 bending moment and its averaged cross term
+    double mb[3] = {0.0, 0.0, 0.0}, be[3] = {0.0, 0.0, 0.0};
+    if (si.has_v) {
+      const double Dh = general ? gp(GP_DH) : rec[REC_LHAT];
+      const double iDh = general ? 1.0 / Dh : rec[REC_ILHAT];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) kap[c] *= iDh;
+      const double D = 0.5 * (X[XL * BLOCK + s - 1] + l);
+      const double ieps = Dh / D;
+      const double ieps3 = ieps * ieps * ieps;
+      double k0[3] = {k0s[0], k0s[1], k0s[2]};
+      if (EXTRA && (si.fl & FL_ACT)) {
+        const double sk = general ? gp(GP_SK) : i * rec[REC_LHAT];
+        // A sin(2 pi (s/L - f t)) = A sinpi(2 (s/L - f t))
+        const double arg = 2.0 * fma(sk, rec[REC_ACTIL], -rec[REC_ACTF] * t_half);
+        k0[p.act_comp] += rec[REC_ACTA] * sinpi(arg);
+      }
+      const double B1 = general ? gp(GP_BV1) : rec[REC_B1];
+      const double B2 = general ? gp(GP_BV2) : rec[REC_B2];
+      const double B3 = general ? gp(GP_BV3) : rec[REC_B3];
+      mb[0] = B1 * (kap[0] - k0[0]) * ieps3;
+      mb[1] = B2 * (kap[1] - k0[1]) * ieps3;
+      mb[2] = B3 * (kap[2] - k0[2]) * ieps3;
+      be[0] = (kap[1] * mb[2] - kap[2] * mb[1]) * Dh;
+      be[1] = (kap[2] * mb[0] - kap[0] * mb[2]) * Dh;
+      be[2] = (kap[0] * mb[1] - kap[1] * mb[0]) * Dh;
+    }
+    // ---- A7 + A9 node force, linear acceleration, kick
+    if (si.active) {
+      double F[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) F[c] = n[c] - (i >= 1 ? X[(XN + c) * BLOCK + s - 1] : 0.0);
+      if ((si.fl & FL_TIP) && i == ((si.fl & FL_CLAMP_MASK) == 2 ? 0 : N)) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) F[c] += rec[REC_TIPX + c];
+      }
+      const double im = general ? gp(GP_IM) : rec[REC_IM] * ((i == 0 || i == N) ? 2.0 : 1.0);
+      const double nu = rec[REC_NU];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double a = fma(F[c], im, fma(-nu, v[c], p.g[c]));
+        v[c] = si.cl_node ? 0.0 : fma(h, a, v[c]);
+      }
+    }
+    // ---- exchange C (aliases A; every A read happened before the B barrier)
+    if (si.active) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) { X[(XM + c) * BLOCK + s] = mb[c]; X[(XB + c) * BLOCK + s] = be[c]; }
+    }
+    __syncthreads();
+
+    // ---- A8 + A9 element couple, angular acceleration, kick
+    if (si.has_e) {
+      double C[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        C[c] = (X[(XM + c) * BLOCK + s + 1] - mb[c]) + 0.5 * (X[(XB + c) * BLOCK + s + 1] + be[c]);
+      C[0] += Ql[1] * nb[2] - Ql[2] * nb[1];  // shear torque lhat (Q t) x S(sigma - sigma0) == (Q l) x nbar
+      C[1] += Ql[2] * nb[0] - Ql[0] * nb[2];
+      C[2] += Ql[0] * nb[1] - Ql[1] * nb[0];
+      if (EXTRA && p.mag) {  // c_mag = lhat m x (Q b(t))
+        double sn, cs;
+        sincos(p.b_omega * t_half, &sn, &cs);
+        const double b[3] = {cs * p.b0[0] - sn * p.b0[1], sn * p.b0[0] + cs * p.b0[1], p.b0[2]};
+        const double Qb[3] = {dot3(Q, b), dot3(Q + 3, b), dot3(Q + 6, b)};
+        double m[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) m[c] = __ldg(p.mag + c * p.ne + si.elem);
+        const double lh = general ? gp(GP_LHAT) : rec[REC_LHAT];
+        C[0] += lh * (m[1] * Qb[2] - m[2] * Qb[1]);
+        C[1] += lh * (m[2] * Qb[0] - m[0] * Qb[2]);
+        C[2] += lh * (m[0] * Qb[1] - m[1] * Qb[0]);
+      }
+      const double nu = rec[REC_NU];
+      const double rate = edot * inv_e - nu;
+      const double eu[3] = {w[1] * w[2], w[2] * w[0], w[0] * w[1]};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double iJ = general ? gp(GP_IJ1 + c) : rec[REC_IJ1 + c];
+        const double kJ = general ? gp(GP_KJ1 + c) : rec[REC_KJ1 + c];
+        const double al = fma(e * iJ, C[c], fma(kJ, eu[c], rate * w[c]));
+        w[c] = si.cl_elem ? 0.0 : fma(h, al, w[c]);
+      }
+    }
+  }
+  if (DRIFT2) {
+    t = t_half + hh;
+    if (!si.cl_node) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) r[c] = fma(hh, v[c], r[c]);
+    }
+    if (si.has_e && !si.cl_elem) rotate_inplace(Q, hh * w[0], hh * w[1], hh * w[2]);
+  }
+  if ((DRIFT1 || DRIFT2) && si.active) {  // fault checks: non-finite state, overspeed
+    double acc = (r[0] + r[1] + r[2]) + (v[0] + v[1] + v[2]);
+    if (si.has_e) {
+#pragma unroll
+      for (int c = 0; c < 9; ++c) acc += Q[c];
+      acc += w[0] + w[1] + w[2];
+    }
+    if (!isfinite(acc)) fbits |= 1u;
+    if (dot3(v, v) > rec[REC_VMAX2]) fbits |= 8u;
+  }
 }
 
 __device__ __forceinline__ void report_fault(const ErStepParams &p, unsigned bits, int rod) {
-  const unsigned mask = __ballot_sync(0xffffffffu, bits != 0);
-  if (mask == 0) return;
+  if (__ballot_sync(0xffffffffu, bits != 0) == 0) return;
   if (bits) {
     atomicOr(p.fault, (unsigned long long)bits);
     atomicMin(p.fault + 1, (unsigned long long)rod);
   }
 }
 
-// The fused step.  MODE_FUSED: p.n_steps full steps per launch with the tile held in
-// registers/shared memory; MODE_DRIFT: one drift(h/2) stage; MODE_DYN: one kick stage.
-template <int BLOCK, int MINB, int MODE>
-__global__ void __launch_bounds__(BLOCK, MINB) step_kernel(const ErStepParams p) {
-  extern __shared__ double smem[];
-  double *xr = smem;               // exchange A: r (3), v (3), Q (9)
-  double *xv = xr + 3 * BLOCK;
-  double *xQ = xv + 3 * BLOCK;
-  double *xl = xQ + 9 * BLOCK;     // exchange B: l (1), n (3)
-  double *xn = xl + BLOCK;
-  double *xm = smem;               // exchange C (aliases A): mbar (3), beta (3)
-  double *xb = smem + 3 * BLOCK;
-  int *rstart = reinterpret_cast<int *>(xn + 3 * BLOCK);
+// ------------------------------------------------------------------------------------------
+// TMA 1-D bulk copy + mbarrier helpers (PTX; sm_90+ async proxy, used here on sm_100a).
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
-  const Slot sl = decode_slot<BLOCK>(p, blockIdx.x, rstart);
-  const int s = threadIdx.x;
-  const int i = sl.i, N = sl.N;
-  const int clamp = sl.fl & FL_CLAMP_MASK;
-  const bool cl_node = sl.active && ((clamp == 1 && i == 0) || (clamp == 2 && i == N));
-  const bool cl_elem = sl.has_e && ((clamp == 1 && i == 0) || (clamp == 2 && i == N - 1));
-  const bool general = (sl.fl & FL_GENERAL) != 0;
-  const double *rec = p.rec + (int64_t)sl.rod * ER_REC;
+// Stage geometry of the persistent kernel: per buffer NPL planes of stride PS doubles, then the
+// rod records (RMAX x ER_REC) and the tile's element offsets (RMAX + 4 int64).
+template <int BLOCK, int FEAT>
+struct Stage {
+  static constexpr int PS = BLOCK + 8;
+  static constexpr int NPL = (FEAT & FEAT_KAPPA0) ? 21 : 18;
+  static constexpr int RMAX = BLOCK / 8;
+  static constexpr int PLANES = (NPL > XPLANES ? NPL : XPLANES) * PS;  // exchange reuses the planes
+  static constexpr int RECOFF = PLANES;
+  static constexpr int EOFF = RECOFF + RMAX * ER_REC;
+  static constexpr int BUFD = EOFF + RMAX + 4;  // doubles per buffer (even)
+  static constexpr size_t bytes() { return (size_t)(2 * BUFD) * 8 + 2 * 8; }
+};
 
-  // ---- load state (once per launch)
-  double r[3], v[3], Q[9], w[3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    r[c] = sl.active ? __ldcs(p.node + c * p.nn + sl.node) : 0.0;
-    v[c] = sl.active ? __ldcs(p.node + (3 + c) * p.nn + sl.node) : 0.0;
+// Thread 0 issues the bulk copies of tile `T` into stage buffer B.
+template <int BLOCK, int FEAT>
+__device__ __forceinline__ void issue_tile(const ErStepParams &p, const ErTile &T, double *B, uint64_t *bar) {
+  using SG = Stage<BLOCK, FEAT>;
+  const int64_t na = T.nbase & ~1ll, ne_ = T.ebase & ~1ll;
+  const uint32_t cn = (uint32_t)(((T.nbase + T.nslots + 1) & ~1ll) - na);
+  const uint32_t ce = (uint32_t)(((T.ebase + T.nel + 1) & ~1ll) - ne_);
+  const int64_t vb = T.ebase - T.r0, nvor = T.nel - T.nr;
+  const int64_t va = vb & ~1ll;
+  const uint32_t cv = nvor > 0 ? (uint32_t)(((vb + nvor + 1) & ~1ll) - va) : 0u;
+  const int64_t ra = T.r0 & ~1ll;
+  const uint32_t ceo = (uint32_t)(((T.r0 + T.nr + 2) & ~1ll) - ra);
+  uint32_t bytes = 8u * (6u * cn + 12u * ce) + (uint32_t)T.nr * ER_REC * 8u + 8u * ceo;
+  if ((FEAT & FEAT_KAPPA0) && cv) bytes += 8u * 3u * cv;
+  mbar_expect_tx(bar, bytes);
+#pragma unroll 1
+  for (int c = 0; c < 6; ++c) bulk_g2s(B + c * SG::PS, p.node + c * p.nn + na, 8u * cn, bar);
+#pragma unroll 1
+  for (int c = 0; c < 12; ++c) bulk_g2s(B + (6 + c) * SG::PS, p.elem + c * p.ne + ne_, 8u * ce, bar);
+  if ((FEAT & FEAT_KAPPA0) && cv) {
+#pragma unroll 1
+    for (int c = 0; c < 3; ++c) bulk_g2s(B + (18 + c) * SG::PS, p.kappa0 + c * p.nv + va, 8u * cv, bar);
   }
-#pragma unroll
-  for (int c = 0; c < 9; ++c) Q[c] = sl.has_e ? __ldcs(p.elem + c * p.ne + sl.elem) : 0.0;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) w[c] = sl.has_e ? __ldcs(p.elem + (9 + c) * p.ne + sl.elem) : 0.0;
+  bulk_g2s(B + SG::RECOFF, p.rec + (int64_t)T.r0 * ER_REC, (uint32_t)T.nr * ER_REC * 8u, bar);
+  bulk_g2s(B + SG::EOFF, p.eoff + ra, 8u * ceo, bar);
+}
 
-  const double h = p.h, hh = 0.5 * p.h;
-  double t = p.t;
-  unsigned fbits = 0;
-
-  const int nsteps = (MODE == MODE_FUSED) ? p.n_steps : 1;
-  for (int step = 0; step < nsteps; ++step) {
-    const double t_half = t + hh;
-    if (MODE == MODE_FUSED || MODE == MODE_DRIFT) {
-      // ---- A1-A3 drift h/2 (clamped node / element are held at their pose)
-      if (!cl_node) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) r[c] = fma(hh, v[c], r[c]);
-      }
-      if (sl.has_e && !cl_elem) rotate_inplace(Q, hh * w[0], hh * w[1], hh * w[2]);
-    }
-    if (MODE == MODE_FUSED || MODE == MODE_DYN) {
-      // ---- exchange A
-      if (sl.active) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) { xr[c * BLOCK + s] = r[c]; xv[c * BLOCK + s] = v[c]; }
-#pragma unroll
-        for (int c = 0; c < 9; ++c) xQ[c * BLOCK + s] = Q[c];
-      }
-      __syncthreads();
-
-      // ---- A4-A5 edge i: kinematics, shear/stretch strain, stress
-      double ell[3] = {0, 0, 0}, Ql[3] = {0, 0, 0}, nb[3] = {0, 0, 0}, n[3] = {0, 0, 0};
-      double l = 0.0, inv_e = 0.0, e = 1.0, edot = 0.0;
-      if (sl.has_e) {
-        const double lh = general ? __ldg(p.gpar + GP_LHAT * p.ng + sl.node) : __ldg(rec + REC_LHAT);
-        const double ilh = general ? __ldg(p.gpar + GP_ILHAT * p.ng + sl.node) : __ldg(rec + REC_ILHAT);
-        double dv[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          ell[c] = xr[c * BLOCK + s + 1] - r[c];
-          dv[c] = xv[c * BLOCK + s + 1] - v[c];
-        }
-        const double l2 = dot3(ell, ell);
-        const double il = rsqrt(l2);
-        l = l2 * il;
-        e = l * ilh;
-        inv_e = lh * il;
-        edot = dot3(ell, dv) * il * ilh;
-        if (!(e >= 1e-12)) fbits |= 2u;  // ER_F_DEGENERATE
-        // sigma = e Q t - e3 = Q l / lhat - e3
-        Ql[0] = dot3(Q, ell);
-        Ql[1] = dot3(Q + 3, ell);
-        Ql[2] = dot3(Q + 6, ell);
-        double sg[3] = {Ql[0] * ilh, Ql[1] * ilh, fma(Ql[2], ilh, -1.0)};
-        if (p.sigma0) {
-#pragma unroll
-          for (int c = 0; c < 3; ++c) sg[c] -= __ldg(p.sigma0 + c * p.ne + sl.elem);
-        }
-        const double S1 = general ? __ldg(p.gpar + GP_S1 * p.ng + sl.node) : __ldg(rec + REC_S1);
-        const double S3 = general ? __ldg(p.gpar + GP_S3 * p.ng + sl.node) : __ldg(rec + REC_S3);
-        nb[0] = S1 * sg[0] * inv_e;
-        nb[1] = S1 * sg[1] * inv_e;
-        nb[2] = S3 * sg[2] * inv_e;
-        // n = Q^T nbar (lab)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) n[c] = fma(Q[c], nb[0], fma(Q[3 + c], nb[1], Q[6 + c] * nb[2]));
-      }
-      // ---- A6 Voronoi i: curvature via inverse Rodrigues
-      double kap[3] = {0, 0, 0};
-      double cth = 1.0, s2 = 0.0;
-      if (sl.has_v) {
-        double Qp[9];
-#pragma unroll
-        for (int c = 0; c < 9; ++c) Qp[c] = xQ[c * BLOCK + s - 1];
-        logrot_pair(Q, Qp, kap, cth, s2);
-        if (cth < 0.0 && s2 <= 1e-12 * cth * cth) fbits |= 4u;  // ER_F_ANTIPODAL: theta >= pi - 1e-6
-      }
-      // ---- exchange B
-      if (sl.has_e) {
-        xl[s] = l;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) xn[c * BLOCK + s] = n[c];
-      }
-      __syncthreads();
-
-      // ---- A6 bending moment and its cross term
-      double mb[3] = {0, 0, 0}, be[3] = {0, 0, 0};
-      if (sl.has_v) {
-        const double Dh = general ? __ldg(p.gpar + GP_DH * p.ng + sl.node) : __ldg(rec + REC_LHAT);
-        const double iDh = general ? 1.0 / Dh : __ldg(rec + REC_ILHAT);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) kap[c] *= iDh;
-        const double D = 0.5 * (xl[s - 1] + l);
-        const double ieps = Dh / D;
-        const double ieps3 = ieps * ieps * ieps;
-        double k0[3] = {0, 0, 0};
-        if (p.kappa0) {
-#pragma unroll
-          for (int c = 0; c < 3; ++c) k0[c] = __ldg(p.kappa0 + c * p.nv + sl.vor);
-        }
-        if (sl.fl & FL_ACT) {
-          const double *r2 = p.rec2 + (int64_t)sl.rod * ER_REC2;
-          const double sk = general ? __ldg(p.gpar + GP_SK * p.ng + sl.node) : i * __ldg(rec + REC_LHAT);
-          // A sin(2 pi (s/L - f t)) = A sinpi(2 (s/L - f t))
-          const double arg = 2.0 * fma(sk, __ldg(r2 + REC2_ACTIL), -__ldg(r2 + REC2_ACTF) * t_half);
-          k0[p.act_comp] += __ldg(r2 + REC2_ACTA) * sinpi(arg);
-        }
-        const double B1 = general ? __ldg(p.gpar + GP_BV1 * p.ng + sl.node) : __ldg(rec + REC_B1);
-        const double B2 = general ? __ldg(p.gpar + GP_BV2 * p.ng + sl.node) : __ldg(rec + REC_B2);
-        const double B3 = general ? __ldg(p.gpar + GP_BV3 * p.ng + sl.node) : __ldg(rec + REC_B3);
-        mb[0] = B1 * (kap[0] - k0[0]) * ieps3;
-        mb[1] = B2 * (kap[1] - k0[1]) * ieps3;
-        mb[2] = B3 * (kap[2] - k0[2]) * ieps3;
-        be[0] = (kap[1] * mb[2] - kap[2] * mb[1]) * Dh;
-        be[1] = (kap[2] * mb[0] - kap[0] * mb[2]) * Dh;
-        be[2] = (kap[0] * mb[1] - kap[1] * mb[0]) * Dh;
-      }
-      // ---- A7 + A9 node force, linear acceleration, kick
-      if (sl.active) {
-        double F[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) F[c] = n[c] - (i >= 1 ? xn[c * BLOCK + s - 1] : 0.0);
-        if ((sl.fl & FL_TIP) && i == (clamp == 2 ? 0 : N)) {
-          const double *r2 = p.rec2 + (int64_t)sl.rod * ER_REC2;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) F[c] += __ldg(r2 + REC2_TIPX + c);
-        }
-        const double im = general ? __ldg(p.gpar + GP_IM * p.ng + sl.node)
-                                  : __ldg(rec + REC_IM) * ((i == 0 || i == N) ? 2.0 : 1.0);
-        const double nu = __ldg(rec + REC_NU);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const double a = fma(F[c], im, fma(-nu, v[c], p.g[c]));
-          v[c] = cl_node ? 0.0 : fma(h, a, v[c]);
-        }
-      }
-      // ---- exchange C (aliases A; all A reads happened before the B barrier)
-      if (sl.active) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) { xm[c * BLOCK + s] = mb[c]; xb[c * BLOCK + s] = be[c]; }
-      }
-      __syncthreads();
-
-      // ---- A8 + A9 element couple, angular acceleration, kick
-      if (sl.has_e) {
-        double C[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-          C[c] = (xm[c * BLOCK + s + 1] - mb[c]) + 0.5 * (xb[c * BLOCK + s + 1] + be[c]);
-        // shear torque lhat (Q t) x S(sigma - sigma0) == (Q l) x nbar
-        C[0] += Ql[1] * nb[2] - Ql[2] * nb[1];
-        C[1] += Ql[2] * nb[0] - Ql[0] * nb[2];
-        C[2] += Ql[0] * nb[1] - Ql[1] * nb[0];
-        if (p.mag) {  // c_mag = lhat m x (Q b(t))
-          double sn, cs;
-          sincos(p.b_omega * t_half, &sn, &cs);
-          const double b[3] = {cs * p.b0[0] - sn * p.b0[1], sn * p.b0[0] + cs * p.b0[1], p.b0[2]};
-          const double Qb[3] = {dot3(Q, b), dot3(Q + 3, b), dot3(Q + 6, b)};
-          double m[3];
-#pragma unroll
-          for (int c = 0; c < 3; ++c) m[c] = __ldg(p.mag + c * p.ne + sl.elem);
-          const double lh = general ? __ldg(p.gpar + GP_LHAT * p.ng + sl.node) : __ldg(rec + REC_LHAT);
-          C[0] += lh * (m[1] * Qb[2] - m[2] * Qb[1]);
-          C[1] += lh * (m[2] * Qb[0] - m[0] * Qb[2]);
-          C[2] += lh * (m[0] * Qb[1] - m[1] * Qb[0]);
-        }
-        double iJ[3], kJ[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          iJ[c] = general ? __ldg(p.gpar + (GP_IJ1 + c) * p.ng + sl.node) : __ldg(rec + REC_IJ1 + c);
-          kJ[c] = general ? __ldg(p.gpar + (GP_KJ1 + c) * p.ng + sl.node) : __ldg(rec + REC_KJ1 + c);
-        }
-        const double nu = __ldg(rec + REC_NU);
-        const double rate = edot * inv_e;
-        const double eu[3] = {w[1] * w[2], w[2] * w[0], w[0] * w[1]};
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const double al = fma(e * iJ[c], C[c], fma(kJ[c], eu[c], (rate - nu) * w[c]));
-          w[c] = cl_elem ? 0.0 : fma(h, al, w[c]);
-        }
-      }
-    }
-    if (MODE == MODE_FUSED) {
-      // ---- A10 drift h/2 with the new rates
-      t = t_half + hh;
-      if (!cl_node) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) r[c] = fma(hh, v[c], r[c]);
-      }
-      if (sl.has_e && !cl_elem) rotate_inplace(Q, hh * w[0], hh * w[1], hh * w[2]);
-      if (step + 1 < nsteps) __syncthreads();  // exchange C buffers are re-used as A next step
-    }
-    // ---- fault checks: non-finite state, overspeed
-    if (sl.active && MODE != MODE_DYN) {
-      double acc = r[0] + r[1] + r[2] + v[0] + v[1] + v[2];
-      if (sl.has_e) {
-#pragma unroll
-        for (int c = 0; c < 9; ++c) acc += Q[c];
-        acc += w[0] + w[1] + w[2];
-      }
-      if (!isfinite(acc)) fbits |= 1u;
-      if (dot3(v, v) > __ldg(rec + REC_VMAX2)) fbits |= 8u;
-    }
+template <int BLOCK, int MINB, int FEAT>
+__global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepParams p) {
+  using SG = Stage<BLOCK, FEAT>;
+  extern __shared__ __align__(16) double sm[];
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sm + 2 * SG::BUFD);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
   }
+  __syncthreads();
+  int64_t tile = blockIdx.x;
+  if (tid == 0 && tile < p.n_tiles) issue_tile<BLOCK, FEAT>(p, p.tiles[tile], sm, &bar[0]);
+  uint32_t phase = 0;  // bit b = parity of buffer b
+  unsigned fbits_all = 0;
+  int frod = 0x7fffffff;
+  for (int k = 0; tile < p.n_tiles; tile += gridDim.x, ++k) {
+    const int b = k & 1;
+    double *B = sm + b * SG::BUFD;
+    const ErTile T = p.tiles[tile];
+    const int64_t tnext = tile + gridDim.x;
+    ErTile Tn;
+    if (tid == 0 && tnext < p.n_tiles) Tn = p.tiles[tnext];  // descriptor load overlaps the wait
+    mbar_wait(&bar[b], (phase >> b) & 1u);
+    phase ^= 1u << b;
 
-  // ---- store state (once per launch)
-  if (sl.active) {
+    // ---- decode this thread's slot from the staged element offsets
+    const int64_t *eo = reinterpret_cast<const int64_t *>(B + SG::EOFF) + (T.r0 & 1);
+    SlotInfo si;
+    si.s = tid;
+    si.active = tid < T.nslots;
+    int lo = 0, hi = T.nr - 1;
+    const int64_t e0 = eo[0];
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if ((int)(eo[mid] - e0) + mid <= tid) lo = mid; else hi = mid - 1;
+    }
+    si.q = lo;
+    si.rod = T.r0 + lo;
+    const int st0 = (int)(eo[lo] - e0) + lo;
+    si.i = tid - st0;
+    si.N = (int)(eo[lo + 1] - eo[lo]);
+    si.node = T.nbase + tid;
+    si.elem = T.ebase + tid - lo;
+    si.vor = si.elem - si.rod - 1;
+    const double *rec = B + SG::RECOFF + lo * ER_REC;
+    si.fl = si.active ? rec_flags(rec) : 0;
+    finish_slot(si);
+
+    // ---- stage -> registers
+    const int ln = tid + (int)(T.nbase & 1);
+    const int le = tid - lo + (int)(T.ebase & 1);
+    double r[3], v[3], Q[9], w[3], k0s[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      __stcs(p.node + c * p.nn + sl.node, r[c]);
-      __stcs(p.node + (3 + c) * p.nn + sl.node, v[c]);
+      r[c] = B[c * SG::PS + ln];
+      v[c] = B[(3 + c) * SG::PS + ln];
+    }
+#pragma unroll
+    for (int c = 0; c < 9; ++c) Q[c] = B[(6 + c) * SG::PS + le];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) w[c] = B[(15 + c) * SG::PS + le];
+    if ((FEAT & FEAT_KAPPA0) && si.has_v) {
+      const int lv = tid - 2 * lo - 1 + (int)((T.ebase - T.r0) & 1);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) k0s[c] = B[(18 + c) * SG::PS + lv];
+    }
+    __syncthreads();  // everyone has read the stage planes: they become this tile's exchange area
+    if (tid == 0 && tnext < p.n_tiles) {
+      fence_proxy_async();  // order the previous generic smem accesses before the async writes
+      issue_tile<BLOCK, FEAT>(p, Tn, sm + (b ^ 1) * SG::BUFD, &bar[b ^ 1]);
+    }
+
+    // ---- the steps
+    double t = p.t;
+    unsigned fbits = 0;
+    for (int st = 0; st < p.n_steps; ++st) {
+      step_body<BLOCK, FEAT, true, true, true>(p, B, rec, si, r, v, Q, w, k0s, t, fbits);
+      if (st + 1 < p.n_steps) __syncthreads();  // exchange C is re-used as A by the next step
+    }
+    if (fbits) { fbits_all |= fbits; frod = min(frod, si.rod); }
+
+    // ---- registers -> HBM (streaming stores)
+    if (si.active) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        __stcs(p.node + c * p.nn + si.node, r[c]);
+        __stcs(p.node + (3 + c) * p.nn + si.node, v[c]);
+      }
+    }
+    if (si.has_e) {
+#pragma unroll
+      for (int c = 0; c < 9; ++c) __stcs(p.elem + c * p.ne + si.elem, Q[c]);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) __stcs(p.elem + (9 + c) * p.ne + si.elem, w[c]);
     }
   }
-  if (sl.has_e) {
-#pragma unroll
-    for (int c = 0; c < 9; ++c) __stcs(p.elem + c * p.ne + sl.elem, Q[c]);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) __stcs(p.elem + (9 + c) * p.ne + sl.elem, w[c]);
+  report_fault(p, fbits_all, frod);
+}
+
+// ------------------------------------------------------------------------------------------
+// simple kernel: one tile per CTA, plain global loads; decode from the global tile table.
+template <int BLOCK>
+__device__ __forceinline__ void decode_global(const ErStepParams &p, const ErTile &T, SlotInfo &si, int *rst) {
+  for (int q = threadIdx.x; q <= T.nr; q += BLOCK) rst[q] = (int)(p.eoff[T.r0 + q] - T.ebase) + q;
+  __syncthreads();
+  const int s = threadIdx.x;
+  si.s = s;
+  si.active = s < T.nslots;
+  int lo = 0, hi = T.nr - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (rst[mid] <= s) lo = mid; else hi = mid - 1;
   }
-  report_fault(p, fbits, sl.rod);
+  si.q = lo;
+  si.rod = T.r0 + lo;
+  si.i = s - rst[lo];
+  si.N = rst[lo + 1] - rst[lo] - 1;
+  si.node = T.nbase + s;
+  si.elem = T.ebase + s - lo;
+  si.vor = si.elem - si.rod - 1;
+  si.fl = si.active ? rec_flags(p.rec + (int64_t)si.rod * ER_REC) : 0;
+  finish_slot(si);
+}
+
+template <int BLOCK, int MINB, int MODE>
+__global__ void __launch_bounds__(BLOCK, MINB) simple_kernel(const ErStepParams p) {
+  constexpr int FEAT = FEAT_GENERAL | FEAT_KAPPA0 | FEAT_EXTRA;
+  extern __shared__ __align__(16) double sm[];
+  int *rst = reinterpret_cast<int *>(sm + XPLANES * BLOCK);
+  const ErTile T = p.tiles[blockIdx.x];
+  SlotInfo si;
+  decode_global<BLOCK>(p, T, si, rst);
+  const double *rec = p.rec + (int64_t)si.rod * ER_REC;
+  double r[3] = {0, 0, 0}, v[3] = {0, 0, 0}, Q[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, w[3] = {0, 0, 0};
+  double k0s[3] = {0.0, 0.0, 0.0};
+  if (si.active) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      r[c] = __ldcs(p.node + c * p.nn + si.node);
+      v[c] = __ldcs(p.node + (3 + c) * p.nn + si.node);
+    }
+  }
+  if (si.has_e) {
+#pragma unroll
+    for (int c = 0; c < 9; ++c) Q[c] = __ldcs(p.elem + c * p.ne + si.elem);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) w[c] = __ldcs(p.elem + (9 + c) * p.ne + si.elem);
+  }
+  if (p.kappa0 && si.has_v) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) k0s[c] = __ldg(p.kappa0 + c * p.nv + si.vor);
+  }
+  double t = p.t;
+  unsigned fbits = 0;
+  const int nsteps = (MODE == MODE_FUSED) ? p.n_steps : 1;
+  for (int st = 0; st < nsteps; ++st) {
+    if (MODE == MODE_FUSED) step_body<BLOCK, FEAT, true, true, true>(p, sm, rec, si, r, v, Q, w, k0s, t, fbits);
+    if (MODE == MODE_DRIFT) step_body<BLOCK, FEAT, true, false, false>(p, sm, rec, si, r, v, Q, w, k0s, t, fbits);
+    if (MODE == MODE_DYN) step_body<BLOCK, FEAT, false, true, false>(p, sm, rec, si, r, v, Q, w, k0s, t, fbits);
+    if (MODE == MODE_FUSED && st + 1 < nsteps) __syncthreads();
+  }
+  if (si.active) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      __stcs(p.node + c * p.nn + si.node, r[c]);
+      __stcs(p.node + (3 + c) * p.nn + si.node, v[c]);
+    }
+  }
+  if (si.has_e) {
+#pragma unroll
+    for (int c = 0; c < 9; ++c) __stcs(p.elem + c * p.ne + si.elem, Q[c]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) __stcs(p.elem + (9 + c) * p.ne + si.elem, w[c]);
+  }
+  report_fault(p, fbits, si.rod);
 }
 
 // --------------------------------------------------------------------------- diagnostics
 // Per-tile partial sums of the energy functional at time p.t; deterministic.
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) diag_kernel(const ErStepParams p) {
-  extern __shared__ double smem[];
-  double *xr = smem;
+  extern __shared__ __align__(16) double sm[];
+  double *xr = sm;
   double *xQ = xr + 3 * BLOCK;
   double *red = xQ + 9 * BLOCK;  // [16][BLOCK/32]
-  int *rstart = reinterpret_cast<int *>(red + 16 * (BLOCK / 32));
-  const Slot sl = decode_slot<BLOCK>(p, blockIdx.x, rstart);
+  int *rst = reinterpret_cast<int *>(red + 16 * (BLOCK / 32));
+  const ErTile T = p.tiles[blockIdx.x];
+  SlotInfo si;
+  decode_global<BLOCK>(p, T, si, rst);
   const int s = threadIdx.x;
-  const int i = sl.i, N = sl.N;
-  const bool general = (sl.fl & FL_GENERAL) != 0;
-  const double *rec = p.rec + (int64_t)sl.rod * ER_REC;
+  const int i = si.i, N = si.N;
+  const bool general = (si.fl & FL_GENERAL) != 0;
+  const double *rec = p.rec + (int64_t)si.rod * ER_REC;
+  auto gp = [&](int plane) { return p.gpar[plane * p.ng + si.node]; };
   double r[3] = {0, 0, 0}, v[3] = {0, 0, 0}, Q[9], w[3] = {0, 0, 0};
   for (int c = 0; c < 3; ++c) {
-    if (sl.active) { r[c] = p.node[c * p.nn + sl.node]; v[c] = p.node[(3 + c) * p.nn + sl.node]; }
-    if (sl.has_e) w[c] = p.elem[(9 + c) * p.ne + sl.elem];
+    if (si.active) { r[c] = p.node[c * p.nn + si.node]; v[c] = p.node[(3 + c) * p.nn + si.node]; }
+    if (si.has_e) w[c] = p.elem[(9 + c) * p.ne + si.elem];
   }
-  for (int c = 0; c < 9; ++c) Q[c] = sl.has_e ? p.elem[c * p.ne + sl.elem] : 0.0;
-  if (sl.active) {
+  for (int c = 0; c < 9; ++c) Q[c] = si.has_e ? p.elem[c * p.ne + si.elem] : 0.0;
+  if (si.active) {
     for (int c = 0; c < 3; ++c) xr[c * BLOCK + s] = r[c];
     for (int c = 0; c < 9; ++c) xQ[c * BLOCK + s] = Q[c];
   }
   __syncthreads();
   double acc[16];
   for (int k = 0; k < 16; ++k) acc[k] = 0.0;
-  if (sl.active) {
-    const double im = general ? p.gpar[GP_IM * p.ng + sl.node] : rec[REC_IM] * ((i == 0 || i == N) ? 2.0 : 1.0);
+  if (si.active) {
+    const double im = general ? gp(GP_IM) : rec[REC_IM] * ((i == 0 || i == N) ? 2.0 : 1.0);
     const double m = 1.0 / im;
     const double vv = dot3(v, v);
     acc[0] = 0.5 * m * vv;
-    acc[4] = -m * dot3(p.g, r);
-    const int clamp = sl.fl & FL_CLAMP_MASK;
-    if ((sl.fl & FL_TIP) && i == (clamp == 2 ? 0 : N)) {
-      const double *r2 = p.rec2 + (int64_t)sl.rod * ER_REC2;
-      acc[5] = -(r2[0] * r[0] + r2[1] * r[1] + r2[2] * r[2]);
-    }
+    acc[4] = -m * (p.g[0] * r[0] + p.g[1] * r[1] + p.g[2] * r[2]);
+    if ((si.fl & FL_TIP) && i == ((si.fl & FL_CLAMP_MASK) == 2 ? 0 : N))
+      acc[5] = -(rec[REC_TIPX] * r[0] + rec[REC_TIPY] * r[1] + rec[REC_TIPZ] * r[2]);
     acc[6] = m * v[0]; acc[7] = m * v[1]; acc[8] = m * v[2];
     acc[9] = sqrt(vv);
     acc[10] = m;
   }
-  if (sl.has_e) {
-    const double lh = general ? p.gpar[GP_LHAT * p.ng + sl.node] : rec[REC_LHAT];
-    const double ilh = general ? p.gpar[GP_ILHAT * p.ng + sl.node] : rec[REC_ILHAT];
+  if (si.has_e) {
+    const double lh = general ? gp(GP_LHAT) : rec[REC_LHAT];
+    const double ilh = general ? gp(GP_ILHAT) : rec[REC_ILHAT];
     double ell[3];
     for (int c = 0; c < 3; ++c) ell[c] = xr[c * BLOCK + s + 1] - r[c];
     const double l = sqrt(dot3(ell, ell));
     const double e = l * ilh;
     double sg[3] = {dot3(Q, ell) * ilh, dot3(Q + 3, ell) * ilh, dot3(Q + 6, ell) * ilh - 1.0};
-    if (p.sigma0) for (int c = 0; c < 3; ++c) sg[c] -= p.sigma0[c * p.ne + sl.elem];
-    const double S1 = general ? p.gpar[GP_S1 * p.ng + sl.node] : rec[REC_S1];
-    const double S3 = general ? p.gpar[GP_S3 * p.ng + sl.node] : rec[REC_S3];
+    if (p.sigma0) for (int c = 0; c < 3; ++c) sg[c] -= p.sigma0[c * p.ne + si.elem];
+    const double S1 = general ? gp(GP_S1) : rec[REC_S1];
+    const double S3 = general ? gp(GP_S3) : rec[REC_S3];
     acc[2] = 0.5 * (S1 * sg[0] * sg[0] + S1 * sg[1] * sg[1] + S3 * sg[2] * sg[2]) * lh;
     for (int c = 0; c < 3; ++c) {
-      const double iJ = general ? p.gpar[(GP_IJ1 + c) * p.ng + sl.node] : rec[REC_IJ1 + c];
+      const double iJ = general ? gp(GP_IJ1 + c) : rec[REC_IJ1 + c];
       acc[1] += 0.5 * w[c] * w[c] / (iJ * e);
     }
     acc[11] = 1.0;
   }
-  if (sl.has_v) {
+  if (si.has_v) {
     double Qp[9], kap[3], cth, s2;
     for (int c = 0; c < 9; ++c) Qp[c] = xQ[c * BLOCK + s - 1];
     logrot_pair(Q, Qp, kap, cth, s2);
-    const double Dh = general ? p.gpar[GP_DH * p.ng + sl.node] : rec[REC_LHAT];
+    const double Dh = general ? gp(GP_DH) : rec[REC_LHAT];
     double k0[3] = {0, 0, 0};
-    if (p.kappa0) for (int c = 0; c < 3; ++c) k0[c] = p.kappa0[c * p.nv + sl.vor];
-    if (sl.fl & FL_ACT) {
-      const double *r2 = p.rec2 + (int64_t)sl.rod * ER_REC2;
-      const double sk = general ? p.gpar[GP_SK * p.ng + sl.node] : i * rec[REC_LHAT];
-      k0[p.act_comp] += r2[REC2_ACTA] * sinpi(2.0 * (sk * r2[REC2_ACTIL] - r2[REC2_ACTF] * p.t));
+    if (p.kappa0) for (int c = 0; c < 3; ++c) k0[c] = p.kappa0[c * p.nv + si.vor];
+    if (si.fl & FL_ACT) {
+      const double sk = general ? gp(GP_SK) : i * rec[REC_LHAT];
+      k0[p.act_comp] += rec[REC_ACTA] * sinpi(2.0 * (sk * rec[REC_ACTIL] - rec[REC_ACTF] * p.t));
     }
     for (int c = 0; c < 3; ++c) {
-      const double Bv = general ? p.gpar[(GP_BV1 + c) * p.ng + sl.node] : rec[REC_B1 + c];
+      const double Bv = general ? gp(GP_BV1 + c) : rec[REC_B1 + c];
       const double d = kap[c] / Dh - k0[c];
       acc[3] += 0.5 * Bv * d * d * Dh;
     }
@@ -426,7 +612,7 @@ __global__ void __launch_bounds__(BLOCK) diag_kernel(const ErStepParams p) {
 }
 
 __global__ void diag_finish_kernel(const double *partial, int64_t n_tiles, double *out) {
-  // one block of 32 threads per diagnostic, fixed-order strided sums then a fixed tree
+  // one warp per diagnostic: fixed-order strided sums, then a fixed shuffle tree
   const int k = blockIdx.x;
   double x = 0.0;
   for (int64_t q = threadIdx.x; q < n_tiles; q += 32) {
@@ -504,52 +690,92 @@ __global__ void validate_state(const double *node, int64_t nn, int64_t n_nodes, 
 }  // namespace er
 
 // --------------------------------------------------------------------------- launch wrappers
-static size_t step_smem(int block) { return (size_t)(15 + 4) * 8 * block + sizeof(int) * (block / 2 + 2); }
-static size_t diag_smem(int block) { return (size_t)12 * 8 * block + 16 * 8 * (block / 32) + sizeof(int) * (block / 2 + 2); }
+namespace {
 
-template <int BLOCK, int MINB, int MODE>
-static cudaError_t launch_step_t(const ErStepParams &p, int64_t n_tiles, cudaStream_t st) {
-  auto k = er::step_kernel<BLOCK, MINB, MODE>;
-  const size_t sm = step_smem(BLOCK);
-  static bool attr = false;
-  if (!attr) {
+size_t simple_smem(int block) { return (size_t)er::XPLANES * 8 * block + sizeof(int) * (block / 8 + 4); }
+size_t diag_smem(int block) { return (size_t)12 * 8 * block + 16 * 8 * (block / 32) + sizeof(int) * (block / 8 + 4); }
+
+template <int BLOCK, int MINB, int FEAT>
+cudaError_t launch_persistent(const ErStepParams &p, cudaStream_t st) {
+  auto k = er::fused_persistent<BLOCK, MINB, FEAT>;
+  const size_t sm = er::Stage<BLOCK, FEAT>::bytes();
+  static int grid_per_sm[64] = {0};  // per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 64) return cudaErrorInvalidDevice;
+  if (grid_per_sm[dev] == 0) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    attr = true;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, BLOCK, sm);
+    if (e != cudaSuccess) return e;
+    grid_per_sm[dev] = per_sm > 0 ? per_sm : 1;
   }
-  k<<<(unsigned)n_tiles, BLOCK, sm, st>>>(p);
+  int n_sm = 148;
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t g = std::min<int64_t>(p.n_tiles, (int64_t)n_sm * grid_per_sm[dev]);
+  k<<<(unsigned)g, BLOCK, sm, st>>>(p);
   return cudaGetLastError();
 }
 
-extern "C" {
-
-// mode: 0 fused, 1 drift, 2 dyn
-cudaError_t er_launch_step(const ErStepParams *p, int64_t n_tiles, int block, int mode, cudaStream_t st) {
-  if (n_tiles <= 0) return cudaSuccess;
-  if (block == 256) {
-    if (mode == 0) return launch_step_t<256, 2, er::MODE_FUSED>(*p, n_tiles, st);
-    if (mode == 1) return launch_step_t<256, 2, er::MODE_DRIFT>(*p, n_tiles, st);
-    return launch_step_t<256, 2, er::MODE_DYN>(*p, n_tiles, st);
+template <int BLOCK, int MINB>
+cudaError_t launch_persistent_feat(const ErStepParams &p, int feat, cudaStream_t st) {
+  switch (feat & 7) {
+    case 0: return launch_persistent<BLOCK, MINB, 0>(p, st);
+    case 1: return launch_persistent<BLOCK, MINB, 1>(p, st);
+    case 2: return launch_persistent<BLOCK, MINB, 2>(p, st);
+    case 3: return launch_persistent<BLOCK, MINB, 3>(p, st);
+    case 4: return launch_persistent<BLOCK, MINB, 4>(p, st);
+    case 5: return launch_persistent<BLOCK, MINB, 5>(p, st);
+    case 6: return launch_persistent<BLOCK, MINB, 6>(p, st);
+    default: return launch_persistent<BLOCK, MINB, 7>(p, st);
   }
-  if (mode == 0) return launch_step_t<512, 1, er::MODE_FUSED>(*p, n_tiles, st);
-  if (mode == 1) return launch_step_t<512, 1, er::MODE_DRIFT>(*p, n_tiles, st);
-  return launch_step_t<512, 1, er::MODE_DYN>(*p, n_tiles, st);
 }
 
-cudaError_t er_launch_diag(const ErStepParams *p, int64_t n_tiles, int block, double *out, cudaStream_t st) {
-  if (n_tiles > 0) {
+template <int BLOCK, int MINB, int MODE>
+cudaError_t launch_simple(const ErStepParams &p, cudaStream_t st) {
+  auto k = er::simple_kernel<BLOCK, MINB, MODE>;
+  const size_t sm = simple_smem(BLOCK);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  k<<<(unsigned)p.n_tiles, BLOCK, sm, st>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+extern "C" {
+
+// kind: 0 persistent fused (production), 1 simple drift stage, 2 simple dynamics stage,
+//       3 simple fused (one tile per CTA; ablation)
+cudaError_t er_launch_step(const ErStepParams *p, int block, int kind, int feat, cudaStream_t st) {
+  if (p->n_tiles <= 0) return cudaSuccess;
+  if (block == 256) {
+    if (kind == 0) return launch_persistent_feat<256, 2>(*p, feat, st);
+    if (kind == 1) return launch_simple<256, 2, er::MODE_DRIFT>(*p, st);
+    if (kind == 2) return launch_simple<256, 2, er::MODE_DYN>(*p, st);
+    return launch_simple<256, 2, er::MODE_FUSED>(*p, st);
+  }
+  if (kind == 0) return launch_persistent_feat<512, 1>(*p, feat, st);
+  if (kind == 1) return launch_simple<512, 1, er::MODE_DRIFT>(*p, st);
+  if (kind == 2) return launch_simple<512, 1, er::MODE_DYN>(*p, st);
+  return launch_simple<512, 1, er::MODE_FUSED>(*p, st);
+}
+
+cudaError_t er_launch_diag(const ErStepParams *p, int block, double *out, cudaStream_t st) {
+  if (p->n_tiles > 0) {
     const size_t sm = diag_smem(block);
     if (block == 256) {
       cudaFuncSetAttribute(er::diag_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      er::diag_kernel<256><<<(unsigned)n_tiles, 256, sm, st>>>(*p);
+      er::diag_kernel<256><<<(unsigned)p->n_tiles, 256, sm, st>>>(*p);
     } else {
       cudaFuncSetAttribute(er::diag_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      er::diag_kernel<512><<<(unsigned)n_tiles, 512, sm, st>>>(*p);
+      er::diag_kernel<512><<<(unsigned)p->n_tiles, 512, sm, st>>>(*p);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  er::diag_finish_kernel<<<12, 32, 0, st>>>(p->diag_partial, n_tiles, out);
+  er::diag_finish_kernel<<<12, 32, 0, st>>>(p->diag_partial, p->n_tiles, out);
   return cudaGetLastError();
 }
 

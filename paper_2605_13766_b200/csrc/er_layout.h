@@ -1,23 +1,23 @@
 // er_layout.h -- device-resident layout of a rod batch (L0) and the kernel parameter block.
 //
 // HBM layout:
-//  - node planes  : 6 fp64 planes [rx ry rz vx vy vz][n_nodes_pad]      (compact SoA, no ghosts)
-//  - elem planes  : 12 fp64 planes [Q00..Q22 wx wy wz][n_elems_pad]      (row a of Q = d_{a+1})
-//  - rod records  : [n_rods][ER_REC] fp64 derived constants of uniform rods + damping + vmax^2
-//  - rod extras   : [n_rods][ER_REC2] fp64 tip force, actuation (read only when flagged)
-//  - rod flags    : [n_rods] int32 (clamp mode, general, tip, actuation)
-//  - eoff         : [n_rods+1] int64 element offsets (node offset = eoff + rod)
-//  - tiles        : [n_tiles+1] int32 first rod of each tile (rod-aligned, <= tile_slots slots)
-//  - gpar         : optional [ER_GP][n_nodes_pad] per-slot parameters of "general" rods
+//  - node planes  : 6 fp64 planes [rx ry rz vx vy vz][nn]      (compact SoA, no ghosts)
+//  - elem planes  : 12 fp64 planes [Q00..Q22 wx wy wz][ne]      (row a of Q = d_{a+1})
+//  - rod records  : [n_rods][ER_REC] fp64: derived constants, damping, v_max^2, tip force,
+//                   actuation and the flag word -- one 192-byte record read per rod per step
+//  - eoff         : [n_rods+3] int64 element offsets (node offset = eoff + rod); padded so
+//                   16-byte-aligned bulk copies may over-read one entry
+//  - tiles        : [n_tiles] ErTile, rod-aligned tiles of <= BLOCK slots and <= BLOCK/8 rods
+//  - gpar         : optional [ER_GP][nn] per-slot parameters of "general" rods
 //                   (non-uniform rest lengths or per-element material)
-//  - sigma0/kappa0/mag : optional [3][n_elems_pad] / [3][n_vor_pad] / [3][n_elems_pad] planes
-// Ghost nodes exist only in shared memory (never in HBM).
+//  - kappa0       : optional [3][nv] static rest curvature;  sigma0, mag: optional [3][ne]
+// Every plane stride is a multiple of 32 doubles plus 32 doubles of slack, so bulk copies that
+// round a range out to 16-byte boundaries stay in bounds.  Ghost nodes exist only in smem.
 #pragma once
 #include <stdint.h>
 
-// ---- rod record (uniform rods): everything one slot needs, read once per rod per step
 enum {
-  REC_LHAT = 0,  // rest length (uniform)
+  REC_LHAT = 0,  // rest length (uniform rod)
   REC_ILHAT,     // 1/lhat
   REC_S1,        // alpha_c G A   (shear, d1 and d2)
   REC_S3,        // E A           (stretch)
@@ -33,11 +33,18 @@ enum {
   REC_IM,        // 1/(rho A lhat): inverse interior node mass (end nodes: 2x)
   REC_NU,        // damping rate
   REC_VMAX2,     // (1e6 sqrt(E/rho))^2
+  REC_TIPX,      // tip force (lab)
+  REC_TIPY,
+  REC_TIPZ,
+  REC_ACTA,      // actuation amplitude A
+  REC_ACTF,      // actuation frequency f
+  REC_ACTIL,     // 1/L of the actuation wave
+  REC_FLAGS,     // flag word (int64 bits)
+  REC_PAD,
   ER_REC
 };
-enum { REC2_TIPX = 0, REC2_TIPY, REC2_TIPZ, REC2_ACTA, REC2_ACTF, REC2_ACTIL, REC2_PAD0, REC2_PAD1, ER_REC2 };
 
-// ---- per-slot general parameters (node-indexed planes), general rods only
+// per-slot general parameters (node-indexed planes), general rods only
 enum {
   GP_LHAT = 0, GP_ILHAT, GP_S1, GP_S3, GP_IJ1, GP_IJ2, GP_IJ3, GP_KJ1, GP_KJ2, GP_KJ3,  // element at slot
   GP_BV1, GP_BV2, GP_BV3, GP_DH,                                                      // Voronoi at slot
@@ -46,12 +53,23 @@ enum {
   ER_GP
 };
 
-// ---- rod flags
 enum {
-  FL_CLAMP_MASK = 3,   // 0 free, 1 clamp s=0 end, 2 clamp s=L end
-  FL_GENERAL = 4,      // per-slot parameters from gpar
-  FL_TIP = 8,          // tip force present
-  FL_ACT = 16,         // rest-curvature actuation
+  FL_CLAMP_MASK = 3,  // 0 free, 1 clamp s=0 end, 2 clamp s=L end
+  FL_GENERAL = 4,     // per-slot parameters from gpar
+  FL_TIP = 8,         // tip force present
+  FL_ACT = 16,        // rest-curvature actuation
+};
+
+// batch-level feature bits (kernel template parameter)
+enum { FEAT_GENERAL = 1, FEAT_KAPPA0 = 2, FEAT_EXTRA = 4 /* sigma0 / magnetization / actuation */ };
+
+struct ErTile {
+  int64_t nbase;   // first node of the tile
+  int64_t ebase;   // first element of the tile
+  int32_t r0;      // first rod
+  int32_t nr;      // rods in the tile
+  int32_t nslots;  // nodes (= slots) in the tile
+  int32_t nel;     // elements in the tile
 };
 
 struct ErStepParams {
@@ -60,10 +78,9 @@ struct ErStepParams {
   int64_t nn;    // node plane stride (doubles)
   int64_t ne;    // element plane stride
   const double *rec;
-  const double *rec2;
-  const int32_t *flags;
   const int64_t *eoff;
-  const int32_t *tiles;
+  const ErTile *tiles;
+  int64_t n_tiles;
   const double *gpar;     // may be null
   int64_t ng;             // gpar plane stride
   const double *sigma0;   // may be null, planes stride ne
