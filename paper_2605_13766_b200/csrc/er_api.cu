@@ -1,9 +1,10 @@
 // er_api.cu -- host implementation of the C-ABI (L3) declared in include/er.h.
 //
 // Validation (collect-all), the rod-layout builder (offsets, derived per-rod
-// constants, rod-aligned tiles), device allocation, stream-ordered stepping with one fault
-// word read per er_step, state read-back and the diagnostics reduction.  Nothing here does
-// per-element physics on the host: every step of the path runs in er_kernels.cu.
+// constants, rod-aligned tiles, tile-blocked SoA state), device allocation, stream-ordered
+// stepping with one fault-word read per er_step, state read-back and the diagnostics
+// reduction.  Nothing here does per-element physics on the host: every step of the path runs
+// in er_kernels.cu.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -21,11 +22,9 @@
 extern "C" {
 cudaError_t er_launch_step(const ErStepParams *p, int block, int kind, int feat, cudaStream_t st);
 cudaError_t er_launch_diag(const ErStepParams *p, int block, double *out, cudaStream_t st);
+cudaError_t er_launch_canon_tiles(const ErStepParams *p, double *canon, int field, int to_tiles, cudaStream_t st);
 cudaError_t er_launch_aos_to_soa(const double *src, double *dst, int64_t n, int k, int64_t stride, cudaStream_t st);
-cudaError_t er_launch_soa_to_aos(const double *src, double *dst, int64_t n, int k, int64_t stride, cudaStream_t st);
-cudaError_t er_launch_fill(double *dst, int64_t n, int k, int64_t stride, double value, cudaStream_t st);
-cudaError_t er_launch_validate(const double *node, int64_t nn, int64_t n_nodes, const double *elem, int64_t ne,
-                               int64_t n_elems, double *out, cudaStream_t st);
+cudaError_t er_launch_validate(const double *aos, int64_t n, int k, int orth, double *out, cudaStream_t st);
 }
 
 namespace {
@@ -69,22 +68,21 @@ struct er_batch {
   int64_t launches = 0;
   int64_t device_bytes = 0;
   // device buffers
-  double *d_node = nullptr, *d_elem = nullptr;
-  int64_t nn = 0, ne = 0, nv = 0, ng = 0;
+  double *d_state = nullptr;  // tile-blocked SoA state (+ static kappa0 planes)
+  int64_t state_doubles = 0;
+  int64_t ng = 0, ne = 0;     // canonical plane strides of gpar (nodes) and sigma0/mag (elements)
   double *d_rec = nullptr;
   int64_t *d_eoff = nullptr;
   ErTile *d_tiles = nullptr;
-  int feat = 0;  // FEAT_* bits of this batch
-  double *d_gpar = nullptr, *d_sigma0 = nullptr, *d_kappa0 = nullptr, *d_mag = nullptr;
+  double *d_gpar = nullptr, *d_sigma0 = nullptr, *d_mag = nullptr;
   unsigned long long *d_fault = nullptr;
   double *d_diag_partial = nullptr, *d_diag_out = nullptr, *d_valid = nullptr;
+  bool has_kappa0 = false, any_general = false, has_sigma0 = false, has_act = false;
   // host mirrors
   std::vector<int32_t> n_elems_h;
   std::vector<int64_t> eoff;
   std::vector<double> rec;
   std::vector<int32_t> flags;
-  bool any_general = false, has_sigma0 = false, has_act = false;
-  std::vector<double> rho_rod, E_rod;  // for vmax
   double g[3] = {0, 0, 0};
   double b0[3] = {0, 0, 0};
   double b_omega = 0.0;
@@ -102,9 +100,9 @@ er_status cuda_fail(er_batch *b, cudaError_t e, const char *what) {
   return e == cudaErrorMemoryAllocation ? ER_ENOMEM : ER_ECUDA;
 }
 
-#define CK(call, what)                                   \
-  do {                                                   \
-    cudaError_t e_ = (call);                             \
+#define CK(call, what)                                    \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
     if (e_ != cudaSuccess) return cuda_fail(b, e_, what); \
   } while (0)
 
@@ -118,8 +116,8 @@ cudaError_t dalloc(er_batch *b, T **p, int64_t count) {
 }
 
 void free_all(er_batch *b) {
-  void *ptrs[] = {b->d_node, b->d_elem, b->d_rec, b->d_eoff, b->d_tiles, b->d_gpar,
-                  b->d_sigma0, b->d_kappa0, b->d_mag, b->d_fault, b->d_diag_partial, b->d_diag_out, b->d_valid};
+  void *ptrs[] = {b->d_state, b->d_rec, b->d_eoff, b->d_tiles, b->d_gpar, b->d_sigma0, b->d_mag,
+                  b->d_fault, b->d_diag_partial, b->d_diag_out, b->d_valid};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (b->own_stream && b->stream) cudaStreamDestroy(b->stream);
@@ -130,47 +128,71 @@ bool pos_finite(double x) { return std::isfinite(x) && x > 0.0; }
 ErStepParams params_of(const er_batch *b) {
   ErStepParams p;
   std::memset(&p, 0, sizeof p);
-  p.node = b->d_node; p.elem = b->d_elem; p.nn = b->nn; p.ne = b->ne;
+  p.state = b->d_state;
   p.rec = b->d_rec; p.eoff = b->d_eoff; p.tiles = b->d_tiles; p.n_tiles = b->n_tiles;
-  p.gpar = b->d_gpar; p.ng = b->ng; p.sigma0 = b->d_sigma0; p.kappa0 = b->d_kappa0; p.nv = b->nv;
-  p.mag = b->d_mag;
+  p.gpar = b->d_gpar; p.ng = b->ng; p.sigma0 = b->d_sigma0; p.mag = b->d_mag; p.ne = b->ne;
+  p.has_kappa0 = b->has_kappa0 ? 1 : 0;
   for (int c = 0; c < 3; ++c) { p.g[c] = b->g[c]; p.b0[c] = b->b0[c]; }
   p.b_omega = b->b_omega; p.act_comp = b->act_comp;
   p.fault = b->d_fault; p.diag_partial = b->d_diag_partial;
   return p;
 }
 
-// Upload a canonical AoS array [n][k] from src (host or device) into k SoA planes.
-er_status upload_planes(er_batch *b, const double *src, int src_mem, double *planes, int64_t n, int k,
-                        int64_t stride) {
+// Field sizes in canonical AoS order.
+int64_t field_rows(const er_batch *b, int field) {
+  return field <= FIELD_VEL ? b->n_nodes : field <= FIELD_OMEGA ? b->n_elems : b->n_vor;
+}
+int field_k(int field) { return field == FIELD_DIR ? 9 : 3; }
+
+// Canonical AoS array (host or device, or NULL = zeros) -> tile-blocked planes.  With
+// `validate`, non-finite counts (and, for directors, max |QQ^T - I| and |det Q - 1|)
+// accumulate in d_valid.
+er_status upload_field(er_batch *b, const double *src, int src_mem, int field, bool validate) {
+  const int64_t n = field_rows(b, field);
   if (n <= 0) return ER_OK;
+  ErStepParams p = params_of(b);
+  const int k = field_k(field);
   if (src == nullptr) {
-    CK(er_launch_fill(planes, n, k, stride, 0.0, b->stream), "fill");
+    CK(er_launch_canon_tiles(&p, nullptr, field, 1, b->stream), "zero field");
     return ER_OK;
   }
-  if (src_mem == ER_DEVICE) {
-    CK(er_launch_aos_to_soa(src, planes, n, k, stride, b->stream), "aos_to_soa");
+  const double *dsrc = src;
+  double *stage = nullptr;
+  if (src_mem == ER_HOST) {
+    CK(cudaMallocAsync((void **)&stage, sizeof(double) * (size_t)(n * k), b->stream), "cudaMallocAsync(stage)");
+    CK(cudaMemcpyAsync(stage, src, sizeof(double) * (size_t)(n * k), cudaMemcpyHostToDevice, b->stream), "H2D");
+    dsrc = stage;
+  }
+  if (validate) CK(er_launch_validate(dsrc, n, k, field == FIELD_DIR, b->d_valid, b->stream), "validate");
+  CK(er_launch_canon_tiles(&p, const_cast<double *>(dsrc), field, 1, b->stream), "canon->tiles");
+  if (stage) CK(cudaFreeAsync(stage, b->stream), "cudaFreeAsync");
+  return ER_OK;
+}
+
+er_status download_field(er_batch *b, double *dst, int dst_mem, int field) {
+  const int64_t n = field_rows(b, field);
+  if (dst == nullptr || n <= 0) return ER_OK;
+  ErStepParams p = params_of(b);
+  const int k = field_k(field);
+  if (dst_mem == ER_DEVICE) {
+    CK(er_launch_canon_tiles(&p, dst, field, 0, b->stream), "tiles->canon");
     return ER_OK;
   }
   double *stage = nullptr;
   CK(cudaMallocAsync((void **)&stage, sizeof(double) * (size_t)(n * k), b->stream), "cudaMallocAsync(stage)");
-  CK(cudaMemcpyAsync(stage, src, sizeof(double) * (size_t)(n * k), cudaMemcpyHostToDevice, b->stream), "H2D");
-  CK(er_launch_aos_to_soa(stage, planes, n, k, stride, b->stream), "aos_to_soa");
+  CK(er_launch_canon_tiles(&p, stage, field, 0, b->stream), "tiles->canon");
+  CK(cudaMemcpyAsync(dst, stage, sizeof(double) * (size_t)(n * k), cudaMemcpyDeviceToHost, b->stream), "D2H");
   CK(cudaFreeAsync(stage, b->stream), "cudaFreeAsync");
   return ER_OK;
 }
 
-er_status download_planes(er_batch *b, const double *planes, double *dst, int dst_mem, int64_t n, int k,
-                          int64_t stride) {
-  if (dst == nullptr || n <= 0) return ER_OK;
-  if (dst_mem == ER_DEVICE) {
-    CK(er_launch_soa_to_aos(planes, dst, n, k, stride, b->stream), "soa_to_aos");
-    return ER_OK;
-  }
+// Canonical AoS [n][3] (host) -> 3 canonical SoA planes (side arrays: sigma0, magnetization).
+er_status upload_side_planes(er_batch *b, const double *src, double *planes, int64_t n, int64_t stride) {
+  if (n <= 0) return ER_OK;
   double *stage = nullptr;
-  CK(cudaMallocAsync((void **)&stage, sizeof(double) * (size_t)(n * k), b->stream), "cudaMallocAsync(stage)");
-  CK(er_launch_soa_to_aos(planes, stage, n, k, stride, b->stream), "soa_to_aos");
-  CK(cudaMemcpyAsync(dst, stage, sizeof(double) * (size_t)(n * k), cudaMemcpyDeviceToHost, b->stream), "D2H");
+  CK(cudaMallocAsync((void **)&stage, sizeof(double) * (size_t)(n * 3), b->stream), "cudaMallocAsync(stage)");
+  CK(cudaMemcpyAsync(stage, src, sizeof(double) * (size_t)(n * 3), cudaMemcpyHostToDevice, b->stream), "H2D");
+  CK(er_launch_aos_to_soa(stage, planes, n, 3, stride, b->stream), "aos_to_soa");
   CK(cudaFreeAsync(stage, b->stream), "cudaFreeAsync");
   return ER_OK;
 }
@@ -179,7 +201,7 @@ er_status download_planes(er_batch *b, const double *planes, double *dst, int ds
 // B = diag(E I1, E I2, G (I1+I2)), J = rho lhat diag(I1, I2, I1+I2), m_node = half element masses.
 struct ElemMat { double rho, A, I1, I2, E, G, ac, lh; };
 
-void fill_record(double *rec, const ElemMat &m, double nu) {
+void fill_record(double *rec, const ElemMat &m) {
   const double J1 = m.rho * m.lh * m.I1, J2 = m.rho * m.lh * m.I2, J3 = m.rho * m.lh * (m.I1 + m.I2);
   rec[REC_LHAT] = m.lh;
   rec[REC_ILHAT] = 1.0 / m.lh;
@@ -195,15 +217,13 @@ void fill_record(double *rec, const ElemMat &m, double nu) {
   rec[REC_KJ2] = (J3 - J1) / J2;
   rec[REC_KJ3] = (J1 - J2) / J3;
   rec[REC_IM] = 1.0 / (m.rho * m.A * m.lh);
-  rec[REC_NU] = nu;
   const double vmax = 1e6 * std::sqrt(m.E / m.rho);
   rec[REC_VMAX2] = vmax * vmax;
 }
 
 // The flag word lives inside each rod record (REC_FLAGS), so one bulk copy brings it along.
 void sync_flags(er_batch *b) {
-  for (int64_t r = 0; r < b->n_rods; ++r)
-  {
+  for (int64_t r = 0; r < b->n_rods; ++r) {
     const int64_t bits = (int64_t)b->flags[r];
     std::memcpy(&b->rec[(size_t)r * ER_REC + REC_FLAGS], &bits, sizeof bits);
   }
@@ -212,9 +232,17 @@ void sync_flags(er_batch *b) {
 int feat_of(const er_batch *b) {
   int f = 0;
   if (b->any_general) f |= FEAT_GENERAL;
-  if (b->d_kappa0) f |= FEAT_KAPPA0;
+  if (b->has_kappa0) f |= FEAT_KAPPA0;
   if (b->has_sigma0 || b->d_mag || b->has_act) f |= FEAT_EXTRA;
   return f;
+}
+
+er_status upload_records(er_batch *b) {
+  sync_flags(b);
+  if (b->n_rods > 0)
+    CK(cudaMemcpyAsync(b->d_rec, b->rec.data(), sizeof(double) * b->rec.size(), cudaMemcpyHostToDevice, b->stream),
+       "H2D rec");
+  return ER_OK;
 }
 
 }  // namespace
@@ -236,7 +264,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   if (d->src_mem != ER_HOST && d->src_mem != ER_DEVICE) err.add("src_mem = %d is not ER_HOST/ER_DEVICE", d->src_mem);
   if (err.count) { g_create_error = err.msg; return ER_EINVAL; }
 
-  std::vector<int64_t> eoff((size_t)R + 1, 0);
+  std::vector<int64_t> eoff((size_t)std::max<int64_t>(R, 0) + 1, 0);
   int32_t max_n = 0;
   for (int64_t r = 0; r < R; ++r) {
     const int32_t n = d->n_elems[r];
@@ -299,7 +327,6 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
     ElemMat m{d->density[k], d->area[k], d->I1[k], d->I2[k], d->youngs[k], d->shear_mod[k], d->alpha_c[k], d->rest_lengths[j]};
     return m;
   };
-  bool any_general = false;
   for (int64_t r = 0; r < R; ++r) {
     const ElemMat m0 = mat_at(r, eoff[r]);
     bool uniform = true;
@@ -308,15 +335,15 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
       uniform = m.rho == m0.rho && m.A == m0.A && m.I1 == m0.I1 && m.I2 == m0.I2 && m.E == m0.E && m.G == m0.G &&
                 m.ac == m0.ac && m.lh == m0.lh;
     }
-    fill_record(&b->rec[(size_t)r * ER_REC], m0, 0.0);
-    if (!uniform) { b->flags[r] |= FL_GENERAL; any_general = true; }
+    fill_record(&b->rec[(size_t)r * ER_REC], m0);
+    if (!uniform) { b->flags[r] |= FL_GENERAL; b->any_general = true; }
   }
-  b->any_general = any_general;
   b->has_sigma0 = d->rest_sigma != nullptr;
-  sync_flags(b);
-  b->nn = pad_to(NN, 32); b->ne = pad_to(E, 32); b->nv = pad_to(NV, 32); b->ng = b->nn;
+  b->has_kappa0 = d->rest_kappa != nullptr && NV > 0;
+  b->ng = pad_to(NN, 32);
+  b->ne = pad_to(E, 32);
   std::vector<double> gpar;
-  if (any_general) {
+  if (b->any_general) {
     gpar.assign((size_t)ER_GP * b->ng, 0.0);
     for (int64_t r = 0; r < R; ++r) {
       if (!(b->flags[r] & FL_GENERAL)) continue;
@@ -329,7 +356,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
         if (i < N) {
           const ElemMat m = mat_at(r, eoff[r] + i);
           double tmp[ER_REC];
-          fill_record(tmp, m, 0.0);
+          fill_record(tmp, m);
           G(GP_LHAT) = tmp[REC_LHAT]; G(GP_ILHAT) = tmp[REC_ILHAT]; G(GP_S1) = tmp[REC_S1]; G(GP_S3) = tmp[REC_S3];
           for (int c = 0; c < 3; ++c) { G(GP_IJ1 + c) = tmp[REC_IJ1 + c]; G(GP_KJ1 + c) = tmp[REC_KJ1 + c]; }
           mass += 0.5 * m.rho * m.A * m.lh;
@@ -353,16 +380,19 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
     }
   }
 
-  // ---- rod-aligned tiles (greedy contiguous packing, <= block slots and <= block/8 rods per tile)
+  // ---- rod-aligned tiles (greedy contiguous packing, <= block slots and <= block/8 rods per
+  // tile); each tile's state is one contiguous SoA block: 6 node planes x nslots, 12 element
+  // planes x nel, [3 Voronoi planes x nvor], padded to an even number of doubles (16 B).
   b->block = (max_n + 1 <= 256) ? 256 : 512;
   std::vector<ErTile> tiles;
   {
-    int64_t r = 0;
+    int64_t r = 0, boff = 0;
     while (r < R) {
       ErTile T;
       T.r0 = (int32_t)r;
       T.nbase = eoff[r] + r;
       T.ebase = eoff[r];
+      T.boff = boff;
       int64_t used = 0;
       int32_t nr = 0;
       while (r < R && nr < b->block / 8 && used + b->n_elems_h[r] + 1 <= b->block) {
@@ -373,14 +403,16 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
       T.nr = nr;
       T.nslots = (int32_t)used;
       T.nel = (int32_t)(eoff[r] - eoff[T.r0]);
+      int64_t sz = 6 * (int64_t)T.nslots + 12 * (int64_t)T.nel + (b->has_kappa0 ? 3 * (int64_t)(T.nel - T.nr) : 0);
+      boff += (sz + 1) & ~1ll;
       tiles.push_back(T);
     }
+    b->state_doubles = boff;
   }
   b->n_tiles = (int64_t)tiles.size();
 
   // ---- device allocation and upload
-  CK(dalloc(b, &b->d_node, 6 * b->nn), "cudaMalloc(node)");
-  CK(dalloc(b, &b->d_elem, 12 * b->ne), "cudaMalloc(elem)");
+  CK(dalloc(b, &b->d_state, b->state_doubles + 64), "cudaMalloc(state)");
   CK(dalloc(b, &b->d_rec, (int64_t)b->rec.size()), "cudaMalloc(rec)");
   CK(dalloc(b, &b->d_eoff, R + 4), "cudaMalloc(eoff)");
   CK(dalloc(b, &b->d_tiles, std::max<int64_t>((int64_t)tiles.size(), 1)), "cudaMalloc(tiles)");
@@ -388,38 +420,34 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   CK(dalloc(b, &b->d_diag_partial, std::max<int64_t>(b->n_tiles, 1) * 16), "cudaMalloc(diag)");
   CK(dalloc(b, &b->d_diag_out, 16), "cudaMalloc(diag_out)");
   CK(dalloc(b, &b->d_valid, 4), "cudaMalloc(valid)");
-  CK(cudaMemsetAsync(b->d_node, 0, sizeof(double) * 6 * b->nn, b->stream), "memset");
-  CK(cudaMemsetAsync(b->d_elem, 0, sizeof(double) * 12 * b->ne, b->stream), "memset");
-  CK(cudaMemcpyAsync(b->d_rec, b->rec.data(), sizeof(double) * b->rec.size(), cudaMemcpyHostToDevice, b->stream), "H2D rec");
+  CK(cudaMemsetAsync(b->d_state, 0, sizeof(double) * (b->state_doubles + 64), b->stream), "memset");
   {
     std::vector<int64_t> ep(eoff);
     ep.resize((size_t)R + 4, eoff[R]);
     CK(cudaMemcpyAsync(b->d_eoff, ep.data(), sizeof(int64_t) * ep.size(), cudaMemcpyHostToDevice, b->stream), "H2D eoff");
-    CK(cudaStreamSynchronize(b->stream), "sync");
-  }
-  if (!tiles.empty())
-    CK(cudaMemcpyAsync(b->d_tiles, tiles.data(), sizeof(ErTile) * tiles.size(), cudaMemcpyHostToDevice, b->stream), "H2D tiles");
-  if (any_general) {
-    CK(dalloc(b, &b->d_gpar, (int64_t)gpar.size()), "cudaMalloc(gpar)");
-    CK(cudaMemcpyAsync(b->d_gpar, gpar.data(), sizeof(double) * gpar.size(), cudaMemcpyHostToDevice, b->stream), "H2D gpar");
+    if (!tiles.empty())
+      CK(cudaMemcpyAsync(b->d_tiles, tiles.data(), sizeof(ErTile) * tiles.size(), cudaMemcpyHostToDevice, b->stream), "H2D tiles");
+    if (b->any_general) {
+      CK(dalloc(b, &b->d_gpar, (int64_t)gpar.size()), "cudaMalloc(gpar)");
+      CK(cudaMemcpyAsync(b->d_gpar, gpar.data(), sizeof(double) * gpar.size(), cudaMemcpyHostToDevice, b->stream), "H2D gpar");
+    }
+    er_status st0 = upload_records(b);
+    if (st0 != ER_OK) return fail(st0);
+    CK(cudaStreamSynchronize(b->stream), "sync");  // host vectors above are freed at scope exit
   }
   er_status st;
-  if ((st = upload_planes(b, d->positions, d->src_mem, b->d_node, NN, 3, b->nn)) != ER_OK) return fail(st);
-  if ((st = upload_planes(b, d->velocities, d->src_mem, b->d_node + 3 * b->nn, NN, 3, b->nn)) != ER_OK) return fail(st);
-  if ((st = upload_planes(b, d->directors, d->src_mem, b->d_elem, E, 9, b->ne)) != ER_OK) return fail(st);
-  if ((st = upload_planes(b, d->omega, d->src_mem, b->d_elem + 9 * b->ne, E, 3, b->ne)) != ER_OK) return fail(st);
+  CK(cudaMemsetAsync(b->d_valid, 0, sizeof(double) * 4, b->stream), "memset");
+  if ((st = upload_field(b, d->positions, d->src_mem, FIELD_POS, true)) != ER_OK) return fail(st);
+  if ((st = upload_field(b, d->velocities, d->src_mem, FIELD_VEL, true)) != ER_OK) return fail(st);
+  if ((st = upload_field(b, d->directors, d->src_mem, FIELD_DIR, true)) != ER_OK) return fail(st);
+  if ((st = upload_field(b, d->omega, d->src_mem, FIELD_OMEGA, true)) != ER_OK) return fail(st);
+  if (b->has_kappa0 && (st = upload_field(b, d->rest_kappa, ER_HOST, FIELD_KAPPA0, false)) != ER_OK) return fail(st);
   if (d->rest_sigma) {
     CK(dalloc(b, &b->d_sigma0, 3 * b->ne), "cudaMalloc(sigma0)");
-    if ((st = upload_planes(b, d->rest_sigma, ER_HOST, b->d_sigma0, E, 3, b->ne)) != ER_OK) return fail(st);
+    if ((st = upload_side_planes(b, d->rest_sigma, b->d_sigma0, E, b->ne)) != ER_OK) return fail(st);
   }
-  if (d->rest_kappa && NV > 0) {
-    CK(dalloc(b, &b->d_kappa0, 3 * b->nv), "cudaMalloc(kappa0)");
-    if ((st = upload_planes(b, d->rest_kappa, ER_HOST, b->d_kappa0, NV, 3, b->nv)) != ER_OK) return fail(st);
-  }
-  // ---- validate the uploaded state on the device (directors orthonormal within 1e-10)
+  // ---- validation of the uploaded state (directors orthonormal within 1e-10, all finite)
   double vres[4] = {0, 0, 0, 0};
-  CK(cudaMemsetAsync(b->d_valid, 0, sizeof(double) * 4, b->stream), "memset");
-  if (R > 0) CK(er_launch_validate(b->d_node, b->nn, NN, b->d_elem, b->ne, E, b->d_valid, b->stream), "validate");
   CK(cudaMemcpyAsync(vres, b->d_valid, sizeof vres, cudaMemcpyDeviceToHost, b->stream), "D2H valid");
   CK(cudaStreamSynchronize(b->stream), "cudaStreamSynchronize");
   if (vres[2] > 0) err.add("%g state entries (positions/velocities/directors/omega) are not finite", vres[2]);
@@ -449,10 +477,9 @@ er_status er_set_bc(er_batch *b, const int8_t *clamp_end) {
     if (clamp_end && clamp_end[r] == 0) b->flags[r] |= 1;
     if (clamp_end && clamp_end[r] == 1) b->flags[r] |= 2;
   }
-  sync_flags(b);
   CK(cudaSetDevice(b->device), "cudaSetDevice");
-  if (b->n_rods > 0)
-    CK(cudaMemcpyAsync(b->d_rec, b->rec.data(), sizeof(double) * b->rec.size(), cudaMemcpyHostToDevice, b->stream), "H2D rec");
+  er_status st = upload_records(b);
+  if (st != ER_OK) return st;
   CK(cudaStreamSynchronize(b->stream), "sync");
   return ER_OK;
 }
@@ -503,15 +530,14 @@ er_status er_set_forcing(er_batch *b, const er_forcing *f) {
     rec[REC_ACTIL] = act ? 1.0 / f->act_L[r] : 0.0;
     if (act) b->flags[r] |= FL_ACT;
   }
-  sync_flags(b);
   CK(cudaSetDevice(b->device), "cudaSetDevice");
-  if (R > 0)
-    CK(cudaMemcpyAsync(b->d_rec, b->rec.data(), sizeof(double) * b->rec.size(), cudaMemcpyHostToDevice, b->stream), "H2D rec");
+  er_status st = upload_records(b);
+  if (st != ER_OK) return st;
   if (f->magnetization && b->n_elems > 0) {
     if (!b->d_mag) CK(dalloc(b, &b->d_mag, 3 * b->ne), "cudaMalloc(mag)");
-    er_status st = upload_planes(b, f->magnetization, ER_HOST, b->d_mag, b->n_elems, 3, b->ne);
-    if (st != ER_OK) return st;
+    if ((st = upload_side_planes(b, f->magnetization, b->d_mag, b->n_elems, b->ne)) != ER_OK) return st;
   } else if (b->d_mag) {
+    CK(cudaStreamSynchronize(b->stream), "sync");
     cudaFree(b->d_mag);
     b->device_bytes -= (int64_t)sizeof(double) * 3 * b->ne;
     b->d_mag = nullptr;
@@ -552,12 +578,13 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
   p.h = dt;
   int64_t done = 0;
   double t = b->t;
+  const int feat = feat_of(b);
   while (done < n_steps) {
     if (b->kernel_mode == 0 || b->kernel_mode == 2) {
       const int64_t k = std::min<int64_t>(b->steps_per_launch, n_steps - done);
       p.n_steps = (int32_t)k;
       p.t = t;
-      CK(er_launch_step(&p, b->block, b->kernel_mode == 0 ? 0 : 3, feat_of(b), b->stream), "step kernel");
+      CK(er_launch_step(&p, b->block, b->kernel_mode == 0 ? 0 : 3, feat, b->stream), "step kernel");
       b->launches += 1;
       for (int64_t q = 0; q < k; ++q) { const double th = t + 0.5 * dt; t = th + 0.5 * dt; }
       done += k;
@@ -597,10 +624,10 @@ er_status er_get_state(er_batch *b, int32_t dst_mem, double *positions, double *
   if (dst_mem != ER_HOST && dst_mem != ER_DEVICE) { b->last_error = "dst_mem must be ER_HOST or ER_DEVICE"; return ER_EINVAL; }
   CK(cudaSetDevice(b->device), "cudaSetDevice");
   er_status st;
-  if ((st = download_planes(b, b->d_node, positions, dst_mem, b->n_nodes, 3, b->nn)) != ER_OK) return st;
-  if ((st = download_planes(b, b->d_node + 3 * b->nn, velocities, dst_mem, b->n_nodes, 3, b->nn)) != ER_OK) return st;
-  if ((st = download_planes(b, b->d_elem, directors, dst_mem, b->n_elems, 9, b->ne)) != ER_OK) return st;
-  if ((st = download_planes(b, b->d_elem + 9 * b->ne, omega, dst_mem, b->n_elems, 3, b->ne)) != ER_OK) return st;
+  if ((st = download_field(b, positions, dst_mem, FIELD_POS)) != ER_OK) return st;
+  if ((st = download_field(b, velocities, dst_mem, FIELD_VEL)) != ER_OK) return st;
+  if ((st = download_field(b, directors, dst_mem, FIELD_DIR)) != ER_OK) return st;
+  if ((st = download_field(b, omega, dst_mem, FIELD_OMEGA)) != ER_OK) return st;
   CK(cudaStreamSynchronize(b->stream), "cudaStreamSynchronize");
   if (t) *t = b->t;
   return ER_OK;
@@ -613,10 +640,10 @@ er_status er_set_state(er_batch *b, int32_t src_mem, const double *positions, co
   if (t && !std::isfinite(*t)) { b->last_error = "t is not finite"; return ER_EINVAL; }
   CK(cudaSetDevice(b->device), "cudaSetDevice");
   er_status st;
-  if (positions && (st = upload_planes(b, positions, src_mem, b->d_node, b->n_nodes, 3, b->nn)) != ER_OK) return st;
-  if (velocities && (st = upload_planes(b, velocities, src_mem, b->d_node + 3 * b->nn, b->n_nodes, 3, b->nn)) != ER_OK) return st;
-  if (directors && (st = upload_planes(b, directors, src_mem, b->d_elem, b->n_elems, 9, b->ne)) != ER_OK) return st;
-  if (omega && (st = upload_planes(b, omega, src_mem, b->d_elem + 9 * b->ne, b->n_elems, 3, b->ne)) != ER_OK) return st;
+  if (positions && (st = upload_field(b, positions, src_mem, FIELD_POS, false)) != ER_OK) return st;
+  if (velocities && (st = upload_field(b, velocities, src_mem, FIELD_VEL, false)) != ER_OK) return st;
+  if (directors && (st = upload_field(b, directors, src_mem, FIELD_DIR, false)) != ER_OK) return st;
+  if (omega && (st = upload_field(b, omega, src_mem, FIELD_OMEGA, false)) != ER_OK) return st;
   CK(cudaStreamSynchronize(b->stream), "cudaStreamSynchronize");
   if (t) b->t = *t;
   return ER_OK;
@@ -653,10 +680,10 @@ er_status er_query(const er_batch *b, er_info *info) {
   info->launches = b->launches;
   info->device_bytes = b->device_bytes;
   info->t = b->t;
-  // state read + written once per step (r, v: 6 per node; Q, w: 12 per element) + rod records
+  // bytes one fused step moves: state read + written once (r, v: 6 per node; Q, w: 12 per
+  // element), the 192-byte rod record read once, static kappa0 read once
   double bytes = 16.0 * (6.0 * b->n_nodes + 12.0 * b->n_elems) + 8.0 * ER_REC * b->n_rods;
-  if (b->d_kappa0) bytes += 24.0 * b->n_vor;
-  bytes += 8.0 * (ER_REC - 16) * b->n_rods;  // the record is 24 doubles (192 B), B_min counts 128 B
+  if (b->has_kappa0) bytes += 24.0 * b->n_vor;
   info->bytes_per_step = bytes;
   return ER_OK;
 }

@@ -293,43 +293,31 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
-// Stage geometry of the persistent kernel: per buffer NPL planes of stride PS doubles, then the
-// rod records (RMAX x ER_REC) and the tile's element offsets (RMAX + 4 int64).
+// Stage geometry of the persistent kernel: per buffer the tile's state block (<= 18 or 21
+// planes of <= BLOCK doubles; the exchange area of XPLANES x BLOCK reuses it), then the rod
+// records (RMAX x ER_REC) and the tile's element offsets (RMAX + 4 int64).
 template <int BLOCK, int FEAT>
 struct Stage {
-  static constexpr int PS = BLOCK + 8;
   static constexpr int NPL = (FEAT & FEAT_KAPPA0) ? 21 : 18;
   static constexpr int RMAX = BLOCK / 8;
-  static constexpr int PLANES = (NPL > XPLANES ? NPL : XPLANES) * PS;  // exchange reuses the planes
+  static constexpr int PLANES = (NPL > XPLANES ? NPL : XPLANES) * BLOCK + 8;
   static constexpr int RECOFF = PLANES;
   static constexpr int EOFF = RECOFF + RMAX * ER_REC;
   static constexpr int BUFD = EOFF + RMAX + 4;  // doubles per buffer (even)
   static constexpr size_t bytes() { return (size_t)(2 * BUFD) * 8 + 2 * 8; }
 };
 
-// Thread 0 issues the bulk copies of tile `T` into stage buffer B.
+// Thread 0 issues the bulk copies of tile `T` into stage buffer B: the tile's contiguous state
+// block, its rod records and its element offsets -- three TMA 1-D bulk copies.
 template <int BLOCK, int FEAT>
 __device__ __forceinline__ void issue_tile(const ErStepParams &p, const ErTile &T, double *B, uint64_t *bar) {
   using SG = Stage<BLOCK, FEAT>;
-  const int64_t na = T.nbase & ~1ll, ne_ = T.ebase & ~1ll;
-  const uint32_t cn = (uint32_t)(((T.nbase + T.nslots + 1) & ~1ll) - na);
-  const uint32_t ce = (uint32_t)(((T.ebase + T.nel + 1) & ~1ll) - ne_);
-  const int64_t vb = T.ebase - T.r0, nvor = T.nel - T.nr;
-  const int64_t va = vb & ~1ll;
-  const uint32_t cv = nvor > 0 ? (uint32_t)(((vb + nvor + 1) & ~1ll) - va) : 0u;
+  const uint32_t cs = (uint32_t)tile_block_size(T, (FEAT & FEAT_KAPPA0) ? p.has_kappa0 : 0);
   const int64_t ra = T.r0 & ~1ll;
   const uint32_t ceo = (uint32_t)(((T.r0 + T.nr + 2) & ~1ll) - ra);
-  uint32_t bytes = 8u * (6u * cn + 12u * ce) + (uint32_t)T.nr * ER_REC * 8u + 8u * ceo;
-  if ((FEAT & FEAT_KAPPA0) && cv) bytes += 8u * 3u * cv;
+  const uint32_t bytes = 8u * cs + (uint32_t)T.nr * ER_REC * 8u + 8u * ceo;
   mbar_expect_tx(bar, bytes);
-#pragma unroll 1
-  for (int c = 0; c < 6; ++c) bulk_g2s(B + c * SG::PS, p.node + c * p.nn + na, 8u * cn, bar);
-#pragma unroll 1
-  for (int c = 0; c < 12; ++c) bulk_g2s(B + (6 + c) * SG::PS, p.elem + c * p.ne + ne_, 8u * ce, bar);
-  if ((FEAT & FEAT_KAPPA0) && cv) {
-#pragma unroll 1
-    for (int c = 0; c < 3; ++c) bulk_g2s(B + (18 + c) * SG::PS, p.kappa0 + c * p.nv + va, 8u * cv, bar);
-  }
+  bulk_g2s(B, p.state + T.boff, 8u * cs, bar);
   bulk_g2s(B + SG::RECOFF, p.rec + (int64_t)T.r0 * ER_REC, (uint32_t)T.nr * ER_REC * 8u, bar);
   bulk_g2s(B + SG::EOFF, p.eoff + ra, 8u * ceo, bar);
 }
@@ -384,23 +372,23 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
     si.fl = si.active ? rec_flags(rec) : 0;
     finish_slot(si);
 
-    // ---- stage -> registers
-    const int ln = tid + (int)(T.nbase & 1);
-    const int le = tid - lo + (int)(T.ebase & 1);
+    // ---- stage -> registers (tile-local SoA planes)
+    const int ns = T.nslots, nel = T.nel;
+    const int le = tid - lo;
     double r[3], v[3], Q[9], w[3], k0s[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      r[c] = B[c * SG::PS + ln];
-      v[c] = B[(3 + c) * SG::PS + ln];
+      r[c] = B[c * ns + tid];
+      v[c] = B[(3 + c) * ns + tid];
     }
 #pragma unroll
-    for (int c = 0; c < 9; ++c) Q[c] = B[(6 + c) * SG::PS + le];
+    for (int c = 0; c < 9; ++c) Q[c] = B[6 * ns + c * nel + le];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) w[c] = B[(15 + c) * SG::PS + le];
+    for (int c = 0; c < 3; ++c) w[c] = B[6 * ns + (9 + c) * nel + le];
     if ((FEAT & FEAT_KAPPA0) && si.has_v) {
-      const int lv = tid - 2 * lo - 1 + (int)((T.ebase - T.r0) & 1);
+      const int nvor = nel - T.nr;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) k0s[c] = B[(18 + c) * SG::PS + lv];
+      for (int c = 0; c < 3; ++c) k0s[c] = B[6 * ns + 12 * nel + c * nvor + (tid - 2 * lo - 1)];
     }
     __syncthreads();  // everyone has read the stage planes: they become this tile's exchange area
     if (tid == 0 && tnext < p.n_tiles) {
@@ -417,19 +405,20 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
     }
     if (fbits) { fbits_all |= fbits; frod = min(frod, si.rod); }
 
-    // ---- registers -> HBM (streaming stores)
+    // ---- registers -> HBM (streaming stores into the tile block)
+    double *G = p.state + T.boff;
     if (si.active) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        __stcs(p.node + c * p.nn + si.node, r[c]);
-        __stcs(p.node + (3 + c) * p.nn + si.node, v[c]);
+        __stcs(G + c * ns + tid, r[c]);
+        __stcs(G + (3 + c) * ns + tid, v[c]);
       }
     }
     if (si.has_e) {
 #pragma unroll
-      for (int c = 0; c < 9; ++c) __stcs(p.elem + c * p.ne + si.elem, Q[c]);
+      for (int c = 0; c < 9; ++c) __stcs(G + 6 * ns + c * nel + le, Q[c]);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) __stcs(p.elem + (9 + c) * p.ne + si.elem, w[c]);
+      for (int c = 0; c < 3; ++c) __stcs(G + 6 * ns + (9 + c) * nel + le, w[c]);
     }
   }
   report_fault(p, fbits_all, frod);
@@ -471,22 +460,24 @@ __global__ void __launch_bounds__(BLOCK, MINB) simple_kernel(const ErStepParams 
   const double *rec = p.rec + (int64_t)si.rod * ER_REC;
   double r[3] = {0, 0, 0}, v[3] = {0, 0, 0}, Q[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, w[3] = {0, 0, 0};
   double k0s[3] = {0.0, 0.0, 0.0};
+  double *G = p.state + T.boff;
+  const int ns = T.nslots, nel = T.nel, s = threadIdx.x, le = s - si.q;
   if (si.active) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      r[c] = __ldcs(p.node + c * p.nn + si.node);
-      v[c] = __ldcs(p.node + (3 + c) * p.nn + si.node);
+      r[c] = __ldcs(G + c * ns + s);
+      v[c] = __ldcs(G + (3 + c) * ns + s);
     }
   }
   if (si.has_e) {
 #pragma unroll
-    for (int c = 0; c < 9; ++c) Q[c] = __ldcs(p.elem + c * p.ne + si.elem);
+    for (int c = 0; c < 9; ++c) Q[c] = __ldcs(G + 6 * ns + c * nel + le);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) w[c] = __ldcs(p.elem + (9 + c) * p.ne + si.elem);
+    for (int c = 0; c < 3; ++c) w[c] = __ldcs(G + 6 * ns + (9 + c) * nel + le);
   }
-  if (p.kappa0 && si.has_v) {
+  if (p.has_kappa0 && si.has_v) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) k0s[c] = __ldg(p.kappa0 + c * p.nv + si.vor);
+    for (int c = 0; c < 3; ++c) k0s[c] = __ldg(G + tile_vor_plane(T, c) + (s - 2 * si.q - 1));
   }
   double t = p.t;
   unsigned fbits = 0;
@@ -500,15 +491,15 @@ __global__ void __launch_bounds__(BLOCK, MINB) simple_kernel(const ErStepParams 
   if (si.active) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      __stcs(p.node + c * p.nn + si.node, r[c]);
-      __stcs(p.node + (3 + c) * p.nn + si.node, v[c]);
+      __stcs(G + c * ns + s, r[c]);
+      __stcs(G + (3 + c) * ns + s, v[c]);
     }
   }
   if (si.has_e) {
 #pragma unroll
-    for (int c = 0; c < 9; ++c) __stcs(p.elem + c * p.ne + si.elem, Q[c]);
+    for (int c = 0; c < 9; ++c) __stcs(G + 6 * ns + c * nel + le, Q[c]);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) __stcs(p.elem + (9 + c) * p.ne + si.elem, w[c]);
+    for (int c = 0; c < 3; ++c) __stcs(G + 6 * ns + (9 + c) * nel + le, w[c]);
   }
   report_fault(p, fbits, si.rod);
 }
@@ -530,12 +521,14 @@ __global__ void __launch_bounds__(BLOCK) diag_kernel(const ErStepParams p) {
   const bool general = (si.fl & FL_GENERAL) != 0;
   const double *rec = p.rec + (int64_t)si.rod * ER_REC;
   auto gp = [&](int plane) { return p.gpar[plane * p.ng + si.node]; };
+  const double *G = p.state + T.boff;
+  const int ns = T.nslots, nel = T.nel, le = s - si.q;
   double r[3] = {0, 0, 0}, v[3] = {0, 0, 0}, Q[9], w[3] = {0, 0, 0};
   for (int c = 0; c < 3; ++c) {
-    if (si.active) { r[c] = p.node[c * p.nn + si.node]; v[c] = p.node[(3 + c) * p.nn + si.node]; }
-    if (si.has_e) w[c] = p.elem[(9 + c) * p.ne + si.elem];
+    if (si.active) { r[c] = G[c * ns + s]; v[c] = G[(3 + c) * ns + s]; }
+    if (si.has_e) w[c] = G[6 * ns + (9 + c) * nel + le];
   }
-  for (int c = 0; c < 9; ++c) Q[c] = si.has_e ? p.elem[c * p.ne + si.elem] : 0.0;
+  for (int c = 0; c < 9; ++c) Q[c] = si.has_e ? G[6 * ns + c * nel + le] : 0.0;
   if (si.active) {
     for (int c = 0; c < 3; ++c) xr[c * BLOCK + s] = r[c];
     for (int c = 0; c < 9; ++c) xQ[c * BLOCK + s] = Q[c];
@@ -579,7 +572,7 @@ __global__ void __launch_bounds__(BLOCK) diag_kernel(const ErStepParams p) {
     logrot_pair(Q, Qp, kap, cth, s2);
     const double Dh = general ? gp(GP_DH) : rec[REC_LHAT];
     double k0[3] = {0, 0, 0};
-    if (p.kappa0) for (int c = 0; c < 3; ++c) k0[c] = p.kappa0[c * p.nv + si.vor];
+    if (p.has_kappa0) for (int c = 0; c < 3; ++c) k0[c] = G[tile_vor_plane(T, c) + (s - 2 * si.q - 1)];
     if (si.fl & FL_ACT) {
       const double sk = general ? gp(GP_SK) : i * rec[REC_LHAT];
       k0[p.act_comp] += rec[REC_ACTA] * sinpi(2.0 * (sk * rec[REC_ACTIL] - rec[REC_ACTF] * p.t));
@@ -637,53 +630,52 @@ __global__ void aos_to_soa(const double *__restrict__ src, double *__restrict__ 
     dst[c * stride + e] = src[q];
   }
 }
-__global__ void soa_to_aos(const double *__restrict__ src, double *__restrict__ dst, int64_t n, int k,
-                           int64_t stride) {
-  const int64_t total = n * k;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = q / k;
-    const int c = (int)(q - e * k);
-    dst[q] = src[c * stride + e];
+// Canonical AoS [rows][k] <-> tile-blocked planes, one CTA per tile.  canon == nullptr with
+// to_tiles writes zeros.
+__global__ void canon_tiles(const ErStepParams p, double *canon, int field, int to_tiles) {
+  const ErTile T = p.tiles[blockIdx.x];
+  const int k = field == FIELD_DIR ? 9 : 3;
+  int64_t base, count, off;
+  if (field <= FIELD_VEL) {
+    base = T.nbase; count = T.nslots; off = tile_node_plane(T, field == FIELD_VEL ? 3 : 0);
+  } else if (field <= FIELD_OMEGA) {
+    base = T.ebase; count = T.nel; off = tile_elem_plane(T, field == FIELD_OMEGA ? 9 : 0);
+  } else {
+    base = T.ebase - T.r0; count = T.nel - T.nr; off = tile_vor_plane(T, 0);
   }
-}
-__global__ void fill_planes(double *dst, int64_t n, int k, int64_t stride, double value) {
-  const int64_t total = n * k;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = q / k;
-    const int c = (int)(q - e * k);
-    dst[c * stride + e] = value;
+  double *blk = p.state + T.boff + off;
+  for (int64_t q = threadIdx.x; q < count * k; q += blockDim.x) {
+    const int64_t u = q / k;
+    const int c = (int)(q - u * k);
+    if (to_tiles) blk[c * count + u] = canon ? canon[base * k + q] : 0.0;
+    else canon[base * k + q] = blk[c * count + u];
   }
 }
 
-// Validation of uploaded state: [0] max |Q Q^T - I|, [1] max |det Q - 1|, [2] non-finite count.
+// Validation of an uploaded canonical AoS array: out[2] += non-finite rows; for directors
+// (orth) out[0] = max |Q Q^T - I|, out[1] = max |det Q - 1|.
 __device__ __forceinline__ void atomic_max_nonneg(double *addr, double v) {
   atomicMax(reinterpret_cast<unsigned long long *>(addr), (unsigned long long)__double_as_longlong(v));
 }
-__global__ void validate_state(const double *node, int64_t nn, int64_t n_nodes, const double *elem, int64_t ne,
-                               int64_t n_elems, double *out) {
+__global__ void validate_aos(const double *a, int64_t n, int k, int orth, double *out) {
   double m_orth = 0.0, m_det = 0.0, bad = 0.0;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_elems; q += (int64_t)gridDim.x * blockDim.x) {
-    double Q[9];
-    for (int c = 0; c < 9; ++c) Q[c] = elem[c * ne + q];
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const double *x = a + q * k;
     bool fin = true;
-    for (int c = 0; c < 12; ++c) fin = fin && isfinite(elem[c * ne + q]);
+    for (int c = 0; c < k; ++c) fin = fin && isfinite(x[c]);
     if (!fin) { bad += 1.0; continue; }
-    for (int a = 0; a < 3; ++a)
-      for (int b = 0; b < 3; ++b) {
-        const double d = dot3(Q + 3 * a, Q + 3 * b) - (a == b ? 1.0 : 0.0);
-        m_orth = fmax(m_orth, fabs(d));
-      }
-    const double det = Q[0] * (Q[4] * Q[8] - Q[5] * Q[7]) - Q[1] * (Q[3] * Q[8] - Q[5] * Q[6]) +
-                       Q[2] * (Q[3] * Q[7] - Q[4] * Q[6]);
-    m_det = fmax(m_det, fabs(det - 1.0));
+    if (orth) {
+      for (int u = 0; u < 3; ++u)
+        for (int w = 0; w < 3; ++w) m_orth = fmax(m_orth, fabs(dot3(x + 3 * u, x + 3 * w) - (u == w ? 1.0 : 0.0)));
+      const double det = x[0] * (x[4] * x[8] - x[5] * x[7]) - x[1] * (x[3] * x[8] - x[5] * x[6]) +
+                         x[2] * (x[3] * x[7] - x[4] * x[6]);
+      m_det = fmax(m_det, fabs(det - 1.0));
+    }
   }
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_nodes; q += (int64_t)gridDim.x * blockDim.x) {
-    bool fin = true;
-    for (int c = 0; c < 6; ++c) fin = fin && isfinite(node[c * nn + q]);
-    if (!fin) bad += 1.0;
+  if (orth) {
+    atomic_max_nonneg(out + 0, m_orth);
+    atomic_max_nonneg(out + 1, m_det);
   }
-  atomic_max_nonneg(out + 0, m_orth);
-  atomic_max_nonneg(out + 1, m_det);
   if (bad > 0.0) atomicAdd(out + 2, bad);
 }
 
@@ -784,19 +776,14 @@ cudaError_t er_launch_aos_to_soa(const double *src, double *dst, int64_t n, int 
   er::aos_to_soa<<<148 * 8, 256, 0, st>>>(src, dst, n, k, stride);
   return cudaGetLastError();
 }
-cudaError_t er_launch_soa_to_aos(const double *src, double *dst, int64_t n, int k, int64_t stride, cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
-  er::soa_to_aos<<<148 * 8, 256, 0, st>>>(src, dst, n, k, stride);
+cudaError_t er_launch_canon_tiles(const ErStepParams *p, double *canon, int field, int to_tiles, cudaStream_t st) {
+  if (p->n_tiles <= 0) return cudaSuccess;
+  er::canon_tiles<<<(unsigned)p->n_tiles, 256, 0, st>>>(*p, canon, field, to_tiles);
   return cudaGetLastError();
 }
-cudaError_t er_launch_fill(double *dst, int64_t n, int k, int64_t stride, double value, cudaStream_t st) {
+cudaError_t er_launch_validate(const double *aos, int64_t n, int k, int orth, double *out, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  er::fill_planes<<<148 * 8, 256, 0, st>>>(dst, n, k, stride, value);
-  return cudaGetLastError();
-}
-cudaError_t er_launch_validate(const double *node, int64_t nn, int64_t n_nodes, const double *elem, int64_t ne,
-                               int64_t n_elems, double *out, cudaStream_t st) {
-  er::validate_state<<<148 * 4, 256, 0, st>>>(node, nn, n_nodes, elem, ne, n_elems, out);
+  er::validate_aos<<<148 * 4, 256, 0, st>>>(aos, n, k, orth, out);
   return cudaGetLastError();
 }
 

@@ -1,20 +1,28 @@
 // er_layout.h -- device-resident layout of a rod batch (L0) and the kernel parameter block.
 //
 // HBM layout:
-//  - node planes  : 6 fp64 planes [rx ry rz vx vy vz][nn]      (compact SoA, no ghosts)
-//  - elem planes  : 12 fp64 planes [Q00..Q22 wx wy wz][ne]      (row a of Q = d_{a+1})
+//  - state        : tile-blocked SoA.  The rods are packed into rod-aligned tiles (<= BLOCK
+//                   slots, <= BLOCK/8 rods); tile T owns one contiguous block at T.boff:
+//                   6 node planes [rx ry rz vx vy vz] x nslots, then 12 element planes
+//                   [Q00..Q22 wx wy wz] x nel, then (static kappa0 only) 3 Voronoi planes x nvor,
+//                   padded to 16 bytes.  SoA per component inside the block, so every warp
+//                   access is coalesced, and one TMA bulk copy moves a whole tile.
 //  - rod records  : [n_rods][ER_REC] fp64: derived constants, damping, v_max^2, tip force,
 //                   actuation and the flag word -- one 192-byte record read per rod per step
-//  - eoff         : [n_rods+3] int64 element offsets (node offset = eoff + rod); padded so
-//                   16-byte-aligned bulk copies may over-read one entry
-//  - tiles        : [n_tiles] ErTile, rod-aligned tiles of <= BLOCK slots and <= BLOCK/8 rods
-//  - gpar         : optional [ER_GP][nn] per-slot parameters of "general" rods
-//                   (non-uniform rest lengths or per-element material)
-//  - kappa0       : optional [3][nv] static rest curvature;  sigma0, mag: optional [3][ne]
-// Every plane stride is a multiple of 32 doubles plus 32 doubles of slack, so bulk copies that
-// round a range out to 16-byte boundaries stay in bounds.  Ghost nodes exist only in smem.
+//  - eoff         : [n_rods+4] int64 element offsets (node offset = eoff + rod); padded so
+//                   16-byte-aligned bulk copies may over-read
+//  - tiles        : [n_tiles] ErTile
+//  - gpar         : optional [ER_GP][ng] per-slot parameters of "general" rods (non-uniform
+//                   rest lengths or per-element material), canonical node index
+//  - sigma0, mag  : optional [3][ne] canonical element planes
+// Ghost nodes exist only in shared memory, never in HBM.
 #pragma once
 #include <stdint.h>
+
+#ifndef __CUDACC__
+#define __host__
+#define __device__
+#endif
 
 enum {
   REC_LHAT = 0,  // rest length (uniform rod)
@@ -63,9 +71,13 @@ enum {
 // batch-level feature bits (kernel template parameter)
 enum { FEAT_GENERAL = 1, FEAT_KAPPA0 = 2, FEAT_EXTRA = 4 /* sigma0 / magnetization / actuation */ };
 
+// canonical fields (er_get_state / er_set_state order)
+enum { FIELD_POS = 0, FIELD_VEL = 1, FIELD_DIR = 2, FIELD_OMEGA = 3, FIELD_KAPPA0 = 4 };
+
 struct ErTile {
-  int64_t nbase;   // first node of the tile
-  int64_t ebase;   // first element of the tile
+  int64_t nbase;   // first node of the tile (canonical index)
+  int64_t ebase;   // first element of the tile (canonical index)
+  int64_t boff;    // offset of the tile's state block (doubles, even)
   int32_t r0;      // first rod
   int32_t nr;      // rods in the tile
   int32_t nslots;  // nodes (= slots) in the tile
@@ -73,10 +85,7 @@ struct ErTile {
 };
 
 struct ErStepParams {
-  double *node;  // 6 planes
-  double *elem;  // 12 planes
-  int64_t nn;    // node plane stride (doubles)
-  int64_t ne;    // element plane stride
+  double *state;          // tile-blocked state
   const double *rec;
   const int64_t *eoff;
   const ErTile *tiles;
@@ -84,16 +93,30 @@ struct ErStepParams {
   const double *gpar;     // may be null
   int64_t ng;             // gpar plane stride
   const double *sigma0;   // may be null, planes stride ne
-  const double *kappa0;   // may be null, planes stride nv
-  int64_t nv;
   const double *mag;      // may be null, planes stride ne
+  int64_t ne;
+  int32_t has_kappa0;     // static kappa0 planes present in the tile blocks
+  int32_t act_comp;
   double g[3];
   double b0[3];
   double b_omega;
-  int32_t act_comp;
   int32_t n_steps;        // steps in this launch
+  int32_t pad_;
   double t;               // time at the start of the launch
   double h;               // dt
   unsigned long long *fault;  // [0] = OR of bits, [1] = min rod id
   double *diag_partial;   // diagnostics: [n_tiles][16]
 };
+
+// offsets inside a tile block (doubles)
+__host__ __device__ inline int64_t tile_node_plane(const ErTile &T, int c) { return (int64_t)c * T.nslots; }
+__host__ __device__ inline int64_t tile_elem_plane(const ErTile &T, int c) {
+  return 6 * (int64_t)T.nslots + (int64_t)c * T.nel;
+}
+__host__ __device__ inline int64_t tile_vor_plane(const ErTile &T, int c) {
+  return 6 * (int64_t)T.nslots + 12 * (int64_t)T.nel + (int64_t)c * (T.nel - T.nr);
+}
+__host__ __device__ inline int64_t tile_block_size(const ErTile &T, int has_kappa0) {
+  const int64_t sz = 6 * (int64_t)T.nslots + 12 * (int64_t)T.nel + (has_kappa0 ? 3 * (int64_t)(T.nel - T.nr) : 0);
+  return (sz + 1) & ~1ll;
+}
