@@ -403,6 +403,14 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
       T.nr = nr;
       T.nslots = (int32_t)used;
       T.nel = (int32_t)(eoff[r] - eoff[T.r0]);
+      std::memset(T.smask, 0, sizeof T.smask);
+      std::memset(T.pfx, 0, sizeof T.pfx);
+      T.pad_ = 0;
+      for (int32_t q = 0, st = 0; q < nr; ++q) {
+        T.smask[st >> 5] |= 1u << (st & 31);
+        st += b->n_elems_h[T.r0 + q] + 1;
+      }
+      for (int wd = 1; wd < 16; ++wd) T.pfx[wd] = (uint8_t)(T.pfx[wd - 1] + __builtin_popcount(T.smask[wd - 1]));
       int64_t sz = 6 * (int64_t)T.nslots + 12 * (int64_t)T.nel + (b->has_kappa0 ? 3 * (int64_t)(T.nel - T.nr) : 0);
       boff += (sz + 1) & ~1ll;
       tiles.push_back(T);

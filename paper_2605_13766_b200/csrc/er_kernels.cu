@@ -290,6 +290,11 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ unsigned lanemask_le() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
+  return m;
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
@@ -303,23 +308,26 @@ struct Stage {
   static constexpr int PLANES = (NPL > XPLANES ? NPL : XPLANES) * BLOCK + 8;
   static constexpr int RECOFF = PLANES;
   static constexpr int EOFF = RECOFF + RMAX * ER_REC;
-  static constexpr int BUFD = EOFF + RMAX + 4;  // doubles per buffer (even)
+  static constexpr int TOFF = EOFF + RMAX + 4;   // staged ErTile (16 doubles)
+  static constexpr int BUFD = TOFF + 16;         // doubles per buffer (even)
   static constexpr size_t bytes() { return (size_t)(2 * BUFD) * 8 + 2 * 8; }
 };
 
 // Thread 0 issues the bulk copies of tile `T` into stage buffer B: the tile's contiguous state
 // block, its rod records and its element offsets -- three TMA 1-D bulk copies.
 template <int BLOCK, int FEAT>
-__device__ __forceinline__ void issue_tile(const ErStepParams &p, const ErTile &T, double *B, uint64_t *bar) {
+__device__ __forceinline__ void issue_tile(const ErStepParams &p, const ErTile &T, const ErTile *tile_ptr, double *B,
+                                           uint64_t *bar) {
   using SG = Stage<BLOCK, FEAT>;
   const uint32_t cs = (uint32_t)tile_block_size(T, (FEAT & FEAT_KAPPA0) ? p.has_kappa0 : 0);
   const int64_t ra = T.r0 & ~1ll;
   const uint32_t ceo = (uint32_t)(((T.r0 + T.nr + 2) & ~1ll) - ra);
-  const uint32_t bytes = 8u * cs + (uint32_t)T.nr * ER_REC * 8u + 8u * ceo;
+  const uint32_t bytes = 8u * cs + (uint32_t)T.nr * ER_REC * 8u + 8u * ceo + (uint32_t)sizeof(ErTile);
   mbar_expect_tx(bar, bytes);
   bulk_g2s(B, p.state + T.boff, 8u * cs, bar);
   bulk_g2s(B + SG::RECOFF, p.rec + (int64_t)T.r0 * ER_REC, (uint32_t)T.nr * ER_REC * 8u, bar);
   bulk_g2s(B + SG::EOFF, p.eoff + ra, 8u * ceo, bar);
+  bulk_g2s(B + SG::TOFF, tile_ptr, (uint32_t)sizeof(ErTile), bar);
 }
 
 template <int BLOCK, int MINB, int FEAT>
@@ -335,31 +343,27 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
   }
   __syncthreads();
   int64_t tile = blockIdx.x;
-  if (tid == 0 && tile < p.n_tiles) issue_tile<BLOCK, FEAT>(p, p.tiles[tile], sm, &bar[0]);
+  if (tid == 0 && tile < p.n_tiles) issue_tile<BLOCK, FEAT>(p, p.tiles[tile], p.tiles + tile, sm, &bar[0]);
   uint32_t phase = 0;  // bit b = parity of buffer b
   unsigned fbits_all = 0;
   int frod = 0x7fffffff;
   for (int k = 0; tile < p.n_tiles; tile += gridDim.x, ++k) {
     const int b = k & 1;
     double *B = sm + b * SG::BUFD;
-    const ErTile T = p.tiles[tile];
     const int64_t tnext = tile + gridDim.x;
     ErTile Tn;
     if (tid == 0 && tnext < p.n_tiles) Tn = p.tiles[tnext];  // descriptor load overlaps the wait
     mbar_wait(&bar[b], (phase >> b) & 1u);
     phase ^= 1u << b;
 
-    // ---- decode this thread's slot from the staged element offsets
+    // ---- decode this thread's slot from the staged tile descriptor and element offsets
+    const ErTile &T = *reinterpret_cast<const ErTile *>(B + SG::TOFF);
     const int64_t *eo = reinterpret_cast<const int64_t *>(B + SG::EOFF) + (T.r0 & 1);
     SlotInfo si;
     si.s = tid;
     si.active = tid < T.nslots;
-    int lo = 0, hi = T.nr - 1;
+    const int lo = T.pfx[tid >> 5] + __popc(T.smask[tid >> 5] & lanemask_le()) - 1;
     const int64_t e0 = eo[0];
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if ((int)(eo[mid] - e0) + mid <= tid) lo = mid; else hi = mid - 1;
-    }
     si.q = lo;
     si.rod = T.r0 + lo;
     const int st0 = (int)(eo[lo] - e0) + lo;
@@ -393,7 +397,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
     __syncthreads();  // everyone has read the stage planes: they become this tile's exchange area
     if (tid == 0 && tnext < p.n_tiles) {
       fence_proxy_async();  // order the previous generic smem accesses before the async writes
-      issue_tile<BLOCK, FEAT>(p, Tn, sm + (b ^ 1) * SG::BUFD, &bar[b ^ 1]);
+      issue_tile<BLOCK, FEAT>(p, Tn, p.tiles + tnext, sm + (b ^ 1) * SG::BUFD, &bar[b ^ 1]);
     }
 
     // ---- the steps
@@ -433,11 +437,7 @@ __device__ __forceinline__ void decode_global(const ErStepParams &p, const ErTil
   const int s = threadIdx.x;
   si.s = s;
   si.active = s < T.nslots;
-  int lo = 0, hi = T.nr - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (rst[mid] <= s) lo = mid; else hi = mid - 1;
-  }
+  const int lo = T.pfx[s >> 5] + __popc(T.smask[s >> 5] & lanemask_le()) - 1;
   si.q = lo;
   si.rod = T.r0 + lo;
   si.i = s - rst[lo];

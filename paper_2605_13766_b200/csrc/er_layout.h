@@ -74,7 +74,10 @@ enum { FEAT_GENERAL = 1, FEAT_KAPPA0 = 2, FEAT_EXTRA = 4 /* sigma0 / magnetizati
 // canonical fields (er_get_state / er_set_state order)
 enum { FIELD_POS = 0, FIELD_VEL = 1, FIELD_DIR = 2, FIELD_OMEGA = 3, FIELD_KAPPA0 = 4 };
 
-struct ErTile {
+// Tile descriptor (128 bytes, 16-byte aligned so a TMA bulk copy can stage it).  smask marks
+// the slots that start a rod; pfx[w] counts the rod starts in words < w, so the rod of slot s
+// is pfx[s/32] + popc(smask[s/32] & lanemask_le) - 1.
+struct __align__(16) ErTile {
   int64_t nbase;   // first node of the tile (canonical index)
   int64_t ebase;   // first element of the tile (canonical index)
   int64_t boff;    // offset of the tile's state block (doubles, even)
@@ -82,6 +85,9 @@ struct ErTile {
   int32_t nr;      // rods in the tile
   int32_t nslots;  // nodes (= slots) in the tile
   int32_t nel;     // elements in the tile
+  uint32_t smask[16];
+  uint8_t pfx[16];
+  int64_t pad_;
 };
 
 struct ErStepParams {

@@ -5,43 +5,45 @@
 
 namespace er {
 
-// sin(t)/t and (1 - cos t)/t^2 as series in x = t^2, valid (to < 1 ulp of truncation) for x < 0.25.
-__device__ __forceinline__ double sinc_x(double x) {
-  double p = 1.0 / 355687428096000.0;
-  p = fma(p, x, -1.0 / 1307674368000.0);
-  p = fma(p, x, 1.0 / 6227020800.0);
-  p = fma(p, x, -1.0 / 39916800.0);
-  p = fma(p, x, 1.0 / 362880.0);
-  p = fma(p, x, -1.0 / 5040.0);
-  p = fma(p, x, 1.0 / 120.0);
-  p = fma(p, x, -1.0 / 6.0);
-  return fma(p, x, 1.0);
+// Series coefficients in constant memory: DFMA reads them as c[][] operands directly.
+// sin(t)/t and (1 - cos t)/t^2 in x = t^2 (Taylor), asin(s)/s in x = s^2.
+__constant__ double kSinc[9] = {1.0, -1.0 / 6.0, 1.0 / 120.0, -1.0 / 5040.0, 1.0 / 362880.0, -1.0 / 39916800.0,
+                                1.0 / 6227020800.0, -1.0 / 1307674368000.0, 1.0 / 355687428096000.0};
+__constant__ double kCosc[9] = {0.5, -1.0 / 24.0, 1.0 / 720.0, -1.0 / 40320.0, 1.0 / 3628800.0, -1.0 / 479001600.0,
+                                1.0 / 87178291200.0, -1.0 / 20922789888000.0, 1.0 / 6402373705728000.0};
+__constant__ double kAsinc[12] = {1.0, 1.0 / 6.0, 3.0 / 40.0, 5.0 / 112.0, 35.0 / 1152.0, 63.0 / 2816.0,
+                                  231.0 / 13312.0, 143.0 / 10240.0, 6435.0 / 557056.0, 12155.0 / 1245184.0,
+                                  46189.0 / 5505024.0, 88179.0 / 12058624.0};
+
+template <int NT>
+__device__ __forceinline__ double horner(const double *c, double x) {
+  double p = c[NT - 1];
+#pragma unroll
+  for (int k = NT - 2; k >= 0; --k) p = fma(p, x, c[k]);
+  return p;
 }
-__device__ __forceinline__ double cosc_x(double x) {
-  double p = 1.0 / 6402373705728000.0;
-  p = fma(p, x, -1.0 / 20922789888000.0);
-  p = fma(p, x, 1.0 / 87178291200.0);
-  p = fma(p, x, -1.0 / 479001600.0);
-  p = fma(p, x, 1.0 / 3628800.0);
-  p = fma(p, x, -1.0 / 40320.0);
-  p = fma(p, x, 1.0 / 720.0);
-  p = fma(p, x, -1.0 / 24.0);
-  return fma(p, x, 0.5);
+
+// Truncation errors (relative, all < 2^-53 / 8):
+//  sinc/cosc: x < 1e-8: 2 terms (x^2/120 < 1e-18);  x < 1e-4: 4 terms (x^4/362880 < 3e-22);
+//             x < 0.25: 9 terms (x^9/19! < 3e-23).
+//  asinc:     x < 1e-8: 2 terms (3x^2/40 < 1e-17);  x < 1e-4: 4 terms (35x^4/1152 < 4e-18);
+//             x < 0.04: 12 terms (< 3e-18).
+__device__ __forceinline__ void sinc_cosc(double x, double &a, double &b) {
+  if (x < 1e-8) {
+    a = horner<2>(kSinc, x);
+    b = horner<2>(kCosc, x);
+  } else if (x < 1e-4) {
+    a = horner<4>(kSinc, x);
+    b = horner<4>(kCosc, x);
+  } else {
+    a = horner<9>(kSinc, x);
+    b = horner<9>(kCosc, x);
+  }
 }
-// asin(s)/s as a series in x = s^2, for x < 0.04 (truncation < 1e-17).
 __device__ __forceinline__ double asinc_x(double x) {
-  double p = 88179.0 / 12058624.0;
-  p = fma(p, x, 46189.0 / 5505024.0);
-  p = fma(p, x, 12155.0 / 1245184.0);
-  p = fma(p, x, 6435.0 / 557056.0);
-  p = fma(p, x, 143.0 / 10240.0);
-  p = fma(p, x, 231.0 / 13312.0);
-  p = fma(p, x, 63.0 / 2816.0);
-  p = fma(p, x, 35.0 / 1152.0);
-  p = fma(p, x, 5.0 / 112.0);
-  p = fma(p, x, 3.0 / 40.0);
-  p = fma(p, x, 1.0 / 6.0);
-  return fma(p, x, 1.0);
+  if (x < 1e-8) return horner<2>(kAsinc, x);
+  if (x < 1e-4) return horner<4>(kAsinc, x);
+  return horner<12>(kAsinc, x);
 }
 
 // Q <- rot(v) Q with rot(v) = exp(-[v]x) = I - a [v]x + b [v]x^2 (Rodrigues; the in-place SO(3)
@@ -50,8 +52,7 @@ __device__ __forceinline__ void rotate_inplace(double Q[9], double vx, double vy
   const double x = fma(vx, vx, fma(vy, vy, vz * vz));
   double a, b;
   if (x < 0.25) {
-    a = sinc_x(x);
-    b = cosc_x(x);
+    sinc_cosc(x, a, b);
   } else {
     const double th = sqrt(x);
     double s, c;
