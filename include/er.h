@@ -85,6 +85,7 @@ typedef enum { ER_HOST = 0, ER_DEVICE = 1 } er_mem;
  *  src_mem            memory space of positions/velocities/directors/omega.
  *  device             CUDA device ordinal.
  *  stream             cudaStream_t to use, or NULL to let the library create its own.
+ *  tile_slots         rod-tile capacity (see the struct); fixes the device layout.
  * Errors: ER_EINVAL (all problems listed), ER_ENOMEM, ER_ECUDA.  *out is NULL on error.
  */
 #define ER_MAX_ELEMS_PER_ROD 511
@@ -105,6 +106,8 @@ typedef struct {
   int32_t src_mem; /* er_mem */
   int32_t device;
   void *stream;
+  int32_t tile_slots; /* 0 = auto (256, or 512 when a rod has more than 255 elements);
+                         128, 256 or 512 = slots (threads) per rod tile; must be >= max N + 1 */
 } er_batch_desc;
 
 er_status er_create_batch(const er_batch_desc *desc, er_batch **out);
@@ -209,7 +212,10 @@ typedef enum {
                                   1: staged three-kernel path (drift / dynamics+kick / drift),
                                   state through HBM between stages (ablation, debugging).
                                   2: fused step, one tile per CTA, plain loads (ablation).
-                                  All three give identical results. */
+                                  All three give identical results.
+                                  3: memory-pipeline probe (measurement aid): the persistent
+                                  kernel moves every tile through its TMA stage and back
+                                  without computing -- the state and t are left unchanged. */
 } er_option;
 er_status er_set_option(er_batch *b, int32_t option, int64_t value);
 

@@ -42,7 +42,7 @@ class er_batch_desc(C.Structure):
         ("shear_mod", _dp), ("alpha_c", _dp), ("rest_lengths", _dp), ("rest_sigma", _dp),
         ("rest_kappa", _dp), ("positions", _dp), ("velocities", _dp), ("directors", _dp),
         ("omega", _dp), ("t0", C.c_double), ("src_mem", C.c_int32), ("device", C.c_int32),
-        ("stream", C.c_void_p),
+        ("stream", C.c_void_p), ("tile_slots", C.c_int32),
     ]
 
 
@@ -210,7 +210,7 @@ class RodBatch:
     damping, tip_force, act_A/act_f/act_L/act_component, magnetization/b_field/b_omega.
     State arrays may be numpy (host) or torch CUDA tensors (device)."""
 
-    def __init__(self, w, device: int = 0, stream=None, apply_bc_forcing: bool = True):
+    def __init__(self, w, device: int = 0, stream=None, apply_bc_forcing: bool = True, tile_slots: int = 0):
         k = _Keep()
         d = er_batch_desc()
         d.n_rods = int(len(w.n_elems))
@@ -232,6 +232,7 @@ class RodBatch:
         d.t0 = float(getattr(w, "t0", 0.0))
         d.device = int(device)
         d.stream = None if stream is None else C.c_void_p(int(getattr(stream, "cuda_stream", stream)))
+        d.tile_slots = int(tile_slots)
         self.handle = er_create_batch(d)
         self.n_rods = d.n_rods
         info = er_query(self.handle)

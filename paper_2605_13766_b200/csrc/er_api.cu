@@ -297,6 +297,10 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
         if (!std::isfinite(d->rest_kappa[k])) { err.add("rest_kappa[%lld] is not finite", (long long)k); break; }
   }
   if (!std::isfinite(d->t0)) err.add("t0 is not finite");
+  if (d->tile_slots != 0 && d->tile_slots != 128 && d->tile_slots != 256 && d->tile_slots != 512)
+    err.add("tile_slots = %d not in {0, 128, 256, 512}", d->tile_slots);
+  else if (d->tile_slots != 0 && max_n + 1 > d->tile_slots)
+    err.add("tile_slots = %d < longest rod's %d slots", d->tile_slots, max_n + 1);
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) err.add("no CUDA device available");
   else if (d->device < 0 || d->device >= ndev) err.add("device %d outside [0, %d)", d->device, ndev);
@@ -383,7 +387,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   // ---- rod-aligned tiles (greedy contiguous packing, <= block slots and <= block/8 rods per
   // tile); each tile's state is one contiguous SoA block: 6 node planes x nslots, 12 element
   // planes x nel, [3 Voronoi planes x nvor], padded to an even number of doubles (16 B).
-  b->block = (max_n + 1 <= 256) ? 256 : 512;
+  b->block = d->tile_slots ? d->tile_slots : (max_n + 1 <= 256) ? 256 : 512;
   std::vector<ErTile> tiles;
   {
     int64_t r = 0, boff = 0;
@@ -562,7 +566,7 @@ er_status er_set_option(er_batch *b, int32_t option, int64_t value) {
     return ER_OK;
   }
   if (option == ER_OPT_KERNEL) {
-    if (value < 0 || value > 2) { b->last_error = "kernel must be 0 (fused persistent), 1 (staged) or 2 (fused, one tile per CTA)"; return ER_EINVAL; }
+    if (value < 0 || value > 3) { b->last_error = "kernel must be 0 (fused persistent), 1 (staged), 2 (fused, one tile per CTA) or 3 (memory probe)"; return ER_EINVAL; }
     b->kernel_mode = (int)value;
     return ER_OK;
   }
@@ -587,6 +591,16 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
   int64_t done = 0;
   double t = b->t;
   const int feat = feat_of(b);
+  if (b->kernel_mode == 3) {  // memory-pipeline probe: n_steps passes of load + store, no physics
+    p.n_steps = 0;
+    p.t = t;
+    for (int64_t q = 0; q < n_steps; ++q) {
+      CK(er_launch_step(&p, b->block, 0, feat, b->stream), "probe kernel");
+      b->launches += 1;
+    }
+    CK(cudaStreamSynchronize(b->stream), "cudaStreamSynchronize");
+    return ER_OK;
+  }
   while (done < n_steps) {
     if (b->kernel_mode == 0 || b->kernel_mode == 2) {
       const int64_t k = std::min<int64_t>(b->steps_per_launch, n_steps - done);

@@ -343,16 +343,21 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
   }
   __syncthreads();
   int64_t tile = blockIdx.x;
-  if (tid == 0 && tile < p.n_tiles) issue_tile<BLOCK, FEAT>(p, p.tiles[tile], p.tiles + tile, sm, &bar[0]);
+  const int64_t G2 = 2 * (int64_t)gridDim.x;
+  if (tid == 0) {  // prologue: the first two tiles of this CTA go into both stage buffers
+    if (tile < p.n_tiles) issue_tile<BLOCK, FEAT>(p, p.tiles[tile], p.tiles + tile, sm, &bar[0]);
+    const int64_t t1 = tile + gridDim.x;
+    if (t1 < p.n_tiles) issue_tile<BLOCK, FEAT>(p, p.tiles[t1], p.tiles + t1, sm + SG::BUFD, &bar[1]);
+  }
   uint32_t phase = 0;  // bit b = parity of buffer b
   unsigned fbits_all = 0;
   int frod = 0x7fffffff;
   for (int k = 0; tile < p.n_tiles; tile += gridDim.x, ++k) {
     const int b = k & 1;
     double *B = sm + b * SG::BUFD;
-    const int64_t tnext = tile + gridDim.x;
+    const int64_t tnext = tile + G2;  // the tile that will re-use this buffer
     ErTile Tn;
-    if (tid == 0 && tnext < p.n_tiles) Tn = p.tiles[tnext];  // descriptor load overlaps the wait
+    if (tid == 0 && tnext < p.n_tiles) Tn = p.tiles[tnext];  // descriptor load overlaps the compute
     mbar_wait(&bar[b], (phase >> b) & 1u);
     phase ^= 1u << b;
 
@@ -394,11 +399,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
 #pragma unroll
       for (int c = 0; c < 3; ++c) k0s[c] = B[6 * ns + 12 * nel + c * nvor + (tid - 2 * lo - 1)];
     }
+    const int64_t boff = T.boff;
     __syncthreads();  // everyone has read the stage planes: they become this tile's exchange area
-    if (tid == 0 && tnext < p.n_tiles) {
-      fence_proxy_async();  // order the previous generic smem accesses before the async writes
-      issue_tile<BLOCK, FEAT>(p, Tn, p.tiles + tnext, sm + (b ^ 1) * SG::BUFD, &bar[b ^ 1]);
-    }
 
     // ---- the steps
     double t = p.t;
@@ -409,8 +411,16 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
     }
     if (fbits) { fbits_all |= fbits; frod = min(frod, si.rod); }
 
+    // ---- this buffer is free again: refill it with the tile after next, before the stores and
+    // the next wait, so two tile loads stay in flight per CTA through most of the cycle
+    __syncthreads();
+    if (tid == 0 && tnext < p.n_tiles) {
+      fence_proxy_async();  // order the generic smem accesses above before the async writes
+      issue_tile<BLOCK, FEAT>(p, Tn, p.tiles + tnext, B, &bar[b]);
+    }
+
     // ---- registers -> HBM (streaming stores into the tile block)
-    double *G = p.state + T.boff;
+    double *G = p.state + boff;
     if (si.active) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -742,6 +752,12 @@ extern "C" {
 //       3 simple fused (one tile per CTA; ablation)
 cudaError_t er_launch_step(const ErStepParams *p, int block, int kind, int feat, cudaStream_t st) {
   if (p->n_tiles <= 0) return cudaSuccess;
+  if (block == 128) {
+    if (kind == 0) return launch_persistent_feat<128, 4>(*p, feat, st);
+    if (kind == 1) return launch_simple<128, 4, er::MODE_DRIFT>(*p, st);
+    if (kind == 2) return launch_simple<128, 4, er::MODE_DYN>(*p, st);
+    return launch_simple<128, 4, er::MODE_FUSED>(*p, st);
+  }
   if (block == 256) {
     if (kind == 0) return launch_persistent_feat<256, 2>(*p, feat, st);
     if (kind == 1) return launch_simple<256, 2, er::MODE_DRIFT>(*p, st);
@@ -757,7 +773,10 @@ cudaError_t er_launch_step(const ErStepParams *p, int block, int kind, int feat,
 cudaError_t er_launch_diag(const ErStepParams *p, int block, double *out, cudaStream_t st) {
   if (p->n_tiles > 0) {
     const size_t sm = diag_smem(block);
-    if (block == 256) {
+    if (block == 128) {
+      cudaFuncSetAttribute(er::diag_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      er::diag_kernel<128><<<(unsigned)p->n_tiles, 128, sm, st>>>(*p);
+    } else if (block == 256) {
       cudaFuncSetAttribute(er::diag_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       er::diag_kernel<256><<<(unsigned)p->n_tiles, 256, sm, st>>>(*p);
     } else {
