@@ -248,7 +248,7 @@ def main():
             traffic = None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "peak_source": peak_src, "bytes_per_el_step": bmin,
-            "kernel": "er::step_kernel<256,2,0> (fused single-pass step)"}
+            "kernel": "er::fused_persistent<256,2,FEAT> (fused single-pass step, TMA bulk load/store pipeline)"}
     if a.steps_per_launch > 1:
         roof["note"] = ("temporal blocking: the state crosses HBM once per launch of "
                         f"{a.steps_per_launch} steps, so 'achieved' counts B_min per step and can exceed the "

@@ -219,6 +219,12 @@ typedef enum {
 } er_option;
 er_status er_set_option(er_batch *b, int32_t option, int64_t value);
 
+/* Measurement aid: when `trace` (DEVICE memory, [grid][64][4] uint64, zeroed by the caller) is
+ * non-NULL, the persistent step kernel records for thread 0 of each CTA and its first 64 tiles
+ * the low 48 bits of %globaltimer at: wait start (bits 56-63 = SM id), data arrival, compute
+ * end, stores issued.  NULL disables it. */
+er_status er_set_trace(er_batch *b, void *trace);
+
 typedef struct {
   int64_t n_rods, n_elems_total, n_nodes_total, n_voronoi_total;
   int64_t n_tiles;         /* CTAs per fused-step launch                       */

@@ -65,7 +65,7 @@ class er_info(C.Structure):
 
 
 EXPORTS = ("er_create_batch", "er_set_bc", "er_set_forcing", "er_step", "er_get_state", "er_set_state",
-           "er_diagnostics", "er_fault", "er_set_option", "er_query", "er_last_error",
+           "er_diagnostics", "er_fault", "er_set_option", "er_set_trace", "er_query", "er_last_error",
            "er_abi_version", "er_destroy")
 
 
@@ -84,6 +84,7 @@ def _load():
     lib.er_diagnostics.argtypes = [h, _dp]
     lib.er_fault.argtypes = [h, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
     lib.er_set_option.argtypes = [h, C.c_int32, C.c_int64]
+    lib.er_set_trace.argtypes = [h, C.c_void_p]
     lib.er_query.argtypes = [h, C.POINTER(er_info)]
     lib.er_last_error.argtypes = [h]
     lib.er_last_error.restype = C.c_char_p
@@ -91,7 +92,7 @@ def _load():
     lib.er_destroy.argtypes = [h]
     lib.er_destroy.restype = None
     for name in ("er_create_batch", "er_set_bc", "er_set_forcing", "er_step", "er_get_state",
-                 "er_set_state", "er_diagnostics", "er_fault", "er_set_option", "er_query"):
+                 "er_set_state", "er_diagnostics", "er_fault", "er_set_option", "er_set_trace", "er_query"):
         getattr(lib, name).restype = C.c_int
     return lib
 
@@ -156,6 +157,10 @@ def er_fault(handle):
 
 def er_set_option(handle, option: int, value: int):
     _check(handle, lib.er_set_option(handle, int(option), int(value)))
+
+
+def er_set_trace(handle, device_ptr):
+    _check(handle, lib.er_set_trace(handle, device_ptr))
 
 
 def er_query(handle) -> er_info:

@@ -76,6 +76,7 @@ struct er_batch {
   ErTile *d_tiles = nullptr;
   double *d_gpar = nullptr, *d_sigma0 = nullptr, *d_mag = nullptr;
   unsigned long long *d_fault = nullptr;
+  unsigned long long *trace = nullptr;  // caller-owned, optional
   double *d_diag_partial = nullptr, *d_diag_out = nullptr, *d_valid = nullptr;
   bool has_kappa0 = false, any_general = false, has_sigma0 = false, has_act = false;
   // host mirrors
@@ -135,6 +136,7 @@ ErStepParams params_of(const er_batch *b) {
   for (int c = 0; c < 3; ++c) { p.g[c] = b->g[c]; p.b0[c] = b->b0[c]; }
   p.b_omega = b->b_omega; p.act_comp = b->act_comp;
   p.fault = b->d_fault; p.diag_partial = b->d_diag_partial;
+  p.trace = b->trace;
   return p;
 }
 
@@ -572,6 +574,12 @@ er_status er_set_option(er_batch *b, int32_t option, int64_t value) {
   }
   b->last_error = "unknown option";
   return ER_EINVAL;
+}
+
+er_status er_set_trace(er_batch *b, void *trace) {
+  if (!b) return ER_EINVAL;
+  b->trace = reinterpret_cast<unsigned long long *>(trace);
+  return ER_OK;
 }
 
 er_status er_step(er_batch *b, int64_t n_steps, double dt) {

@@ -290,11 +290,35 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// acq_rel add on a shared counter: releases this warp's reads of a stage buffer and, for the
+// last arriving warp, acquires everyone else's (it then refills the buffer).
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned *addr, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(addr)), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 __device__ __forceinline__ unsigned lanemask_le() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
   return m;
 }
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
@@ -310,6 +334,7 @@ struct Stage {
   static constexpr int EOFF = RECOFF + RMAX * ER_REC;
   static constexpr int TOFF = EOFF + RMAX + 4;   // staged ErTile (16 doubles)
   static constexpr int BUFD = TOFF + 16;         // doubles per buffer (even)
+  // two buffers and their two mbarriers
   static constexpr size_t bytes() { return (size_t)(2 * BUFD) * 8 + 2 * 8; }
 };
 
@@ -343,23 +368,27 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
   }
   __syncthreads();
   int64_t tile = blockIdx.x;
-  const int64_t G2 = 2 * (int64_t)gridDim.x;
-  if (tid == 0) {  // prologue: the first two tiles of this CTA go into both stage buffers
-    if (tile < p.n_tiles) issue_tile<BLOCK, FEAT>(p, p.tiles[tile], p.tiles + tile, sm, &bar[0]);
-    const int64_t t1 = tile + gridDim.x;
-    if (t1 < p.n_tiles) issue_tile<BLOCK, FEAT>(p, p.tiles[t1], p.tiles + t1, sm + SG::BUFD, &bar[1]);
-  }
+  if (tid == 0 && tile < p.n_tiles) issue_tile<BLOCK, FEAT>(p, p.tiles[tile], p.tiles + tile, sm, &bar[0]);
   uint32_t phase = 0;  // bit b = parity of buffer b
   unsigned fbits_all = 0;
   int frod = 0x7fffffff;
+  // Pipeline per tile k in buffer b (the other buffer b^1 held tile k-1):
+  //   wait load(k) -> stage to registers -> barrier -> [t0: once the bulk store of tile k-1 has
+  //   read b^1, load tile k+1 into b^1] -> steps (exchange in b) -> barrier -> results to b ->
+  //   barrier -> [t0: bulk store b -> HBM].  Loads and stores are TMA bulk copies, so no warp
+  //   ever waits on HBM except for the (prefetched) load of its next tile.
   for (int k = 0; tile < p.n_tiles; tile += gridDim.x, ++k) {
     const int b = k & 1;
     double *B = sm + b * SG::BUFD;
-    const int64_t tnext = tile + G2;  // the tile that will re-use this buffer
+    const int64_t tnext = tile + gridDim.x;
     ErTile Tn;
-    if (tid == 0 && tnext < p.n_tiles) Tn = p.tiles[tnext];  // descriptor load overlaps the compute
+    if (tid == 0 && tnext < p.n_tiles) Tn = p.tiles[tnext];  // descriptor load overlaps the wait
+    unsigned long long *tr = (p.trace && tid == 0 && k < ER_TRACE_ITERS)
+                                 ? p.trace + ((int64_t)blockIdx.x * ER_TRACE_ITERS + k) * 4 : nullptr;
+    if (tr) tr[0] = (gtimer() & ((1ull << 48) - 1)) | ((unsigned long long)smid() << 56);
     mbar_wait(&bar[b], (phase >> b) & 1u);
     phase ^= 1u << b;
+    if (tr) tr[1] = gtimer() & ((1ull << 48) - 1);
 
     // ---- decode this thread's slot from the staged tile descriptor and element offsets
     const ErTile &T = *reinterpret_cast<const ErTile *>(B + SG::TOFF);
@@ -384,6 +413,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
     // ---- stage -> registers (tile-local SoA planes)
     const int ns = T.nslots, nel = T.nel;
     const int le = tid - lo;
+    const int64_t boff = T.boff;
     double r[3], v[3], Q[9], w[3], k0s[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -399,8 +429,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
 #pragma unroll
       for (int c = 0; c < 3; ++c) k0s[c] = B[6 * ns + 12 * nel + c * nvor + (tid - 2 * lo - 1)];
     }
-    const int64_t boff = T.boff;
-    __syncthreads();  // everyone has read the stage planes: they become this tile's exchange area
+    __syncthreads();  // stage planes consumed: they become this tile's exchange area
+    if (tid == 0 && tnext < p.n_tiles) {
+      bulk_wait_read_all();  // the bulk store of tile k-1 has finished reading buffer b^1
+      issue_tile<BLOCK, FEAT>(p, Tn, p.tiles + tnext, sm + (b ^ 1) * SG::BUFD, &bar[b ^ 1]);
+    }
 
     // ---- the steps
     double t = p.t;
@@ -410,31 +443,32 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
       if (st + 1 < p.n_steps) __syncthreads();  // exchange C is re-used as A by the next step
     }
     if (fbits) { fbits_all |= fbits; frod = min(frod, si.rod); }
+    if (tr) tr[2] = gtimer() & ((1ull << 48) - 1);
 
-    // ---- this buffer is free again: refill it with the tile after next, before the stores and
-    // the next wait, so two tile loads stay in flight per CTA through most of the cycle
-    __syncthreads();
-    if (tid == 0 && tnext < p.n_tiles) {
-      fence_proxy_async();  // order the generic smem accesses above before the async writes
-      issue_tile<BLOCK, FEAT>(p, Tn, p.tiles + tnext, B, &bar[b]);
-    }
-
-    // ---- registers -> HBM (streaming stores into the tile block)
-    double *G = p.state + boff;
+    // ---- registers -> stage (block layout) -> HBM with one TMA bulk store
+    __syncthreads();  // every exchange read of this tile is done
     if (si.active) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        __stcs(G + c * ns + tid, r[c]);
-        __stcs(G + (3 + c) * ns + tid, v[c]);
+        B[c * ns + tid] = r[c];
+        B[(3 + c) * ns + tid] = v[c];
       }
     }
     if (si.has_e) {
 #pragma unroll
-      for (int c = 0; c < 9; ++c) __stcs(G + 6 * ns + c * nel + le, Q[c]);
+      for (int c = 0; c < 9; ++c) B[6 * ns + c * nel + le] = Q[c];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) __stcs(G + 6 * ns + (9 + c) * nel + le, w[c]);
+      for (int c = 0; c < 3; ++c) B[6 * ns + (9 + c) * nel + le] = w[c];
     }
+    fence_proxy_async();  // this thread's generic smem writes -> visible to the async proxy
+    __syncthreads();
+    if (tid == 0) {
+      bulk_s2g(p.state + boff, B, 8u * (uint32_t)(6 * ns + 12 * nel));
+      bulk_commit();
+    }
+    if (tr) tr[3] = gtimer() & ((1ull << 48) - 1);
   }
+  if (tid == 0) bulk_wait_all();  // stores complete before the kernel retires
   report_fault(p, fbits_all, frod);
 }
 

@@ -112,7 +112,9 @@ struct ErStepParams {
   double h;               // dt
   unsigned long long *fault;  // [0] = OR of bits, [1] = min rod id
   double *diag_partial;   // diagnostics: [n_tiles][16]
+  unsigned long long *trace;  // optional timeline (measurement aid): [cta][ER_TRACE_ITERS][4]
 };
+#define ER_TRACE_ITERS 64
 
 // offsets inside a tile block (doubles)
 __host__ __device__ inline int64_t tile_node_plane(const ErTile &T, int c) { return (int64_t)c * T.nslots; }
