@@ -78,13 +78,13 @@ enum { FIELD_POS = 0, FIELD_VEL = 1, FIELD_DIR = 2, FIELD_OMEGA = 3, FIELD_KAPPA
 // the slots that start a rod; pfx[w] counts the rod starts in words < w, so the rod of slot s
 // is pfx[s/32] + popc(smask[s/32] & lanemask_le) - 1.
 struct __align__(16) ErTile {
-  int64_t nbase;   // first node of the tile (canonical index)
-  int64_t ebase;   // first element of the tile (canonical index)
-  int64_t boff;    // offset of the tile's state block (doubles, even)
-  int32_t r0;      // first rod
+  int32_t r0;      // first rod                       (r0..nel: one 16-byte load)
   int32_t nr;      // rods in the tile
   int32_t nslots;  // nodes (= slots) in the tile
   int32_t nel;     // elements in the tile
+  int64_t nbase;   // first node of the tile (canonical index)
+  int64_t ebase;   // first element of the tile (canonical index)
+  int64_t boff;    // offset of the tile's state block (doubles, even)
   uint32_t smask[16];
   uint8_t pfx[16];
   int64_t pad_;
@@ -128,3 +128,4 @@ __host__ __device__ inline int64_t tile_block_size(const ErTile &T, int has_kapp
   const int64_t sz = 6 * (int64_t)T.nslots + 12 * (int64_t)T.nel + (has_kappa0 ? 3 * (int64_t)(T.nel - T.nr) : 0);
   return (sz + 1) & ~1ll;
 }
+static_assert(sizeof(ErTile) == 128, "ErTile must stay 128 bytes (bulk-copied)");

@@ -46,6 +46,26 @@ __device__ __forceinline__ double asinc_x(double x) {
   return horner<12>(kAsinc, x);
 }
 
+// 1/x and 1/sqrt(x) for finite positive normal x without the IEEE slow paths: hardware
+// approximation (MUFU.RCP64H / MUFU.RSQ64H, ~2^-20) refined by Newton steps to <= 1 ulp.
+__device__ __forceinline__ double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double rsqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  double e = fma(-hx * y, y, 0.5);
+  y = fma(y, e, y);
+  e = fma(-hx * y, y, 0.5);
+  return fma(y, e, y);
+}
+
 // Q <- rot(v) Q with rot(v) = exp(-[v]x) = I - a [v]x + b [v]x^2 (Rodrigues; the in-place SO(3)
 // rotation of PAPER.md:30).  Rows of Q are the directors.  v = 0 leaves Q bit-identical.
 __device__ __forceinline__ void rotate_inplace(double Q[9], double vx, double vy, double vz) {
