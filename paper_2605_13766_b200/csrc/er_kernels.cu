@@ -164,7 +164,11 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
         const double sk = general ? gp(GP_SK) : i * rec[REC_LHAT];
         // A sin(2 pi (s/L - f t)) = A sinpi(2 (s/L - f t))
         const double arg = 2.0 * fma(sk, rec[REC_ACTIL], -rec[REC_ACTF] * t_half);
-        k0[p.act_comp] += rec[REC_ACTA] * sinpi(arg);
+        const double act = rec[REC_ACTA] * sinpi(arg);
+        // no dynamically indexed register array (it would live in local memory)
+        k0[0] += p.act_comp == 0 ? act : 0.0;
+        k0[1] += p.act_comp == 1 ? act : 0.0;
+        k0[2] += p.act_comp == 2 ? act : 0.0;
       }
       const double B1 = general ? gp(GP_BV1) : rec[REC_B1];
       const double B2 = general ? gp(GP_BV2) : rec[REC_B2];
@@ -271,6 +275,9 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
   asm volatile(
       "{\n"
@@ -327,12 +334,15 @@ template <int BLOCK, int FEAT>
 struct Stage {
   static constexpr int NPL = (FEAT & FEAT_KAPPA0) ? 21 : 18;
   static constexpr int RMAX = BLOCK / 8;
-  static constexpr int PLANES = (NPL > XPLANES ? NPL : XPLANES) * BLOCK + 8;
+  // the results of a tile are written at OUTOFF (clear of the exchange-C planes 0-5, which other
+  // warps may still read) and bulk-stored from there
+  static constexpr int OUTOFF = 6 * BLOCK;
+  static constexpr int PLANES = 24 * BLOCK + 8;
   static constexpr int RECOFF = PLANES;
   static constexpr int EOFF = RECOFF + RMAX * ER_REC;
   static constexpr int TOFF = EOFF + RMAX + 4;   // staged ErTile (16 doubles)
   static constexpr int BUFD = TOFF + 16;         // doubles per buffer (even)
-  // two buffers and their two mbarriers
+  // two buffers and their load mbarriers
   static constexpr size_t bytes() { return (size_t)(2 * BUFD) * 8 + 2 * 8; }
 };
 
@@ -381,7 +391,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
   __syncthreads();
   int64_t tile = blockIdx.x;
   if (tid == 0 && tile < p.n_tiles) issue_tile<BLOCK, FEAT>(p, load_head(p.tiles + tile), p.tiles + tile, sm, &bar[0]);
-  uint32_t phase = 0;  // bit b = parity of buffer b
+  uint32_t phase = 0;  // bit b = load parity of buffer b
   unsigned fbits_all = 0;
   int frod = 0x7fffffff;
   // Pipeline per tile k in buffer b (the other buffer b^1 held tile k-1):
@@ -457,25 +467,25 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
     if (fbits) { fbits_all |= fbits; frod = min(frod, si.rod); }
     if (tr) tr[2] = gtimer() & ((1ull << 48) - 1);
 
-    // ---- registers -> stage (block layout) -> HBM with one TMA bulk store
-    __syncthreads();  // every exchange read of this tile is done
+    // ---- registers -> stage (block layout at OUTOFF) -> HBM with one TMA bulk store
+    double *O = B + SG::OUTOFF;
     if (si.active) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        B[c * ns + tid] = r[c];
-        B[(3 + c) * ns + tid] = v[c];
+        O[c * ns + tid] = r[c];
+        O[(3 + c) * ns + tid] = v[c];
       }
     }
     if (si.has_e) {
 #pragma unroll
-      for (int c = 0; c < 9; ++c) B[6 * ns + c * nel + le] = Q[c];
+      for (int c = 0; c < 9; ++c) O[6 * ns + c * nel + le] = Q[c];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) B[6 * ns + (9 + c) * nel + le] = w[c];
+      for (int c = 0; c < 3; ++c) O[6 * ns + (9 + c) * nel + le] = w[c];
     }
     fence_proxy_async();  // this thread's generic smem writes -> visible to the async proxy
     __syncthreads();
     if (tid == 0) {
-      bulk_s2g(p.state + boff, B, 8u * (uint32_t)(6 * ns + 12 * nel));
+      bulk_s2g(p.state + boff, O, 8u * (uint32_t)(6 * ns + 12 * nel));
       bulk_commit();
     }
     if (tr) tr[3] = gtimer() & ((1ull << 48) - 1);
@@ -631,7 +641,10 @@ __global__ void __launch_bounds__(BLOCK) diag_kernel(const ErStepParams p) {
     if (p.has_kappa0) for (int c = 0; c < 3; ++c) k0[c] = G[tile_vor_plane(T, c) + (s - 2 * si.q - 1)];
     if (si.fl & FL_ACT) {
       const double sk = general ? gp(GP_SK) : i * rec[REC_LHAT];
-      k0[p.act_comp] += rec[REC_ACTA] * sinpi(2.0 * (sk * rec[REC_ACTIL] - rec[REC_ACTF] * p.t));
+      const double act = rec[REC_ACTA] * sinpi(2.0 * (sk * rec[REC_ACTIL] - rec[REC_ACTF] * p.t));
+      k0[0] += p.act_comp == 0 ? act : 0.0;
+      k0[1] += p.act_comp == 1 ? act : 0.0;
+      k0[2] += p.act_comp == 2 ? act : 0.0;
     }
     for (int c = 0; c < 3; ++c) {
       const double Bv = general ? gp(GP_BV1 + c) : rec[REC_B1 + c];
