@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-temporal", action="store_true")
     ap.add_argument("--cpu-sample-rods", type=int, default=8192)
     ap.add_argument("--cpu-sample-steps", type=int, default=300)
     return ap.parse_args()
@@ -254,6 +255,27 @@ def main():
                         f"{a.steps_per_launch} steps, so 'achieved' counts B_min per step and can exceed the "
                         "HBM peak; the binding resource is the FP64 pipe")
 
+    # NEXT-1 context: the same job with the rod tile kept on chip for several steps per launch
+    # (temporal blocking; bitwise-identical results), timed the same way on the same batch
+    temporal = None
+    if a.steps_per_launch == 1 and not a.no_temporal:
+        spl = 100
+        b.set_option(er.ER_OPT_STEPS_PER_LAUNCH, spl)
+        b.step(spl, dt)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        b.step(a.steps, dt)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        tms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=f"cuda:{local}")
+        if world > 1:
+            dist.all_reduce(tms, op=dist.ReduceOp.MAX)
+        b.set_option(er.ER_OPT_STEPS_PER_LAUNCH, 1)
+        temporal = {"steps_per_launch": spl, "ms_per_step": float(tms.item()) / a.steps,
+                    "value": float(el_total.item()) * a.steps / (float(tms.item()) * 1e-3),
+                    "note": "SURVEY NEXT-1: state crosses HBM once per launch; FP64/issue-bound"}
+
     # end-to-end through the public API with HOST buffers (pinned): create from host, K steps,
     # state back to host; the H2D/D2H bytes are amortised over the K steps of the job
     e2e = None
@@ -285,6 +307,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
+            "temporal_blocking": temporal,
             "clocks": clk.summary(),
             "diagnostics": {k: float(v) for k, v in zip(er.DIAG_NAMES, diag.cpu().numpy())},
         }
