@@ -133,8 +133,9 @@ er_status er_set_bc(er_batch *b, const int8_t *clamp_end);
  *                  kappa0_k[act_component] += A sin(2 pi (s_k/L - f t)), s_k = arc length of
  *                  interior node k, evaluated at t_n + h/2 (DESIGN §3 #13, #14).
  *  magnetization   [n_elems_total*3] local magnetic moment per unit rest length m, or NULL;
- *                  element couple c_j = lhat_j m_j x (Q_j b(t)) with
- *                  b(t) = Rz(b_omega t) b_field (a field rotating in the lab x-y plane).
+ *                  element couple c_j = lhat_j m_j x (Q_j b(t)) with b(t) = b_field rotated by
+ *                  the angle b_omega t about b_axis (right-handed; b_axis = 0 means lab z):
+ *                  a homogeneous field rotating in the plane normal to b_axis.
  * Replaces all previous forcing.  Default after create: none.   Errors: ER_EINVAL.
  */
 typedef struct {
@@ -147,6 +148,7 @@ typedef struct {
   const double *magnetization;
   double b_field[3];
   double b_omega;
+  double b_axis[3];
 } er_forcing;
 
 er_status er_set_forcing(er_batch *b, const er_forcing *f);

@@ -47,7 +47,7 @@ class _Problem(C.Structure):
         ("rest_kappa", _dp), ("clamp", _bp), ("gravity", C.c_double * 3), ("damping", _dp),
         ("tip_force", _dp), ("act_A", _dp), ("act_f", _dp), ("act_L", _dp),
         ("act_component", C.c_int32), ("magnetization", _dp), ("b_field", C.c_double * 3),
-        ("b_omega", C.c_double),
+        ("b_omega", C.c_double), ("b_axis", C.c_double * 3),
     ]
 
 
@@ -113,6 +113,8 @@ class Problem:
         b = w.b_field if w.b_field is not None else np.zeros(3)
         p.b_field = (C.c_double * 3)(*[float(x) for x in b])
         p.b_omega = float(w.b_omega)
+        ax = w.b_axis if getattr(w, "b_axis", None) is not None else np.zeros(3)
+        p.b_axis = (C.c_double * 3)(*[float(x) for x in ax])
         self.c = p
 
 

@@ -225,12 +225,19 @@ static void rest_kappa_at(const orc_problem *P, int32_t rod, const rod_ctx *c, i
   }
 }
 
+/* b(t): b(0) rotated by the angle b_omega t about the unit axis a (Rodrigues' rotation formula,
+ * right-handed): b = b0 cos + (a x b0) sin + a (a . b0)(1 - cos).  a = 0 means the lab z axis. */
 static void b_field_at(const orc_problem *P, double t, double *b) {
+  double a[3] = {P->b_axis[0], P->b_axis[1], P->b_axis[2]};
+  double na = sqrt(v_dot(a, a));
+  if (na == 0.0) { a[0] = 0.0; a[1] = 0.0; a[2] = 1.0; na = 1.0; }
+  for (int q = 0; q < 3; ++q) a[q] /= na;
   double ph = P->b_omega * t;
   double cs = cos(ph), sn = sin(ph);
-  b[0] = cs * P->b_field[0] - sn * P->b_field[1];
-  b[1] = sn * P->b_field[0] + cs * P->b_field[1];
-  b[2] = P->b_field[2];
+  double axb[3];
+  v_cross(a, P->b_field, axb);
+  double ad = v_dot(a, P->b_field);
+  for (int q = 0; q < 3; ++q) b[q] = P->b_field[q] * cs + axb[q] * sn + a[q] * ad * (1.0 - cs);
 }
 
 /* ---------------------------------------------------------------- strains (C.3 steps 2-3) */

@@ -37,7 +37,8 @@ typedef struct {
   int32_t act_component;           /* 0,1,2: which local component of kappa0            */
   const double *magnetization;     /* [E*3] local m̄ per unit rest length, or NULL      */
   double b_field[3];               /* b(0) lab                                          */
-  double b_omega;                  /* b(t) = Rz(b_omega t) b(0)                          */
+  double b_omega;                  /* b(t) = R_axis(b_omega t) b(0)                      */
+  double b_axis[3];                /* rotation axis of b(t) (normalised here), 0 = lab z */
 } orc_problem;
 
 enum { ORC_OK = 0, ORC_EINVAL = 1, ORC_EUNSTABLE = 2 };

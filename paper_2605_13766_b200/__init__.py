@@ -51,7 +51,7 @@ class er_forcing(C.Structure):
         ("gravity", C.c_double * 3), ("damping", _dp), ("damping_all", C.c_double),
         ("tip_force", _dp), ("act_A", _dp), ("act_f", _dp), ("act_L", _dp),
         ("act_component", C.c_int32), ("magnetization", _dp), ("b_field", C.c_double * 3),
-        ("b_omega", C.c_double),
+        ("b_omega", C.c_double), ("b_axis", C.c_double * 3),
     ]
 
 
@@ -254,7 +254,7 @@ class RodBatch:
 
     def set_forcing(self, gravity=(0, 0, 0), damping=None, damping_all=0.0, tip_force=None,
                     act_A=None, act_f=None, act_L=None, act_component=0, magnetization=None,
-                    b_field=(0, 0, 0), b_omega=0.0):
+                    b_field=(0, 0, 0), b_omega=0.0, b_axis=(0, 0, 0)):
         k = _Keep()
         f = er_forcing()
         f.gravity = (C.c_double * 3)(*[float(x) for x in gravity])
@@ -266,6 +266,7 @@ class RodBatch:
         f.magnetization = k.host(magnetization)
         f.b_field = (C.c_double * 3)(*[float(x) for x in (b_field if b_field is not None else (0, 0, 0))])
         f.b_omega = float(b_omega)
+        f.b_axis = (C.c_double * 3)(*[float(x) for x in (b_axis if b_axis is not None else (0, 0, 0))])
         er_set_forcing(self.handle, f)
 
     def set_forcing_from(self, w):
@@ -274,7 +275,8 @@ class RodBatch:
                          act_f=getattr(w, "act_f", None), act_L=getattr(w, "act_L", None),
                          act_component=getattr(w, "act_component", 0),
                          magnetization=getattr(w, "magnetization", None),
-                         b_field=getattr(w, "b_field", None), b_omega=getattr(w, "b_omega", 0.0))
+                         b_field=getattr(w, "b_field", None), b_omega=getattr(w, "b_omega", 0.0),
+                         b_axis=getattr(w, "b_axis", None))
 
     # -- stepping / state
     def step(self, n_steps: int, dt: float):

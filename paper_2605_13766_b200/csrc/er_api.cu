@@ -85,7 +85,7 @@ struct er_batch {
   std::vector<double> rec;
   std::vector<int32_t> flags;
   double g[3] = {0, 0, 0};
-  double b0[3] = {0, 0, 0};
+  double b0[3] = {0, 0, 0}, b1[3] = {0, 0, 0}, b2[3] = {0, 0, 0};  // b(t) = b0 cos + b1 sin + b2
   double b_omega = 0.0;
   int act_comp = 0;
   int64_t fault_rod = -1;
@@ -133,7 +133,7 @@ ErStepParams params_of(const er_batch *b) {
   p.rec = b->d_rec; p.eoff = b->d_eoff; p.tiles = b->d_tiles; p.n_tiles = b->n_tiles;
   p.gpar = b->d_gpar; p.ng = b->ng; p.sigma0 = b->d_sigma0; p.mag = b->d_mag; p.ne = b->ne;
   p.has_kappa0 = b->has_kappa0 ? 1 : 0;
-  for (int c = 0; c < 3; ++c) { p.g[c] = b->g[c]; p.b0[c] = b->b0[c]; }
+  for (int c = 0; c < 3; ++c) { p.g[c] = b->g[c]; p.b0[c] = b->b0[c]; p.b1[c] = b->b1[c]; p.b2[c] = b->b2[c]; }
   p.b_omega = b->b_omega; p.act_comp = b->act_comp;
   p.fault = b->d_fault; p.diag_partial = b->d_diag_partial;
   p.trace = b->trace;
@@ -505,6 +505,7 @@ er_status er_set_forcing(er_batch *b, const er_forcing *f) {
   for (int c = 0; c < 3; ++c) {
     if (!std::isfinite(f->gravity[c])) err.add("gravity[%d] not finite", c);
     if (!std::isfinite(f->b_field[c])) err.add("b_field[%d] not finite", c);
+    if (!std::isfinite(f->b_axis[c])) err.add("b_axis[%d] not finite", c);
   }
   if (!std::isfinite(f->b_omega)) err.add("b_omega not finite");
   if (f->damping) {
@@ -529,7 +530,22 @@ er_status er_set_forcing(er_batch *b, const er_forcing *f) {
       if (!std::isfinite(f->magnetization[k])) { err.add("magnetization[%lld] not finite", (long long)k); break; }
   if (err.count) { b->last_error = err.msg; return ER_EINVAL; }
 
-  for (int c = 0; c < 3; ++c) { b->g[c] = f->gravity[c]; b->b0[c] = f->b_field[c]; }
+  {
+    // b(t) = R_axis(w t) b_field = bp cos + (a x b_field) sin + a (a . b_field), bp = b_field - a (a . b_field)
+    double ax[3] = {f->b_axis[0], f->b_axis[1], f->b_axis[2]};
+    double na = std::sqrt(ax[0] * ax[0] + ax[1] * ax[1] + ax[2] * ax[2]);
+    if (na == 0.0) { ax[0] = 0.0; ax[1] = 0.0; ax[2] = 1.0; na = 1.0; }
+    for (int c = 0; c < 3; ++c) ax[c] /= na;
+    const double *bf = f->b_field;
+    const double ad = ax[0] * bf[0] + ax[1] * bf[1] + ax[2] * bf[2];
+    const double axb[3] = {ax[1] * bf[2] - ax[2] * bf[1], ax[2] * bf[0] - ax[0] * bf[2], ax[0] * bf[1] - ax[1] * bf[0]};
+    for (int c = 0; c < 3; ++c) {
+      b->g[c] = f->gravity[c];
+      b->b2[c] = ax[c] * ad;
+      b->b0[c] = bf[c] - b->b2[c];
+      b->b1[c] = axb[c];
+    }
+  }
   b->b_omega = f->b_omega;
   b->act_comp = act ? f->act_component : 0;
   b->has_act = act;

@@ -216,7 +216,8 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
       if (EXTRA && p.mag) {  // c_mag = lhat m x (Q b(t))
         double sn, cs;
         sincos(p.b_omega * t_half, &sn, &cs);
-        const double b[3] = {cs * p.b0[0] - sn * p.b0[1], sn * p.b0[0] + cs * p.b0[1], p.b0[2]};
+        const double b[3] = {fma(cs, p.b0[0], fma(sn, p.b1[0], p.b2[0])), fma(cs, p.b0[1], fma(sn, p.b1[1], p.b2[1])),
+                             fma(cs, p.b0[2], fma(sn, p.b1[2], p.b2[2]))};
         const double Qb[3] = {dot3(Q, b), dot3(Q + 3, b), dot3(Q + 6, b)};
         double m[3];
 #pragma unroll

@@ -104,7 +104,9 @@ struct ErStepParams {
   int32_t has_kappa0;     // static kappa0 planes present in the tile blocks
   int32_t act_comp;
   double g[3];
-  double b0[3];
+  double b0[3];           // b(t) = b0 cos(b_omega t) + b1 sin(b_omega t) + b2
+  double b1[3];
+  double b2[3];
   double b_omega;
   int32_t n_steps;        // steps in this launch
   int32_t pad_;

@@ -324,3 +324,29 @@ def test_resume_from_snapshot_bitwise(er):
     rest, _ = run_gpu(er, w2, 25)
     for x, y in zip(full, rest):
         assert np.array_equal(x, y)
+
+
+# ----------------------------------------------------------------------------- NEXT-2 cilia
+@pytest.mark.parametrize("n_steps,tol", [(1, TOL_1STEP), (1000, TOL_1000)])
+def test_cilia_carpet_parity(er, orc, n_steps, tol):
+    w = W.make("cilia8")
+    g, tg = run_gpu(er, w, n_steps)
+    o, to = run_orc(orc, w, n_steps)
+    assert tg == to
+    assert_parity(w, g, o, tol, raw=("r", "Q"), label=f"cilia8 x{n_steps}")
+
+
+def test_cilia_farm_sampled(er, orc):
+    """111,797 magnetic cilia on the GPU; a seeded sample re-run by the oracle."""
+    w = W.make("ciliafarm")
+    with er.RodBatch(w) as b:
+        b.step(200, w.dt)
+        pos, vel, dirs, om, t = b.get_state()
+    rods = W.sample_rods(w, 32, seed=5)
+    ws = w.subset(rods)
+    no, eo = w.node_offsets(), w.elem_offsets()
+    nidx = np.concatenate([np.arange(no[r], no[r + 1]) for r in rods])
+    eidx = np.concatenate([np.arange(eo[r], eo[r + 1]) for r in rods])
+    o, to = run_orc(orc, ws, 200)
+    assert t == to
+    assert_parity(ws, (pos[nidx], vel[nidx], dirs[eidx], om[eidx]), o, TOL_1000, raw=("r", "Q"), label="farm")

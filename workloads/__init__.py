@@ -68,7 +68,8 @@ class Workload:
     # magnetic couple (NEXT-2): per-element m̄ (local) and field b(t)
     magnetization: Optional[np.ndarray] = None  # f64 [E, 3]
     b_field: Optional[np.ndarray] = None        # f64 [3] amplitude (lab)
-    b_omega: float = 0.0                        # rad/s (rotating field in x-y plane), 0 = constant
+    b_omega: float = 0.0                        # rad/s, b(t) = R_axis(b_omega t) b_field
+    b_axis: Optional[np.ndarray] = None         # f64 [3] rotation axis of b(t); None = lab z
 
     # ---- layout helpers (integer bookkeeping only) ----
     @property
@@ -216,9 +217,18 @@ def _rod_material(R, radius, E, rho=1000.0, alpha_c=4.0 / 3.0):
 # the five configs (BASELINE.json configs[0..4])
 # ---------------------------------------------------------------------------
 
+EXTRA_CONFIGS = ("cilia8", "ciliafarm")
+
+
 def make(name: str, n_rods: Optional[int] = None, n_steps: Optional[int] = None) -> Workload:
-    """Build config `name` ("cfg1".."cfg5").  `n_rods` shrinks the batch (a different
-    seeded draw of the same recipe); use `.subset()` to sample rods of the full draw."""
+    """Build config `name` ("cfg1".."cfg5", or the NEXT-2 cilia workloads).  `n_rods` shrinks
+    the batch (a different seeded draw of the same recipe); use `.subset()` to sample rods of the
+    full draw."""
+    if name in EXTRA_CONFIGS:
+        w = _cilia(name, n_rods)
+        if n_steps is not None:
+            w.n_steps = int(n_steps)
+        return w
     k = CONFIG_NAMES.index(name) + 1
     rng = np.random.Generator(np.random.Philox(SEED_BASE + k))
     fn = {1: _cfg1, 2: _cfg2, 3: _cfg3, 4: _cfg4, 5: _cfg5}[k]
@@ -347,3 +357,44 @@ def sample_rods(w: Workload, k: int, seed: int = 0) -> np.ndarray:
     rng = np.random.Generator(np.random.Philox(SEED_BASE + 1000 + seed))
     mid = rng.choice(np.arange(1, R - 1), size=max(k - 2, 0), replace=False)
     return np.sort(np.concatenate([[0], mid, [R - 1]]))
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2: magnetic cilia.  Not a BASELINE config; parameters are
+# a synthetic stand-in (the paper's cilia parameters live in its missing supplement).
+# ---------------------------------------------------------------------------
+CILIA = dict(N=20, L=0.01, radius=5e-4, E=1e5, rho=1000.0, spacing=3e-3, b=0.02,
+             theta_lin=0.1, beat_hz=10.0, wavelength_cols=8, damping=50.0, dt=2e-5)
+
+
+def _cilia(name, n_rods):
+    """Clamped (s = 0) cilia standing along +z on a square grid; magnetisation per unit length
+    of magnitude m (set so the quasi-static tip angle m b L^2 / (2 E I) is theta_lin) at an angle
+    psi = 2 pi ix / wavelength_cols from d3 towards d1 (a programmed metachronal phase);
+    homogeneous field b(t) = b (cos, 0, -sin)(2 pi f t) rotating about lab y."""
+    c = CILIA
+    if name == "cilia8":
+        nx = ny = 8
+    else:
+        nx, ny = 335, 334          # 111,890 sites; the first 111,797 are used (PAPER.md:164)
+    R_full = 111797 if name == "ciliafarm" else nx * ny
+    R = R_full if n_rods is None else int(n_rods)
+    N = c["N"]
+    ids = np.arange(R)
+    ix, iy = ids % nx, ids // nx
+    n_elems = np.full(R, N, np.int32)
+    lhat = np.full(R, c["L"] / N)
+    mat = _rod_material(R, c["radius"], c["E"], rho=c["rho"])
+    base = np.stack([ix * c["spacing"], iy * c["spacing"], np.zeros(R)], axis=1)
+    d3 = np.tile([0.0, 0.0, 1.0], (R, 1))
+    pos = straight_rods(n_elems, lhat, base, d3)
+    EI = c["E"] * mat["I1"][0]
+    m = c["theta_lin"] * 2.0 * EI / (c["b"] * c["L"] ** 2)
+    psi = 2.0 * math.pi * ix / c["wavelength_cols"]
+    mag_rod = np.stack([m * np.sin(psi), np.zeros(R), m * np.cos(psi)], axis=1)
+    return Workload(name, n_elems, _expand(lhat, n_elems), **mat, positions=pos,
+                    velocities=np.zeros_like(pos), directors=np.tile(np.eye(3), (R * N, 1, 1)),
+                    omega=np.zeros((R * N, 3)), clamp=np.zeros(R, np.int8), gravity=np.zeros(3),
+                    damping=np.full(R, c["damping"]), magnetization=_expand(mag_rod, n_elems),
+                    b_field=np.array([c["b"], 0.0, 0.0]), b_omega=2.0 * math.pi * c["beat_hz"],
+                    b_axis=np.array([0.0, 1.0, 0.0]), dt=c["dt"], n_steps=20000)
