@@ -136,6 +136,11 @@ er_status er_set_bc(er_batch *b, const int8_t *clamp_end);
  *                  element couple c_j = lhat_j m_j x (Q_j b(t)) with b(t) = b_field rotated by
  *                  the angle b_omega t about b_axis (right-handed; b_axis = 0 means lab z):
  *                  a homogeneous field rotating in the plane normal to b_axis.
+ *  musc_A, musc_T, musc_lambda, musc_phi  [n_rods] each, or all NULL: muscular torque wave
+ *                  (DESIGN §3 #26) tau_k(t) = A sin(2 pi (t/T - s_k/lambda) + phi)
+ *                  about the local axis musc_component at every interior node k, applied as a
+ *                  couple pair (+tau_k on element k, -tau_k on element k-1: net zero per rod),
+ *                  evaluated at t_n + h/2.  T, lambda > 0.
  * Replaces all previous forcing.  Default after create: none.   Errors: ER_EINVAL.
  */
 typedef struct {
@@ -149,6 +154,8 @@ typedef struct {
   double b_field[3];
   double b_omega;
   double b_axis[3];
+  const double *musc_A, *musc_T, *musc_lambda, *musc_phi;
+  int32_t musc_component;
 } er_forcing;
 
 er_status er_set_forcing(er_batch *b, const er_forcing *f);

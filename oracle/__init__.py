@@ -48,6 +48,7 @@ class _Problem(C.Structure):
         ("tip_force", _dp), ("act_A", _dp), ("act_f", _dp), ("act_L", _dp),
         ("act_component", C.c_int32), ("magnetization", _dp), ("b_field", C.c_double * 3),
         ("b_omega", C.c_double), ("b_axis", C.c_double * 3),
+        ("musc_A", _dp), ("musc_T", _dp), ("musc_lambda", _dp), ("musc_phi", _dp), ("musc_component", C.c_int32),
     ]
 
 
@@ -105,8 +106,8 @@ class Problem:
         p.material_per_rod = 1 if per_rod else 0
         for name in ("density", "area", "I1", "I2", "youngs", "shear_mod", "alpha_c", "rest_lengths",
                      "rest_sigma", "rest_kappa", "damping", "tip_force", "act_A", "act_f", "act_L",
-                     "magnetization"):
-            setattr(p, name, _ptr(k(getattr(w, name))))
+                     "magnetization", "musc_A", "musc_T", "musc_lambda", "musc_phi"):
+            setattr(p, name, _ptr(k(getattr(w, name, None))))
         p.clamp = _ptr(k(w.clamp, np.int8), _bp)
         p.gravity = (C.c_double * 3)(*[float(x) for x in w.gravity])
         p.act_component = int(w.act_component)
@@ -115,6 +116,7 @@ class Problem:
         p.b_omega = float(w.b_omega)
         ax = w.b_axis if getattr(w, "b_axis", None) is not None else np.zeros(3)
         p.b_axis = (C.c_double * 3)(*[float(x) for x in ax])
+        p.musc_component = int(getattr(w, "musc_component", 0))
         self.c = p
 
 

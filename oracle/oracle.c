@@ -227,6 +227,16 @@ static void rest_kappa_at(const orc_problem *P, int32_t rod, const rod_ctx *c, i
 
 /* b(t): b(0) rotated by the angle b_omega t about the unit axis a (Rodrigues' rotation formula,
  * right-handed): b = b0 cos + (a x b0) sin + a (a . b0)(1 - cos).  a = 0 means the lab z axis. */
+/* Muscular torque at interior node k ("internal (net-zero) muscular torques as a
+ * traveling wave with period T and wavelength L"; reading DESIGN §3 #26):
+ * tau_k(t) = A sin(2 pi (t/T - s_k/lambda) + phi0) about local axis `musc_component`,
+ * s_k = sum_{j<k} lhat_j.  Applied as a couple pair: +tau_k on element k, -tau_k on element k-1. */
+static double muscle_tau(const orc_problem *P, int32_t rod, const rod_ctx *c, int32_t k, double t) {
+  double s = 0.0;
+  for (int32_t j = 0; j < k; ++j) s += c->lhat[j];
+  return P->musc_A[rod] * sin(2.0 * PI * (t / P->musc_T[rod] - s / P->musc_lambda[rod]) + P->musc_phi[rod]);
+}
+
 static void b_field_at(const orc_problem *P, double t, double *b) {
   double a[3] = {P->b_axis[0], P->b_axis[1], P->b_axis[2]};
   double na = sqrt(v_dot(a, a));
@@ -353,6 +363,10 @@ static int rod_dynamics(const orc_problem *P, int32_t rod, rod_ctx *c, const dou
     v_cross(tmp, w + 3 * j, tmp);
     for (int q = 0; q < 3; ++q) Cj[q] += tmp[q];
     for (int q = 0; q < 3; ++q) Cj[q] += Jw[q] / (c->e[j] * c->e[j]) * c->edot[j];  /* unsteady dilatation */
+    if (P->musc_A) {                                        /* muscular couple pair */
+      if (j >= 1) Cj[P->musc_component] += muscle_tau(P, rod, c, j, t);
+      if (j + 1 <= N - 1) Cj[P->musc_component] -= muscle_tau(P, rod, c, j + 1, t);
+    }
     if (P->magnetization) {                                 /* c_mag = m x (Q b(t)) */
       double Qb[3], mb[3];
       m_vec(Q + 9 * j, b, Qb);

@@ -39,6 +39,8 @@ typedef struct {
   double b_field[3];               /* b(0) lab                                          */
   double b_omega;                  /* b(t) = R_axis(b_omega t) b(0)                      */
   double b_axis[3];                /* rotation axis of b(t) (normalised here), 0 = lab z */
+  const double *musc_A, *musc_T, *musc_lambda, *musc_phi; /* [R] muscular torque wave, or NULL */
+  int32_t musc_component;          /* local axis of the muscle couple (0 = d1)           */
 } orc_problem;
 
 enum { ORC_OK = 0, ORC_EINVAL = 1, ORC_EUNSTABLE = 2 };

@@ -52,6 +52,7 @@ class er_forcing(C.Structure):
         ("tip_force", _dp), ("act_A", _dp), ("act_f", _dp), ("act_L", _dp),
         ("act_component", C.c_int32), ("magnetization", _dp), ("b_field", C.c_double * 3),
         ("b_omega", C.c_double), ("b_axis", C.c_double * 3),
+        ("musc_A", _dp), ("musc_T", _dp), ("musc_lambda", _dp), ("musc_phi", _dp), ("musc_component", C.c_int32),
     ]
 
 
@@ -254,7 +255,8 @@ class RodBatch:
 
     def set_forcing(self, gravity=(0, 0, 0), damping=None, damping_all=0.0, tip_force=None,
                     act_A=None, act_f=None, act_L=None, act_component=0, magnetization=None,
-                    b_field=(0, 0, 0), b_omega=0.0, b_axis=(0, 0, 0)):
+                    b_field=(0, 0, 0), b_omega=0.0, b_axis=(0, 0, 0), musc_A=None, musc_T=None,
+                    musc_lambda=None, musc_phi=None, musc_component=0):
         k = _Keep()
         f = er_forcing()
         f.gravity = (C.c_double * 3)(*[float(x) for x in gravity])
@@ -267,6 +269,9 @@ class RodBatch:
         f.b_field = (C.c_double * 3)(*[float(x) for x in (b_field if b_field is not None else (0, 0, 0))])
         f.b_omega = float(b_omega)
         f.b_axis = (C.c_double * 3)(*[float(x) for x in (b_axis if b_axis is not None else (0, 0, 0))])
+        f.musc_A, f.musc_T = k.host(musc_A), k.host(musc_T)
+        f.musc_lambda, f.musc_phi = k.host(musc_lambda), k.host(musc_phi)
+        f.musc_component = int(musc_component)
         er_set_forcing(self.handle, f)
 
     def set_forcing_from(self, w):
@@ -276,7 +281,9 @@ class RodBatch:
                          act_component=getattr(w, "act_component", 0),
                          magnetization=getattr(w, "magnetization", None),
                          b_field=getattr(w, "b_field", None), b_omega=getattr(w, "b_omega", 0.0),
-                         b_axis=getattr(w, "b_axis", None))
+                         b_axis=getattr(w, "b_axis", None), musc_A=getattr(w, "musc_A", None),
+                         musc_T=getattr(w, "musc_T", None), musc_lambda=getattr(w, "musc_lambda", None),
+                         musc_phi=getattr(w, "musc_phi", None), musc_component=getattr(w, "musc_component", 0))
 
     # -- stepping / state
     def step(self, n_steps: int, dt: float):

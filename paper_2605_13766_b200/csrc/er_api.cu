@@ -74,11 +74,12 @@ struct er_batch {
   double *d_rec = nullptr;
   int64_t *d_eoff = nullptr;
   ErTile *d_tiles = nullptr;
-  double *d_gpar = nullptr, *d_sigma0 = nullptr, *d_mag = nullptr;
+  double *d_gpar = nullptr, *d_sigma0 = nullptr, *d_mag = nullptr, *d_musc = nullptr;
   unsigned long long *d_fault = nullptr;
   unsigned long long *trace = nullptr;  // caller-owned, optional
   double *d_diag_partial = nullptr, *d_diag_out = nullptr, *d_valid = nullptr;
-  bool has_kappa0 = false, any_general = false, has_sigma0 = false, has_act = false;
+  bool has_kappa0 = false, any_general = false, has_sigma0 = false, has_act = false, has_musc = false;
+  int musc_comp = 0;
   // host mirrors
   std::vector<int32_t> n_elems_h;
   std::vector<int64_t> eoff;
@@ -117,7 +118,7 @@ cudaError_t dalloc(er_batch *b, T **p, int64_t count) {
 }
 
 void free_all(er_batch *b) {
-  void *ptrs[] = {b->d_state, b->d_rec, b->d_eoff, b->d_tiles, b->d_gpar, b->d_sigma0, b->d_mag,
+  void *ptrs[] = {b->d_state, b->d_rec, b->d_eoff, b->d_tiles, b->d_gpar, b->d_sigma0, b->d_mag, b->d_musc,
                   b->d_fault, b->d_diag_partial, b->d_diag_out, b->d_valid};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -132,6 +133,8 @@ ErStepParams params_of(const er_batch *b) {
   p.state = b->d_state;
   p.rec = b->d_rec; p.eoff = b->d_eoff; p.tiles = b->d_tiles; p.n_tiles = b->n_tiles;
   p.gpar = b->d_gpar; p.ng = b->ng; p.sigma0 = b->d_sigma0; p.mag = b->d_mag; p.ne = b->ne;
+  p.musc = b->has_musc ? b->d_musc : nullptr;
+  p.musc_comp = b->musc_comp;
   p.has_kappa0 = b->has_kappa0 ? 1 : 0;
   for (int c = 0; c < 3; ++c) { p.g[c] = b->g[c]; p.b0[c] = b->b0[c]; p.b1[c] = b->b1[c]; p.b2[c] = b->b2[c]; }
   p.b_omega = b->b_omega; p.act_comp = b->act_comp;
@@ -235,7 +238,7 @@ int feat_of(const er_batch *b) {
   int f = 0;
   if (b->any_general) f |= FEAT_GENERAL;
   if (b->has_kappa0) f |= FEAT_KAPPA0;
-  if (b->has_sigma0 || b->d_mag || b->has_act) f |= FEAT_EXTRA;
+  if (b->has_sigma0 || b->d_mag || b->has_act || b->has_musc) f |= FEAT_EXTRA;
   return f;
 }
 
@@ -525,6 +528,16 @@ er_status er_set_forcing(er_batch *b, const er_forcing *f) {
       }
     if (f->act_component < 0 || f->act_component > 2) err.add("act_component = %d not in {0,1,2}", f->act_component);
   }
+  const bool musc = f->musc_A || f->musc_T || f->musc_lambda || f->musc_phi;
+  if (musc) {
+    if (!(f->musc_A && f->musc_T && f->musc_lambda && f->musc_phi)) err.add("musc_A, musc_T, musc_lambda and musc_phi must be all set or all NULL");
+    else
+      for (int64_t r = 0; r < R; ++r) {
+        if (!std::isfinite(f->musc_A[r]) || !std::isfinite(f->musc_phi[r])) { err.add("musc_A/musc_phi[%lld] not finite", (long long)r); break; }
+        if (!pos_finite(f->musc_T[r]) || !pos_finite(f->musc_lambda[r])) { err.add("musc_T/musc_lambda[%lld] must be positive", (long long)r); break; }
+      }
+    if (f->musc_component < 0 || f->musc_component > 2) err.add("musc_component = %d not in {0,1,2}", f->musc_component);
+  }
   if (f->magnetization)
     for (int64_t k = 0; k < 3 * b->n_elems; ++k)
       if (!std::isfinite(f->magnetization[k])) { err.add("magnetization[%lld] not finite", (long long)k); break; }
@@ -559,10 +572,26 @@ er_status er_set_forcing(er_batch *b, const er_forcing *f) {
     rec[REC_ACTF] = act ? f->act_f[r] : 0.0;
     rec[REC_ACTIL] = act ? 1.0 / f->act_L[r] : 0.0;
     if (act) b->flags[r] |= FL_ACT;
+    b->flags[r] &= ~FL_MUS;
+    if (musc) b->flags[r] |= FL_MUS;
   }
+  b->has_musc = musc;
+  b->musc_comp = musc ? f->musc_component : 0;
   CK(cudaSetDevice(b->device), "cudaSetDevice");
   er_status st = upload_records(b);
   if (st != ER_OK) return st;
+  if (musc && R > 0) {
+    std::vector<double> mh((size_t)R * 4);
+    for (int64_t r = 0; r < R; ++r) {
+      mh[4 * r + 0] = f->musc_A[r];
+      mh[4 * r + 1] = 1.0 / f->musc_T[r];
+      mh[4 * r + 2] = 1.0 / f->musc_lambda[r];
+      mh[4 * r + 3] = f->musc_phi[r] / 3.14159265358979323846;
+    }
+    if (!b->d_musc) CK(dalloc(b, &b->d_musc, 4 * R), "cudaMalloc(musc)");
+    CK(cudaMemcpyAsync(b->d_musc, mh.data(), sizeof(double) * mh.size(), cudaMemcpyHostToDevice, b->stream), "H2D musc");
+    CK(cudaStreamSynchronize(b->stream), "sync");
+  }
   if (f->magnetization && b->n_elems > 0) {
     if (!b->d_mag) CK(dalloc(b, &b->d_mag, 3 * b->ne), "cudaMalloc(mag)");
     if ((st = upload_side_planes(b, f->magnetization, b->d_mag, b->n_elems, b->ne)) != ER_OK) return st;

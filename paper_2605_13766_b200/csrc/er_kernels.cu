@@ -179,6 +179,16 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
       be[0] = (kap[1] * mb[2] - kap[2] * mb[1]) * Dh;
       be[1] = (kap[2] * mb[0] - kap[0] * mb[2]) * Dh;
       be[2] = (kap[0] * mb[1] - kap[1] * mb[0]) * Dh;
+      if (EXTRA && (si.fl & FL_MUS)) {
+        // muscular couple pair (+tau_k on element k, -tau_k on element k-1) folded into the
+        // exchanged moment: C_j += (mb - tau)_{j+1} - (mb - tau)_j; beta keeps the elastic mb
+        const double *mu = p.musc + 4 * (int64_t)si.rod;
+        const double sk = general ? gp(GP_SK) : i * rec[REC_LHAT];
+        const double tau = __ldg(mu) * sinpi(fma(2.0, fma(t_half, __ldg(mu + 1), -sk * __ldg(mu + 2)), __ldg(mu + 3)));
+        mb[0] -= p.musc_comp == 0 ? tau : 0.0;
+        mb[1] -= p.musc_comp == 1 ? tau : 0.0;
+        mb[2] -= p.musc_comp == 2 ? tau : 0.0;
+      }
     }
     // ---- A7 + A9 node force, linear acceleration, kick
     if (si.active) {

@@ -66,6 +66,7 @@ enum {
   FL_GENERAL = 4,     // per-slot parameters from gpar
   FL_TIP = 8,         // tip force present
   FL_ACT = 16,        // rest-curvature actuation
+  FL_MUS = 32,        // muscular torque wave (side array `musc`)
 };
 
 // batch-level feature bits (kernel template parameter)
@@ -100,9 +101,12 @@ struct ErStepParams {
   int64_t ng;             // gpar plane stride
   const double *sigma0;   // may be null, planes stride ne
   const double *mag;      // may be null, planes stride ne
+  const double *musc;     // may be null: [n_rods][4] = A, 1/T, 1/lambda, phi/pi
   int64_t ne;
   int32_t has_kappa0;     // static kappa0 planes present in the tile blocks
   int32_t act_comp;
+  int32_t musc_comp;
+  int32_t pad2_;
   double g[3];
   double b0[3];           // b(t) = b0 cos(b_omega t) + b1 sin(b_omega t) + b2
   double b1[3];

@@ -51,7 +51,7 @@ def test_struct_layouts_match_header(er):
 #include "er.h"
 int main(void) {
   printf("%zu %zu %zu %zu %zu\n", sizeof(er_batch_desc), offsetof(er_batch_desc, t0), offsetof(er_batch_desc, stream), offsetof(er_batch_desc, omega), offsetof(er_batch_desc, tile_slots));
-  printf("%zu %zu %zu %zu\n", sizeof(er_forcing), offsetof(er_forcing, act_component), offsetof(er_forcing, b_omega), offsetof(er_forcing, b_axis));
+  printf("%zu %zu %zu %zu %zu\n", sizeof(er_forcing), offsetof(er_forcing, act_component), offsetof(er_forcing, b_omega), offsetof(er_forcing, b_axis), offsetof(er_forcing, musc_component));
   printf("%zu %zu %zu\n", sizeof(er_info), offsetof(er_info, stream), offsetof(er_info, bytes_per_step));
   return 0;
 }'''
@@ -67,7 +67,7 @@ int main(void) {
                  er.er_batch_desc.omega.offset, er.er_batch_desc.tile_slots.offset]
     b = [int(x) for x in lines[1].split()]
     assert b == [C.sizeof(er.er_forcing), er.er_forcing.act_component.offset, er.er_forcing.b_omega.offset,
-                 er.er_forcing.b_axis.offset]
+                 er.er_forcing.b_axis.offset, er.er_forcing.musc_component.offset]
     c = [int(x) for x in lines[2].split()]
     assert c == [C.sizeof(er.er_info), er.er_info.stream.offset, er.er_info.bytes_per_step.offset]
 

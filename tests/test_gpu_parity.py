@@ -242,10 +242,28 @@ def test_general_rods_parity(er, orc):
     w.act_component = 2
     w.magnetization = rng.standard_normal((E, 3)) * 1e-3
     w.b_field, w.b_omega = np.array([1e-2, 0.0, 5e-3]), 30.0
+    w.b_axis = np.array([0.3, 1.0, -0.2])
+    w.musc_A, w.musc_T = rng.uniform(1e-6, 1e-5, 4), rng.uniform(0.5, 2, 4)
+    w.musc_lambda, w.musc_phi = rng.uniform(0.1, 0.5, 4), rng.uniform(0, 6, 4)
+    w.musc_component = 1
     for n in (1, 200):
         g, _ = run_gpu(er, w, n)
         o, _ = run_orc(orc, w, n)
         assert_parity(w, g, o, TOL_1STEP if n == 1 else TOL_1000, raw=("r", "v", "Q", "w"), label=f"general x{n}")
+
+
+def test_muscle_wave_parity(er, orc):
+    """NEXT-3 muscular torque wave on uniform rods (couple pairs folded into the exchanged moment)."""
+    w = W.make("cfg4", n_rods=24)
+    R = w.n_rods
+    rng = np.random.default_rng(12)
+    w.act_A = w.act_f = w.act_L = None
+    w.musc_A, w.musc_T = rng.uniform(1e-5, 1e-4, R), rng.uniform(0.5, 2, R)
+    w.musc_lambda, w.musc_phi = rng.uniform(0.2, 1.0, R), rng.uniform(0, 6, R)
+    for n in (1, 1000):
+        g, _ = run_gpu(er, w, n)
+        o, _ = run_orc(orc, w, n)
+        assert_parity(w, g, o, TOL_1STEP if n == 1 else TOL_1000, raw=("r", "Q"), label=f"muscle x{n}")
 
 
 def test_fault_reports_rod(er):

@@ -70,6 +70,12 @@ class Workload:
     b_field: Optional[np.ndarray] = None        # f64 [3] amplitude (lab)
     b_omega: float = 0.0                        # rad/s, b(t) = R_axis(b_omega t) b_field
     b_axis: Optional[np.ndarray] = None         # f64 [3] rotation axis of b(t); None = lab z
+    # muscular torque wave (NEXT-3): tau = A sin(2 pi (t/T - s/lambda) + phi)
+    musc_A: Optional[np.ndarray] = None         # f64 [R]
+    musc_T: Optional[np.ndarray] = None         # f64 [R]
+    musc_lambda: Optional[np.ndarray] = None    # f64 [R]
+    musc_phi: Optional[np.ndarray] = None       # f64 [R]
+    musc_component: int = 0
 
     # ---- layout helpers (integer bookkeeping only) ----
     @property
@@ -131,6 +137,8 @@ class Workload:
             rest_sigma=gather(eo, self.rest_sigma), rest_kappa=gather(vo, self.rest_kappa),
             act_A=per_rod(self.act_A), act_f=per_rod(self.act_f), act_L=per_rod(self.act_L),
             magnetization=gather(eo, self.magnetization),
+            musc_A=per_rod(self.musc_A), musc_T=per_rod(self.musc_T),
+            musc_lambda=per_rod(self.musc_lambda), musc_phi=per_rod(self.musc_phi),
         )
 
     def copy_state(self):
