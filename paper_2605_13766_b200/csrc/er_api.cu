@@ -11,9 +11,11 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "er.h"
@@ -25,11 +27,29 @@ cudaError_t er_launch_diag(const ErStepParams *p, int block, double *out, cudaSt
 cudaError_t er_launch_canon_tiles(const ErStepParams *p, double *canon, int field, int to_tiles, cudaStream_t st);
 cudaError_t er_launch_aos_to_soa(const double *src, double *dst, int64_t n, int k, int64_t stride, cudaStream_t st);
 cudaError_t er_launch_validate(const double *aos, int64_t n, int k, int orth, double *out, cudaStream_t st);
+cudaError_t er_launch_apply_forcing(double *rec, int64_t n_rods, const int32_t *flags, const double *damping,
+                                    double damping_all, const double *tip, const double *actA, const double *actF,
+                                    const double *actL, int forcing, cudaStream_t st);
 }
+
+#include <chrono>
 
 namespace {
 
 thread_local std::string g_create_error;
+
+// Optional phase timing of er_create_batch (env ER_TIMING=1), printed to stderr.
+struct PhaseTimer {
+  bool on = std::getenv("ER_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char *what, cudaStream_t st = nullptr) {
+    if (!on) return;
+    if (st) cudaStreamSynchronize(st);
+    auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[er_create_batch] %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  }
+};
 
 int64_t pad_to(int64_t n, int64_t q) { return ((n + q - 1) / q) * q + q; }
 
@@ -250,6 +270,37 @@ er_status upload_records(er_batch *b) {
   return ER_OK;
 }
 
+// Upload the per-rod flags (and, with `forcing`, the caller's damping / tip / actuation arrays as
+// given) and let a kernel write those record fields -- no 192-byte records cross PCIe again.
+er_status apply_forcing(er_batch *b, const er_forcing *f, bool forcing) {
+  const int64_t R = b->n_rods;
+  if (R == 0) return ER_OK;
+  size_t n = (size_t)R;  // int32 flags, packed as doubles below
+  const bool damp = forcing && f->damping, tip = forcing && f->tip_force, act = forcing && f->act_A;
+  size_t total = (n + 1) / 2 + (damp ? n : 0) + (tip ? 3 * n : 0) + (act ? 3 * n : 0);
+  double *d = nullptr;
+  CK(cudaMallocAsync((void **)&d, sizeof(double) * (total + 4), b->stream), "cudaMallocAsync(forcing)");
+  double *p = d;
+  int32_t *dflags = reinterpret_cast<int32_t *>(p);
+  CK(cudaMemcpyAsync(dflags, b->flags.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, b->stream), "H2D flags");
+  p += (n + 1) / 2;
+  const double *ddamp = nullptr, *dtip = nullptr, *dA = nullptr, *dF = nullptr, *dL = nullptr;
+  auto up = [&](const double *src, size_t cnt) -> const double * {
+    double *q = p;
+    p += cnt;
+    return cudaMemcpyAsync(q, src, sizeof(double) * cnt, cudaMemcpyHostToDevice, b->stream) == cudaSuccess ? q : nullptr;
+  };
+  if (damp) ddamp = up(f->damping, n);
+  if (tip) dtip = up(f->tip_force, 3 * n);
+  if (act) { dA = up(f->act_A, n); dF = up(f->act_f, n); dL = up(f->act_L, n); }
+  CK(cudaGetLastError(), "H2D forcing");
+  CK(er_launch_apply_forcing(b->d_rec, R, dflags, ddamp, forcing ? f->damping_all : 0.0, dtip, dA, dF, dL,
+                             forcing ? 1 : 0, b->stream), "apply forcing");
+  CK(cudaFreeAsync(d, b->stream), "cudaFreeAsync");
+  CK(cudaStreamSynchronize(b->stream), "sync");
+  return ER_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -262,6 +313,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   g_create_error.clear();
   if (out) *out = nullptr;
   if (!d || !out) { g_create_error = "desc and out must be non-NULL"; return ER_EINVAL; }
+  PhaseTimer tm;
   Errors err;
   const int64_t R = d->n_rods;
   if (R < 0) err.add("n_rods = %lld < 0", (long long)R);
@@ -311,6 +363,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   else if (d->device < 0 || d->device >= ndev) err.add("device %d outside [0, %d)", d->device, ndev);
   if (err.count) { g_create_error = err.msg; return ER_EINVAL; }
 
+  tm.mark("host validation");
   er_batch *b = new er_batch();
   b->device = d->device;
   b->n_rods = R; b->n_elems = E; b->n_nodes = NN; b->n_vor = NV; b->max_n = max_n;
@@ -336,17 +389,36 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
     ElemMat m{d->density[k], d->area[k], d->I1[k], d->I2[k], d->youngs[k], d->shear_mod[k], d->alpha_c[k], d->rest_lengths[j]};
     return m;
   };
-  for (int64_t r = 0; r < R; ++r) {
+  // per-rod records in parallel over host threads (independent rods)
+  const int nthr = (int)std::max<unsigned>(1u, std::min<unsigned>(16u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> pool;
+  std::vector<char> gen_flag((size_t)std::max<int64_t>(R, 1), 0);
+  auto rec_range = [&](int64_t ra, int64_t rb) {
+  for (int64_t r = ra; r < rb; ++r) {
     const ElemMat m0 = mat_at(r, eoff[r]);
     bool uniform = true;
-    for (int64_t j = eoff[r] + 1; j < eoff[r + 1] && uniform; ++j) {
-      const ElemMat m = mat_at(r, j);
-      uniform = m.rho == m0.rho && m.A == m0.A && m.I1 == m0.I1 && m.I2 == m0.I2 && m.E == m0.E && m.G == m0.G &&
-                m.ac == m0.ac && m.lh == m0.lh;
+    if (d->material_per_rod) {  // only the rest lengths can vary along the rod
+      const double *lh = d->rest_lengths;
+      for (int64_t j = eoff[r] + 1; j < eoff[r + 1]; ++j) uniform &= lh[j] == m0.lh;
+    } else {
+      for (int64_t j = eoff[r] + 1; j < eoff[r + 1] && uniform; ++j) {
+        const ElemMat m = mat_at(r, j);
+        uniform = m.rho == m0.rho && m.A == m0.A && m.I1 == m0.I1 && m.I2 == m0.I2 && m.E == m0.E && m.G == m0.G &&
+                  m.ac == m0.ac && m.lh == m0.lh;
+      }
     }
     fill_record(&b->rec[(size_t)r * ER_REC], m0);
-    if (!uniform) { b->flags[r] |= FL_GENERAL; b->any_general = true; }
+    if (!uniform) gen_flag[r] = 1;
   }
+  };
+  if (R < 65536) rec_range(0, R);
+  else {
+    for (int q = 0; q < nthr; ++q) pool.emplace_back(rec_range, R * q / nthr, R * (q + 1) / nthr);
+    for (auto &th : pool) th.join();
+  }
+  for (int64_t r = 0; r < R; ++r)
+    if (gen_flag[r]) { b->flags[r] |= FL_GENERAL; b->any_general = true; }
+  tm.mark("records");
   b->has_sigma0 = d->rest_sigma != nullptr;
   b->has_kappa0 = d->rest_kappa != nullptr && NV > 0;
   b->ng = pad_to(NN, 32);
@@ -427,6 +499,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
     b->state_doubles = boff;
   }
   b->n_tiles = (int64_t)tiles.size();
+  tm.mark("gpar + tiles");
 
   // ---- device allocation and upload
   CK(dalloc(b, &b->d_state, b->state_doubles + 64), "cudaMalloc(state)");
@@ -452,6 +525,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
     if (st0 != ER_OK) return fail(st0);
     CK(cudaStreamSynchronize(b->stream), "sync");  // host vectors above are freed at scope exit
   }
+  tm.mark("alloc + small uploads", b->stream);
   er_status st;
   CK(cudaMemsetAsync(b->d_valid, 0, sizeof(double) * 4, b->stream), "memset");
   if ((st = upload_field(b, d->positions, d->src_mem, FIELD_POS, true)) != ER_OK) return fail(st);
@@ -463,6 +537,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
     CK(dalloc(b, &b->d_sigma0, 3 * b->ne), "cudaMalloc(sigma0)");
     if ((st = upload_side_planes(b, d->rest_sigma, b->d_sigma0, E, b->ne)) != ER_OK) return fail(st);
   }
+  tm.mark("state upload + layout", b->stream);
   // ---- validation of the uploaded state (directors orthonormal within 1e-10, all finite)
   double vres[4] = {0, 0, 0, 0};
   CK(cudaMemcpyAsync(vres, b->d_valid, sizeof vres, cudaMemcpyDeviceToHost, b->stream), "D2H valid");
@@ -472,6 +547,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   if (vres[1] > 1e-10) err.add("directors not proper rotations: max |det Q - 1| = %.3g", vres[1]);
   if (err.count) { b->last_error = err.msg; return fail(ER_EINVAL); }
 #undef CK
+  std::vector<double>().swap(b->rec);  // the device records are authoritative from here on
   *out = b;
   return ER_OK;
 }
@@ -495,10 +571,7 @@ er_status er_set_bc(er_batch *b, const int8_t *clamp_end) {
     if (clamp_end && clamp_end[r] == 1) b->flags[r] |= 2;
   }
   CK(cudaSetDevice(b->device), "cudaSetDevice");
-  er_status st = upload_records(b);
-  if (st != ER_OK) return st;
-  CK(cudaStreamSynchronize(b->stream), "sync");
-  return ER_OK;
+  return apply_forcing(b, nullptr, false);
 }
 
 er_status er_set_forcing(er_batch *b, const er_forcing *f) {
@@ -563,22 +636,15 @@ er_status er_set_forcing(er_batch *b, const er_forcing *f) {
   b->act_comp = act ? f->act_component : 0;
   b->has_act = act;
   for (int64_t r = 0; r < R; ++r) {
-    double *rec = &b->rec[(size_t)r * ER_REC];
-    rec[REC_NU] = f->damping ? f->damping[r] : f->damping_all;
-    b->flags[r] &= ~(FL_TIP | FL_ACT);
-    for (int c = 0; c < 3; ++c) rec[REC_TIPX + c] = f->tip_force ? f->tip_force[3 * r + c] : 0.0;
+    b->flags[r] &= ~(FL_TIP | FL_ACT | FL_MUS);
     if (f->tip_force) b->flags[r] |= FL_TIP;
-    rec[REC_ACTA] = act ? f->act_A[r] : 0.0;
-    rec[REC_ACTF] = act ? f->act_f[r] : 0.0;
-    rec[REC_ACTIL] = act ? 1.0 / f->act_L[r] : 0.0;
     if (act) b->flags[r] |= FL_ACT;
-    b->flags[r] &= ~FL_MUS;
     if (musc) b->flags[r] |= FL_MUS;
   }
   b->has_musc = musc;
   b->musc_comp = musc ? f->musc_component : 0;
   CK(cudaSetDevice(b->device), "cudaSetDevice");
-  er_status st = upload_records(b);
+  er_status st = apply_forcing(b, f, true);
   if (st != ER_OK) return st;
   if (musc && R > 0) {
     std::vector<double> mh((size_t)R * 4);

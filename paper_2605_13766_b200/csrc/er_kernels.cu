@@ -759,6 +759,23 @@ __global__ void validate_aos(const double *a, int64_t n, int k, int orth, double
   if (bad > 0.0) atomicAdd(out + 2, bad);
 }
 
+// er_set_bc / er_set_forcing: write the flag word and (forcing) damping, tip force and actuation
+// fields of every rod record from the caller's per-rod arrays.
+__global__ void apply_forcing(double *rec, int64_t n_rods, const int32_t *flags, const double *damping,
+                              double damping_all, const double *tip, const double *actA, const double *actF,
+                              const double *actL, int forcing) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rods; r += (int64_t)gridDim.x * blockDim.x) {
+    double *x = rec + r * ER_REC;
+    x[REC_FLAGS] = __longlong_as_double((long long)flags[r]);
+    if (!forcing) continue;
+    x[REC_NU] = damping ? damping[r] : damping_all;
+    for (int c = 0; c < 3; ++c) x[REC_TIPX + c] = tip ? tip[3 * r + c] : 0.0;
+    x[REC_ACTA] = actA ? actA[r] : 0.0;
+    x[REC_ACTF] = actA ? actF[r] : 0.0;
+    x[REC_ACTIL] = actA ? 1.0 / actL[r] : 0.0;
+  }
+}
+
 }  // namespace er
 
 // --------------------------------------------------------------------------- launch wrappers
@@ -868,6 +885,13 @@ cudaError_t er_launch_aos_to_soa(const double *src, double *dst, int64_t n, int 
 cudaError_t er_launch_canon_tiles(const ErStepParams *p, double *canon, int field, int to_tiles, cudaStream_t st) {
   if (p->n_tiles <= 0) return cudaSuccess;
   er::canon_tiles<<<(unsigned)p->n_tiles, 256, 0, st>>>(*p, canon, field, to_tiles);
+  return cudaGetLastError();
+}
+cudaError_t er_launch_apply_forcing(double *rec, int64_t n_rods, const int32_t *flags, const double *damping,
+                                    double damping_all, const double *tip, const double *actA, const double *actF,
+                                    const double *actL, int forcing, cudaStream_t st) {
+  if (n_rods <= 0) return cudaSuccess;
+  er::apply_forcing<<<148 * 4, 256, 0, st>>>(rec, n_rods, flags, damping, damping_all, tip, actA, actF, actL, forcing);
   return cudaGetLastError();
 }
 cudaError_t er_launch_validate(const double *aos, int64_t n, int k, int orth, double *out, cudaStream_t st) {
