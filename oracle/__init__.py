@@ -39,6 +39,14 @@ _ip = C.POINTER(C.c_int32)
 _bp = C.POINTER(C.c_int8)
 
 
+class _Contact(C.Structure):
+    _fields_ = [
+        ("enable", C.c_int32), ("k_n", C.c_double), ("gamma_n", C.c_double), ("mu_s", C.c_double),
+        ("mu_k", C.c_double), ("v_stick", C.c_double), ("radius", _dp), ("exclude", C.c_int32),
+        ("plane_on", C.c_int32), ("plane_n", C.c_double * 3), ("plane_d", C.c_double),
+    ]
+
+
 class _Problem(C.Structure):
     _fields_ = [
         ("n_rods", C.c_int32), ("n_elems", _ip), ("material_per_rod", C.c_int32),
@@ -49,6 +57,7 @@ class _Problem(C.Structure):
         ("act_component", C.c_int32), ("magnetization", _dp), ("b_field", C.c_double * 3),
         ("b_omega", C.c_double), ("b_axis", C.c_double * 3),
         ("musc_A", _dp), ("musc_T", _dp), ("musc_lambda", _dp), ("musc_phi", _dp), ("musc_component", C.c_int32),
+        ("contact", C.POINTER(_Contact)),
     ]
 
 
@@ -74,6 +83,10 @@ def lib():
         _lib.orc_step.restype = C.c_int
         _lib.orc_energy.argtypes = [C.POINTER(_Problem), _dp, _dp, _dp, _dp, C.c_double, _dp]
         _lib.orc_energy.restype = C.c_int
+        _lib.orc_segment_closest.argtypes = [_dp, _dp, _dp, _dp, _dp, _dp, _dp]
+        _lib.orc_contact_pairs.argtypes = [C.POINTER(_Problem), _dp, C.c_int64, C.POINTER(C.c_int64), _dp]
+        _lib.orc_contact_pairs.restype = C.c_int64
+        _lib.orc_contact_forces.argtypes = [C.POINTER(_Problem), _dp, _dp, _dp]
     return _lib
 
 
@@ -117,6 +130,18 @@ class Problem:
         ax = w.b_axis if getattr(w, "b_axis", None) is not None else np.zeros(3)
         p.b_axis = (C.c_double * 3)(*[float(x) for x in ax])
         p.musc_component = int(getattr(w, "musc_component", 0))
+        ct = getattr(w, "contact", None)
+        if ct is not None:
+            c = _Contact()
+            c.enable = 1
+            c.k_n, c.gamma_n, c.mu_s, c.mu_k, c.v_stick = ct.k_n, ct.gamma_n, ct.mu_s, ct.mu_k, ct.v_stick
+            c.radius = _ptr(k(ct.radius))
+            c.exclude = int(ct.exclude)
+            c.plane_on = 0 if ct.plane_n is None else 1
+            c.plane_n = (C.c_double * 3)(*([float(x) for x in ct.plane_n] if ct.plane_n is not None else [0, 0, 1]))
+            c.plane_d = float(ct.plane_d)
+            self._keep.append(c)
+            p.contact = C.pointer(c)
         self.c = p
 
 
@@ -205,3 +230,31 @@ def energy(w, state: Optional[State] = None):
     lib().orc_energy(C.byref(P.c), _ptr(st.positions), _ptr(st.velocities), _ptr(st.directors),
                      _ptr(st.omega), st.t, _ptr(out))
     return out
+
+
+# ------------------------------------------------------------------ contact (NEXT-4)
+def segment_closest(p0, p1, q0, q1):
+    p0, p1, q0, q1 = (_f64(x) for x in (p0, p1, q0, q1))
+    s, t, d = C.c_double(), C.c_double(), C.c_double()
+    lib().orc_segment_closest(_ptr(p0), _ptr(p1), _ptr(q0), _ptr(q1), C.byref(s), C.byref(t), C.byref(d))
+    return s.value, t.value, d.value
+
+
+def contact_pairs(w, positions, max_pairs=1 << 20):
+    """Exhaustive O(E^2) detection: element pairs (a < b) with gap < 0, and their gaps."""
+    P = Problem(w)
+    pos = _f64(positions)
+    pairs = np.zeros((max_pairs, 2), np.int64)
+    gaps = np.zeros(max_pairs)
+    n = lib().orc_contact_pairs(C.byref(P.c), _ptr(pos), max_pairs, pairs.ctypes.data_as(C.POINTER(C.c_int64)),
+                                _ptr(gaps))
+    n = min(n, max_pairs)
+    return pairs[:n], gaps[:n]
+
+
+def contact_forces(w, positions, velocities):
+    P = Problem(w)
+    pos, vel = _f64(positions), _f64(velocities)
+    F = np.zeros_like(pos)
+    lib().orc_contact_forces(C.byref(P.c), _ptr(pos), _ptr(vel), _ptr(F))
+    return F

@@ -18,6 +18,11 @@
  * All readings of silent/ambiguous passages are SURVEY §8 C.4 and are listed in
  * DESIGN.md §3.
  *
+ * Contact: exhaustive O(E^2) pair search,
+ * exact segment-segment closest points, penalty normal force + regularised Coulomb
+ * friction, optional half-space -- reading DESIGN.md §3 #27 (the paper's formulas
+ * are in its missing supplement).  Pinned by tests/test_oracle_contact.py.
+ *
  * Deliberately plain: no blocking, no fusion, no reordering beyond the algorithm
  * as written; every intermediate of C.3 is materialised per rod.
  */
@@ -281,7 +286,7 @@ int orc_rod_strains(int32_t N, const double *lhat, const double *pos, const doub
 /* ---------------------------------------------------------------- dynamics (C.3 steps 2-6) */
 
 static int rod_dynamics(const orc_problem *P, int32_t rod, rod_ctx *c, const double *r, const double *v,
-                        const double *Q, const double *w, double t) {
+                        const double *Q, const double *w, double t, const double *Fext) {
   const int32_t N = c->N;
   int fault = 0;
   const double e3[3] = {0.0, 0.0, 1.0};
@@ -334,6 +339,7 @@ static int rod_dynamics(const orc_problem *P, int32_t rod, rod_ctx *c, const dou
       if (i < N) f += c->nlab[3 * i + q];
       if (i > 0) f -= c->nlab[3 * (i - 1) + q];
       f += c->m[i] * P->gravity[q];
+      if (Fext) f += Fext[3 * i + q];                       /* contact forces (NEXT-4) */
       if (P->tip_force && i == c->tip_node) f += P->tip_force[3 * rod + q];
       c->F[3 * i + q] = f;
       c->a[3 * i + q] = f / c->m[i] - c->nu * v[3 * i + q];
@@ -431,7 +437,7 @@ int orc_rod_loads(const orc_problem *P, int32_t rod, const double *pos, const do
   rod_ctx c;
   ctx_alloc(&c, P->n_elems[rod]);
   ctx_setup(P, rod, e0, &c);
-  int fault = rod_dynamics(P, rod, &c, pos, vel, dirs, omega, t);
+  int fault = rod_dynamics(P, rod, &c, pos, vel, dirs, omega, t, NULL);
   int32_t N = c.N;
   memcpy(F, c.F, sizeof(double) * 3 * (size_t)(N + 1));
   memcpy(a, c.a, sizeof(double) * 3 * (size_t)(N + 1));
@@ -443,14 +449,14 @@ int orc_rod_loads(const orc_problem *P, int32_t rod, const double *pos, const do
 
 /* One rod, one stage; stage 1/3 = drift h/2 + pose constraint, stage 2 = kick + rate constraint. */
 static int rod_stage(const orc_problem *P, int32_t rod, rod_ctx *c, int stage, double *pos, double *vel,
-                     double *dirs, double *omega, double h, double t_half) {
+                     double *dirs, double *omega, double h, double t_half, const double *Fext) {
   double *r = pos + 3 * c->n0, *v = vel + 3 * c->n0, *Q = dirs + 9 * c->e0, *w = omega + 3 * c->e0;
   int fault = 0;
   if (stage == 1 || stage == 3) {
     stage_drift(c, r, v, Q, w, 0.5 * h);
     clamp_pose(c, r, Q);
   } else {
-    fault |= rod_dynamics(P, rod, c, r, v, Q, w, t_half);
+    fault |= rod_dynamics(P, rod, c, r, v, Q, w, t_half, Fext ? Fext + 3 * c->n0 : NULL);
     for (int32_t i = 0; i <= c->N; ++i)
       for (int q = 0; q < 3; ++q) v[3 * i + q] += h * c->a[3 * i + q];
     for (int32_t j = 0; j < c->N; ++j)
@@ -487,14 +493,23 @@ int orc_step(const orc_problem *P, double *pos, double *vel, double *dirs, doubl
     ctx_setup(P, (r), eoff[(r)], &c);                                                    \
     memcpy(c.rfix, rfix + 3 * (r), sizeof c.rfix);                                       \
     memcpy(c.Qfix, Qfix + 9 * (r), sizeof c.Qfix);                                       \
-    int f_ = rod_stage(P, (r), &c, (stage), pos, vel, dirs, omega, dt, t_half);          \
+    int f_ = rod_stage(P, (r), &c, (stage), pos, vel, dirs, omega, dt, t_half, Fext);    \
     if (f_) { bits |= f_; if (first_bad < 0 || (r) < first_bad) first_bad = (r); }       \
   } while (0)
+  const int contact = P->contact && P->contact->enable;
+  double *Fext = NULL;
+  if (contact) Fext = (double *)calloc((size_t)(eoff[R] + R) * 3 + 3, sizeof(double));
   for (int64_t s = 0; s < n_steps; ++s) {
     double t_half = tt + 0.5 * dt;
-    if (protocol == ORC_SYNC) {          /* barrier after every stage */
-      for (int stage = 1; stage <= 3; ++stage)
+    if (protocol == ORC_SYNC || contact) { /* barrier after every stage; rods that
+                                              interact need it */
+      for (int stage = 1; stage <= 3; ++stage) {
+        if (stage == 2 && contact) {       /* contact forces at the half-step configuration, v^n */
+          memset(Fext, 0, sizeof(double) * 3 * (size_t)(eoff[R] + R));
+          orc_contact_forces(P, pos, vel, Fext);
+        }
         for (int32_t r = 0; r < R; ++r) RUN_STAGE(r, stage);
+      }
     } else {                             /* barrier once per step */
       for (int32_t r = 0; r < R; ++r)
         for (int stage = 1; stage <= 3; ++stage) RUN_STAGE(r, stage);
@@ -502,12 +517,176 @@ int orc_step(const orc_problem *P, double *pos, double *vel, double *dirs, doubl
     tt = t_half + 0.5 * dt;
   }
 #undef RUN_STAGE
+  free(Fext);
   *t = tt;
   ctx_free(&c);
   free(eoff); free(rfix); free(Qfix);
   if (bad_rod) *bad_rod = first_bad;
   if (fault_out) *fault_out = bits;
   return first_bad >= 0 ? ORC_EUNSTABLE : ORC_OK;
+}
+
+/* ---------------------------------------------------------------- contact (NEXT-4) */
+
+/* Closest points of two segments: minimise |p0 + s d1 - q0 - t d2|^2 over [0,1]^2.  Candidates
+ * (in this order): the interior stationary point when it lies inside the square, then the four
+ * edges s = 0, s = 1, t = 0, t = 1 each with its clamped 1-D minimiser; the first candidate with
+ * the smallest distance wins (so ties resolve deterministically). */
+static double seg_dist2(const double *p0, const double *d1, const double *q0, const double *d2, double s, double t) {
+  double x[3];
+  for (int q = 0; q < 3; ++q) x[q] = p0[q] + s * d1[q] - q0[q] - t * d2[q];
+  return v_dot(x, x);
+}
+static double clamp01(double x) { return x < 0.0 ? 0.0 : (x > 1.0 ? 1.0 : x); }
+
+void orc_segment_closest(const double p0[3], const double p1[3], const double q0[3], const double q1[3],
+                         double *s_out, double *t_out, double *dist) {
+  double d1[3], d2[3], r[3];
+  v_sub(p1, p0, d1);
+  v_sub(q1, q0, d2);
+  v_sub(p0, q0, r);
+  double a = v_dot(d1, d1), e = v_dot(d2, d2), b = v_dot(d1, d2), c = v_dot(d1, r), f = v_dot(d2, r);
+  double best = -1.0, bs = 0.0, bt = 0.0;
+  double cs[5], ct[5];
+  int n = 0;
+  double den = a * e - b * b;
+  if (den > 0.0) {
+    double s = (b * f - c * e) / den, t = (a * f - b * c) / den;
+    if (s >= 0.0 && s <= 1.0 && t >= 0.0 && t <= 1.0) { cs[n] = s; ct[n] = t; ++n; }
+  }
+  /* s = 0: minimise over t |r - t d2|^2 -> t = f / e;  s = 1: t = (f + b) / e */
+  cs[n] = 0.0; ct[n] = e > 0.0 ? clamp01(f / e) : 0.0; ++n;
+  cs[n] = 1.0; ct[n] = e > 0.0 ? clamp01((f + b) / e) : 0.0; ++n;
+  /* t = 0: minimise over s |r + s d1|^2 -> s = -c / a;  t = 1: s = (b - c) / a */
+  cs[n] = a > 0.0 ? clamp01(-c / a) : 0.0; ct[n] = 0.0; ++n;
+  cs[n] = a > 0.0 ? clamp01((b - c) / a) : 0.0; ct[n] = 1.0; ++n;
+  for (int k = 0; k < n; ++k) {
+    double d = seg_dist2(p0, d1, q0, d2, cs[k], ct[k]);
+    if (best < 0.0 || d < best) { best = d; bs = cs[k]; bt = ct[k]; }
+  }
+  *s_out = bs;
+  *t_out = bt;
+  *dist = sqrt(best);
+}
+
+static double contact_radius(const orc_problem *P, int32_t rod, int64_t e0) {
+  if (P->contact->radius) return P->contact->radius[rod];
+  return sqrt(matv(P, P->area, rod, e0) / PI);
+}
+
+/* element -> rod, element -> first node, rod radius / stiffness scale, for the whole batch */
+typedef struct { int32_t *rod; int64_t *node; double *rad, *Er; } elem_map;
+static void elem_map_build(const orc_problem *P, elem_map *m, int64_t *E_out) {
+  int64_t E = 0;
+  for (int32_t r = 0; r < P->n_rods; ++r) E += P->n_elems[r];
+  m->rod = (int32_t *)malloc(sizeof(int32_t) * (size_t)(E + 1));
+  m->node = (int64_t *)malloc(sizeof(int64_t) * (size_t)(E + 1));
+  m->rad = (double *)malloc(sizeof(double) * (size_t)(P->n_rods + 1));
+  m->Er = (double *)malloc(sizeof(double) * (size_t)(P->n_rods + 1));
+  int64_t e = 0;
+  for (int32_t r = 0; r < P->n_rods; ++r) {
+    m->rad[r] = contact_radius(P, r, e);
+    m->Er[r] = matv(P, P->youngs, r, e) * m->rad[r];
+    for (int32_t j = 0; j < P->n_elems[r]; ++j, ++e) { m->rod[e] = r; m->node[e] = e + r; }
+  }
+  *E_out = E;
+}
+static void elem_map_free(elem_map *m) { free(m->rod); free(m->node); free(m->rad); free(m->Er); }
+
+static int excluded(const orc_problem *P, const elem_map *m, int64_t a, int64_t b) {
+  if (m->rod[a] != m->rod[b]) return 0;
+  int64_t dj = a > b ? a - b : b - a;
+  return dj <= P->contact->exclude;
+}
+
+int64_t orc_contact_pairs(const orc_problem *P, const double *pos, int64_t max_pairs, int64_t *pairs, double *gaps) {
+  elem_map m;
+  int64_t E, found = 0;
+  elem_map_build(P, &m, &E);
+  for (int64_t a = 0; a < E; ++a)
+    for (int64_t b = a + 1; b < E; ++b) {
+      if (excluded(P, &m, a, b)) continue;
+      double s, t, d;
+      orc_segment_closest(pos + 3 * m.node[a], pos + 3 * (m.node[a] + 1), pos + 3 * m.node[b], pos + 3 * (m.node[b] + 1),
+                          &s, &t, &d);
+      double gap = d - (m.rad[m.rod[a]] + m.rad[m.rod[b]]);
+      if (gap < 0.0) {
+        if (found < max_pairs) { pairs[2 * found] = a; pairs[2 * found + 1] = b; gaps[found] = gap; }
+        ++found;
+      }
+    }
+  elem_map_free(&m);
+  return found;
+}
+
+/* Penalty normal force F_n = max(0, k (-gap) - gamma v_n) along n (from b to a), regularised
+ * Coulomb friction F_t = -mu_k F_n v_t/|v_t| when |v_t| > v_stick, else -mu_s F_n v_t / v_stick
+ * (SPEC.md:385-400 design decisions).  Returns the force on body a. */
+static void contact_law(const orc_contact *C, double k, double gap, const double *n, const double *vr, double *F) {
+  double vn = v_dot(vr, n);
+  double fn = k * (-gap) - C->gamma_n * vn;
+  if (fn < 0.0) fn = 0.0;
+  double vt[3];
+  for (int q = 0; q < 3; ++q) vt[q] = vr[q] - vn * n[q];
+  double svt = sqrt(v_dot(vt, vt));
+  for (int q = 0; q < 3; ++q) {
+    double ft = 0.0;
+    if (svt > C->v_stick) ft = -C->mu_k * fn * vt[q] / svt;
+    else if (C->v_stick > 0.0) ft = -C->mu_s * fn * vt[q] / C->v_stick;
+    F[q] = fn * n[q] + ft;
+  }
+}
+
+void orc_contact_forces(const orc_problem *P, const double *pos, const double *vel, double *F) {
+  const orc_contact *C = P->contact;
+  elem_map m;
+  int64_t E;
+  elem_map_build(P, &m, &E);
+  for (int64_t a = 0; a < E; ++a)
+    for (int64_t b = a + 1; b < E; ++b) {
+      if (excluded(P, &m, a, b)) continue;
+      int64_t ja = m.node[a], jb = m.node[b];
+      double s, t, d;
+      orc_segment_closest(pos + 3 * ja, pos + 3 * (ja + 1), pos + 3 * jb, pos + 3 * (jb + 1), &s, &t, &d);
+      int32_t ra = m.rod[a], rb = m.rod[b];
+      double gap = d - (m.rad[ra] + m.rad[rb]);
+      if (!(gap < 0.0) || d == 0.0) continue;
+      double pa[3], pb[3], n[3], va[3], vb[3], vr[3], f[3];
+      for (int q = 0; q < 3; ++q) {
+        pa[q] = (1.0 - s) * pos[3 * ja + q] + s * pos[3 * (ja + 1) + q];
+        pb[q] = (1.0 - t) * pos[3 * jb + q] + t * pos[3 * (jb + 1) + q];
+      }
+      for (int q = 0; q < 3; ++q) n[q] = (pa[q] - pb[q]) / d;
+      for (int q = 0; q < 3; ++q) {
+        va[q] = (1.0 - s) * vel[3 * ja + q] + s * vel[3 * (ja + 1) + q];
+        vb[q] = (1.0 - t) * vel[3 * jb + q] + t * vel[3 * (jb + 1) + q];
+        vr[q] = va[q] - vb[q];
+      }
+      double k = C->k_n > 0.0 ? C->k_n : (m.Er[ra] < m.Er[rb] ? m.Er[ra] : m.Er[rb]);
+      contact_law(C, k, gap, n, vr, f);
+      for (int q = 0; q < 3; ++q) {
+        F[3 * ja + q] += (1.0 - s) * f[q];
+        F[3 * (ja + 1) + q] += s * f[q];
+        F[3 * jb + q] -= (1.0 - t) * f[q];
+        F[3 * (jb + 1) + q] -= t * f[q];
+      }
+    }
+  if (C->plane_on) {                   /* half-space n . x >= d, node-wise (capsule ends) */
+    double nn = sqrt(v_dot(C->plane_n, C->plane_n)), n[3];
+    for (int q = 0; q < 3; ++q) n[q] = C->plane_n[q] / nn;
+    int64_t node = 0;
+    for (int32_t r = 0; r < P->n_rods; ++r) {
+      double k = C->k_n > 0.0 ? C->k_n : m.Er[r];
+      for (int32_t i = 0; i <= P->n_elems[r]; ++i, ++node) {
+        double gap = v_dot(n, pos + 3 * node) - C->plane_d - m.rad[r];
+        if (!(gap < 0.0)) continue;
+        double f[3];
+        contact_law(C, k, gap, n, vel + 3 * node, f);
+        for (int q = 0; q < 3; ++q) F[3 * node + q] += f[q];
+      }
+    }
+  }
+  elem_map_free(&m);
 }
 
 /* Diagnostics (SURVEY §8 C.3 "energy"):

@@ -20,6 +20,21 @@
 extern "C" {
 #endif
 
+/* Contact (SURVEY NEXT-4; PAPER.md:73, :80-84 name "normal force and friction" and an HHG broad
+ * phase, the formulas are in the missing supplement -- readings DESIGN §3 #27). */
+typedef struct {
+  int32_t enable;
+  double k_n;            /* penalty stiffness; <= 0: min(E_A r_A, E_B r_B) per pair            */
+  double gamma_n;        /* normal damping                                                     */
+  double mu_s, mu_k;     /* static / kinetic friction coefficients                              */
+  double v_stick;        /* regularised Coulomb: |v_t| <= v_stick -> static branch              */
+  const double *radius;  /* [R] contact radius, or NULL = sqrt(A / pi)                          */
+  int32_t exclude;       /* same-rod element pairs with |j - k| <= exclude never touch            */
+  int32_t plane_on;      /* half-space boundary n . x >= d                                       */
+  double plane_n[3];
+  double plane_d;
+} orc_contact;
+
 typedef struct {
   int32_t n_rods;
   const int32_t *n_elems;          /* [R], each >= 1                                   */
@@ -41,6 +56,7 @@ typedef struct {
   double b_axis[3];                /* rotation axis of b(t) (normalised here), 0 = lab z */
   const double *musc_A, *musc_T, *musc_lambda, *musc_phi; /* [R] muscular torque wave, or NULL */
   int32_t musc_component;          /* local axis of the muscle couple (0 = d1)           */
+  const orc_contact *contact;      /* NULL = rods do not interact                        */
 } orc_problem;
 
 enum { ORC_OK = 0, ORC_EINVAL = 1, ORC_EUNSTABLE = 2 };
@@ -75,6 +91,17 @@ int orc_rod_loads(const orc_problem *P, int32_t rod, const double *pos, const do
 int orc_step(const orc_problem *P, double *pos, double *vel, double *dirs, double *omega,
              double *t, int64_t n_steps, double dt, int32_t protocol,
              int64_t *bad_rod, int32_t *fault);
+
+/* closest points of segments p0-p1 and q0-q1: parameters s, t in [0,1] and distance */
+void orc_segment_closest(const double p0[3], const double p1[3], const double q0[3], const double q1[3],
+                         double *s, double *t, double *dist);
+
+/* exhaustive contact detection at the given positions: element pairs (a < b, global element ids)
+ * with gap = dist - (r_a + r_b) < 0; returns the number found (writes at most max_pairs) */
+int64_t orc_contact_pairs(const orc_problem *P, const double *pos, int64_t max_pairs, int64_t *pairs, double *gaps);
+
+/* contact forces on every node (added into F[n_nodes*3], which the caller zeroes) */
+void orc_contact_forces(const orc_problem *P, const double *pos, const double *vel, double *F);
 
 /* diagnostics at the current (integer-time) state: out[ORC_NDIAG] */
 int orc_energy(const orc_problem *P, const double *pos, const double *vel, const double *dirs,

@@ -37,6 +37,22 @@ CONFIG_NAMES = ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5")
 
 
 @dataclasses.dataclass
+class Contact:
+    """Contact parameters (NEXT-4; reading DESIGN §3 #27): penalty k_n (<= 0: min(E_A r_A, E_B r_B)),
+    normal damping gamma_n, regularised Coulomb friction (mu_s, mu_k, v_stick), contact radius per
+    rod (None = sqrt(A/pi)), same-rod exclusion |j - k| <= exclude, optional half-space n.x >= d."""
+    k_n: float = 0.0
+    gamma_n: float = 0.0
+    mu_s: float = 0.0
+    mu_k: float = 0.0
+    v_stick: float = 1e-4
+    radius: Optional[np.ndarray] = None
+    exclude: int = 2
+    plane_n: Optional[np.ndarray] = None
+    plane_d: float = 0.0
+
+
+@dataclasses.dataclass
 class Workload:
     name: str
     n_elems: np.ndarray            # int32 [R]
@@ -76,6 +92,7 @@ class Workload:
     musc_lambda: Optional[np.ndarray] = None    # f64 [R]
     musc_phi: Optional[np.ndarray] = None       # f64 [R]
     musc_component: int = 0
+    contact: Optional[Contact] = None           # NEXT-4: rods interact through contact
 
     # ---- layout helpers (integer bookkeeping only) ----
     @property
@@ -139,6 +156,8 @@ class Workload:
             magnetization=gather(eo, self.magnetization),
             musc_A=per_rod(self.musc_A), musc_T=per_rod(self.musc_T),
             musc_lambda=per_rod(self.musc_lambda), musc_phi=per_rod(self.musc_phi),
+            contact=None if self.contact is None else dataclasses.replace(
+                self.contact, radius=per_rod(self.contact.radius)),
         )
 
     def copy_state(self):
