@@ -65,6 +65,9 @@ typedef enum { ER_HOST = 0, ER_DEVICE = 1 } er_mem;
 #define ER_F_DEGENERATE 2  /* dilatation e = |edge|/lhat < 1e-12                               */
 #define ER_F_ANTIPODAL 4   /* adjacent-element relative rotation angle >= pi - 1e-6            */
 #define ER_F_OVERSPEED 8   /* |v| > 1e6 sqrt(E/rho)                                           */
+#define ER_F_CONTACT 16    /* contact broad phase could not bin an element (wider than the top
+                              HHG level, non-finite or |coordinate| > 2^30 cells) or the
+                              cross-level record pool / per-element record list overflowed    */
 
 /* ------------------------------------------------------------------------- er_create_batch
  * A ragged batch of rods with per-rod element counts (north_star "er_create_batch").
@@ -209,6 +212,58 @@ er_status er_diagnostics(er_batch *b, double out[ER_NDIAG]);
  * After ER_EUNSTABLE: lowest faulted rod id (canonical order) and the OR of fault bits.
  */
 er_status er_fault(const er_batch *b, int64_t *rod, int32_t *bits);
+
+/* ------------------------------------------------------------------------- er_set_contact
+ * Rod-rod and rod-boundary contact with friction.  The paper names the
+ * model -- "rod interactions via normal force and friction", a collision engine with
+ * a hierarchical hash-grid (HHG) broad phase (Fig. 2e) that forces synchronous
+ * stepping -- and leaves the formulas to its missing supplement; the law below is
+ * reading DESIGN §3 #27.  Each element is a capsule (segment between its nodes, radius r_rod).
+ * A pair of elements (a, b), not of the same rod within `exclude` elements, whose closest points
+ * pa, pb (exact segment-segment minimiser) are closer than r_a + r_b (gap = |pa - pb| - r_a - r_b
+ * < 0, |pa - pb| > 0) receives, with n = (pa - pb)/|pa - pb| and v_r the relative velocity of the
+ * closest points (barycentric in the segment's nodes):
+ *   F = max(0, k (-gap) - gamma_n v_r.n) n + F_t  on a, -F on b,
+ *   F_t = -mu_k F_n v_t/|v_t| if |v_t| > v_stick, else -mu_s F_n v_t/v_stick  (v_t = v_r - (v_r.n) n),
+ * each distributed to the segment's two nodes with the closest-point weights (1 - s, s).
+ * k = k_n if k_n > 0, else min(E_a r_a, E_b r_b).  With plane_on, every node x with
+ * gap = n.x - d - r < 0 receives the same law against the half-space n.x >= d (v_r = its velocity).
+ * Contact forces are evaluated once per step at the half-step configuration (after drift-1) with
+ * v^n, so er_step runs the staged (synchronous) path while contact is enabled.
+ *  radius      HOST [n_rods] contact radius, or NULL = sqrt(A/pi) of the rod's first element.
+ *  cell0       finest HHG cell (m); 0 = auto: 1.25 x the smallest rest capsule extent
+ *              (lhat + 2r).  n_levels (1..8); 0 = auto: enough levels of doubling cells for the
+ *              largest rest extent x 1.25, plus one level of headroom.
+ *  pool_factor cross-level record pool = pool_factor x n_elems records (0 = auto, 4).
+ * An element whose AABB outgrows the top level, or a full pool, faults the step with
+ * ER_F_CONTACT.  c == NULL or c->enable == 0 disables contact.  Errors: ER_EINVAL, ER_ENOMEM.
+ */
+typedef struct {
+  int32_t enable;
+  double k_n, gamma_n, mu_s, mu_k, v_stick;
+  const double *radius;
+  int32_t exclude;
+  int32_t plane_on;
+  double plane_n[3];  /* need not be unit; normalised by the library */
+  double plane_d;
+  double cell0;
+  int32_t n_levels;
+  double pool_factor;
+} er_contact;
+er_status er_set_contact(er_batch *b, const er_contact *c);
+
+/* Contact statistics of the last step of the last er_step call (synchronises the stream). */
+typedef struct {
+  int64_t candidates;      /* element pairs whose AABBs overlap (each pair once)        */
+  int64_t contacts;        /* element pairs in contact (gap < 0)                         */
+  int64_t cross_level;     /* of those, pairs across HHG levels                          */
+  int64_t plane_contacts;  /* nodes in contact with the half-space                       */
+  int64_t pool_used;       /* cross-level records written                                */
+  int32_t n_levels;        /* HHG levels configured                                      */
+  int32_t level_mask;      /* levels populated (bit l)                                   */
+  double cell0;            /* finest cell size                                           */
+} er_contact_stats;
+er_status er_get_contact_stats(er_batch *b, er_contact_stats *out);
 
 /* ------------------------------------------------------------------------- options / info */
 typedef enum {

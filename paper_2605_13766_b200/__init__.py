@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(_HERE, "lib", "libelasticarod.so")
 
 ER_OK, ER_EINVAL, ER_EUNSTABLE, ER_EIO, ER_ENOMEM, ER_ECUDA = range(6)
 ER_HOST, ER_DEVICE = 0, 1
-ER_F_NONFINITE, ER_F_DEGENERATE, ER_F_ANTIPODAL, ER_F_OVERSPEED = 1, 2, 4, 8
+ER_F_NONFINITE, ER_F_DEGENERATE, ER_F_ANTIPODAL, ER_F_OVERSPEED, ER_F_CONTACT = 1, 2, 4, 8, 16
 ER_OPT_STEPS_PER_LAUNCH, ER_OPT_KERNEL = 1, 2
 ER_NDIAG = 12
 DIAG_NAMES = ("ke_trans", "ke_rot", "pe_shear", "pe_bend", "pe_grav", "pe_tip",
@@ -65,9 +65,26 @@ class er_info(C.Structure):
     ]
 
 
+class er_contact(C.Structure):
+    _fields_ = [
+        ("enable", C.c_int32), ("k_n", C.c_double), ("gamma_n", C.c_double), ("mu_s", C.c_double),
+        ("mu_k", C.c_double), ("v_stick", C.c_double), ("radius", _dp), ("exclude", C.c_int32),
+        ("plane_on", C.c_int32), ("plane_n", C.c_double * 3), ("plane_d", C.c_double),
+        ("cell0", C.c_double), ("n_levels", C.c_int32), ("pool_factor", C.c_double),
+    ]
+
+
+class er_contact_stats(C.Structure):
+    _fields_ = [
+        ("candidates", C.c_int64), ("contacts", C.c_int64), ("cross_level", C.c_int64),
+        ("plane_contacts", C.c_int64), ("pool_used", C.c_int64), ("n_levels", C.c_int32),
+        ("level_mask", C.c_int32), ("cell0", C.c_double),
+    ]
+
+
 EXPORTS = ("er_create_batch", "er_set_bc", "er_set_forcing", "er_step", "er_get_state", "er_set_state",
            "er_diagnostics", "er_fault", "er_set_option", "er_set_trace", "er_query", "er_last_error",
-           "er_abi_version", "er_destroy")
+           "er_abi_version", "er_destroy", "er_set_contact", "er_get_contact_stats")
 
 
 def _load():
@@ -89,11 +106,14 @@ def _load():
     lib.er_query.argtypes = [h, C.POINTER(er_info)]
     lib.er_last_error.argtypes = [h]
     lib.er_last_error.restype = C.c_char_p
+    lib.er_set_contact.argtypes = [h, C.POINTER(er_contact)]
+    lib.er_get_contact_stats.argtypes = [h, C.POINTER(er_contact_stats)]
     lib.er_abi_version.restype = C.c_int32
     lib.er_destroy.argtypes = [h]
     lib.er_destroy.restype = None
     for name in ("er_create_batch", "er_set_bc", "er_set_forcing", "er_step", "er_get_state",
-                 "er_set_state", "er_diagnostics", "er_fault", "er_set_option", "er_set_trace", "er_query"):
+                 "er_set_state", "er_diagnostics", "er_fault", "er_set_option", "er_set_trace", "er_query",
+                 "er_set_contact", "er_get_contact_stats"):
         getattr(lib, name).restype = C.c_int
     return lib
 
@@ -168,6 +188,16 @@ def er_query(handle) -> er_info:
     info = er_info()
     _check(handle, lib.er_query(handle, C.byref(info)))
     return info
+
+
+def er_set_contact(handle, contact):
+    _check(handle, lib.er_set_contact(handle, None if contact is None else C.byref(contact)))
+
+
+def er_get_contact_stats(handle) -> er_contact_stats:
+    out = er_contact_stats()
+    _check(handle, lib.er_get_contact_stats(handle, C.byref(out)))
+    return out
 
 
 def er_destroy(handle):
@@ -247,6 +277,8 @@ class RodBatch:
         if apply_bc_forcing:
             self.set_bc(getattr(w, "clamp", None))
             self.set_forcing_from(w)
+            if getattr(w, "contact", None) is not None:
+                self.set_contact(w.contact)
 
     # -- boundary conditions / forcing
     def set_bc(self, clamp_end=None):
@@ -284,6 +316,32 @@ class RodBatch:
                          b_axis=getattr(w, "b_axis", None), musc_A=getattr(w, "musc_A", None),
                          musc_T=getattr(w, "musc_T", None), musc_lambda=getattr(w, "musc_lambda", None),
                          musc_phi=getattr(w, "musc_phi", None), musc_component=getattr(w, "musc_component", 0))
+
+    def set_contact(self, c=None, cell0: float = 0.0, n_levels: int = 0, pool_factor: float = 0.0):
+        """Enable rod-rod / half-space contact from an object with the attributes of
+        workloads.Contact (k_n, gamma_n, mu_s, mu_k, v_stick, radius, exclude, plane_n, plane_d);
+        None disables it."""
+        if c is None:
+            er_set_contact(self.handle, None)
+            return
+        k = _Keep()
+        s = er_contact()
+        s.enable = 1
+        s.k_n, s.gamma_n = float(c.k_n), float(c.gamma_n)
+        s.mu_s, s.mu_k, s.v_stick = float(c.mu_s), float(c.mu_k), float(c.v_stick)
+        s.radius = k.host(getattr(c, "radius", None))
+        s.exclude = int(c.exclude)
+        pn = getattr(c, "plane_n", None)
+        s.plane_on = 0 if pn is None else 1
+        s.plane_n = (C.c_double * 3)(*([float(x) for x in pn] if pn is not None else [0.0, 0.0, 1.0]))
+        s.plane_d = float(getattr(c, "plane_d", 0.0))
+        s.cell0 = float(getattr(c, "cell0", cell0) or cell0)
+        s.n_levels = int(getattr(c, "n_levels", n_levels) or n_levels)
+        s.pool_factor = float(pool_factor)
+        er_set_contact(self.handle, s)
+
+    def contact_stats(self) -> er_contact_stats:
+        return er_get_contact_stats(self.handle)
 
     # -- stepping / state
     def step(self, n_steps: int, dt: float):

@@ -30,6 +30,9 @@ cudaError_t er_launch_validate(const double *aos, int64_t n, int k, int orth, do
 cudaError_t er_launch_apply_forcing(double *rec, int64_t n_rods, const int32_t *flags, const double *damping,
                                     double damping_all, const double *tip, const double *actA, const double *actF,
                                     const double *actL, int forcing, cudaStream_t st);
+cudaError_t er_contact_sort_bytes(int64_t n, int bits, size_t *bytes);
+cudaError_t er_contact_eval(const ErContactParams *p, void *sort_tmp, size_t sort_bytes, cudaStream_t st,
+                            int64_t *launches);
 }
 
 #include <chrono>
@@ -112,6 +115,12 @@ struct er_batch {
   int64_t fault_rod = -1;
   int32_t fault_bits = 0;
   std::string last_error;
+  // contact (NEXT-4)
+  bool contact_on = false;
+  ErContactParams cp{};
+  void *sort_tmp = nullptr;
+  size_t sort_bytes = 0;
+  std::vector<double> rod_A0, rod_E0, rod_lmin, rod_lmax;  // host, per rod (contact radius, stiffness, HHG)
 };
 
 namespace {
@@ -137,11 +146,24 @@ cudaError_t dalloc(er_batch *b, T **p, int64_t count) {
   return e;
 }
 
+void free_contact(er_batch *b) {
+  ErContactParams &c = b->cp;
+  void *ptrs[] = {(void *)c.rad, (void *)c.kr, (void *)c.erod, c.cnode, c.key, c.key_s, c.val, c.val_s, c.cstart,
+                  c.cend, c.p01, c.v01, c.meta, c.cellc, c.fc, c.head, c.pnext, c.psrc, c.pf, c.ctr, b->sort_tmp};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+  b->cp = ErContactParams{};
+  b->sort_tmp = nullptr;
+  b->sort_bytes = 0;
+  b->contact_on = false;
+}
+
 void free_all(er_batch *b) {
   void *ptrs[] = {b->d_state, b->d_rec, b->d_eoff, b->d_tiles, b->d_gpar, b->d_sigma0, b->d_mag, b->d_musc,
                   b->d_fault, b->d_diag_partial, b->d_diag_out, b->d_valid};
   for (void *p : ptrs)
     if (p) cudaFree(p);
+  free_contact(b);
   if (b->own_stream && b->stream) cudaStreamDestroy(b->stream);
 }
 
@@ -393,6 +415,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   const int nthr = (int)std::max<unsigned>(1u, std::min<unsigned>(16u, std::thread::hardware_concurrency()));
   std::vector<std::thread> pool;
   std::vector<char> gen_flag((size_t)std::max<int64_t>(R, 1), 0);
+  for (auto *v : {&b->rod_A0, &b->rod_E0, &b->rod_lmin, &b->rod_lmax}) v->assign((size_t)std::max<int64_t>(R, 1), 0.0);
   auto rec_range = [&](int64_t ra, int64_t rb) {
   for (int64_t r = ra; r < rb; ++r) {
     const ElemMat m0 = mat_at(r, eoff[r]);
@@ -409,6 +432,15 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
     }
     fill_record(&b->rec[(size_t)r * ER_REC], m0);
     if (!uniform) gen_flag[r] = 1;
+    double lmin = d->rest_lengths[eoff[r]], lmax = lmin;
+    for (int64_t j = eoff[r] + 1; j < eoff[r + 1]; ++j) {
+      lmin = std::min(lmin, d->rest_lengths[j]);
+      lmax = std::max(lmax, d->rest_lengths[j]);
+    }
+    b->rod_A0[r] = m0.A;
+    b->rod_E0[r] = m0.E;
+    b->rod_lmin[r] = lmin;
+    b->rod_lmax[r] = lmax;
   }
   };
   if (R < 65536) rec_range(0, R);
@@ -721,7 +753,24 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
     return ER_OK;
   }
   while (done < n_steps) {
-    if (b->kernel_mode == 0 || b->kernel_mode == 2) {
+    if (b->contact_on) {  // NEXT-4: drift | contact (broad + narrow phase) | dynamics + kick | drift
+      p.n_steps = 1;
+      p.t = t;
+      p.cnode = b->cp.cnode;
+      p.cns = b->cp.ns;
+      CK(er_launch_step(&p, b->block, 1, 7, b->stream), "drift kernel");
+      p.cnode = nullptr;
+      CK(er_contact_eval(&b->cp, b->sort_tmp, b->sort_bytes, b->stream, &b->launches), "contact");
+      p.cfc = b->cp.fc;
+      p.cfs = b->cp.fs;
+      CK(er_launch_step(&p, b->block, 2, 7, b->stream), "dyn kernel");
+      p.cfc = nullptr;
+      CK(er_launch_step(&p, b->block, 1, 7, b->stream), "drift kernel");
+      b->launches += 3;
+      const double th = t + 0.5 * dt;
+      t = th + 0.5 * dt;
+      done += 1;
+    } else if (b->kernel_mode == 0 || b->kernel_mode == 2) {
       const int64_t k = std::min<int64_t>(b->steps_per_launch, n_steps - done);
       p.n_steps = (int32_t)k;
       p.t = t;
@@ -756,6 +805,133 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
     b->last_error = buf;
     return ER_EUNSTABLE;
   }
+  return ER_OK;
+}
+
+er_status er_set_contact(er_batch *b, const er_contact *c) {
+  if (!b) return ER_EINVAL;
+  if (!c || !c->enable) {
+    CK(cudaSetDevice(b->device), "cudaSetDevice");
+    CK(cudaStreamSynchronize(b->stream), "sync");
+    free_contact(b);
+    return ER_OK;
+  }
+  Errors err;
+  const int64_t R = b->n_rods, E = b->n_elems;
+  auto nonneg = [&](double x, const char *what) { if (!(std::isfinite(x) && x >= 0.0)) err.add("%s = %g must be finite and >= 0", what, x); };
+  if (!std::isfinite(c->k_n)) err.add("k_n = %g not finite", c->k_n);
+  nonneg(c->gamma_n, "gamma_n");
+  nonneg(c->mu_s, "mu_s");
+  nonneg(c->mu_k, "mu_k");
+  nonneg(c->v_stick, "v_stick");
+  nonneg(c->cell0, "cell0");
+  nonneg(c->pool_factor, "pool_factor");
+  if (c->exclude < 0) err.add("exclude = %d < 0", c->exclude);
+  if (c->n_levels < 0 || c->n_levels > ER_HHG_MAXLEV) err.add("n_levels = %d not in [0, %d]", c->n_levels, ER_HHG_MAXLEV);
+  double nn = 0.0;
+  if (c->plane_on) {
+    for (int q = 0; q < 3; ++q) if (!std::isfinite(c->plane_n[q])) err.add("plane_n[%d] not finite", q);
+    nn = std::sqrt(c->plane_n[0] * c->plane_n[0] + c->plane_n[1] * c->plane_n[1] + c->plane_n[2] * c->plane_n[2]);
+    if (!(nn > 0.0)) err.add("plane_n must be non-zero");
+    if (!std::isfinite(c->plane_d)) err.add("plane_d not finite");
+  }
+  if (c->radius)
+    for (int64_t r = 0; r < R; ++r)
+      if (!pos_finite(c->radius[r])) { err.add("radius[%lld] = %g must be positive and finite", (long long)r, c->radius[r]); break; }
+  if (E >= (1ll << 31) - 1) err.add("contact supports < 2^31 elements per batch (got %lld)", (long long)E);
+  if (err.count) { b->last_error = err.msg; return ER_EINVAL; }
+  CK(cudaSetDevice(b->device), "cudaSetDevice");
+  CK(cudaStreamSynchronize(b->stream), "sync");
+  free_contact(b);
+  ErContactParams &cp = b->cp;
+  ErContactLaw &L = cp.law;
+  L.k_n = c->k_n; L.gamma_n = c->gamma_n; L.mu_s = c->mu_s; L.mu_k = c->mu_k; L.v_stick = c->v_stick;
+  L.plane_on = c->plane_on ? 1 : 0;
+  for (int q = 0; q < 3; ++q) L.pn[q] = c->plane_on ? c->plane_n[q] / nn : 0.0;
+  L.pd = c->plane_d;
+  L.exclude = c->exclude;
+  // per-rod contact radius (default sqrt(A/pi)) and stiffness scale E r; rest capsule extents
+  std::vector<double> rad((size_t)std::max<int64_t>(R, 1)), kr((size_t)std::max<int64_t>(R, 1));
+  double xmin = 0.0, xmax = 0.0;
+  for (int64_t r = 0; r < R; ++r) {
+    rad[r] = c->radius ? c->radius[r] : std::sqrt(b->rod_A0[r] / 3.14159265358979323846);
+    kr[r] = b->rod_E0[r] * rad[r];
+    const double lo = b->rod_lmin[r] + 2.0 * rad[r], hi = b->rod_lmax[r] + 2.0 * rad[r];
+    xmin = r == 0 ? lo : std::min(xmin, lo);
+    xmax = r == 0 ? hi : std::max(xmax, hi);
+  }
+  // HHG levels: cell_l = cell0 2^l
+  double cell0 = c->cell0 > 0.0 ? c->cell0 : 1.25 * xmin;
+  int nlev = c->n_levels;
+  if (nlev == 0) {
+    nlev = 1;
+    while (nlev < ER_HHG_MAXLEV && cell0 * std::ldexp(1.0, nlev - 1) < 1.25 * xmax) ++nlev;
+    if (c->cell0 == 0.0 && cell0 * std::ldexp(1.0, nlev - 1) < 1.25 * xmax) cell0 = 1.25 * xmax / std::ldexp(1.0, nlev - 1);
+    nlev = std::min(nlev + 1, ER_HHG_MAXLEV);  // one level of headroom for stretched elements
+  }
+  if (R > 0 && !(cell0 > 0.0)) { b->last_error = "HHG cell size must be positive"; return ER_EINVAL; }
+  cp.nlev = nlev;
+  for (int l = 0; l < ER_HHG_MAXLEV; ++l) {
+    cp.cell[l] = cell0 * std::ldexp(1.0, l);
+    cp.icell[l] = 1.0 / cp.cell[l];
+  }
+  int hb = 10;
+  while (hb < 29 && (1ll << hb) < 2 * E) ++hb;
+  cp.hbits = hb;
+  cp.n_elems = E; cp.n_nodes = b->n_nodes; cp.n_rods = R;
+  cp.ns = b->n_nodes;
+  cp.fs = b->ne;
+  const double pf = c->pool_factor > 0.0 ? c->pool_factor : 4.0;
+  cp.pcap = std::max<int64_t>(1024, (int64_t)(pf * (double)E));
+  std::vector<int32_t> erod((size_t)std::max<int64_t>(E, 1));
+  for (int64_t r = 0; r < R; ++r)
+    for (int64_t j = b->eoff[r]; j < b->eoff[r + 1]; ++j) erod[j] = (int32_t)r;
+  double *d_rad = nullptr, *d_kr = nullptr;
+  int32_t *d_erod = nullptr;
+  const int64_t T = 1ll << hb;
+#define CA(ptr, n) CK(dalloc(b, &(ptr), (n)), "cudaMalloc(contact)")
+  CA(d_rad, R); CA(d_kr, R); CA(d_erod, E);
+  cp.rad = d_rad; cp.kr = d_kr; cp.erod = d_erod;
+  CA(cp.cnode, 6 * b->n_nodes);
+  CA(cp.key, E); CA(cp.key_s, E); CA(cp.val, E); CA(cp.val_s, E);
+  CA(cp.cstart, T); CA(cp.cend, T);
+  CA(cp.p01, 6 * E); CA(cp.v01, 6 * E); CA(cp.meta, E); CA(cp.cellc, E);
+  CA(cp.fc, 6 * b->ne);
+  CA(cp.head, E); CA(cp.pnext, cp.pcap); CA(cp.psrc, cp.pcap); CA(cp.pf, 6 * cp.pcap);
+  CA(cp.ctr, 8);
+#undef CA
+  cp.fault = b->d_fault;
+  CK(er_contact_sort_bytes(E, hb, &b->sort_bytes), "cub sort size");
+  CK(cudaMalloc(&b->sort_tmp, std::max<size_t>(b->sort_bytes, 16)), "cudaMalloc(sort)");
+  b->device_bytes += (int64_t)b->sort_bytes;
+  if (R > 0) {
+    CK(cudaMemcpyAsync(d_rad, rad.data(), sizeof(double) * R, cudaMemcpyHostToDevice, b->stream), "H2D rad");
+    CK(cudaMemcpyAsync(d_kr, kr.data(), sizeof(double) * R, cudaMemcpyHostToDevice, b->stream), "H2D kr");
+    CK(cudaMemcpyAsync(d_erod, erod.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice, b->stream), "H2D erod");
+  }
+  CK(cudaMemsetAsync(cp.ctr, 0, 8 * sizeof(unsigned long long), b->stream), "memset");
+  CK(cudaMemsetAsync(cp.fc, 0, 6 * sizeof(double) * b->ne, b->stream), "memset");
+  CK(cudaStreamSynchronize(b->stream), "sync");
+  b->contact_on = true;
+  return ER_OK;
+}
+
+er_status er_get_contact_stats(er_batch *b, er_contact_stats *out) {
+  if (!b || !out) return ER_EINVAL;
+  std::memset(out, 0, sizeof *out);
+  if (!b->contact_on) return ER_OK;
+  CK(cudaSetDevice(b->device), "cudaSetDevice");
+  unsigned long long c[8];
+  CK(cudaMemcpyAsync(c, b->cp.ctr, sizeof c, cudaMemcpyDeviceToHost, b->stream), "D2H contact stats");
+  CK(cudaStreamSynchronize(b->stream), "sync");
+  out->candidates = (int64_t)c[1];
+  out->contacts = (int64_t)c[2];
+  out->cross_level = (int64_t)c[3];
+  out->plane_contacts = (int64_t)c[5];
+  out->pool_used = (int64_t)c[0];
+  out->n_levels = b->cp.nlev;
+  out->level_mask = (int32_t)c[4];
+  out->cell0 = b->cp.cell[0];
   return ER_OK;
 }
 

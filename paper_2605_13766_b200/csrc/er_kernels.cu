@@ -58,6 +58,20 @@ __device__ __forceinline__ void finish_slot(SlotInfo &si) {
   si.cl_elem = si.has_e && ((clamp == 1 && si.i == 0) || (clamp == 2 && si.i == si.N - 1));
 }
 
+// Contact force on node i (NEXT-4, DESIGN §3 #27): er_contact.cu left, per element j, the force
+// on its nodes j and j+1 in ErContactParams.fc (half-space forces included); node i collects
+// element i's first and element i-1's second share.
+__device__ __forceinline__ void contact_node_force(const ErStepParams &p, const SlotInfo &si, double F[3]) {
+  if (si.has_e) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) F[c] += __ldg(p.cfc + c * p.cfs + si.elem);
+  }
+  if (si.i >= 1) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) F[c] += __ldg(p.cfc + (3 + c) * p.cfs + si.elem - 1);
+  }
+}
+
 __device__ __forceinline__ int rec_flags(const double *rec) {
   return (int)__double_as_longlong(rec[REC_FLAGS]);
 }
@@ -199,6 +213,7 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
 #pragma unroll
         for (int c = 0; c < 3; ++c) F[c] += rec[REC_TIPX + c];
       }
+      if (EXTRA && p.cfc) contact_node_force(p, si, F);  // NEXT-4: rod-rod + half-space contact
       const double im = general ? gp(GP_IM) : rec[REC_IM] * ((i == 0 || i == N) ? 2.0 : 1.0);
       const double nu = rec[REC_NU];
 #pragma unroll
@@ -570,6 +585,13 @@ __global__ void __launch_bounds__(BLOCK, MINB) simple_kernel(const ErStepParams 
     for (int c = 0; c < 3; ++c) {
       __stcs(G + c * ns + s, r[c]);
       __stcs(G + (3 + c) * ns + s, v[c]);
+    }
+    if (MODE == MODE_DRIFT && p.cnode) {  // contact: positions after drift-1 (and v^n) for the broad phase
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        p.cnode[c * p.cns + si.node] = r[c];
+        p.cnode[(3 + c) * p.cns + si.node] = v[c];
+      }
     }
   }
   if (si.has_e) {

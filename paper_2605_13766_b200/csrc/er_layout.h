@@ -18,6 +18,7 @@
 // Ghost nodes exist only in shared memory, never in HBM.
 #pragma once
 #include <stdint.h>
+#include <vector_types.h>
 
 #ifndef __CUDACC__
 #define __host__
@@ -91,6 +92,49 @@ struct __align__(16) ErTile {
   int64_t pad_;
 };
 
+// Contact law (DESIGN §3 #27): penalty normal force with damping, regularised
+// Coulomb friction, optional half-space n.x >= d.
+struct ErContactLaw {
+  double k_n;             // > 0: fixed stiffness; else min(E_a r_a, E_b r_b) per pair (kr below)
+  double gamma_n;
+  double mu_s, mu_k, v_stick;
+  double pn[3], pd;       // plane (unit normal, offset)
+  int32_t plane_on;
+  int32_t exclude;        // same-rod pairs with |j - k| <= exclude never touch
+};
+
+// Broad phase (hierarchical hash grid) + narrow phase buffers, all device memory.
+#define ER_HHG_MAXLEV 8
+struct ErContactParams {
+  ErContactLaw law;
+  double cell[ER_HHG_MAXLEV];   // cell size of level l (= cell[0] * 2^l)
+  double icell[ER_HHG_MAXLEV];
+  int32_t nlev;
+  int32_t hbits;                // hash table size 2^hbits per level
+  int64_t n_elems, n_nodes, n_rods;
+  const double *rad;            // [R] contact radius
+  const double *kr;             // [R] E r (pair stiffness scale)
+  const int32_t *erod;          // [E] rod of each element
+  double *cnode;                // [6][ns] canonical node r, v after drift-1
+  int64_t ns;
+  uint32_t *key, *key_s;        // [E] cell keys, unsorted / sorted
+  int32_t *val, *val_s;         // [E] element ids, unsorted / sorted
+  int32_t *cstart, *cend;       // [nlev << hbits] sorted-proxy range of each hash bucket
+  double *p01;                  // [E][6] sorted proxies: segment end points
+  double *v01;                  // [E][6] sorted proxies: end-point velocities
+  int4 *meta;                   // [E] sorted proxies: elem, rod, level, 0
+  int4 *cellc;                  // [E] sorted proxies: cell x, y, z, level
+  double *fc;                   // [6][fs] contact force on the element's (node j, node j+1)
+  int64_t fs;
+  int32_t *head;                // [E] cross-level records per coarse element (-1 = none)
+  int32_t *pnext, *psrc;        // [pcap] record chain / source (fine) element
+  double *pf;                   // [pcap][6] record force on the coarse element's two nodes
+  int64_t pcap;
+  unsigned long long *ctr;      // [8]: 0 pool used, 1 AABB candidates, 2 contacts, 3 cross-level
+                                //      contacts, 4 level mask, 5 plane contacts, 6 max bucket
+  unsigned long long *fault;    // shared with the step kernels
+};
+
 struct ErStepParams {
   double *state;          // tile-blocked state
   const double *rec;
@@ -119,6 +163,11 @@ struct ErStepParams {
   unsigned long long *fault;  // [0] = OR of bits, [1] = min rod id
   double *diag_partial;   // diagnostics: [n_tiles][16]
   unsigned long long *trace;  // optional timeline (measurement aid): [cta][ER_TRACE_ITERS][4]
+  // contact (NEXT-4): null cfc = rods do not interact
+  const double *cfc;      // [6][cfs] contact force on each element's two nodes (ErContactParams.fc)
+  int64_t cfs;
+  double *cnode;          // drift-1 stage: canonical node planes r, v for the broad phase
+  int64_t cns;
 };
 #define ER_TRACE_ITERS 64
 

@@ -244,7 +244,7 @@ def _rod_material(R, radius, E, rho=1000.0, alpha_c=4.0 / 3.0):
 # the five configs (BASELINE.json configs[0..4])
 # ---------------------------------------------------------------------------
 
-EXTRA_CONFIGS = ("cilia8", "ciliafarm")
+EXTRA_CONFIGS = ("cilia8", "ciliafarm", "fibres")
 
 
 def make(name: str, n_rods: Optional[int] = None, n_steps: Optional[int] = None) -> Workload:
@@ -252,7 +252,7 @@ def make(name: str, n_rods: Optional[int] = None, n_steps: Optional[int] = None)
     the batch (a different seeded draw of the same recipe); use `.subset()` to sample rods of the
     full draw."""
     if name in EXTRA_CONFIGS:
-        w = _cilia(name, n_rods)
+        w = _fibres(n_rods) if name == "fibres" else _cilia(name, n_rods)
         if n_steps is not None:
             w.n_steps = int(n_steps)
         return w
@@ -425,3 +425,52 @@ def _cilia(name, n_rods):
                     damping=np.full(R, c["damping"]), magnetization=_expand(mag_rod, n_elems),
                     b_field=np.array([c["b"], 0.0, 0.0]), b_omega=2.0 * math.pi * c["beat_hz"],
                     b_axis=np.array([0.0, 1.0, 0.0]), dt=c["dt"], n_steps=20000)
+
+
+# ---------------------------------------------------------------------------
+# NEXT-4: contact stand-in for the fibrous-packing study (1536 filaments,
+# frictional rod-rod and rod-boundary contact, HHG broad phase).  The paper's packing parameters
+# live in its missing supplement; this is a synthetic recipe with cfg3's rods (L = 0.1, r = 1e-3,
+# E = 1e6, 16 elements): stacks of crossed layers ("woven mats") resting on a floor, every layer
+# pressed into the next by a small overlap, so contacts exist from the first step.
+# ---------------------------------------------------------------------------
+FIBRES = dict(N=16, L=0.1, radius=1e-3, E=1e6, rho=1000.0, per_layer=16, layers=16, overlap=2e-6,
+              jitter_angle=0.02, v_sd=1e-4, damping=0.1, gamma_n=0.02, mu=0.4, v_stick=1e-3,
+              dt=1e-6)
+
+
+def _fibres(n_rods):
+    """Rods fill stacks (layer by layer) of `layers` x `per_layer` rods; stacks sit on a square
+    grid of pitch 1.2 L.  Layer k of a stack: rods along x (k even) or y (k odd), evenly spaced
+    across the stack's L x L footprint, in-plane angle jitter U(-0.02, 0.02) rad, height
+    z_k = r - overlap/2 + k (2r - overlap) + U(-overlap/4, overlap/4) (the bottom layer presses into
+    the floor z = 0 by overlap/2 +- overlap/4); velocities N(0, 1e-4) per component.  Default full size: 256 stacks
+    of 16 x 16 rods = 65,536 rods x 16 elements (1,048,576 elements, cfg3's element count)."""
+    c = FIBRES
+    rng = np.random.Generator(np.random.Philox(SEED_BASE + 6))
+    per_stack = c["layers"] * c["per_layer"]
+    R = 256 * per_stack if n_rods is None else int(n_rods)
+    N, L, r, ov = c["N"], c["L"], c["radius"], c["overlap"]
+    ids = np.arange(R)
+    stack, k, j = ids // per_stack, (ids % per_stack) // c["per_layer"], ids % c["per_layer"]
+    G = max(1, int(math.ceil(math.sqrt(max(1, (R + per_stack - 1) // per_stack)))))
+    ox, oy = (stack % G) * 1.2 * L, (stack // G) * 1.2 * L
+    phi = np.where(k % 2 == 0, 0.0, 0.5 * math.pi) + rng.uniform(-c["jitter_angle"], c["jitter_angle"], R)
+    z = r - ov / 2 + k * (2 * r - ov) + rng.uniform(-ov / 4, ov / 4, R)
+    across = (j + 0.5) * L / c["per_layer"]
+    cx = ox + np.where(k % 2 == 0, 0.5 * L, across)
+    cy = oy + np.where(k % 2 == 0, across, 0.5 * L)
+    d3 = np.stack([np.cos(phi), np.sin(phi), np.zeros(R)], axis=1)
+    base = np.stack([cx, cy, z], axis=1) - 0.5 * L * d3
+    n_elems = np.full(R, N, np.int32)
+    lhat = np.full(R, L / N)
+    frames = complete_frame(d3)
+    pos = straight_rods(n_elems, lhat, base, d3)
+    vel = rng.normal(0.0, c["v_sd"], pos.shape)
+    mat = _rod_material(R, r, c["E"], rho=c["rho"])
+    contact = Contact(k_n=0.0, gamma_n=c["gamma_n"], mu_s=c["mu"], mu_k=c["mu"], v_stick=c["v_stick"],
+                      exclude=2, plane_n=np.array([0.0, 0.0, 1.0]), plane_d=0.0)
+    return Workload("fibres", n_elems, _expand(lhat, n_elems), **mat, positions=pos, velocities=vel,
+                    directors=_expand(frames, n_elems), omega=np.zeros((R * N, 3)),
+                    clamp=np.full(R, -1, np.int8), gravity=np.array([0.0, 0.0, -9.81]),
+                    damping=np.full(R, c["damping"]), dt=c["dt"], n_steps=1000, contact=contact)
