@@ -235,8 +235,14 @@ er_status er_fault(const er_batch *b, int64_t *rod, int32_t *bits);
  *              (lhat + 2r).  n_levels (1..8); 0 = auto: enough levels of doubling cells for the
  *              largest rest extent x 1.25, plus one level of headroom.
  *  pool_factor cross-level record pool = pool_factor x n_elems records (0 = auto, 4).
+ *  skin        Verlet skin (m; 0 = auto: a quarter of the smallest contact radius).  The broad
+ *              phase bins capsule AABBs grown by skin/2 and its candidate lists are reused until
+ *              a node has moved more than skin/2 from where it was at the last build (checked on
+ *              the device every step; the lists are then rebuilt in the same step).  Results do
+ *              not depend on the skin beyond round-off of the summation order.
  * An element whose AABB outgrows the top level, or a full pool, faults the step with
- * ER_F_CONTACT.  c == NULL or c->enable == 0 disables contact.  Errors: ER_EINVAL, ER_ENOMEM.
+ * ER_F_CONTACT.  c == NULL or c->enable == 0 disables contact.
+ * Errors: ER_EINVAL, ER_ENOMEM.
  */
 typedef struct {
   int32_t enable;
@@ -249,19 +255,26 @@ typedef struct {
   double cell0;
   int32_t n_levels;
   double pool_factor;
+  double skin;
 } er_contact;
 er_status er_set_contact(er_batch *b, const er_contact *c);
 
-/* Contact statistics of the last step of the last er_step call (synchronises the stream). */
+/* Contact statistics (synchronises the stream): per step = of the last step of the last er_step
+ * call; per build = of the last candidate-list build. */
 typedef struct {
-  int64_t candidates;      /* element pairs whose AABBs overlap (each pair once)        */
-  int64_t contacts;        /* element pairs in contact (gap < 0)                         */
-  int64_t cross_level;     /* of those, pairs across HHG levels                          */
-  int64_t plane_contacts;  /* nodes in contact with the half-space                       */
-  int64_t pool_used;       /* cross-level records written                                */
-  int32_t n_levels;        /* HHG levels configured                                      */
-  int32_t level_mask;      /* levels populated (bit l)                                   */
-  double cell0;            /* finest cell size                                           */
+  int64_t candidates;      /* build: element pairs whose grown AABBs overlap (each pair once) */
+  int64_t contacts;        /* step:  element pairs in contact (gap < 0)                       */
+  int64_t cross_level;     /* step:  of those, pairs across HHG levels                        */
+  int64_t plane_contacts;  /* step:  nodes in contact with the half-space                     */
+  int64_t pool_used;       /* step:  cross-level records written                              */
+  int64_t list_entries;    /* build: candidate-list entries (both sides of a pair)            */
+  int64_t scanned;         /* build: proxies the broad phase scanned (its work measure)       */
+  int64_t long_lists;      /* build: elements with more than 16 candidates (re-visited)       */
+  int64_t builds;          /* list builds so far                                              */
+  int32_t n_levels;        /* HHG levels configured                                           */
+  int32_t level_mask;      /* build: levels populated (bit l)                                 */
+  double cell0;            /* finest cell size                                                */
+  double skin;             /* Verlet skin in use                                              */
 } er_contact_stats;
 er_status er_get_contact_stats(er_batch *b, er_contact_stats *out);
 

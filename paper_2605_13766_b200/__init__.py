@@ -71,14 +71,16 @@ class er_contact(C.Structure):
         ("mu_k", C.c_double), ("v_stick", C.c_double), ("radius", _dp), ("exclude", C.c_int32),
         ("plane_on", C.c_int32), ("plane_n", C.c_double * 3), ("plane_d", C.c_double),
         ("cell0", C.c_double), ("n_levels", C.c_int32), ("pool_factor", C.c_double),
+        ("skin", C.c_double),
     ]
 
 
 class er_contact_stats(C.Structure):
     _fields_ = [
         ("candidates", C.c_int64), ("contacts", C.c_int64), ("cross_level", C.c_int64),
-        ("plane_contacts", C.c_int64), ("pool_used", C.c_int64), ("n_levels", C.c_int32),
-        ("level_mask", C.c_int32), ("cell0", C.c_double),
+        ("plane_contacts", C.c_int64), ("pool_used", C.c_int64), ("list_entries", C.c_int64),
+        ("scanned", C.c_int64), ("long_lists", C.c_int64), ("builds", C.c_int64),
+        ("n_levels", C.c_int32), ("level_mask", C.c_int32), ("cell0", C.c_double), ("skin", C.c_double),
     ]
 
 
@@ -317,7 +319,8 @@ class RodBatch:
                          musc_T=getattr(w, "musc_T", None), musc_lambda=getattr(w, "musc_lambda", None),
                          musc_phi=getattr(w, "musc_phi", None), musc_component=getattr(w, "musc_component", 0))
 
-    def set_contact(self, c=None, cell0: float = 0.0, n_levels: int = 0, pool_factor: float = 0.0):
+    def set_contact(self, c=None, cell0: float = 0.0, n_levels: int = 0, pool_factor: float = 0.0,
+                    skin: float = 0.0):
         """Enable rod-rod / half-space contact from an object with the attributes of
         workloads.Contact (k_n, gamma_n, mu_s, mu_k, v_stick, radius, exclude, plane_n, plane_d);
         None disables it."""
@@ -338,6 +341,7 @@ class RodBatch:
         s.cell0 = float(getattr(c, "cell0", cell0) or cell0)
         s.n_levels = int(getattr(c, "n_levels", n_levels) or n_levels)
         s.pool_factor = float(pool_factor)
+        s.skin = float(skin)
         er_set_contact(self.handle, s)
 
     def contact_stats(self) -> er_contact_stats:

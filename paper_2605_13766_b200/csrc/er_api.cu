@@ -30,8 +30,8 @@ cudaError_t er_launch_validate(const double *aos, int64_t n, int k, int orth, do
 cudaError_t er_launch_apply_forcing(double *rec, int64_t n_rods, const int32_t *flags, const double *damping,
                                     double damping_all, const double *tip, const double *actA, const double *actF,
                                     const double *actL, int forcing, cudaStream_t st);
-cudaError_t er_contact_sort_bytes(int64_t n, int bits, size_t *bytes);
-cudaError_t er_contact_eval(const ErContactParams *p, void *sort_tmp, size_t sort_bytes, cudaStream_t st,
+cudaError_t er_contact_tmp_bytes(int64_t n, int bits, size_t *bytes);
+cudaError_t er_contact_eval(const ErContactParams *p, void *sort_tmp, size_t sort_bytes, int build, cudaStream_t st,
                             int64_t *launches);
 }
 
@@ -148,8 +148,9 @@ cudaError_t dalloc(er_batch *b, T **p, int64_t count) {
 
 void free_contact(er_batch *b) {
   ErContactParams &c = b->cp;
-  void *ptrs[] = {(void *)c.rad, (void *)c.kr, (void *)c.erod, c.cnode, c.key, c.key_s, c.val, c.val_s, c.cstart,
-                  c.cend, c.p01, c.v01, c.meta, c.cellc, c.fc, c.head, c.pnext, c.psrc, c.pf, c.ctr, b->sort_tmp};
+  void *ptrs[] = {(void *)c.rad, (void *)c.kr, (void *)c.erod, c.cnode, c.cbuild, c.rebuild, c.gext, c.gdim, c.key,
+                  c.key_s, c.val, c.val_s, c.table, c.code_s, c.boxa, c.boxb, c.qidx, c.cnt, c.cand, c.fc, c.head,
+                  c.pnext, c.psrc, c.pf, c.ctr, c.bctr, b->sort_tmp};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   b->cp = ErContactParams{};
@@ -757,10 +758,12 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
       p.n_steps = 1;
       p.t = t;
       p.cnode = b->cp.cnode;
-      p.cns = b->cp.ns;
+      p.cbuild = b->cp.cbuild;
+      p.disp2 = 0.25 * b->cp.skin * b->cp.skin;
+      p.rebuild = b->cp.rebuild;
       CK(er_launch_step(&p, b->block, 1, 7, b->stream), "drift kernel");
       p.cnode = nullptr;
-      CK(er_contact_eval(&b->cp, b->sort_tmp, b->sort_bytes, b->stream, &b->launches), "contact");
+      CK(er_contact_eval(&b->cp, b->sort_tmp, b->sort_bytes, 1, b->stream, &b->launches), "contact");
       p.cfc = b->cp.fc;
       p.cfs = b->cp.fs;
       CK(er_launch_step(&p, b->block, 2, 7, b->stream), "dyn kernel");
@@ -826,6 +829,7 @@ er_status er_set_contact(er_batch *b, const er_contact *c) {
   nonneg(c->v_stick, "v_stick");
   nonneg(c->cell0, "cell0");
   nonneg(c->pool_factor, "pool_factor");
+  nonneg(c->skin, "skin");
   if (c->exclude < 0) err.add("exclude = %d < 0", c->exclude);
   if (c->n_levels < 0 || c->n_levels > ER_HHG_MAXLEV) err.add("n_levels = %d not in [0, %d]", c->n_levels, ER_HHG_MAXLEV);
   double nn = 0.0;
@@ -838,7 +842,7 @@ er_status er_set_contact(er_batch *b, const er_contact *c) {
   if (c->radius)
     for (int64_t r = 0; r < R; ++r)
       if (!pos_finite(c->radius[r])) { err.add("radius[%lld] = %g must be positive and finite", (long long)r, c->radius[r]); break; }
-  if (E >= (1ll << 31) - 1) err.add("contact supports < 2^31 elements per batch (got %lld)", (long long)E);
+  if (E >= (1ll << 30)) err.add("contact supports < 2^30 elements per batch (got %lld)", (long long)E);
   if (err.count) { b->last_error = err.msg; return ER_EINVAL; }
   CK(cudaSetDevice(b->device), "cudaSetDevice");
   CK(cudaStreamSynchronize(b->stream), "sync");
@@ -860,6 +864,12 @@ er_status er_set_contact(er_batch *b, const er_contact *c) {
     xmin = r == 0 ? lo : std::min(xmin, lo);
     xmax = r == 0 ? hi : std::max(xmax, hi);
   }
+  // Verlet skin (default: a quarter of the smallest contact radius)
+  double rmin = 0.0;
+  for (int64_t r = 0; r < R; ++r) rmin = r == 0 ? rad[r] : std::min(rmin, rad[r]);
+  cp.skin = c->skin > 0.0 ? c->skin : 0.25 * rmin;
+  xmin += cp.skin;
+  xmax += cp.skin;
   // HHG levels: cell_l = cell0 2^l
   double cell0 = c->cell0 > 0.0 ? c->cell0 : 1.25 * xmin;
   int nlev = c->n_levels;
@@ -879,10 +889,10 @@ er_status er_set_contact(er_batch *b, const er_contact *c) {
   while (hb < 29 && (1ll << hb) < 2 * E) ++hb;
   cp.hbits = hb;
   cp.n_elems = E; cp.n_nodes = b->n_nodes; cp.n_rods = R;
-  cp.ns = b->n_nodes;
   cp.fs = b->ne;
   const double pf = c->pool_factor > 0.0 ? c->pool_factor : 4.0;
   cp.pcap = std::max<int64_t>(1024, (int64_t)(pf * (double)E));
+
   std::vector<int32_t> erod((size_t)std::max<int64_t>(E, 1));
   for (int64_t r = 0; r < R; ++r)
     for (int64_t j = b->eoff[r]; j < b->eoff[r + 1]; ++j) erod[j] = (int32_t)r;
@@ -892,16 +902,18 @@ er_status er_set_contact(er_batch *b, const er_contact *c) {
 #define CA(ptr, n) CK(dalloc(b, &(ptr), (n)), "cudaMalloc(contact)")
   CA(d_rad, R); CA(d_kr, R); CA(d_erod, E);
   cp.rad = d_rad; cp.kr = d_kr; cp.erod = d_erod;
-  CA(cp.cnode, 6 * b->n_nodes);
+  CA(cp.cnode, 6 * b->n_nodes); CA(cp.cbuild, 3 * b->n_nodes); CA(cp.rebuild, 1);
+  CA(cp.gext, 3 * ER_HHG_MAXLEV); CA(cp.gdim, 4 * ER_HHG_MAXLEV);
   CA(cp.key, E); CA(cp.key_s, E); CA(cp.val, E); CA(cp.val_s, E);
-  CA(cp.cstart, T); CA(cp.cend, T);
-  CA(cp.p01, 6 * E); CA(cp.v01, 6 * E); CA(cp.meta, E); CA(cp.cellc, E);
+  CA(cp.table, T); CA(cp.code_s, E);
+  CA(cp.boxa, E); CA(cp.boxb, E); CA(cp.qidx, E);
+  CA(cp.cnt, E); CA(cp.cand, ER_CAND_K * E);
   CA(cp.fc, 6 * b->ne);
   CA(cp.head, E); CA(cp.pnext, cp.pcap); CA(cp.psrc, cp.pcap); CA(cp.pf, 6 * cp.pcap);
-  CA(cp.ctr, 8);
+  CA(cp.ctr, 8); CA(cp.bctr, 8);
 #undef CA
   cp.fault = b->d_fault;
-  CK(er_contact_sort_bytes(E, hb, &b->sort_bytes), "cub sort size");
+  CK(er_contact_tmp_bytes(E, hb, &b->sort_bytes), "cub temp size");
   CK(cudaMalloc(&b->sort_tmp, std::max<size_t>(b->sort_bytes, 16)), "cudaMalloc(sort)");
   b->device_bytes += (int64_t)b->sort_bytes;
   if (R > 0) {
@@ -910,6 +922,8 @@ er_status er_set_contact(er_batch *b, const er_contact *c) {
     CK(cudaMemcpyAsync(d_erod, erod.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice, b->stream), "H2D erod");
   }
   CK(cudaMemsetAsync(cp.ctr, 0, 8 * sizeof(unsigned long long), b->stream), "memset");
+  CK(cudaMemsetAsync(cp.bctr, 0, 8 * sizeof(unsigned long long), b->stream), "memset");
+  CK(cudaMemsetAsync(cp.rebuild, 1, sizeof(int32_t), b->stream), "memset");
   CK(cudaMemsetAsync(cp.fc, 0, 6 * sizeof(double) * b->ne, b->stream), "memset");
   CK(cudaStreamSynchronize(b->stream), "sync");
   b->contact_on = true;
@@ -921,16 +935,22 @@ er_status er_get_contact_stats(er_batch *b, er_contact_stats *out) {
   std::memset(out, 0, sizeof *out);
   if (!b->contact_on) return ER_OK;
   CK(cudaSetDevice(b->device), "cudaSetDevice");
-  unsigned long long c[8];
+  unsigned long long c[8], bc[8];
   CK(cudaMemcpyAsync(c, b->cp.ctr, sizeof c, cudaMemcpyDeviceToHost, b->stream), "D2H contact stats");
+  CK(cudaMemcpyAsync(bc, b->cp.bctr, sizeof bc, cudaMemcpyDeviceToHost, b->stream), "D2H contact stats");
   CK(cudaStreamSynchronize(b->stream), "sync");
-  out->candidates = (int64_t)c[1];
-  out->contacts = (int64_t)c[2];
-  out->cross_level = (int64_t)c[3];
-  out->plane_contacts = (int64_t)c[5];
+  out->candidates = (int64_t)bc[0];
+  out->list_entries = (int64_t)bc[1];
+  out->scanned = (int64_t)bc[2];
+  out->long_lists = (int64_t)bc[4];
+  out->builds = (int64_t)bc[5];
+  out->contacts = (int64_t)c[1];
+  out->cross_level = (int64_t)c[2];
+  out->plane_contacts = (int64_t)c[3];
   out->pool_used = (int64_t)c[0];
+  out->skin = b->cp.skin;
   out->n_levels = b->cp.nlev;
-  out->level_mask = (int32_t)c[4];
+  out->level_mask = (int32_t)bc[3];
   out->cell0 = b->cp.cell[0];
   return ER_OK;
 }
@@ -961,6 +981,7 @@ er_status er_set_state(er_batch *b, int32_t src_mem, const double *positions, co
   if (velocities && (st = upload_field(b, velocities, src_mem, FIELD_VEL, false)) != ER_OK) return st;
   if (directors && (st = upload_field(b, directors, src_mem, FIELD_DIR, false)) != ER_OK) return st;
   if (omega && (st = upload_field(b, omega, src_mem, FIELD_OMEGA, false)) != ER_OK) return st;
+  if (b->contact_on && positions) CK(cudaMemsetAsync(b->cp.rebuild, 1, sizeof(int32_t), b->stream), "memset");
   CK(cudaStreamSynchronize(b->stream), "cudaStreamSynchronize");
   if (t) b->t = *t;
   return ER_OK;

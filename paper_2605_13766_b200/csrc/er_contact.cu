@@ -6,19 +6,35 @@
 // (PAPER.md:86).  Readings: DESIGN.md §3 #27.  Contact forces are evaluated once per step, at
 // the half-step configuration (after drift-1) with v^n, like every other force (reading #12).
 //
-// Per step, after the drift-1 kernel has written the canonical node planes (r, v):
-//   hhg_keys    one thread per element: capsule AABB, HHG level (smallest cell >= the AABB's
-//               largest extent), cell of the AABB centre, hashed key
+// Broad phase with Verlet lists (the standard neighbour-list reuse of particle codes): proxies
+// are capsule AABBs grown by skin/2, so a candidate list built now stays a superset of the
+// touching pairs until some node has moved skin/2 from its build position (a pair's distance
+// then dropped by less than skin).  The drift-1 kernel, which writes the node planes (r, v),
+// checks that bound and raises a device flag; the build kernels below run their work only
+// when it is set (no host round trip).
+//
+// Build (flagged steps only):
+//   hhg_aabb     one thread per element: grown AABB, its HHG level (the smallest level whose
+//                cell is >= the AABB's largest extent), per level and axis the
+//                largest extent (warp-reduced atomicMax) -> query margins and cell boxes
+//   hhg_dims     cell box of each level: per axis the largest extent of its proxies (>= 1/4 of
+//                the largest axis) -- anisotropic boxes for flat packings
+//   hhg_keys     cell of each AABB centre at its level, hashed bucket key; build positions
 //   CUB radix sort of (key, element) -- stable, so a bucket lists its elements in id order
-//   hhg_cells   bucket ranges; proxies gathered into sorted (spatially coherent) order
-//   hhg_narrow  one thread per sorted proxy a: the 27 cells around a at a's level and at every
-//               coarser populated level; per candidate b the AABB test, the exact segment-segment
-//               closest points, the penalty + friction law.  Same-level pairs are evaluated by
-//               BOTH proxies (gather, no atomics) in one canonical order (lower element id first),
-//               so the two sides compute bit-identical forces; a pair across levels is evaluated
-//               once, by the finer proxy, which leaves a record for the coarser one.
-//   hhg_finish  one thread per element: cross-level records summed in source-id order, the
-//               half-space law on the element's node(s), result in fc.
+//   hhg_cells    sorted float AABB records and cell codes
+//   hhg_table    per bucket: (range, the cell code when all its proxies share one cell, else MIXED)
+//   hhg_broad    one thread per sorted proxy a: the cells around a's AABB (margin: the largest
+//                half extent at that level) at a's level and every coarser populated level;
+//                conservative float AABB test + same-rod exclusion -> a's candidate list
+// Every step:
+//   hhg_narrow   one thread per element a: exact segment-segment closest points and the
+//                penalty + friction law for each candidate, gathered into a's two nodes.  Pairs
+//                within a level are evaluated by BOTH elements (no atomics) in one canonical
+//                order (lower element id first), so the two sides compute bit-identical forces;
+//                a pair across levels is evaluated once, by the finer element, which leaves a
+//                record for the coarser one.
+//   hhg_finish   one thread per element: cross-level records summed in source-id order, the
+//                half-space law on the element's node(s).
 // Every sum has a fixed order: results are bitwise reproducible run to run.
 //
 // This file is compiled with -fmad=false: the closest-point selection and the contact / friction
@@ -36,6 +52,8 @@
 namespace erc {
 
 constexpr unsigned long long F_CONTACT = 16ull;  // ER_F_CONTACT (include/er.h)
+constexpr int CBITS = 20;                        // cell index bits per axis in a cell code
+constexpr int CHALF = 1 << (CBITS - 1);
 
 __device__ __forceinline__ void flag_fault(const ErContactParams &p, int rod) {
   atomicOr(p.fault, F_CONTACT);
@@ -46,6 +64,10 @@ __device__ __forceinline__ uint32_t cell_hash(int cx, int cy, int cz, int l, int
   const uint32_t h = ((uint32_t)cx * 73856093u) ^ ((uint32_t)cy * 19349663u) ^ ((uint32_t)cz * 83492791u) ^
                      ((uint32_t)l * 2654435761u);
   return h & ((1u << hbits) - 1u);
+}
+__device__ __forceinline__ long long cell_code(int cx, int cy, int cz, int l) {
+  return ((long long)l << (3 * CBITS)) | ((long long)(cx + CHALF) << (2 * CBITS)) |
+         ((long long)(cy + CHALF) << CBITS) | (long long)(cz + CHALF);
 }
 
 // AABB of the capsule (segment p0-p1, radius r).
@@ -58,73 +80,246 @@ __device__ __forceinline__ void capsule_aabb(const double p0[3], const double p1
   }
 }
 
-// HHG level and cell of a proxy: the smallest level whose cell is >= the AABB's largest extent
-// (SPEC.md:339), cell of the AABB centre.  Returns false when the proxy cannot be binned
-// (wider than the top level, non-finite, or a cell index beyond +-2^30).
-__device__ __forceinline__ bool proxy_cell(const ErContactParams &p, const double lo[3], const double hi[3], int &l,
-                                           int c[3]) {
+// HHG level of an AABB: the smallest level whose cell is >= its largest extent.  false when it
+// is wider than the top level (or not finite).
+__device__ __forceinline__ bool proxy_level(const ErContactParams &p, const double lo[3], const double hi[3], int &l) {
   const double w = fmax(hi[0] - lo[0], fmax(hi[1] - lo[1], hi[2] - lo[2]));
   l = 0;
   while (l < p.nlev - 1 && w > p.cell[l]) ++l;
-  bool ok = w <= p.cell[l];
+  return w <= p.cell[l];
+}
+
+// Segment of element e: its two nodes, 96 contiguous bytes of the AoS node array.
+__device__ __forceinline__ void load_seg(const ErContactParams &p, int64_t e, int &rod, double p0[3], double p1[3]) {
+  rod = __ldg(p.erod + e);
+  const double *x = p.cnode + 6 * (e + rod);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    p0[c] = x[c];
+    p1[c] = x[6 + c];
+  }
+}
+
+__device__ __forceinline__ double grown(const ErContactParams &p, int rod) { return __ldg(p.rad + rod) + 0.5 * p.skin; }
+
+__device__ __forceinline__ void atomic_max_pos(unsigned long long *a, double x) {
+  atomicMax(a, (unsigned long long)__double_as_longlong(x));  // x >= 0: bit order = value order
+}
+
+__device__ __forceinline__ double warp_max(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+
+__global__ void hhg_aabb(const ErContactParams p) {
+  if (!*p.rebuild) return;
+  double ext[ER_HHG_MAXLEV][3];
+#pragma unroll
+  for (int l = 0; l < ER_HHG_MAXLEV; ++l) ext[l][0] = ext[l][1] = ext[l][2] = 0.0;
+  unsigned lmask = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < p.n_elems; e += (int64_t)gridDim.x * blockDim.x) {
+    int rod, l;
+    double p0[3], p1[3], lo[3], hi[3];
+    load_seg(p, e, rod, p0, p1);
+    capsule_aabb(p0, p1, grown(p, rod), lo, hi);
+    if (!proxy_level(p, lo, hi, l)) { flag_fault(p, rod); continue; }
+    lmask |= 1u << l;
+#pragma unroll
+    for (int m = 0; m < ER_HHG_MAXLEV; ++m)  // static register indexing
+      if (m == l) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ext[m][c] = fmax(ext[m][c], hi[c] - lo[c]);
+      }
+  }
+  lmask = __reduce_or_sync(0xffffffffu, lmask);
+  const bool lead = (threadIdx.x & 31) == 0;
+#pragma unroll
+  for (int m = 0; m < ER_HHG_MAXLEV; ++m) {
+    if (!((lmask >> m) & 1u)) continue;  // warp-uniform
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double x = warp_max(ext[m][c]);
+      if (lead) atomic_max_pos(p.gext + 3 * m + c, x);
+    }
+  }
+  if (lead && lmask) atomicOr(p.bctr + 3, (unsigned long long)lmask);
+}
+
+// Cell box of each populated level: per axis the largest extent of its proxies, at least 1/4 of
+// the largest axis.  Any box is correct (the query margin is the real largest half extent);
+// the box only sets how many proxies a query scans.
+__global__ void hhg_dims(const ErContactParams p) {
+  const int l = threadIdx.x;
+  if (!*p.rebuild || l >= p.nlev) return;
+  double x[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) x[c] = __longlong_as_double((long long)p.gext[3 * l + c]);
+  const double m = fmax(x[0], fmax(x[1], x[2]));
+  const bool pop = (p.bctr[3] >> l) & 1ull;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) p.gdim[4 * l + c] = pop ? fmax(x[c], 0.25 * m) : p.cell[l];
+  p.gdim[4 * l + 3] = pop ? 1.0 : 0.0;
+}
+
+__device__ __forceinline__ bool proxy_cell(const ErContactParams &p, const double lo[3], const double hi[3], int l,
+                                           int c[3]) {
+  bool ok = true;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    const double x = floor((0.5 * (lo[k] + hi[k])) * p.icell[l]);
-    ok = ok && (x > -1073741824.0 && x < 1073741824.0);  // also false for NaN
+    const double x = floor((0.5 * (lo[k] + hi[k])) / p.gdim[4 * l + k]);
+    ok = ok && (x > -(double)CHALF + 2.0 && x < (double)CHALF - 2.0);  // also false for NaN
     c[k] = ok ? (int)x : 0;
   }
   return ok;
 }
 
-__device__ __forceinline__ void load_nodes(const ErContactParams &p, int64_t n0, double p0[3], double p1[3]) {
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    p0[c] = p.cnode[c * p.ns + n0];
-    p1[c] = p.cnode[c * p.ns + n0 + 1];
-  }
-}
-
 __global__ void hhg_keys(const ErContactParams p) {
-  unsigned lmask = 0;
+  if (!*p.rebuild) return;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < p.n_elems; e += (int64_t)gridDim.x * blockDim.x) {
-    const int rod = __ldg(p.erod + e);
+    int rod, l, c[3];
     double p0[3], p1[3], lo[3], hi[3];
-    load_nodes(p, e + rod, p0, p1);
-    capsule_aabb(p0, p1, __ldg(p.rad + rod), lo, hi);
-    int l, c[3];
-    if (!proxy_cell(p, lo, hi, l, c)) flag_fault(p, rod);
-    lmask |= 1u << l;
+    load_seg(p, e, rod, p0, p1);
+    capsule_aabb(p0, p1, grown(p, rod), lo, hi);
+    const bool okl = proxy_level(p, lo, hi, l);
+    if (!proxy_cell(p, lo, hi, l, c) && okl) flag_fault(p, rod);
     p.key[e] = cell_hash(c[0], c[1], c[2], l, p.hbits);
     p.val[e] = (int32_t)e;
+    // build positions (node j of element j; the rod's last node with its last element)
+    double *b = p.cbuild + 3 * (e + rod);
+    const bool last = e + 1 == p.n_elems || __ldg(p.erod + e + 1) != rod;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      b[k] = p0[k];
+      if (last) b[3 + k] = p1[k];
+    }
   }
-  lmask = __reduce_or_sync(0xffffffffu, lmask);
-  if ((threadIdx.x & 31) == 0 && lmask) atomicOr(p.ctr + 4, (unsigned long long)lmask);
 }
 
 __global__ void hhg_cells(const ErContactParams p) {
+  if (!*p.rebuild) return;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < p.n_elems; q += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t e = p.val_s[q];
+    int rod, l, c[3];
+    double p0[3], p1[3], lo[3], hi[3];
+    load_seg(p, e, rod, p0, p1);
+    capsule_aabb(p0, p1, grown(p, rod), lo, hi);
+    proxy_level(p, lo, hi, l);
+    proxy_cell(p, lo, hi, l, c);
+    p.code_s[q] = cell_code(c[0], c[1], c[2], l);
+    p.boxa[q] = make_float4(__double2float_rd(lo[0]), __double2float_rd(lo[1]), __double2float_rd(lo[2]), __int_as_float(e));
+    p.boxb[q] = make_float4(__double2float_ru(hi[0]), __double2float_ru(hi[1]), __double2float_ru(hi[2]), __int_as_float(rod));
+    p.qidx[e] = (int32_t)q;
+  }
+}
+
+// Bucket table: for the first sorted proxy of each bucket, (start | end << 32, cell code of the
+// bucket when all its proxies share one cell, else MIXED).  Empty buckets keep start = -1.
+__global__ void hhg_table(const ErContactParams p) {
+  if (!*p.rebuild) return;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < p.n_elems; q += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t k = p.key_s[q];
-    if (q == 0 || p.key_s[q - 1] != k) p.cstart[k] = (int32_t)q;
-    if (q == p.n_elems - 1 || p.key_s[q + 1] != k) p.cend[k] = (int32_t)(q + 1);
-    const int32_t e = p.val_s[q];
-    const int rod = __ldg(p.erod + e);
-    const int64_t n0 = (int64_t)e + rod;
-    double p0[3], p1[3], lo[3], hi[3];
-    load_nodes(p, n0, p0, p1);
-    capsule_aabb(p0, p1, __ldg(p.rad + rod), lo, hi);
-    int l, c[3];
-    proxy_cell(p, lo, hi, l, c);
-    double *P = p.p01 + 6 * q, *V = p.v01 + 6 * q;
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      P[d] = p0[d];
-      P[3 + d] = p1[d];
-      V[d] = p.cnode[(3 + d) * p.ns + n0];
-      V[3 + d] = p.cnode[(3 + d) * p.ns + n0 + 1];
-    }
-    p.meta[q] = make_int4(e, rod, l, 0);
-    p.cellc[q] = make_int4(c[0], c[1], c[2], l);
+    if (q > 0 && p.key_s[q - 1] == k) continue;
+    const long long c0 = p.code_s[q];
+    long long code = c0;
+    int64_t j = q + 1;
+    for (; j < p.n_elems && p.key_s[j] == k; ++j)
+      if (p.code_s[j] != c0) code = ER_CELL_MIXED;
+    p.table[k] = make_longlong2((long long)q | ((long long)j << 32), code);
   }
+}
+
+// Broad phase of sorted proxy q: calls visit(b) for every candidate b in a fixed order -- the
+// proxies of a's level and of every coarser populated level whose centre cell lies within a's
+// AABB grown by that level's largest half extent, and whose float AABB overlaps a's, minus a
+// itself and the same-rod stencil.
+template <class F>
+__device__ __forceinline__ void broad_visit(const ErContactParams &p, int64_t q, F &&visit, unsigned &scanned) {
+  const float4 A = p.boxa[q], B = p.boxb[q];
+  const int ea = __float_as_int(A.w), roda = __float_as_int(B.w);
+  const int la = (int)(p.code_s[q] >> (3 * CBITS));
+  const double lo[3] = {(double)A.x, (double)A.y, (double)A.z}, hi[3] = {(double)B.x, (double)B.y, (double)B.z};
+  const unsigned lmask = (unsigned)p.bctr[3];
+  for (int L = la; L < p.nlev; ++L) {
+    if (!((lmask >> L) & 1u)) continue;
+    int c0[3], c1[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double d = p.gdim[4 * L + k];
+      const double hm = 0.5 * __longlong_as_double((long long)p.gext[3 * L + k]) * (1.0 + 1e-9) + 1e-300;
+      c0[k] = (int)floor((lo[k] - hm) / d);
+      c1[k] = (int)floor((hi[k] + hm) / d);
+    }
+    for (int cz = c0[2]; cz <= c1[2]; ++cz)
+      for (int cy = c0[1]; cy <= c1[1]; ++cy)
+        for (int cx = c0[0]; cx <= c1[0]; ++cx) {
+          const uint32_t key = cell_hash(cx, cy, cz, L, p.hbits);
+          const longlong2 bk = __ldg(p.table + key);  // (start | end << 32, cell code)
+          const int b0 = (int)(bk.x & 0xffffffffll);
+          if (b0 < 0) continue;
+          const long long want = cell_code(cx, cy, cz, L), tc = bk.y;
+          if (tc != want && tc != ER_CELL_MIXED) continue;  // bucket of another cell
+          const int b1 = (int)(bk.x >> 32);
+          scanned += (unsigned)(b1 - b0);
+          for (int b = b0; b < b1; ++b) {
+            if (tc == ER_CELL_MIXED && __ldg(p.code_s + b) != want) continue;
+            if (b == q) continue;
+            const float4 Ab = __ldg(p.boxa + b), Bb = __ldg(p.boxb + b);
+            if (fmaxf(A.x, Ab.x) > fminf(B.x, Bb.x) || fmaxf(A.y, Ab.y) > fminf(B.y, Bb.y) ||
+                fmaxf(A.z, Ab.z) > fminf(B.z, Bb.z))
+              continue;
+            const int eb = __float_as_int(Ab.w);
+            if (__float_as_int(Bb.w) == roda && abs(ea - eb) <= p.law.exclude) continue;
+            visit(eb, L > la, L > la || ea < eb);
+          }
+        }
+  }
+}
+
+// One broad pass over the sorted proxies: the first ER_CAND_K candidates of element e go to
+// cand[k * E + e], cnt[e] = the full count; an element with more candidates re-runs the broad
+// visit in hhg_narrow (same order).
+__global__ void __launch_bounds__(128) hhg_broad(const ErContactParams p) {
+  if (!*p.rebuild) return;
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned n = 0, own = 0, scanned = 0;
+  if (q < p.n_elems) {
+    const int64_t E = p.n_elems;
+    const int e = __float_as_int(p.boxa[q].w);
+    broad_visit(p, q, [&](int eb, bool cross, bool owner) {
+      if (n < ER_CAND_K) p.cand[n * E + e] = eb | (cross ? ER_CAND_CROSS : 0);
+      ++n;
+      own += owner;
+    }, scanned);
+    p.cnt[e] = (int32_t)n;
+  }
+  const unsigned lng = __reduce_add_sync(0xffffffffu, n > ER_CAND_K ? 1u : 0u);
+  const unsigned tot = __reduce_add_sync(0xffffffffu, n);
+  own = __reduce_add_sync(0xffffffffu, own);
+  scanned = __reduce_add_sync(0xffffffffu, scanned);
+  if ((threadIdx.x & 31) == 0) {
+    if (own) atomicAdd(p.bctr + 0, (unsigned long long)own);
+    if (tot) atomicAdd(p.bctr + 1, (unsigned long long)tot);
+    if (scanned) atomicAdd(p.bctr + 2, (unsigned long long)scanned);
+    if (lng) atomicAdd(p.bctr + 4, (unsigned long long)lng);
+  }
+}
+
+// Start of a build: empty bucket table, zero build statistics (the cumulative build count stays).
+__global__ void hhg_reset(const ErContactParams p, int64_t T) {
+  if (!*p.rebuild) return;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < T; k += (int64_t)gridDim.x * blockDim.x)
+    p.table[k] = make_longlong2(-1ll, 0ll);
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < 5) p.bctr[t] = 0ull;
+  if (t < 3 * ER_HHG_MAXLEV) p.gext[t] = 0ull;
+}
+
+// End of a build: clear the flag, count the build.
+__global__ void hhg_built(const ErContactParams p) {
+  if (!*p.rebuild) return;
+  *p.rebuild = 0;
+  p.bctr[5] += 1;
 }
 
 __device__ __forceinline__ double dot3(const double a[3], const double b[3]) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
@@ -134,8 +329,8 @@ __device__ __forceinline__ double clamp01(double x) { return x < 0.0 ? 0.0 : (x 
 // the minimiser of |P(s) - Q(t)|^2 over the unit square.  Candidates in this order: the interior
 // stationary point (when inside the square), then the edges s = 0, s = 1, t = 0, t = 1 each with
 // its clamped 1-D minimiser; the first candidate of least distance wins (DESIGN §3 #27).
-__device__ void segment_closest(const double p0[3], const double p1[3], const double q0[3], const double q1[3], double &s,
-                                double &t, double &dist) {
+__device__ __forceinline__ void segment_closest(const double p0[3], const double p1[3], const double q0[3],
+                                                const double q1[3], double &s, double &t, double &dist) {
   double u[3], v[3], w[3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
@@ -144,27 +339,25 @@ __device__ void segment_closest(const double p0[3], const double p1[3], const do
     w[c] = p0[c] - q0[c];
   }
   const double uu = dot3(u, u), vv = dot3(v, v), uv = dot3(u, v), uw = dot3(u, w), vw = dot3(v, w);
-  double cs[5], ct[5];
-  int n = 0;
-  const double det = uu * vv - uv * uv;
-  if (det > 0.0) {
-    const double si = (uv * vw - uw * vv) / det, ti = (uu * vw - uv * uw) / det;
-    if (si >= 0.0 && si <= 1.0 && ti >= 0.0 && ti <= 1.0) { cs[n] = si; ct[n] = ti; ++n; }
-  }
-  cs[n] = 0.0; ct[n] = vv > 0.0 ? clamp01(vw / vv) : 0.0; ++n;
-  cs[n] = 1.0; ct[n] = vv > 0.0 ? clamp01((vw + uv) / vv) : 0.0; ++n;
-  cs[n] = uu > 0.0 ? clamp01(-uw / uu) : 0.0; ct[n] = 0.0; ++n;
-  cs[n] = uu > 0.0 ? clamp01((uv - uw) / uu) : 0.0; ct[n] = 1.0; ++n;
   double best = -1.0;
   s = 0.0;
   t = 0.0;
-  for (int k = 0; k < n; ++k) {
+  auto consider = [&](double cs, double ct) {
     double x[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) x[c] = p0[c] + cs[k] * u[c] - q0[c] - ct[k] * v[c];
+    for (int c = 0; c < 3; ++c) x[c] = p0[c] + cs * u[c] - q0[c] - ct * v[c];
     const double d2 = dot3(x, x);
-    if (best < 0.0 || d2 < best) { best = d2; s = cs[k]; t = ct[k]; }
+    if (best < 0.0 || d2 < best) { best = d2; s = cs; t = ct; }
+  };
+  const double det = uu * vv - uv * uv;
+  if (det > 0.0) {
+    const double si = (uv * vw - uw * vv) / det, ti = (uu * vw - uv * uw) / det;
+    if (si >= 0.0 && si <= 1.0 && ti >= 0.0 && ti <= 1.0) consider(si, ti);
   }
+  consider(0.0, vv > 0.0 ? clamp01(vw / vv) : 0.0);
+  consider(1.0, vv > 0.0 ? clamp01((vw + uv) / vv) : 0.0);
+  consider(uu > 0.0 ? clamp01(-uw / uu) : 0.0, 0.0);
+  consider(uu > 0.0 ? clamp01((uv - uw) / uu) : 0.0, 1.0);
   dist = sqrt(best);
 }
 
@@ -214,101 +407,76 @@ __device__ __forceinline__ bool pair_force(const ErContactParams &p, const doubl
   return true;
 }
 
-template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) hhg_narrow(const ErContactParams p) {
-  const int64_t q = blockIdx.x * (int64_t)BLOCK + threadIdx.x;
-  unsigned long long n_cand = 0, n_cont = 0, n_cross = 0;
-  if (q < p.n_elems) {
-    const int4 ma = p.meta[q];
-    const int ea = ma.x, roda = ma.y, la = ma.z;
+__global__ void __launch_bounds__(128) hhg_narrow(const ErContactParams p) {
+  const int64_t ea = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned n_cont = 0, n_cross = 0;
+  if (ea < p.n_elems) {
+    int roda;
     double Pa[6], Va[6];
+    {
+      roda = __ldg(p.erod + ea);
+      const double *x = p.cnode + 6 * (ea + roda);
 #pragma unroll
-    for (int c = 0; c < 6; ++c) { Pa[c] = p.p01[6 * q + c]; Va[c] = p.v01[6 * q + c]; }
+      for (int c = 0; c < 3; ++c) { Pa[c] = x[c]; Va[c] = x[3 + c]; Pa[3 + c] = x[6 + c]; Va[3 + c] = x[9 + c]; }
+    }
     const double ra = __ldg(p.rad + roda), kra = __ldg(p.kr + roda);
-    double lo[3], hi[3];
-    capsule_aabb(Pa, Pa + 3, ra, lo, hi);
     double f[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    const unsigned lmask = (unsigned)*((volatile unsigned long long *)(p.ctr + 4));
-    for (int L = la; L < p.nlev; ++L) {
-      if (!((lmask >> L) & 1u)) continue;
-      const double cs = p.cell[L], ics = p.icell[L], mg = 0.5 * cs * (1.0 + 1e-9);
-      int c0[3], c1[3];
+    auto pair = [&](int eb, bool cross) {
+      const int rodb = __ldg(p.erod + eb);
+      double Pb[6], Vb[6];
+      const double *x = p.cnode + 6 * ((int64_t)eb + rodb);
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        c0[k] = (int)floor((lo[k] - mg) * ics);
-        c1[k] = (int)floor((hi[k] + mg) * ics);
+      for (int c = 0; c < 3; ++c) {
+        Pb[c] = __ldg(x + c); Vb[c] = __ldg(x + 3 + c); Pb[3 + c] = __ldg(x + 6 + c); Vb[3 + c] = __ldg(x + 9 + c);
       }
-      for (int cz = c0[2]; cz <= c1[2]; ++cz)
-        for (int cy = c0[1]; cy <= c1[1]; ++cy)
-          for (int cx = c0[0]; cx <= c1[0]; ++cx) {
-            const uint32_t key = cell_hash(cx, cy, cz, L, p.hbits);
-            const int b0 = p.cstart[key];
-            if (b0 < 0) continue;
-            const int b1 = p.cend[key];
-            for (int b = b0; b < b1; ++b) {
-              if (b == q) continue;
-              const int4 cb = __ldg(p.cellc + b);
-              if (cb.w != L || cb.x != cx || cb.y != cy || cb.z != cz) continue;  // another cell in the bucket
-              const int4 mb = __ldg(p.meta + b);
-              const int eb = mb.x, rodb = mb.y;
-              if (roda == rodb && abs(ea - eb) <= p.law.exclude) continue;
-              const double *Pb = p.p01 + 6 * (int64_t)b;
-              const double rb = __ldg(p.rad + rodb);
-              double lob[3], hib[3], Pbl[6];
+      const double rb = __ldg(p.rad + rodb);
+      const double k = p.law.k_n > 0.0 ? p.law.k_n : fmin(kra, __ldg(p.kr + rodb));
+      const bool a_first = ea < eb;
+      double F[3], s, t;
+      const bool hit = a_first ? pair_force(p, Pa, Pb, Va, Vb, ra, rb, k, F, s, t)
+                               : pair_force(p, Pb, Pa, Vb, Va, rb, ra, k, F, s, t);
+      if (!hit) return;
+      n_cont += (cross || a_first);  // each pair once
+      // F acts on the first (lower-id) element at weights (1-s, s); -F on the second at (1-t, t)
+      const double w0 = a_first ? 1.0 - s : 1.0 - t, w1 = a_first ? s : t;
+      const double sg = a_first ? 1.0 : -1.0;
 #pragma unroll
-              for (int c = 0; c < 6; ++c) Pbl[c] = __ldg(Pb + c);
-              capsule_aabb(Pbl, Pbl + 3, rb, lob, hib);
-              const bool ov = fmax(lo[0], lob[0]) <= fmin(hi[0], hib[0]) && fmax(lo[1], lob[1]) <= fmin(hi[1], hib[1]) &&
-                              fmax(lo[2], lob[2]) <= fmin(hi[2], hib[2]);
-              if (!ov) continue;
-              const bool owner = L > la || ea < eb;  // counts each pair once
-              n_cand += owner;
-              double Vb[6];
+      for (int c = 0; c < 3; ++c) {
+        f[c] += w0 * (sg * F[c]);
+        f[3 + c] += w1 * (sg * F[c]);
+      }
+      if (cross) {  // the coarser element b never sees this pair: leave it a record
+        ++n_cross;
+        const unsigned long long r = atomicAdd(p.ctr + 0, 1ull);
+        if (r >= (unsigned long long)p.pcap) { flag_fault(p, rodb); return; }
+        const double v0 = a_first ? 1.0 - t : 1.0 - s, v1 = a_first ? t : s;
 #pragma unroll
-              for (int c = 0; c < 6; ++c) Vb[c] = __ldg(p.v01 + 6 * (int64_t)b + c);
-              const double krb = __ldg(p.kr + rodb);
-              const double k = p.law.k_n > 0.0 ? p.law.k_n : fmin(kra, krb);
-              const bool a_first = ea < eb;
-              double F[3], s, t;
-              const bool hit = a_first ? pair_force(p, Pa, Pbl, Va, Vb, ra, rb, k, F, s, t)
-                                       : pair_force(p, Pbl, Pa, Vb, Va, rb, ra, k, F, s, t);
-              if (!hit) continue;
-              n_cont += owner;
-              // F acts on the first (lower-id) element at weights (1-s, s); -F on the second at (1-t, t)
-              const double wa0 = a_first ? 1.0 - s : 1.0 - t, wa1 = a_first ? s : t;
-              const double sg = a_first ? 1.0 : -1.0;
-#pragma unroll
-              for (int c = 0; c < 3; ++c) {
-                f[c] += wa0 * (sg * F[c]);
-                f[3 + c] += wa1 * (sg * F[c]);
-              }
-              if (L > la) {  // the coarser proxy b never sees this pair: leave it a record
-                ++n_cross;
-                const unsigned long long r = atomicAdd(p.ctr + 0, 1ull);
-                if (r >= (unsigned long long)p.pcap) { flag_fault(p, rodb); continue; }
-                const double wb0 = a_first ? 1.0 - t : 1.0 - s, wb1 = a_first ? t : s;
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                  p.pf[6 * r + c] = wb0 * (-sg * F[c]);
-                  p.pf[6 * r + 3 + c] = wb1 * (-sg * F[c]);
-                }
-                p.psrc[r] = ea;
-                p.pnext[r] = atomicExch(p.head + eb, (int32_t)r);
-              }
-            }
-          }
+        for (int c = 0; c < 3; ++c) {
+          p.pf[6 * r + c] = v0 * (-sg * F[c]);
+          p.pf[6 * r + 3 + c] = v1 * (-sg * F[c]);
+        }
+        p.psrc[r] = (int32_t)ea;
+        p.pnext[r] = atomicExch(p.head + eb, (int32_t)r);
+      }
+    };
+    const int n = p.cnt[ea];
+    if (n <= ER_CAND_K) {
+      for (int j = 0; j < n; ++j) {
+        const int c = p.cand[j * p.n_elems + ea];
+        pair(c & ~ER_CAND_CROSS, (c & ER_CAND_CROSS) != 0);
+      }
+    } else {  // long list: re-run the broad visit of the last build (same order)
+      unsigned sc = 0;
+      broad_visit(p, p.qidx[ea], [&](int eb, bool cross, bool) { pair(eb, cross); }, sc);
     }
 #pragma unroll
     for (int c = 0; c < 6; ++c) p.fc[c * p.fs + ea] = f[c];
   }
-  // statistics: warp sums, one atomic per warp
-  n_cand = __reduce_add_sync(0xffffffffu, (unsigned)n_cand);
-  n_cont = __reduce_add_sync(0xffffffffu, (unsigned)n_cont);
-  n_cross = __reduce_add_sync(0xffffffffu, (unsigned)n_cross);
+  n_cont = __reduce_add_sync(0xffffffffu, n_cont);
+  n_cross = __reduce_add_sync(0xffffffffu, n_cross);
   if ((threadIdx.x & 31) == 0) {
-    if (n_cand) atomicAdd(p.ctr + 1, n_cand);
-    if (n_cont) atomicAdd(p.ctr + 2, n_cont);
-    if (n_cross) atomicAdd(p.ctr + 3, n_cross);
+    if (n_cont) atomicAdd(p.ctr + 1, (unsigned long long)n_cont);
+    if (n_cross) atomicAdd(p.ctr + 2, (unsigned long long)n_cross);
   }
 }
 
@@ -319,8 +487,8 @@ __global__ void hhg_finish(const ErContactParams p, int cross) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < p.n_elems; e += (int64_t)gridDim.x * blockDim.x) {
     const int rod = __ldg(p.erod + e);
     int h = cross ? p.head[e] : -1;
-    const bool plane_last = p.law.plane_on && (e + 1 == p.n_elems || __ldg(p.erod + e + 1) != rod);
     if (h < 0 && !p.law.plane_on) continue;
+    const bool plane_last = p.law.plane_on && (e + 1 == p.n_elems || __ldg(p.erod + e + 1) != rod);
     double f[6];
 #pragma unroll
     for (int c = 0; c < 6; ++c) f[c] = p.fc[c * p.fs + e];
@@ -346,7 +514,7 @@ __global__ void hhg_finish(const ErContactParams p, int cross) {
         const int64_t node = e + rod + side;
         double x[3], v[3];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) { x[c] = p.cnode[c * p.ns + node]; v[c] = p.cnode[(3 + c) * p.ns + node]; }
+        for (int c = 0; c < 3; ++c) { x[c] = p.cnode[6 * node + c]; v[c] = p.cnode[6 * node + 3 + c]; }
         const double gap = dot3(L.pn, x) - L.pd - r;
         if (!(gap < 0.0)) continue;
         ++n_plane;
@@ -360,43 +528,56 @@ __global__ void hhg_finish(const ErContactParams p, int cross) {
     for (int c = 0; c < 6; ++c) p.fc[c * p.fs + e] = f[c];
   }
   n_plane = __reduce_add_sync(0xffffffffu, n_plane);
-  if ((threadIdx.x & 31) == 0 && n_plane) atomicAdd(p.ctr + 5, (unsigned long long)n_plane);
+  if ((threadIdx.x & 31) == 0 && n_plane) atomicAdd(p.ctr + 3, (unsigned long long)n_plane);
 }
 
 }  // namespace erc
 
 extern "C" {
 
-// Temporary-storage bytes of the broad-phase sort for n keys of `bits` bits.
-cudaError_t er_contact_sort_bytes(int64_t n, int bits, size_t *bytes) {
+// Temporary-storage bytes of the broad-phase sort (n keys of `bits` bits).
+cudaError_t er_contact_tmp_bytes(int64_t n, int bits, size_t *bytes) {
   *bytes = 0;
   return cub::DeviceRadixSort::SortPairs(nullptr, *bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr,
                                          (const int32_t *)nullptr, (int32_t *)nullptr, (int)n, 0, bits);
 }
 
-// One contact evaluation (broad + narrow phase) at the positions/velocities in p.cnode: fills
-// p.fc.  Stream-ordered; no host synchronisation.  `launches` += kernels launched.
-cudaError_t er_contact_eval(const ErContactParams *pp, void *sort_tmp, size_t sort_bytes, cudaStream_t st,
+// One contact evaluation at the positions/velocities in p.cnode: fills p.fc.  With `build`, the
+// list-build kernels are enqueued too (they do work only when the device flag is set).
+// Stream-ordered; no host synchronisation.  `launches` += kernels launched.
+cudaError_t er_contact_eval(const ErContactParams *pp, void *tmp, size_t tmp_bytes, int build, cudaStream_t st,
                             int64_t *launches) {
   const ErContactParams &p = *pp;
   const int64_t E = p.n_elems;
   if (E <= 0) return cudaSuccess;
   const int64_t T = 1ll << p.hbits;
   cudaError_t e;
-  if ((e = cudaMemsetAsync(p.ctr, 0, 8 * sizeof(unsigned long long), st)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(p.cstart, 0xff, sizeof(int32_t) * T, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(p.ctr, 0, 4 * sizeof(unsigned long long), st)) != cudaSuccess) return e;
   const int cross = p.nlev > 1;
   if (cross && (e = cudaMemsetAsync(p.head, 0xff, sizeof(int32_t) * E, st)) != cudaSuccess) return e;
   const unsigned g = (unsigned)std::min<int64_t>((E + 255) / 256, 148 * 16);
-  erc::hhg_keys<<<g, 256, 0, st>>>(p);
-  size_t bytes = sort_bytes;
-  if ((e = cub::DeviceRadixSort::SortPairs(sort_tmp, bytes, p.key, p.key_s, p.val, p.val_s, (int)E, 0, p.hbits, st)) !=
-      cudaSuccess)
-    return e;
-  erc::hhg_cells<<<g, 256, 0, st>>>(p);
-  erc::hhg_narrow<128><<<(unsigned)((E + 127) / 128), 128, 0, st>>>(p);
-  erc::hhg_finish<<<g, 256, 0, st>>>(p, cross);
-  *launches += 5;  // keys, sort (counted once), cells, narrow, finish
+  const unsigned gq = (unsigned)((E + 127) / 128);
+  if (build) {  // list build: every kernel returns at once unless the device flag is set
+    erc::hhg_reset<<<(T + 255) / 256 < 148 * 16 ? (unsigned)((T + 255) / 256) : 148 * 16, 256, 0, st>>>(p, T);
+    erc::hhg_aabb<<<g, 256, 0, st>>>(p);
+    erc::hhg_dims<<<1, 32, 0, st>>>(p);
+    erc::hhg_keys<<<g, 256, 0, st>>>(p);
+    size_t bytes = tmp_bytes;
+    if ((e = cub::DeviceRadixSort::SortPairs(tmp, bytes, p.key, p.key_s, p.val, p.val_s, (int)E, 0, p.hbits, st)) !=
+        cudaSuccess)
+      return e;
+    erc::hhg_cells<<<g, 256, 0, st>>>(p);
+    erc::hhg_table<<<g, 256, 0, st>>>(p);
+    erc::hhg_broad<<<gq, 128, 0, st>>>(p);
+    erc::hhg_built<<<1, 1, 0, st>>>(p);
+    *launches += 9;
+  }
+  erc::hhg_narrow<<<gq, 128, 0, st>>>(p);
+  *launches += 1;
+  if (cross || p.law.plane_on) {
+    erc::hhg_finish<<<g, 256, 0, st>>>(p, cross);
+    *launches += 1;
+  }
   return cudaGetLastError();
 }
 

@@ -586,13 +586,23 @@ __global__ void __launch_bounds__(BLOCK, MINB) simple_kernel(const ErStepParams 
       __stcs(G + c * ns + s, r[c]);
       __stcs(G + (3 + c) * ns + s, v[c]);
     }
-    if (MODE == MODE_DRIFT && p.cnode) {  // contact: positions after drift-1 (and v^n) for the broad phase
+  }
+  if (MODE == MODE_DRIFT && p.cnode) {  // contact: positions after drift-1 (and v^n); Verlet-list check
+    bool moved = false;
+    if (si.active) {
+      double *o = p.cnode + 6 * si.node;
+      const double *rb = p.cbuild + 3 * si.node;
+      double d2 = 0.0;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        p.cnode[c * p.cns + si.node] = r[c];
-        p.cnode[(3 + c) * p.cns + si.node] = v[c];
+        o[c] = r[c];
+        o[3 + c] = v[c];
+        const double d = r[c] - rb[c];
+        d2 = fma(d, d, d2);
       }
+      moved = !(d2 <= p.disp2);  // also for NaN
     }
+    if (__any_sync(0xffffffffu, moved) && (threadIdx.x & 31) == 0) atomicOr(p.rebuild, 1);
   }
   if (si.has_e) {
 #pragma unroll

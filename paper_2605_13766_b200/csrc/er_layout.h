@@ -105,33 +105,49 @@ struct ErContactLaw {
 
 // Broad phase (hierarchical hash grid) + narrow phase buffers, all device memory.
 #define ER_HHG_MAXLEV 8
+#define ER_CELL_MIXED (-1ll)   // hash bucket holding proxies of more than one cell
+#define ER_CAND_K 16           // candidate list slots per element (longer lists are re-visited)
+#define ER_CAND_CROSS (1 << 30) // candidate flag: the partner is on a coarser level (leave it a record)
 struct ErContactParams {
   ErContactLaw law;
-  double cell[ER_HHG_MAXLEV];   // cell size of level l (= cell[0] * 2^l)
-  double icell[ER_HHG_MAXLEV];
+  double cell[ER_HHG_MAXLEV];   // level l holds the proxies whose AABB's largest extent is
+  double icell[ER_HHG_MAXLEV];  // <= cell[l] (= cell[0] * 2^l), the smallest such level
   int32_t nlev;
-  int32_t hbits;                // hash table size 2^hbits per level
+  int32_t hbits;                // hash table size 2^hbits
+  double skin;                  // Verlet skin: proxies are AABBs grown by skin/2; lists are rebuilt
+                                //   when a node has moved more than skin/2 since the last build
   int64_t n_elems, n_nodes, n_rods;
   const double *rad;            // [R] contact radius
   const double *kr;             // [R] E r (pair stiffness scale)
   const int32_t *erod;          // [E] rod of each element
-  double *cnode;                // [6][ns] canonical node r, v after drift-1
-  int64_t ns;
-  uint32_t *key, *key_s;        // [E] cell keys, unsorted / sorted
+  double *cnode;                // [n_nodes][6] node r, v after drift-1 (AoS: an element's two
+                                //   nodes are 96 contiguous bytes)
+  double *cbuild;               // [n_nodes][3] node positions at the last list build
+  int32_t *rebuild;             // [1] device flag: rebuild the lists this step
+  unsigned long long *gext;     // [nlev][3] max AABB extent per level and axis (double bits), at build
+  double *gdim;                 // [nlev][4] cell box per level (x, y, z) and 1 if populated
+  uint32_t *key, *key_s;        // [E] bucket keys, unsorted / sorted
   int32_t *val, *val_s;         // [E] element ids, unsorted / sorted
-  int32_t *cstart, *cend;       // [nlev << hbits] sorted-proxy range of each hash bucket
-  double *p01;                  // [E][6] sorted proxies: segment end points
-  double *v01;                  // [E][6] sorted proxies: end-point velocities
-  int4 *meta;                   // [E] sorted proxies: elem, rod, level, 0
-  int4 *cellc;                  // [E] sorted proxies: cell x, y, z, level
+  longlong2 *table;             // [2^hbits] bucket: (start | end << 32, cell code of a pure bucket
+                                //   or ER_CELL_MIXED); start = -1 (all bits set): empty
+  long long *code_s;            // [E] cell code (level, cx, cy, cz) of each sorted proxy
+  float4 *boxa, *boxb;          // [E] sorted proxies: float AABB (lo rounded down, hi up);
+                                //     boxa.w = element id bits, boxb.w = rod id bits
+  int32_t *qidx;                // [E] sorted position of each element
+  int32_t *cnt;                 // [E] candidates of each element (at the last build)
+  int32_t *cand;                // [ER_CAND_K][E] the first ER_CAND_K of them: element id,
+                                //   | ER_CAND_CROSS when the partner is on a coarser level
   double *fc;                   // [6][fs] contact force on the element's (node j, node j+1)
   int64_t fs;
   int32_t *head;                // [E] cross-level records per coarse element (-1 = none)
   int32_t *pnext, *psrc;        // [pcap] record chain / source (fine) element
   double *pf;                   // [pcap][6] record force on the coarse element's two nodes
   int64_t pcap;
-  unsigned long long *ctr;      // [8]: 0 pool used, 1 AABB candidates, 2 contacts, 3 cross-level
-                                //      contacts, 4 level mask, 5 plane contacts, 6 max bucket
+  unsigned long long *ctr;      // [8] per step: 0 pool used, 1 contacts, 2 cross-level contacts,
+                                //      3 plane contacts
+  unsigned long long *bctr;     // [8] of the last build: 0 candidate pairs, 1 list entries (both
+                                //      sides), 2 proxies scanned, 3 level mask, 4 long lists;
+                                //      5 builds so far (cumulative)
   unsigned long long *fault;    // shared with the step kernels
 };
 
@@ -166,8 +182,10 @@ struct ErStepParams {
   // contact (NEXT-4): null cfc = rods do not interact
   const double *cfc;      // [6][cfs] contact force on each element's two nodes (ErContactParams.fc)
   int64_t cfs;
-  double *cnode;          // drift-1 stage: canonical node planes r, v for the broad phase
-  int64_t cns;
+  double *cnode;          // drift-1 stage: [n_nodes][6] node r, v for the contact phase
+  const double *cbuild;   // [n_nodes][3] positions at the last contact-list build
+  double disp2;           // (skin/2)^2: a larger squared displacement since the build ...
+  int32_t *rebuild;       // ... sets this flag
 };
 #define ER_TRACE_ITERS 64
 

@@ -171,3 +171,40 @@ def test_full_size_sampled_stacks(er, orc):
             g = (s[0][nsl], s[1][nsl], s[2][esl], s[3][esl])
             o, _ = run_orc(orc, ws, n)
             assert_parity(ws, g, o, tol, raw=("r", "Q"), label=f"stack {stack} after {n} steps")
+
+
+def test_verlet_skin_changes_nothing(er, orc):
+    """Candidate lists are reused until a node moves skin/2: a tiny skin (a rebuild almost every
+    step) and a large one give the same trajectory to round-off, and both match the oracle."""
+    w = mixed_radii()
+    w.velocities = w.velocities * 300.0                  # ~3 cm/s: 3e-8 m per step
+    runs = {}
+    for skin in (1e-7, 0.0, 2e-3):
+        with er.RodBatch(w) as b:
+            b.set_contact(w.contact, skin=skin)
+            b.step(200, w.dt)
+            runs[skin] = (b.get_state()[:4], b.contact_stats())
+    assert runs[1e-7][1].builds > 50 and runs[2e-3][1].builds == 1
+    for skin in (0.0, 2e-3):
+        e = errors(w, runs[1e-7][0], runs[skin][0])
+        assert max(v for k, v in e.items() if not k.endswith("_raw")) < 1e-13, (skin, e)
+    o, _ = run_orc(orc, w, 200)
+    assert_parity(w, runs[0.0][0], o, TOL_1000, raw=("r", "Q"), label="moving mixed radii 200 steps")
+
+
+def test_set_state_forces_rebuild(er, orc):
+    """Teleporting rods with er_set_state invalidates the lists: the next step rebuilds."""
+    w = W.make("fibres", n_rods=32)
+    with er.RodBatch(w) as b:
+        b.step(3, w.dt)
+        n0 = b.contact_stats().builds
+        pos = w.positions.copy()
+        pos[:, 0] += 0.5                                # every rod moved by 0.5 m: no stale pair
+        b.set_state(positions=pos, velocities=w.velocities, directors=w.directors, omega=w.omega, t=0.0)
+        b.step(1, w.dt)
+        st = b.contact_stats()
+        g = b.get_state()[:4]
+    assert st.builds == n0 + 1
+    w2 = dataclasses.replace(w, positions=pos)
+    o, _ = run_orc(orc, w2, 1)
+    assert_parity(w2, g, o, TOL_1STEP, raw=("r", "v", "Q"), label="after set_state")

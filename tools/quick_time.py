@@ -21,3 +21,6 @@ s0.record(stream); b.step(steps, w.dt); s1.record(stream); torch.cuda.synchroniz
 ms = s0.elapsed_time(s1) / steps
 rate = w.n_elems_total / (ms * 1e-3)
 print(f"{name}: {ms:.4f} ms/step  {rate:.4e} el-steps/s  HBM {info.bytes_per_step/(ms*1e-3)/1e9:.1f} GB/s (B_min)")
+if getattr(w, "contact", None) is not None:
+    st = b.contact_stats()
+    print({k: getattr(st, k) for k, _ in st._fields_})

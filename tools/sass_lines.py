@@ -9,7 +9,7 @@ lib = os.path.join(ROOT, "paper_2605_13766_b200", "lib", "libelasticarod.so")
 tmp = "/tmp/_cubins"
 os.makedirs(tmp, exist_ok=True)
 subprocess.run(["cuobjdump", "-xelf", "all", lib], cwd=tmp, capture_output=True)
-cub = [f for f in os.listdir(tmp) if f.startswith("er_kernels") and f.endswith(".cubin")][0]
+cub = [f for f in os.listdir(tmp) if f.startswith(os.environ.get("CUBIN", "er_kernels")) and f.endswith(".cubin")][0]
 dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)], capture_output=True, text=True).stdout.split("\n")
 i0 = [i for i, l in enumerate(dis) if l.startswith(fn + ":")][0]
 seq, cur, curf = [], None, None
