@@ -373,16 +373,13 @@ __device__ __forceinline__ void contact_law(const ErContactLaw &L, double k, dou
 #pragma unroll
   for (int c = 0; c < 3; ++c) vt[c] = vr[c] - vn * n[c];
   const double svt = sqrt(dot3(vt, vt));
+  const double ck = svt > L.v_stick ? -L.mu_k * fn / svt : (L.v_stick > 0.0 ? -L.mu_s * fn / L.v_stick : 0.0);
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    double ft = 0.0;
-    if (svt > L.v_stick) ft = -L.mu_k * fn * vt[c] / svt;
-    else if (L.v_stick > 0.0) ft = -L.mu_s * fn * vt[c] / L.v_stick;
-    F[c] = fn * n[c] + ft;
-  }
+  for (int c = 0; c < 3; ++c) F[c] = fn * n[c] + ck * vt[c];
 }
 
-// Force of the pair (x, y), x the lower element id, on x; false when not in contact.
+// Force of the pair (x, y), x the lower element id, on x; false when not in contact.  Px, Py:
+// segment end points; Vx, Vy: end-point velocities (node records, read only for touching pairs).
 __device__ __forceinline__ bool pair_force(const ErContactParams &p, const double *Px, const double *Py,
                                            const double *Vx, const double *Vy, double rx, double ry, double k,
                                            double F[3], double &s, double &t) {
@@ -391,44 +388,68 @@ __device__ __forceinline__ bool pair_force(const ErContactParams &p, const doubl
   const double gap = d - (rx + ry);
   if (!(gap < 0.0) || d == 0.0) return false;
   double n[3], vr[3];
+  const double id = 1.0 / d;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     const double pa = (1.0 - s) * Px[c] + s * Px[3 + c];
     const double pb = (1.0 - t) * Py[c] + t * Py[3 + c];
-    n[c] = (pa - pb) / d;
+    n[c] = (pa - pb) * id;
   }
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    const double va = (1.0 - s) * Vx[c] + s * Vx[3 + c];
-    const double vb = (1.0 - t) * Vy[c] + t * Vy[3 + c];
+    const double va = (1.0 - s) * __ldg(Vx + c) + s * __ldg(Vx + 6 + c);
+    const double vb = (1.0 - t) * __ldg(Vy + c) + t * __ldg(Vy + 6 + c);
     vr[c] = va - vb;
   }
   contact_law(p.law, k, gap, n, vr, F);
   return true;
 }
 
-__global__ void __launch_bounds__(128) hhg_narrow(const ErContactParams p) {
-  const int64_t ea = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  unsigned n_cont = 0, n_cross = 0;
-  if (ea < p.n_elems) {
-    int roda;
-    double Pa[6], Va[6];
-    {
-      roda = __ldg(p.erod + ea);
-      const double *x = p.cnode + 6 * (ea + roda);
+// Half-space n.x >= d on node j of element j (and node j+1 for a rod's last element), added to
+// the element's node shares f[0..2] / f[3..5]; returns the nodes in contact.
+__device__ __forceinline__ unsigned plane_forces(const ErContactParams &p, int64_t e, int rod, double f[6]) {
+  const ErContactLaw &L = p.law;
+  const double k = L.k_n > 0.0 ? L.k_n : __ldg(p.kr + rod);
+  const double r = __ldg(p.rad + rod);
+  const bool last = e + 1 == p.n_elems || __ldg(p.erod + e + 1) != rod;
+  unsigned n = 0;
+  for (int side = 0; side < (last ? 2 : 1); ++side) {
+    const double *x = p.cnode + 6 * (e + rod + side);
+    const double X[3] = {x[0], x[1], x[2]};
+    const double gap = dot3(L.pn, X) - L.pd - r;
+    if (!(gap < 0.0)) continue;
+    ++n;
+    const double V[3] = {x[3], x[4], x[5]};
+    double F[3];
+    contact_law(L, k, gap, L.pn, V, F);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) { Pa[c] = x[c]; Va[c] = x[3 + c]; Pa[3 + c] = x[6 + c]; Va[3 + c] = x[9 + c]; }
-    }
+    for (int c = 0; c < 3; ++c) f[3 * side + c] += F[c];
+  }
+  return n;
+}
+
+// LONG = false: elements with <= ER_CAND_K candidates (their stored list); LONG = true: the
+// others, which re-run the broad visit of the last build (same order) -- a separate kernel so the
+// common path does not carry the broad visit's registers.
+template <bool LONG>
+__global__ void __launch_bounds__(128, LONG ? 4 : 6) hhg_narrow(const ErContactParams p) {
+  const int64_t ea = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned n_cont = 0, n_cross = 0, n_plane = 0;
+  if (ea < p.n_elems && ((p.cnt[ea] > ER_CAND_K) == LONG)) {
+    const int roda = __ldg(p.erod + ea);
+    const double *Va = p.cnode + 6 * (ea + roda) + 3;  // velocities: read only on contact
+    double Pa[6];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) { Pa[c] = Va[c - 3]; Pa[3 + c] = Va[3 + c]; }
     const double ra = __ldg(p.rad + roda), kra = __ldg(p.kr + roda);
     double f[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     auto pair = [&](int eb, bool cross) {
       const int rodb = __ldg(p.erod + eb);
-      double Pb[6], Vb[6];
+      double Pb[6];
       const double *x = p.cnode + 6 * ((int64_t)eb + rodb);
+      const double *Vb = x + 3;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        Pb[c] = __ldg(x + c); Vb[c] = __ldg(x + 3 + c); Pb[3 + c] = __ldg(x + 6 + c); Vb[3 + c] = __ldg(x + 9 + c);
-      }
+      for (int c = 0; c < 3; ++c) { Pb[c] = __ldg(x + c); Pb[3 + c] = __ldg(x + 6 + c); }
       const double rb = __ldg(p.rad + rodb);
       const double k = p.law.k_n > 0.0 ? p.law.k_n : fmin(kra, __ldg(p.kr + rodb));
       const bool a_first = ea < eb;
@@ -459,19 +480,22 @@ __global__ void __launch_bounds__(128) hhg_narrow(const ErContactParams p) {
         p.pnext[r] = atomicExch(p.head + eb, (int32_t)r);
       }
     };
-    const int n = p.cnt[ea];
-    if (n <= ER_CAND_K) {
+    if (!LONG) {
+      const int n = p.cnt[ea];
       for (int j = 0; j < n; ++j) {
         const int c = p.cand[j * p.n_elems + ea];
         pair(c & ~ER_CAND_CROSS, (c & ER_CAND_CROSS) != 0);
       }
-    } else {  // long list: re-run the broad visit of the last build (same order)
+    } else {
       unsigned sc = 0;
       broad_visit(p, p.qidx[ea], [&](int eb, bool cross, bool) { pair(eb, cross); }, sc);
     }
+    if (p.law.plane_on) n_plane = plane_forces(p, ea, roda, f);
 #pragma unroll
     for (int c = 0; c < 6; ++c) p.fc[c * p.fs + ea] = f[c];
   }
+  n_plane = __reduce_add_sync(0xffffffffu, n_plane);
+  if ((threadIdx.x & 31) == 0 && n_plane) atomicAdd(p.ctr + 3, (unsigned long long)n_plane);
   n_cont = __reduce_add_sync(0xffffffffu, n_cont);
   n_cross = __reduce_add_sync(0xffffffffu, n_cross);
   if ((threadIdx.x & 31) == 0) {
@@ -482,53 +506,30 @@ __global__ void __launch_bounds__(128) hhg_narrow(const ErContactParams p) {
 
 constexpr int MAX_CROSS = 64;
 
-__global__ void hhg_finish(const ErContactParams p, int cross) {
-  unsigned n_plane = 0;
+// Cross-level records of each coarse element, summed in increasing source-element order.
+__global__ void hhg_finish(const ErContactParams p) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < p.n_elems; e += (int64_t)gridDim.x * blockDim.x) {
+    int h = p.head[e];
+    if (h < 0) continue;
     const int rod = __ldg(p.erod + e);
-    int h = cross ? p.head[e] : -1;
-    if (h < 0 && !p.law.plane_on) continue;
-    const bool plane_last = p.law.plane_on && (e + 1 == p.n_elems || __ldg(p.erod + e + 1) != rod);
     double f[6];
 #pragma unroll
     for (int c = 0; c < 6; ++c) f[c] = p.fc[c * p.fs + e];
-    if (h >= 0) {  // cross-level records, summed in increasing source-element order
-      int src[MAX_CROSS], idx[MAX_CROSS], m = 0;
-      for (; h >= 0; h = p.pnext[h]) {
-        if (m == MAX_CROSS) { flag_fault(p, rod); break; }
-        int j = m++;
-        const int sv = p.psrc[h];
-        while (j > 0 && src[j - 1] > sv) { src[j] = src[j - 1]; idx[j] = idx[j - 1]; --j; }
-        src[j] = sv;
-        idx[j] = h;
-      }
-      for (int j = 0; j < m; ++j)
-#pragma unroll
-        for (int c = 0; c < 6; ++c) f[c] += p.pf[6 * (int64_t)idx[j] + c];
+    int src[MAX_CROSS], idx[MAX_CROSS], m = 0;
+    for (; h >= 0; h = p.pnext[h]) {
+      if (m == MAX_CROSS) { flag_fault(p, rod); break; }
+      int j = m++;
+      const int sv = p.psrc[h];
+      while (j > 0 && src[j - 1] > sv) { src[j] = src[j - 1]; idx[j] = idx[j - 1]; --j; }
+      src[j] = sv;
+      idx[j] = h;
     }
-    if (p.law.plane_on) {  // half-space n.x >= d on node j (and node j+1 for a rod's last element)
-      const ErContactLaw &L = p.law;
-      const double k = L.k_n > 0.0 ? L.k_n : __ldg(p.kr + rod);
-      const double r = __ldg(p.rad + rod);
-      for (int side = 0; side < (plane_last ? 2 : 1); ++side) {
-        const int64_t node = e + rod + side;
-        double x[3], v[3];
+    for (int j = 0; j < m; ++j)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) { x[c] = p.cnode[6 * node + c]; v[c] = p.cnode[6 * node + 3 + c]; }
-        const double gap = dot3(L.pn, x) - L.pd - r;
-        if (!(gap < 0.0)) continue;
-        ++n_plane;
-        double F[3];
-        contact_law(L, k, gap, L.pn, v, F);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) f[3 * side + c] += F[c];
-      }
-    }
+      for (int c = 0; c < 6; ++c) f[c] += p.pf[6 * (int64_t)idx[j] + c];
 #pragma unroll
     for (int c = 0; c < 6; ++c) p.fc[c * p.fs + e] = f[c];
   }
-  n_plane = __reduce_add_sync(0xffffffffu, n_plane);
-  if ((threadIdx.x & 31) == 0 && n_plane) atomicAdd(p.ctr + 3, (unsigned long long)n_plane);
 }
 
 }  // namespace erc
@@ -572,10 +573,11 @@ cudaError_t er_contact_eval(const ErContactParams *pp, void *tmp, size_t tmp_byt
     erc::hhg_built<<<1, 1, 0, st>>>(p);
     *launches += 9;
   }
-  erc::hhg_narrow<<<gq, 128, 0, st>>>(p);
-  *launches += 1;
-  if (cross || p.law.plane_on) {
-    erc::hhg_finish<<<g, 256, 0, st>>>(p, cross);
+  erc::hhg_narrow<false><<<gq, 128, 0, st>>>(p);
+  erc::hhg_narrow<true><<<gq, 128, 0, st>>>(p);
+  *launches += 2;
+  if (cross) {
+    erc::hhg_finish<<<g, 256, 0, st>>>(p);
     *launches += 1;
   }
   return cudaGetLastError();
