@@ -753,15 +753,39 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
     CK(cudaStreamSynchronize(b->stream), "cudaStreamSynchronize");
     return ER_OK;
   }
+  if (b->contact_on && b->kernel_mode != 1) {
+    // NEXT-4, fused: drift-1 of the first step (+ node records); then per step the contact
+    // evaluation and one persistent launch doing kick + drift-2 + the next step's drift-1
+    p.n_steps = 1;
+    p.t = t;
+    p.cnode = b->cp.cnode;
+    p.cbuild = b->cp.cbuild;
+    p.disp2 = 0.25 * b->cp.skin * b->cp.skin;
+    p.rebuild = b->cp.rebuild;
+    CK(er_launch_step(&p, b->block, 1, 15, b->stream), "drift kernel");
+    b->launches += 1;
+    p.cfc = b->cp.fc;
+    p.cfs = b->cp.fs;
+    for (int64_t q = 0; q < n_steps; ++q) {
+      CK(er_contact_eval(&b->cp, b->sort_tmp, b->sort_bytes, 1, b->stream, &b->launches), "contact");
+      p.t = t;
+      p.cnode = q + 1 < n_steps ? b->cp.cnode : nullptr;
+      CK(er_launch_step(&p, b->block, 0, feat | FEAT_CONTACT, b->stream), "step kernel");
+      b->launches += 1;
+      const double th = t + 0.5 * dt;
+      t = th + 0.5 * dt;
+    }
+    done = n_steps;
+  }
   while (done < n_steps) {
-    if (b->contact_on) {  // NEXT-4: drift | contact (broad + narrow phase) | dynamics + kick | drift
+    if (b->contact_on) {  // NEXT-4 staged: drift | contact (broad + narrow phase) | dynamics + kick | drift
       p.n_steps = 1;
       p.t = t;
       p.cnode = b->cp.cnode;
       p.cbuild = b->cp.cbuild;
       p.disp2 = 0.25 * b->cp.skin * b->cp.skin;
       p.rebuild = b->cp.rebuild;
-      CK(er_launch_step(&p, b->block, 1, 7, b->stream), "drift kernel");
+      CK(er_launch_step(&p, b->block, 1, 15, b->stream), "drift kernel");
       p.cnode = nullptr;
       CK(er_contact_eval(&b->cp, b->sort_tmp, b->sort_bytes, 1, b->stream, &b->launches), "contact");
       p.cfc = b->cp.fc;

@@ -72,6 +72,28 @@ __device__ __forceinline__ void contact_node_force(const ErStepParams &p, const 
   }
 }
 
+// Contact mode, after drift-1: node r (half step) and v^n to the AoS node records the contact
+// kernels read, and the Verlet-list check against the positions of the last list build (a node
+// farther than skin/2 from it raises the rebuild flag).  Called by every thread of the CTA.
+__device__ __forceinline__ void contact_emit(const ErStepParams &p, const SlotInfo &si, const double r[3],
+                                             const double v[3]) {
+  bool moved = false;
+  if (si.active) {
+    double *o = p.cnode + 6 * si.node;
+    const double *rb = p.cbuild + 3 * si.node;
+    double d2 = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      o[c] = r[c];
+      o[3 + c] = v[c];
+      const double d = r[c] - __ldg(rb + c);
+      d2 = fma(d, d, d2);
+    }
+    moved = !(d2 <= p.disp2);  // also for NaN
+  }
+  if (__any_sync(0xffffffffu, moved) && (threadIdx.x & 31) == 0) atomicOr(p.rebuild, 1);
+}
+
 __device__ __forceinline__ int rec_flags(const double *rec) {
   return (int)__double_as_longlong(rec[REC_FLAGS]);
 }
@@ -88,6 +110,7 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
                                           const double k0s[3], double &t, unsigned &fbits) {
   constexpr bool GEN = (FEAT & FEAT_GENERAL) != 0;
   constexpr bool EXTRA = (FEAT & FEAT_EXTRA) != 0;
+  constexpr bool CONTACT = (FEAT & FEAT_CONTACT) != 0;
   const int s = si.s, i = si.i, N = si.N;
   const double h = p.h, hh = 0.5 * p.h;
   const bool general = GEN && (si.fl & FL_GENERAL);
@@ -213,7 +236,7 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
 #pragma unroll
         for (int c = 0; c < 3; ++c) F[c] += rec[REC_TIPX + c];
       }
-      if (EXTRA && p.cfc) contact_node_force(p, si, F);  // NEXT-4: rod-rod + half-space contact
+      if (CONTACT && p.cfc) contact_node_force(p, si, F);  // NEXT-4: rod-rod + half-space contact
       const double im = general ? gp(GP_IM) : rec[REC_IM] * ((i == 0 || i == N) ? 2.0 : 1.0);
       const double nu = rec[REC_NU];
 #pragma unroll
@@ -468,10 +491,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
       r[c] = B[c * ns + tid];
       v[c] = B[(3 + c) * ns + tid];
     }
+    // a rod's last node owns no element: its Q, w stay 0 (le would index past the element planes,
+    // into stale stage contents that the non-finite check would otherwise see)
 #pragma unroll
-    for (int c = 0; c < 9; ++c) Q[c] = B[6 * ns + c * nel + le];
+    for (int c = 0; c < 9; ++c) Q[c] = si.has_e ? B[6 * ns + c * nel + le] : 0.0;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) w[c] = B[6 * ns + (9 + c) * nel + le];
+    for (int c = 0; c < 3; ++c) w[c] = si.has_e ? B[6 * ns + (9 + c) * nel + le] : 0.0;
     if ((FEAT & FEAT_KAPPA0) && si.has_v) {
       const int nvor = nel - T.nr;
 #pragma unroll
@@ -486,9 +511,20 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
     // ---- the steps
     double t = p.t;
     unsigned fbits = 0;
-    for (int st = 0; st < p.n_steps; ++st) {
-      step_body<BLOCK, FEAT, true, true, true>(p, B, rec, si, r, v, Q, w, k0s, t, fbits);
-      if (st + 1 < p.n_steps) __syncthreads();  // exchange C is re-used as A by the next step
+    if (FEAT & FEAT_CONTACT) {
+      // contact mode: the state arrives after drift-1 (contact forces were evaluated there);
+      // kick + drift-2, then -- unless this is the call's last step -- the next step's drift-1
+      // and the node records for the next contact evaluation
+      step_body<BLOCK, FEAT, false, true, true>(p, B, rec, si, r, v, Q, w, k0s, t, fbits);
+      if (p.cnode) {
+        step_body<BLOCK, FEAT, true, false, false>(p, B, rec, si, r, v, Q, w, k0s, t, fbits);
+        contact_emit(p, si, r, v);
+      }
+    } else {
+      for (int st = 0; st < p.n_steps; ++st) {
+        step_body<BLOCK, FEAT, true, true, true>(p, B, rec, si, r, v, Q, w, k0s, t, fbits);
+        if (st + 1 < p.n_steps) __syncthreads();  // exchange C is re-used as A by the next step
+      }
     }
     if (fbits) { fbits_all |= fbits; frod = min(frod, si.rod); }
     if (tr) tr[2] = gtimer() & ((1ull << 48) - 1);
@@ -543,7 +579,7 @@ __device__ __forceinline__ void decode_global(const ErStepParams &p, const ErTil
 
 template <int BLOCK, int MINB, int MODE>
 __global__ void __launch_bounds__(BLOCK, MINB) simple_kernel(const ErStepParams p) {
-  constexpr int FEAT = FEAT_GENERAL | FEAT_KAPPA0 | FEAT_EXTRA;
+  constexpr int FEAT = FEAT_GENERAL | FEAT_KAPPA0 | FEAT_EXTRA | FEAT_CONTACT;
   extern __shared__ __align__(16) double sm[];
   int *rst = reinterpret_cast<int *>(sm + XPLANES * BLOCK);
   const ErTile T = p.tiles[blockIdx.x];
@@ -587,23 +623,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) simple_kernel(const ErStepParams 
       __stcs(G + (3 + c) * ns + s, v[c]);
     }
   }
-  if (MODE == MODE_DRIFT && p.cnode) {  // contact: positions after drift-1 (and v^n); Verlet-list check
-    bool moved = false;
-    if (si.active) {
-      double *o = p.cnode + 6 * si.node;
-      const double *rb = p.cbuild + 3 * si.node;
-      double d2 = 0.0;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        o[c] = r[c];
-        o[3 + c] = v[c];
-        const double d = r[c] - rb[c];
-        d2 = fma(d, d, d2);
-      }
-      moved = !(d2 <= p.disp2);  // also for NaN
-    }
-    if (__any_sync(0xffffffffu, moved) && (threadIdx.x & 31) == 0) atomicOr(p.rebuild, 1);
-  }
+  if (MODE == MODE_DRIFT && p.cnode) contact_emit(p, si, r, v);
   if (si.has_e) {
 #pragma unroll
     for (int c = 0; c < 9; ++c) __stcs(G + 6 * ns + c * nel + le, Q[c]);
@@ -841,7 +861,7 @@ cudaError_t launch_persistent(const ErStepParams &p, cudaStream_t st) {
 
 template <int BLOCK, int MINB>
 cudaError_t launch_persistent_feat(const ErStepParams &p, int feat, cudaStream_t st) {
-  switch (feat & 7) {
+  switch (feat & 15) {
     case 0: return launch_persistent<BLOCK, MINB, 0>(p, st);
     case 1: return launch_persistent<BLOCK, MINB, 1>(p, st);
     case 2: return launch_persistent<BLOCK, MINB, 2>(p, st);
@@ -849,7 +869,15 @@ cudaError_t launch_persistent_feat(const ErStepParams &p, int feat, cudaStream_t
     case 4: return launch_persistent<BLOCK, MINB, 4>(p, st);
     case 5: return launch_persistent<BLOCK, MINB, 5>(p, st);
     case 6: return launch_persistent<BLOCK, MINB, 6>(p, st);
-    default: return launch_persistent<BLOCK, MINB, 7>(p, st);
+    case 7: return launch_persistent<BLOCK, MINB, 7>(p, st);
+    case 8: return launch_persistent<BLOCK, MINB, 8>(p, st);
+    case 9: return launch_persistent<BLOCK, MINB, 9>(p, st);
+    case 10: return launch_persistent<BLOCK, MINB, 10>(p, st);
+    case 11: return launch_persistent<BLOCK, MINB, 11>(p, st);
+    case 12: return launch_persistent<BLOCK, MINB, 12>(p, st);
+    case 13: return launch_persistent<BLOCK, MINB, 13>(p, st);
+    case 14: return launch_persistent<BLOCK, MINB, 14>(p, st);
+    default: return launch_persistent<BLOCK, MINB, 15>(p, st);
   }
 }
 

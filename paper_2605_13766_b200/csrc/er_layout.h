@@ -71,7 +71,8 @@ enum {
 };
 
 // batch-level feature bits (kernel template parameter)
-enum { FEAT_GENERAL = 1, FEAT_KAPPA0 = 2, FEAT_EXTRA = 4 /* sigma0 / magnetization / actuation */ };
+enum { FEAT_GENERAL = 1, FEAT_KAPPA0 = 2, FEAT_EXTRA = 4 /* sigma0 / magnetization / actuation */,
+       FEAT_CONTACT = 8 /* contact forces from ErStepParams.cfc; launch = kick + drift-2 [+ next drift-1] */ };
 
 // canonical fields (er_get_state / er_set_state order)
 enum { FIELD_POS = 0, FIELD_VEL = 1, FIELD_DIR = 2, FIELD_OMEGA = 3, FIELD_KAPPA0 = 4 };

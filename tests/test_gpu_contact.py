@@ -208,3 +208,18 @@ def test_set_state_forces_rebuild(er, orc):
     w2 = dataclasses.replace(w, positions=pos)
     o, _ = run_orc(orc, w2, 1)
     assert_parity(w2, g, o, TOL_1STEP, raw=("r", "v", "Q"), label="after set_state")
+
+
+def test_fused_equals_staged(er):
+    """The fused contact step (one persistent launch: kick + drift-2 + next drift-1 + node
+    records) is bitwise the staged one (drift | contact | dynamics | drift as separate kernels)."""
+    w = mixed_radii()
+    out = []
+    for kernel in (0, 1):
+        with er.RodBatch(w) as b:
+            b.set_option(er.ER_OPT_KERNEL, kernel)
+            b.step(37, w.dt)
+            b.step(13, w.dt)
+            out.append(b.get_state())
+    for x, y in zip(out[0], out[1]):
+        assert np.array_equal(x, y)
