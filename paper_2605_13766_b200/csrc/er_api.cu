@@ -31,8 +31,9 @@ cudaError_t er_launch_apply_forcing(double *rec, int64_t n_rods, const int32_t *
                                     double damping_all, const double *tip, const double *actA, const double *actF,
                                     const double *actL, int forcing, cudaStream_t st);
 cudaError_t er_contact_tmp_bytes(int64_t n, int bits, size_t *bytes);
-cudaError_t er_contact_eval(const ErContactParams *p, void *sort_tmp, size_t sort_bytes, int build, cudaStream_t st,
-                            int64_t *launches);
+cudaError_t er_contact_eval(const ErContactParams *p, void *tmp, size_t tmp_bytes, cudaGraphExec_t exec,
+                            cudaStream_t st, int64_t *launches, int graph_kernels);
+cudaError_t er_contact_graph(const ErContactParams *p, void *tmp, size_t tmp_bytes, cudaGraphExec_t *exec, int *kernels);
 }
 
 #include <chrono>
@@ -120,6 +121,8 @@ struct er_batch {
   ErContactParams cp{};
   void *sort_tmp = nullptr;
   size_t sort_bytes = 0;
+  cudaGraphExec_t cgraph = nullptr;  // per-step contact evaluation (conditional build)
+  int cgraph_kernels = 0;
   std::vector<double> rod_A0, rod_E0, rod_lmin, rod_lmax;  // host, per rod (contact radius, stiffness, HHG)
 };
 
@@ -153,6 +156,8 @@ void free_contact(er_batch *b) {
                   c.pnext, c.psrc, c.pf, c.ctr, c.bctr, b->sort_tmp};
   for (void *p : ptrs)
     if (p) cudaFree(p);
+  if (b->cgraph) cudaGraphExecDestroy(b->cgraph);
+  b->cgraph = nullptr;
   b->cp = ErContactParams{};
   b->sort_tmp = nullptr;
   b->sort_bytes = 0;
@@ -767,7 +772,7 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
     p.cfc = b->cp.fc;
     p.cfs = b->cp.fs;
     for (int64_t q = 0; q < n_steps; ++q) {
-      CK(er_contact_eval(&b->cp, b->sort_tmp, b->sort_bytes, 1, b->stream, &b->launches), "contact");
+      CK(er_contact_eval(&b->cp, b->sort_tmp, b->sort_bytes, b->cgraph, b->stream, &b->launches, b->cgraph_kernels), "contact");
       p.t = t;
       p.cnode = q + 1 < n_steps ? b->cp.cnode : nullptr;
       CK(er_launch_step(&p, b->block, 0, feat | FEAT_CONTACT, b->stream), "step kernel");
@@ -787,7 +792,7 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
       p.rebuild = b->cp.rebuild;
       CK(er_launch_step(&p, b->block, 1, 15, b->stream), "drift kernel");
       p.cnode = nullptr;
-      CK(er_contact_eval(&b->cp, b->sort_tmp, b->sort_bytes, 1, b->stream, &b->launches), "contact");
+      CK(er_contact_eval(&b->cp, b->sort_tmp, b->sort_bytes, b->cgraph, b->stream, &b->launches, b->cgraph_kernels), "contact");
       p.cfc = b->cp.fc;
       p.cfs = b->cp.fs;
       CK(er_launch_step(&p, b->block, 2, 7, b->stream), "dyn kernel");
@@ -950,6 +955,8 @@ er_status er_set_contact(er_batch *b, const er_contact *c) {
   CK(cudaMemsetAsync(cp.rebuild, 1, sizeof(int32_t), b->stream), "memset");
   CK(cudaMemsetAsync(cp.fc, 0, 6 * sizeof(double) * b->ne, b->stream), "memset");
   CK(cudaStreamSynchronize(b->stream), "sync");
+  if (!std::getenv("ER_NO_GRAPH"))
+    CK(er_contact_graph(&cp, b->sort_tmp, b->sort_bytes, &b->cgraph, &b->cgraph_kernels), "contact graph");
   b->contact_on = true;
   return ER_OK;
 }

@@ -315,6 +315,15 @@ __global__ void hhg_reset(const ErContactParams p, int64_t T) {
   if (t < 3 * ER_HHG_MAXLEV) p.gext[t] = 0ull;
 }
 
+// Graph conditions: the list build runs when the device flag is set; the long-list narrow
+// phase when the last build left any list longer than ER_CAND_K.
+__global__ void hhg_cond_build(const ErContactParams p, cudaGraphConditionalHandle h) {
+  cudaGraphSetConditional(h, *p.rebuild ? 1u : 0u);
+}
+__global__ void hhg_cond_long(const ErContactParams p, cudaGraphConditionalHandle h) {
+  cudaGraphSetConditional(h, p.bctr[4] ? 1u : 0u);
+}
+
 // End of a build: clear the flag, count the build.
 __global__ void hhg_built(const ErContactParams p) {
   if (!*p.rebuild) return;
@@ -534,6 +543,58 @@ __global__ void hhg_finish(const ErContactParams p) {
 
 }  // namespace erc
 
+namespace {
+
+cudaError_t enqueue_build(const ErContactParams &p, void *tmp, size_t tmp_bytes, cudaStream_t st) {
+  const int64_t E = p.n_elems, T = 1ll << p.hbits;
+  const unsigned g = (unsigned)std::min<int64_t>((E + 255) / 256, 148 * 16);
+  const unsigned gq = (unsigned)((E + 127) / 128);
+  erc::hhg_reset<<<(unsigned)std::min<int64_t>((T + 255) / 256, 148 * 16), 256, 0, st>>>(p, T);
+  erc::hhg_aabb<<<g, 256, 0, st>>>(p);
+  erc::hhg_dims<<<1, 32, 0, st>>>(p);
+  erc::hhg_keys<<<g, 256, 0, st>>>(p);
+  size_t bytes = tmp_bytes;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, bytes, p.key, p.key_s, p.val, p.val_s, (int)E, 0, p.hbits, st);
+  if (e != cudaSuccess) return e;
+  erc::hhg_cells<<<g, 256, 0, st>>>(p);
+  erc::hhg_table<<<g, 256, 0, st>>>(p);
+  erc::hhg_broad<<<gq, 128, 0, st>>>(p);
+  erc::hhg_built<<<1, 1, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+// Append an IF node (condition set on the device by `cond`) to the capture on `st`; its body is
+// captured from `body` on the side stream `side`.
+template <class Cond, class Body>
+cudaError_t capture_if(cudaStream_t st, cudaStream_t side, Cond &&cond, Body &&body) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g;
+  const cudaGraphNode_t *deps = nullptr;
+  size_t nd = 0;
+  cudaError_t e = cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd);
+  if (e != cudaSuccess) return e;
+  cudaGraphConditionalHandle h;
+  if ((e = cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault)) != cudaSuccess) return e;
+  cond(h);  // the kernel that sets h, captured on st
+  if ((e = cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd)) != cudaSuccess) return e;
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = cudaGraphCondTypeIf;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  if ((e = cudaGraphAddNode(&node, g, deps, nd, &np)) != cudaSuccess) return e;
+  if ((e = cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies)) != cudaSuccess) return e;
+  cudaGraph_t bg = np.conditional.phGraph_out[0];
+  if ((e = cudaStreamBeginCaptureToGraph(side, bg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+    return e;
+  cudaError_t eb = body(side);
+  e = cudaStreamEndCapture(side, &bg);
+  return eb != cudaSuccess ? eb : e;
+}
+
+}  // namespace
+
 extern "C" {
 
 // Temporary-storage bytes of the broad-phase sort (n keys of `bits` bits).
@@ -543,39 +604,73 @@ cudaError_t er_contact_tmp_bytes(int64_t n, int bits, size_t *bytes) {
                                          (const int32_t *)nullptr, (int32_t *)nullptr, (int)n, 0, bits);
 }
 
-// One contact evaluation at the positions/velocities in p.cnode: fills p.fc.  With `build`, the
-// list-build kernels are enqueued too (they do work only when the device flag is set).
-// Stream-ordered; no host synchronisation.  `launches` += kernels launched.
-cudaError_t er_contact_eval(const ErContactParams *pp, void *tmp, size_t tmp_bytes, int build, cudaStream_t st,
-                            int64_t *launches) {
+
+// The per-step contact evaluation as one CUDA graph: counters reset, [IF rebuild flag: list build],
+// narrow phase, [IF long lists: long-list narrow phase], cross-level gather.  The build (CUB sort
+// included) and the long-list pass are skipped on the device when not needed -- no host round trip.
+cudaError_t er_contact_graph(const ErContactParams *pp, void *tmp, size_t tmp_bytes, cudaGraphExec_t *exec,
+                             int *kernels) {
+  const ErContactParams &p = *pp;
+  const int64_t E = p.n_elems;
+  *exec = nullptr;
+  *kernels = 0;
+  if (E <= 0) return cudaSuccess;
+  cudaStream_t st, side;
+  cudaError_t e;
+  if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  if ((e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking)) != cudaSuccess) { cudaStreamDestroy(st); return e; }
+  cudaGraph_t graph = nullptr;
+  const int cross = p.nlev > 1;
+  const unsigned g = (unsigned)std::min<int64_t>((E + 255) / 256, 148 * 16);
+  const unsigned gq = (unsigned)((E + 127) / 128);
+  e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    cudaMemsetAsync(p.ctr, 0, 4 * sizeof(unsigned long long), st);
+    if (cross) cudaMemsetAsync(p.head, 0xff, sizeof(int32_t) * E, st);
+    e = capture_if(st, side, [&](cudaGraphConditionalHandle h) { erc::hhg_cond_build<<<1, 1, 0, st>>>(p, h); },
+                   [&](cudaStream_t s2) { return enqueue_build(p, tmp, tmp_bytes, s2); });
+    if (e == cudaSuccess) {
+      erc::hhg_narrow<false><<<gq, 128, 0, st>>>(p);
+      e = capture_if(st, side, [&](cudaGraphConditionalHandle h) { erc::hhg_cond_long<<<1, 1, 0, st>>>(p, h); },
+                     [&](cudaStream_t s2) {
+                       erc::hhg_narrow<true><<<gq, 128, 0, s2>>>(p);
+                       return cudaGetLastError();
+                     });
+    }
+    if (e == cudaSuccess && cross) erc::hhg_finish<<<g, 256, 0, st>>>(p);
+    cudaError_t e2 = cudaStreamEndCapture(st, &graph);
+    if (e == cudaSuccess) e = e2;
+  }
+  if (e == cudaSuccess) e = cudaGraphInstantiate(exec, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  cudaStreamDestroy(side);
+  cudaStreamDestroy(st);
+  *kernels = 3 + cross;  // kernels every step runs (narrow, two conditions, [cross gather])
+  return e;
+}
+
+// One contact evaluation at the positions/velocities in p.cnode: fills p.fc.  Stream-ordered, no
+// host synchronisation.  With `exec` (er_contact_graph) one graph launch; else the same work as
+// plain launches, the build kernels returning at once unless the device flag is set.
+cudaError_t er_contact_eval(const ErContactParams *pp, void *tmp, size_t tmp_bytes, cudaGraphExec_t exec,
+                            cudaStream_t st, int64_t *launches, int graph_kernels) {
   const ErContactParams &p = *pp;
   const int64_t E = p.n_elems;
   if (E <= 0) return cudaSuccess;
-  const int64_t T = 1ll << p.hbits;
+  if (exec) {
+    *launches += graph_kernels;
+    return cudaGraphLaunch(exec, st);
+  }
   cudaError_t e;
   if ((e = cudaMemsetAsync(p.ctr, 0, 4 * sizeof(unsigned long long), st)) != cudaSuccess) return e;
   const int cross = p.nlev > 1;
   if (cross && (e = cudaMemsetAsync(p.head, 0xff, sizeof(int32_t) * E, st)) != cudaSuccess) return e;
   const unsigned g = (unsigned)std::min<int64_t>((E + 255) / 256, 148 * 16);
   const unsigned gq = (unsigned)((E + 127) / 128);
-  if (build) {  // list build: every kernel returns at once unless the device flag is set
-    erc::hhg_reset<<<(T + 255) / 256 < 148 * 16 ? (unsigned)((T + 255) / 256) : 148 * 16, 256, 0, st>>>(p, T);
-    erc::hhg_aabb<<<g, 256, 0, st>>>(p);
-    erc::hhg_dims<<<1, 32, 0, st>>>(p);
-    erc::hhg_keys<<<g, 256, 0, st>>>(p);
-    size_t bytes = tmp_bytes;
-    if ((e = cub::DeviceRadixSort::SortPairs(tmp, bytes, p.key, p.key_s, p.val, p.val_s, (int)E, 0, p.hbits, st)) !=
-        cudaSuccess)
-      return e;
-    erc::hhg_cells<<<g, 256, 0, st>>>(p);
-    erc::hhg_table<<<g, 256, 0, st>>>(p);
-    erc::hhg_broad<<<gq, 128, 0, st>>>(p);
-    erc::hhg_built<<<1, 1, 0, st>>>(p);
-    *launches += 9;
-  }
+  if ((e = enqueue_build(p, tmp, tmp_bytes, st)) != cudaSuccess) return e;
   erc::hhg_narrow<false><<<gq, 128, 0, st>>>(p);
   erc::hhg_narrow<true><<<gq, 128, 0, st>>>(p);
-  *launches += 2;
+  *launches += 10;
   if (cross) {
     erc::hhg_finish<<<g, 256, 0, st>>>(p);
     *launches += 1;

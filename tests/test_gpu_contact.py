@@ -223,3 +223,21 @@ def test_fused_equals_staged(er):
             out.append(b.get_state())
     for x, y in zip(out[0], out[1]):
         assert np.array_equal(x, y)
+
+
+def test_graph_equals_plain_launches(er, monkeypatch):
+    """The per-step contact graph (conditional list build / long-list pass decided on the device)
+    is bitwise the plain launch sequence; rebuilds happen inside the graph."""
+    w = mixed_radii()
+    w.velocities = w.velocities * 300.0
+    out = []
+    for no_graph in (False, True):
+        if no_graph:
+            monkeypatch.setenv("ER_NO_GRAPH", "1")
+        with er.RodBatch(w) as b:
+            b.set_contact(w.contact, skin=2e-7)
+            b.step(60, w.dt)
+            out.append((b.get_state(), b.contact_stats().builds))
+    assert out[0][1] == out[1][1] > 10
+    for x, y in zip(out[0][0], out[1][0]):
+        assert np.array_equal(x, y)
