@@ -331,43 +331,43 @@ __global__ void hhg_built(const ErContactParams p) {
   p.bctr[5] += 1;
 }
 
-__device__ __forceinline__ double dot3(const double a[3], const double b[3]) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+__device__ __forceinline__ double dot3(const double a[3], const double b[3]) { return fma(a[0], b[0], fma(a[1], b[1], a[2] * b[2])); }
 __device__ __forceinline__ double clamp01(double x) { return x < 0.0 ? 0.0 : (x > 1.0 ? 1.0 : x); }
 
-// Closest points of segments P(s) = p0 + s (p1 - p0), Q(t) = q0 + t (q1 - q0), s, t in [0, 1]:
-// the minimiser of |P(s) - Q(t)|^2 over the unit square.  Candidates in this order: the interior
-// stationary point (when inside the square), then the edges s = 0, s = 1, t = 0, t = 1 each with
-// its clamped 1-D minimiser; the first candidate of least distance wins (DESIGN §3 #27).
-__device__ __forceinline__ void segment_closest(const double p0[3], const double p1[3], const double q0[3],
-                                                const double q1[3], double &s, double &t, double &dist) {
-  double u[3], v[3], w[3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    u[c] = p1[c] - p0[c];
-    v[c] = q1[c] - q0[c];
-    w[c] = p0[c] - q0[c];
-  }
+// Closest points of segments P(s) = p0 + s u, Q(t) = q0 + t v, s, t in [0, 1], given u, v and
+// w = p0 - q0: the minimiser of |P(s) - Q(t)|^2 over the unit square.  Candidates in this order:
+// the interior stationary point (when inside the square), then the edges s = 0, s = 1, t = 0,
+// t = 1 each with its clamped 1-D minimiser; the first candidate of least distance wins (DESIGN
+// §3 #27).  Returns s, t, x = P(s) - Q(t) and |x|^2.
+__device__ __forceinline__ double segment_closest(const double u[3], const double v[3], const double w[3], double &s,
+                                                  double &t, double x[3]) {
   const double uu = dot3(u, u), vv = dot3(v, v), uv = dot3(u, v), uw = dot3(u, w), vw = dot3(v, w);
   double best = -1.0;
   s = 0.0;
   t = 0.0;
   auto consider = [&](double cs, double ct) {
-    double x[3];
+    double y[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) x[c] = p0[c] + cs * u[c] - q0[c] - ct * v[c];
-    const double d2 = dot3(x, x);
-    if (best < 0.0 || d2 < best) { best = d2; s = cs; t = ct; }
+    for (int c = 0; c < 3; ++c) y[c] = fma(-ct, v[c], fma(cs, u[c], w[c]));
+    const double d2 = dot3(y, y);
+    if (best < 0.0 || d2 < best) {
+      best = d2; s = cs; t = ct;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) x[c] = y[c];
+    }
   };
-  const double det = uu * vv - uv * uv;
+  const double det = fma(uu, vv, -uv * uv);
   if (det > 0.0) {
-    const double si = (uv * vw - uw * vv) / det, ti = (uu * vw - uv * uw) / det;
+    const double idet = 1.0 / det;
+    const double si = fma(uv, vw, -uw * vv) * idet, ti = fma(uu, vw, -uv * uw) * idet;
     if (si >= 0.0 && si <= 1.0 && ti >= 0.0 && ti <= 1.0) consider(si, ti);
   }
-  consider(0.0, vv > 0.0 ? clamp01(vw / vv) : 0.0);
-  consider(1.0, vv > 0.0 ? clamp01((vw + uv) / vv) : 0.0);
-  consider(uu > 0.0 ? clamp01(-uw / uu) : 0.0, 0.0);
-  consider(uu > 0.0 ? clamp01((uv - uw) / uu) : 0.0, 1.0);
-  dist = sqrt(best);
+  const double ivv = vv > 0.0 ? 1.0 / vv : 0.0, iuu = uu > 0.0 ? 1.0 / uu : 0.0;
+  consider(0.0, clamp01(vw * ivv));
+  consider(1.0, clamp01((vw + uv) * ivv));
+  consider(clamp01(-uw * iuu), 0.0);
+  consider(clamp01((uv - uw) * iuu), 1.0);
+  return best;
 }
 
 // Penalty normal force F_n = max(0, k (-gap) - gamma_n v_n) along n, regularised Coulomb friction
@@ -387,27 +387,23 @@ __device__ __forceinline__ void contact_law(const ErContactLaw &L, double k, dou
   for (int c = 0; c < 3; ++c) F[c] = fn * n[c] + ck * vt[c];
 }
 
-// Force of the pair (x, y), x the lower element id, on x; false when not in contact.  Px, Py:
-// segment end points; Vx, Vy: end-point velocities (node records, read only for touching pairs).
-__device__ __forceinline__ bool pair_force(const ErContactParams &p, const double *Px, const double *Py,
-                                           const double *Vx, const double *Vy, double rx, double ry, double k,
-                                           double F[3], double &s, double &t) {
-  double d;
-  segment_closest(Px, Px + 3, Py, Py + 3, s, t, d);
+// Force of the pair (x, y), x the lower element id, on x; false when not in contact.  u, v: the
+// segments' edge vectors, w = x's first node - y's first node; Vx, Vy: end-point velocity
+// records (node stride 6), read only for touching pairs.
+__device__ __forceinline__ bool pair_force(const ErContactParams &p, const double u[3], const double v[3],
+                                           const double w[3], const double *Vx, const double *Vy, double rx,
+                                           double ry, double k, double F[3], double &s, double &t) {
+  double x[3];
+  const double d = sqrt(segment_closest(u, v, w, s, t, x));
   const double gap = d - (rx + ry);
   if (!(gap < 0.0) || d == 0.0) return false;
   double n[3], vr[3];
   const double id = 1.0 / d;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    const double pa = (1.0 - s) * Px[c] + s * Px[3 + c];
-    const double pb = (1.0 - t) * Py[c] + t * Py[3 + c];
-    n[c] = (pa - pb) * id;
-  }
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const double va = (1.0 - s) * __ldg(Vx + c) + s * __ldg(Vx + 6 + c);
-    const double vb = (1.0 - t) * __ldg(Vy + c) + t * __ldg(Vy + 6 + c);
+    n[c] = x[c] * id;
+    const double va = fma(s, __ldg(Vx + 6 + c), (1.0 - s) * __ldg(Vx + c));
+    const double vb = fma(t, __ldg(Vy + 6 + c), (1.0 - t) * __ldg(Vy + c));
     vr[c] = va - vb;
   }
   contact_law(p.law, k, gap, n, vr, F);
@@ -447,24 +443,38 @@ __global__ void __launch_bounds__(128, LONG ? 4 : 6) hhg_narrow(const ErContactP
   if (ea < p.n_elems && ((p.cnt[ea] > ER_CAND_K) == LONG)) {
     const int roda = __ldg(p.erod + ea);
     const double *Va = p.cnode + 6 * (ea + roda) + 3;  // velocities: read only on contact
-    double Pa[6];
+    double A0[3], ua[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) { Pa[c] = Va[c - 3]; Pa[3 + c] = Va[3 + c]; }
+    for (int c = 0; c < 3; ++c) { A0[c] = Va[c - 3]; ua[c] = Va[3 + c] - A0[c]; }
     const double ra = __ldg(p.rad + roda), kra = __ldg(p.kr + roda);
     double f[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     auto pair = [&](int eb, bool cross) {
       const int rodb = __ldg(p.erod + eb);
-      double Pb[6];
-      const double *x = p.cnode + 6 * ((int64_t)eb + rodb);
-      const double *Vb = x + 3;
+      const double *xb = p.cnode + 6 * ((int64_t)eb + rodb);
+      const double *Vb = xb + 3;
+      double ub[3], wab[3];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) { Pb[c] = __ldg(x + c); Pb[3 + c] = __ldg(x + 6 + c); }
+      for (int c = 0; c < 3; ++c) {
+        const double b0 = __ldg(xb + c);
+        ub[c] = __ldg(xb + 6 + c) - b0;
+        wab[c] = A0[c] - b0;
+      }
       const double rb = __ldg(p.rad + rodb);
       const double k = p.law.k_n > 0.0 ? p.law.k_n : fmin(kra, __ldg(p.kr + rodb));
       const bool a_first = ea < eb;
+      // one call site in canonical order (lower element id first): both elements of a pair run the
+      // same instructions on the same operands (w changes sign exactly), so their forces are
+      // bitwise opposite
+      double u[3], v[3], w[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        u[c] = a_first ? ua[c] : ub[c];
+        v[c] = a_first ? ub[c] : ua[c];
+        w[c] = a_first ? wab[c] : -wab[c];
+      }
       double F[3], s, t;
-      const bool hit = a_first ? pair_force(p, Pa, Pb, Va, Vb, ra, rb, k, F, s, t)
-                               : pair_force(p, Pb, Pa, Vb, Va, rb, ra, k, F, s, t);
+      const bool hit = pair_force(p, u, v, w, a_first ? Va : Vb, a_first ? Vb : Va, a_first ? ra : rb,
+                                  a_first ? rb : ra, k, F, s, t);
       if (!hit) return;
       n_cont += (cross || a_first);  // each pair once
       // F acts on the first (lower-id) element at weights (1-s, s); -F on the second at (1-t, t)
