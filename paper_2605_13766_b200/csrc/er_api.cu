@@ -151,7 +151,7 @@ cudaError_t dalloc(er_batch *b, T **p, int64_t count) {
 
 void free_contact(er_batch *b) {
   ErContactParams &c = b->cp;
-  void *ptrs[] = {(void *)c.rad, (void *)c.kr, (void *)c.erod, c.cnode, c.cbuild, c.rebuild, c.gext, c.gdim, c.key,
+  void *ptrs[] = {(void *)c.rad, (void *)c.kr, (void *)c.erod, (void *)c.nrad, (void *)c.nkr, c.cnode, c.cbuild, c.rebuild, c.gext, c.gdim, c.key,
                   c.key_s, c.val, c.val_s, c.table, c.code_s, c.boxa, c.boxb, c.qidx, c.cnt, c.cand, c.fc, c.head,
                   c.pnext, c.psrc, c.pf, c.ctr, c.bctr, b->sort_tmp};
   for (void *p : ptrs)
@@ -923,14 +923,19 @@ er_status er_set_contact(er_batch *b, const er_contact *c) {
   cp.pcap = std::max<int64_t>(1024, (int64_t)(pf * (double)E));
 
   std::vector<int32_t> erod((size_t)std::max<int64_t>(E, 1));
-  for (int64_t r = 0; r < R; ++r)
+  std::vector<double> nrad((size_t)std::max<int64_t>(b->n_nodes, 1)), nkr((size_t)std::max<int64_t>(b->n_nodes, 1));
+  for (int64_t r = 0; r < R; ++r) {
     for (int64_t j = b->eoff[r]; j < b->eoff[r + 1]; ++j) erod[j] = (int32_t)r;
+    for (int64_t n = b->eoff[r] + r; n <= b->eoff[r + 1] + r; ++n) { nrad[n] = rad[r]; nkr[n] = kr[r]; }
+  }
+  double *d_nrad = nullptr, *d_nkr = nullptr;
   double *d_rad = nullptr, *d_kr = nullptr;
   int32_t *d_erod = nullptr;
   const int64_t T = 1ll << hb;
 #define CA(ptr, n) CK(dalloc(b, &(ptr), (n)), "cudaMalloc(contact)")
   CA(d_rad, R); CA(d_kr, R); CA(d_erod, E);
-  cp.rad = d_rad; cp.kr = d_kr; cp.erod = d_erod;
+  CA(d_nrad, b->n_nodes); CA(d_nkr, b->n_nodes);
+  cp.rad = d_rad; cp.kr = d_kr; cp.erod = d_erod; cp.nrad = d_nrad; cp.nkr = d_nkr;
   CA(cp.cnode, 6 * b->n_nodes); CA(cp.cbuild, 3 * b->n_nodes); CA(cp.rebuild, 1);
   CA(cp.gext, 3 * ER_HHG_MAXLEV); CA(cp.gdim, 4 * ER_HHG_MAXLEV);
   CA(cp.key, E); CA(cp.key_s, E); CA(cp.val, E); CA(cp.val_s, E);
@@ -938,7 +943,7 @@ er_status er_set_contact(er_batch *b, const er_contact *c) {
   CA(cp.boxa, E); CA(cp.boxb, E); CA(cp.qidx, E);
   CA(cp.cnt, E); CA(cp.cand, ER_CAND_K * E);
   CA(cp.fc, 6 * b->ne);
-  CA(cp.head, E); CA(cp.pnext, cp.pcap); CA(cp.psrc, cp.pcap); CA(cp.pf, 6 * cp.pcap);
+  CA(cp.head, b->n_nodes); CA(cp.pnext, cp.pcap); CA(cp.psrc, cp.pcap); CA(cp.pf, 6 * cp.pcap);
   CA(cp.ctr, 8); CA(cp.bctr, 8);
 #undef CA
   cp.fault = b->d_fault;
@@ -949,6 +954,8 @@ er_status er_set_contact(er_batch *b, const er_contact *c) {
     CK(cudaMemcpyAsync(d_rad, rad.data(), sizeof(double) * R, cudaMemcpyHostToDevice, b->stream), "H2D rad");
     CK(cudaMemcpyAsync(d_kr, kr.data(), sizeof(double) * R, cudaMemcpyHostToDevice, b->stream), "H2D kr");
     CK(cudaMemcpyAsync(d_erod, erod.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice, b->stream), "H2D erod");
+    CK(cudaMemcpyAsync(d_nrad, nrad.data(), sizeof(double) * b->n_nodes, cudaMemcpyHostToDevice, b->stream), "H2D nrad");
+    CK(cudaMemcpyAsync(d_nkr, nkr.data(), sizeof(double) * b->n_nodes, cudaMemcpyHostToDevice, b->stream), "H2D nkr");
   }
   CK(cudaMemsetAsync(cp.ctr, 0, 8 * sizeof(unsigned long long), b->stream), "memset");
   CK(cudaMemsetAsync(cp.bctr, 0, 8 * sizeof(unsigned long long), b->stream), "memset");

@@ -270,7 +270,7 @@ __device__ __forceinline__ void broad_visit(const ErContactParams &p, int64_t q,
               continue;
             const int eb = __float_as_int(Ab.w);
             if (__float_as_int(Bb.w) == roda && abs(ea - eb) <= p.law.exclude) continue;
-            visit(eb, L > la, L > la || ea < eb);
+            visit(eb + __float_as_int(Bb.w), L > la, L > la || ea < eb);  // partner's first node
           }
         }
   }
@@ -286,8 +286,8 @@ __global__ void __launch_bounds__(128) hhg_broad(const ErContactParams p) {
   if (q < p.n_elems) {
     const int64_t E = p.n_elems;
     const int e = __float_as_int(p.boxa[q].w);
-    broad_visit(p, q, [&](int eb, bool cross, bool owner) {
-      if (n < ER_CAND_K) p.cand[n * E + e] = eb | (cross ? ER_CAND_CROSS : 0);
+    broad_visit(p, q, [&](int nb, bool cross, bool owner) {
+      if (n < ER_CAND_K) p.cand[n * E + e] = nb | (cross ? ER_CAND_CROSS : 0);
       ++n;
       own += owner;
     }, scanned);
@@ -322,6 +322,9 @@ __global__ void hhg_cond_build(const ErContactParams p, cudaGraphConditionalHand
 }
 __global__ void hhg_cond_long(const ErContactParams p, cudaGraphConditionalHandle h) {
   cudaGraphSetConditional(h, p.bctr[4] ? 1u : 0u);
+}
+__global__ void hhg_cond_cross(const ErContactParams p, cudaGraphConditionalHandle h) {
+  cudaGraphSetConditional(h, p.ctr[2] ? 1u : 0u);
 }
 
 // End of a build: clear the flag, count the build.
@@ -441,16 +444,17 @@ __global__ void __launch_bounds__(128, LONG ? 4 : 6) hhg_narrow(const ErContactP
   const int64_t ea = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   unsigned n_cont = 0, n_cross = 0, n_plane = 0;
   if (ea < p.n_elems && ((p.cnt[ea] > ER_CAND_K) == LONG)) {
-    const int roda = __ldg(p.erod + ea);
-    const double *Va = p.cnode + 6 * (ea + roda) + 3;  // velocities: read only on contact
+    const int64_t na = ea + __ldg(p.erod + ea);        // first node of element a
+    const double *Va = p.cnode + 6 * na + 3;          // velocities: read only on contact
     double A0[3], ua[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) { A0[c] = Va[c - 3]; ua[c] = Va[3 + c] - A0[c]; }
-    const double ra = __ldg(p.rad + roda), kra = __ldg(p.kr + roda);
+    const double ra = __ldg(p.nrad + na), kra = __ldg(p.nkr + na);
     double f[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    auto pair = [&](int eb, bool cross) {
-      const int rodb = __ldg(p.erod + eb);
-      const double *xb = p.cnode + 6 * ((int64_t)eb + rodb);
+    // candidates are named by their first node: node order = element order, so the canonical
+    // (lower element id first) order is the lower first node
+    auto pair = [&](int nb, bool cross) {
+      const double *xb = p.cnode + 6 * (int64_t)nb;
       const double *Vb = xb + 3;
       double ub[3], wab[3];
 #pragma unroll
@@ -459,9 +463,9 @@ __global__ void __launch_bounds__(128, LONG ? 4 : 6) hhg_narrow(const ErContactP
         ub[c] = __ldg(xb + 6 + c) - b0;
         wab[c] = A0[c] - b0;
       }
-      const double rb = __ldg(p.rad + rodb);
-      const double k = p.law.k_n > 0.0 ? p.law.k_n : fmin(kra, __ldg(p.kr + rodb));
-      const bool a_first = ea < eb;
+      const double rb = __ldg(p.nrad + nb);
+      const double k = p.law.k_n > 0.0 ? p.law.k_n : fmin(kra, __ldg(p.nkr + nb));
+      const bool a_first = na < nb;
       // one call site in canonical order (lower element id first): both elements of a pair run the
       // same instructions on the same operands (w changes sign exactly), so their forces are
       // bitwise opposite
@@ -488,15 +492,15 @@ __global__ void __launch_bounds__(128, LONG ? 4 : 6) hhg_narrow(const ErContactP
       if (cross) {  // the coarser element b never sees this pair: leave it a record
         ++n_cross;
         const unsigned long long r = atomicAdd(p.ctr + 0, 1ull);
-        if (r >= (unsigned long long)p.pcap) { flag_fault(p, rodb); return; }
+        if (r >= (unsigned long long)p.pcap) { flag_fault(p, 0); return; }
         const double v0 = a_first ? 1.0 - t : 1.0 - s, v1 = a_first ? t : s;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           p.pf[6 * r + c] = v0 * (-sg * F[c]);
           p.pf[6 * r + 3 + c] = v1 * (-sg * F[c]);
         }
-        p.psrc[r] = (int32_t)ea;
-        p.pnext[r] = atomicExch(p.head + eb, (int32_t)r);
+        p.psrc[r] = (int32_t)na;
+        p.pnext[r] = atomicExch(p.head + nb, (int32_t)r);
       }
     };
     if (!LONG) {
@@ -507,9 +511,9 @@ __global__ void __launch_bounds__(128, LONG ? 4 : 6) hhg_narrow(const ErContactP
       }
     } else {
       unsigned sc = 0;
-      broad_visit(p, p.qidx[ea], [&](int eb, bool cross, bool) { pair(eb, cross); }, sc);
+      broad_visit(p, p.qidx[ea], [&](int nb, bool cross, bool) { pair(nb, cross); }, sc);
     }
-    if (p.law.plane_on) n_plane = plane_forces(p, ea, roda, f);
+    if (p.law.plane_on) n_plane = plane_forces(p, ea, (int)(na - ea), f);
 #pragma unroll
     for (int c = 0; c < 6; ++c) p.fc[c * p.fs + ea] = f[c];
   }
@@ -528,9 +532,9 @@ constexpr int MAX_CROSS = 64;
 // Cross-level records of each coarse element, summed in increasing source-element order.
 __global__ void hhg_finish(const ErContactParams p) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < p.n_elems; e += (int64_t)gridDim.x * blockDim.x) {
-    int h = p.head[e];
-    if (h < 0) continue;
     const int rod = __ldg(p.erod + e);
+    int h = p.head[e + rod];  // records are filed under the element's first node
+    if (h < 0) continue;
     double f[6];
 #pragma unroll
     for (int c = 0; c < 6; ++c) f[c] = p.fc[c * p.fs + e];
@@ -636,7 +640,7 @@ cudaError_t er_contact_graph(const ErContactParams *pp, void *tmp, size_t tmp_by
   e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
   if (e == cudaSuccess) {
     cudaMemsetAsync(p.ctr, 0, 4 * sizeof(unsigned long long), st);
-    if (cross) cudaMemsetAsync(p.head, 0xff, sizeof(int32_t) * E, st);
+    if (cross) cudaMemsetAsync(p.head, 0xff, sizeof(int32_t) * p.n_nodes, st);
     e = capture_if(st, side, [&](cudaGraphConditionalHandle h) { erc::hhg_cond_build<<<1, 1, 0, st>>>(p, h); },
                    [&](cudaStream_t s2) { return enqueue_build(p, tmp, tmp_bytes, s2); });
     if (e == cudaSuccess) {
@@ -647,7 +651,12 @@ cudaError_t er_contact_graph(const ErContactParams *pp, void *tmp, size_t tmp_by
                        return cudaGetLastError();
                      });
     }
-    if (e == cudaSuccess && cross) erc::hhg_finish<<<g, 256, 0, st>>>(p);
+    if (e == cudaSuccess && cross)
+      e = capture_if(st, side, [&](cudaGraphConditionalHandle h) { erc::hhg_cond_cross<<<1, 1, 0, st>>>(p, h); },
+                     [&](cudaStream_t s2) {
+                       erc::hhg_finish<<<g, 256, 0, s2>>>(p);
+                       return cudaGetLastError();
+                     });
     cudaError_t e2 = cudaStreamEndCapture(st, &graph);
     if (e == cudaSuccess) e = e2;
   }
@@ -655,7 +664,7 @@ cudaError_t er_contact_graph(const ErContactParams *pp, void *tmp, size_t tmp_by
   if (graph) cudaGraphDestroy(graph);
   cudaStreamDestroy(side);
   cudaStreamDestroy(st);
-  *kernels = 3 + cross;  // kernels every step runs (narrow, two conditions, [cross gather])
+  *kernels = 3 + cross;  // kernels every step runs (narrow, conditions)
   return e;
 }
 
@@ -674,7 +683,7 @@ cudaError_t er_contact_eval(const ErContactParams *pp, void *tmp, size_t tmp_byt
   cudaError_t e;
   if ((e = cudaMemsetAsync(p.ctr, 0, 4 * sizeof(unsigned long long), st)) != cudaSuccess) return e;
   const int cross = p.nlev > 1;
-  if (cross && (e = cudaMemsetAsync(p.head, 0xff, sizeof(int32_t) * E, st)) != cudaSuccess) return e;
+  if (cross && (e = cudaMemsetAsync(p.head, 0xff, sizeof(int32_t) * p.n_nodes, st)) != cudaSuccess) return e;
   const unsigned g = (unsigned)std::min<int64_t>((E + 255) / 256, 148 * 16);
   const unsigned gq = (unsigned)((E + 127) / 128);
   if ((e = enqueue_build(p, tmp, tmp_bytes, st)) != cudaSuccess) return e;

@@ -121,6 +121,7 @@ struct ErContactParams {
   const double *rad;            // [R] contact radius
   const double *kr;             // [R] E r (pair stiffness scale)
   const int32_t *erod;          // [E] rod of each element
+  const double *nrad, *nkr;     // [n_nodes] contact radius / E r of the node's rod
   double *cnode;                // [n_nodes][6] node r, v after drift-1 (AoS: an element's two
                                 //   nodes are 96 contiguous bytes)
   double *cbuild;               // [n_nodes][3] node positions at the last list build
@@ -136,12 +137,13 @@ struct ErContactParams {
                                 //     boxa.w = element id bits, boxb.w = rod id bits
   int32_t *qidx;                // [E] sorted position of each element
   int32_t *cnt;                 // [E] candidates of each element (at the last build)
-  int32_t *cand;                // [ER_CAND_K][E] the first ER_CAND_K of them: element id,
-                                //   | ER_CAND_CROSS when the partner is on a coarser level
+  int32_t *cand;                // [ER_CAND_K][E] the first ER_CAND_K of them: the partner's first
+                                //   node | ER_CAND_CROSS when the partner is on a coarser level
   double *fc;                   // [6][fs] contact force on the element's (node j, node j+1)
   int64_t fs;
-  int32_t *head;                // [E] cross-level records per coarse element (-1 = none)
-  int32_t *pnext, *psrc;        // [pcap] record chain / source (fine) element
+  int32_t *head;                // [n_nodes] cross-level records per coarse element, filed under its
+                                //   first node (-1 = none)
+  int32_t *pnext, *psrc;        // [pcap] record chain / source (fine) element's first node
   double *pf;                   // [pcap][6] record force on the coarse element's two nodes
   int64_t pcap;
   unsigned long long *ctr;      // [8] per step: 0 pool used, 1 contacts, 2 cross-level contacts,
