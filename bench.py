@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg3", choices=list(W.CONFIG_NAMES))
+    ap.add_argument("--config", default="cfg3", choices=list(W.CONFIG_NAMES) + list(W.EXTRA_CONFIGS))
     ap.add_argument("--steps-per-launch", type=int, default=1,
                     help="1 = every step streams the state through HBM (the B_min design); "
                          ">1 = temporal blocking (SURVEY NEXT-1)")
@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-temporal", action="store_true")
+    ap.add_argument("--no-contact", action="store_true")
     ap.add_argument("--cpu-sample-rods", type=int, default=8192)
     ap.add_argument("--cpu-sample-steps", type=int, default=300)
     return ap.parse_args()
@@ -128,14 +129,23 @@ def shard(w, rank, world, scaling):
     slots = np.cumsum(w.n_elems.astype(np.int64) + 1)
     total = slots[-1]
     cuts = [0] + [int(np.searchsorted(slots, total * k / world, side="left")) + 1 for k in range(1, world)] + [w.n_rods]
+    if getattr(w, "contact", None) is not None:
+        # rods that touch must stay on one GPU: cut only between the fibres stacks, which never
+        # touch (0.2 L apart), so the shards need no halo exchange
+        per = W.FIBRES["layers"] * W.FIBRES["per_layer"]
+        cuts = [int(round(c / per)) * per for c in cuts]
     cuts = np.clip(cuts, 0, w.n_rods)
     return w.subset(np.arange(cuts[rank], cuts[rank + 1]))
 
 
 def oracle_rate(w, n_rods, n_steps, seed=3):
-    """The oracle as it stands (single-threaded C), on a seeded rod sample."""
+    """The oracle as it stands (single-threaded C), on a seeded rod sample (for contact workloads:
+    the first whole stack, an independent sub-problem)."""
     import oracle
-    rods = W.sample_rods(w, n_rods, seed=seed)
+    if getattr(w, "contact", None) is not None:
+        rods = np.arange(min(w.n_rods, W.FIBRES["layers"] * W.FIBRES["per_layer"]))
+    else:
+        rods = W.sample_rods(w, n_rods, seed=seed)
     ws = w.subset(rods)
     t0 = time.perf_counter()
     st, s, _, _ = oracle.step(ws, n_steps=n_steps)
@@ -149,7 +159,10 @@ def run_reference(a):
         return
     w = W.make(a.config)
     import oracle
-    rods = W.sample_rods(w, min(4096, w.n_rods), seed=4)
+    if getattr(w, "contact", None) is not None:   # a whole stack: an independent contact sub-problem
+        rods = np.arange(min(w.n_rods, W.FIBRES["layers"] * W.FIBRES["per_layer"]))
+    else:
+        rods = W.sample_rods(w, min(4096, w.n_rods), seed=4)
     ws = w.subset(rods)
     st = oracle.State.of(ws)
     for _ in range(max(a.warmup, 0)):
@@ -258,7 +271,7 @@ def main():
     # NEXT-1 context: the same job with the rod tile kept on chip for several steps per launch
     # (temporal blocking; bitwise-identical results), timed the same way on the same batch
     temporal = None
-    if a.steps_per_launch == 1 and not a.no_temporal:
+    if a.steps_per_launch == 1 and not a.no_temporal and getattr(w, "contact", None) is None:
         spl = 100
         b.set_option(er.ER_OPT_STEPS_PER_LAUNCH, spl)
         b.step(spl, dt)
@@ -275,6 +288,12 @@ def main():
         temporal = {"steps_per_launch": spl, "ms_per_step": float(tms.item()) / a.steps,
                     "value": float(el_total.item()) * a.steps / (float(tms.item()) * 1e-3),
                     "note": "SURVEY NEXT-1: state crosses HBM once per launch; FP64/issue-bound"}
+
+    # NEXT-4 context: the contact workload (fibres: 65,536 rods x 16 elements in crossed layers,
+    # HHG broad phase + Verlet lists + narrow phase every step), same timing protocol
+    contact = None
+    if world == 1 and not a.no_contact and a.config != "fibres":
+        contact = contact_run(er, a.steps, local, stream)
 
     # end-to-end through the public API with HOST buffers (pinned): create from host, K steps,
     # state back to host; the H2D/D2H bytes are amortised over the K steps of the job
@@ -308,6 +327,7 @@ def main():
             "e2e": e2e,
             "gpu_launches": launches,
             "temporal_blocking": temporal,
+            "contact": contact,
             "clocks": clk.summary(),
             "diagnostics": {k: float(v) for k, v in zip(er.DIAG_NAMES, diag.cpu().numpy())},
         }
@@ -315,6 +335,31 @@ def main():
     b.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def contact_run(er, steps, local, stream):
+    import torch
+    wc = W.make("fibres")
+    bc = er.RodBatch(wc, device=local, stream=stream)
+    bc.step(20, wc.dt)
+    torch.cuda.synchronize()
+    l0 = bc.info().launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    bc.step(steps, wc.dt)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    st = bc.contact_stats()
+    launches = bc.info().launches - l0
+    bc.close()
+    return {"workload": f"fibres: {wc.n_rods} rods x 16 elements ({wc.n_elems_total} elements) in crossed layers "
+                        "on a floor, contact + friction every step, dt=1e-6",
+            "ms_per_step": ms / steps, "value": wc.n_elems_total * steps / (ms * 1e-3), "unit": "element-steps/s",
+            "contacts": st.contacts, "plane_contacts": st.plane_contacts, "candidates": st.candidates,
+            "list_builds": st.builds, "gpu_launches": launches,
+            "note": "SURVEY NEXT-4: HHG broad phase with Verlet lists (device-side rebuild), exact "
+                    "segment-segment narrow phase; one CUDA graph + one persistent step kernel per step"}
 
 
 def e2e_run(er, w, steps, dt, local, world):

@@ -71,3 +71,15 @@ def test_gloo_diagnostics_allreduce(orc):
     ref = orc.energy(w, st)
     assert np.allclose(got, ref, rtol=1e-12, atol=1e-300)
     assert got[9] == ref[9] and got[11] == ref[11]
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_contact_shards_cut_between_stacks(world):
+    """Contact workloads shard only at fibres-stack boundaries (stacks never touch), so every
+    touching pair stays on one rank and no halo exchange is needed."""
+    per = W.FIBRES["layers"] * W.FIBRES["per_layer"]
+    w = W.make("fibres", n_rods=16 * per)
+    shards = [bench.shard(w, r, world, "strong") for r in range(world)]
+    assert sum(s.n_rods for s in shards) == w.n_rods
+    assert all(s.n_rods % per == 0 for s in shards)
+    assert np.array_equal(np.concatenate([s.positions for s in shards]), w.positions)

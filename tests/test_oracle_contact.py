@@ -124,3 +124,23 @@ def test_head_on_impact_conserves_momentum(orc):
     P1 = orc.energy(w, st)[6:9]
     assert np.allclose(P1, P0, rtol=0, atol=1e-12 * np.abs(P0).max())
     assert st.velocities[nB, 2].mean() > -0.5                          # B was slowed by the contact
+
+
+def test_fibres_recipe(orc):
+    """The NEXT-4 contact workload: neighbouring layers of a stack overlap by overlap +- overlap/4
+    at every crossing, the bottom layer presses into the floor, and two neighbouring stacks never
+    touch (so a stack is an independent sub-problem, used for full-size parity and sharding)."""
+    c = W.FIBRES
+    per = c["layers"] * c["per_layer"]
+    w = W.make("fibres", n_rods=2 * per)
+    pairs, gaps = orc.contact_pairs(w, w.positions)
+    assert len(pairs) > 0
+    assert np.all(gaps < -c["overlap"] / 4) and np.all(gaps > -7 * c["overlap"] / 4)
+    rod_of = np.repeat(np.arange(w.n_rods), w.n_elems)
+    assert np.all(rod_of[pairs[:, 0]] // per == rod_of[pairs[:, 1]] // per)      # no pair across stacks
+    # each crossing of neighbouring layers in stack 0 is one contact (16 x 16 crossings x 15 layer pairs,
+    # a crossing at an element boundary can count twice)
+    st0 = pairs[rod_of[pairs[:, 0]] < per]
+    assert 16 * 16 * 15 <= len(st0) <= 2 * 16 * 16 * 15
+    z0 = w.positions[:, 2][np.repeat(np.arange(w.n_rods), w.n_elems + 1) % per < c["per_layer"]]
+    assert np.all(z0 < c["radius"]) and np.all(z0 > c["radius"] - c["overlap"])
