@@ -64,9 +64,14 @@ def peaks():
 
 
 def b_min_per_el_step(w) -> float:
-    """16 [6(N+1) + 12 N] + P + 24 (N-1) chi_kappa0 bytes per rod-step, / N."""
+    """16 [6(N+1) + 12 N] + P + 24 (N-1) chi_kappa0 bytes per rod-step, / N.
+    Contact mode (NEXT-4) adds, for the step kernel: the contact force on each element's
+    two nodes read (48 B per element), the node records for the next contact evaluation written
+    (48 B per node) and the build positions read for the Verlet check (24 B per node)."""
     N = w.n_elems.astype(np.float64)
     per_rod = 16.0 * (6.0 * (N + 1) + 12.0 * N) + 128.0 + (24.0 * (N - 1) if w.rest_kappa is not None else 0.0)
+    if getattr(w, "contact", None) is not None:
+        per_rod = per_rod + 48.0 * N + 72.0 * (N + 1)
     return float(per_rod.sum() / N.sum())
 
 
@@ -215,6 +220,7 @@ def main():
     torch.cuda.synchronize()
     launches0 = b.info().launches
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    b.set_option(er.ER_OPT_PHASE_TIMING, 1)  # CUDA events around every step-kernel launch (own stream)
     with ClockSampler(local) as clk:
         time.sleep(0.3)                     # let the sampler start
         if world > 1:
@@ -227,6 +233,8 @@ def main():
         if world > 1:
             dist.barrier()
     launches = b.info().launches - launches0
+    ph = b.phase_times()
+    b.set_option(er.ER_OPT_PHASE_TIMING, 0)
     ms = ev0.elapsed_time(ev1)
     t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
     if world > 1:
@@ -244,10 +252,13 @@ def main():
         diag[9] = vmax
     value = float(el_total.item()) * a.steps / (ms_max * 1e-3)
 
-    # roofline of the dominant (only) kernel: one launch = one step (steps_per_launch=1)
+    # roofline of the dominant kernel (the rod step kernel; in contact mode the step kernel beside
+    # the contact graph): algorithmic bytes per launch / its mean launch duration from the CUDA
+    # events er_step records around each launch on its stream (ER_OPT_PHASE_TIMING)
     bmin = b_min_per_el_step(w)
     per_launch_bytes = bmin * el_local * max(1, a.steps_per_launch)
-    launch_ms = ms / max(launches, 1)
+    n_kl = max(int(ph.step_kernel_launches), 1)
+    launch_ms = ph.step_kernel_ms / n_kl if ph.step_kernel_launches else ms / max(launches, 1)
     achieved = per_launch_bytes / (launch_ms * 1e-3) / 1e9
     peak, peak_src = peaks()
     traffic = None
@@ -262,7 +273,10 @@ def main():
             traffic = None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "peak_source": peak_src, "bytes_per_el_step": bmin,
-            "kernel": "er::fused_persistent<256,2,FEAT> (fused single-pass step, TMA bulk load/store pipeline)"}
+            "kernel": "er::fused_persistent<256,2,FEAT> (fused single-pass step, TMA bulk load/store pipeline)",
+            "kernel_ms_per_launch": launch_ms, "kernel_share_of_step": ph.step_kernel_ms / ms if ms > 0 else None}
+    if ph.contact_evals:
+        roof["contact_ms_per_step"] = ph.contact_ms / ph.contact_evals
     if a.steps_per_launch > 1:
         roof["note"] = ("temporal blocking: the state crosses HBM once per launch of "
                         f"{a.steps_per_launch} steps, so 'achieved' counts B_min per step and can exceed the "
@@ -305,10 +319,12 @@ def main():
     if rank == 0:
         cpu = None
         if world == 1 and not a.no_cpu_baseline:
-            rate, secs, ws = oracle_rate(wfull, a.cpu_sample_rods, a.cpu_sample_steps)
+            cs = a.cpu_sample_steps if getattr(wfull, "contact", None) is None else max(5, a.cpu_sample_steps // 6)
+            rate, secs, ws = oracle_rate(wfull, a.cpu_sample_rods, cs)
+            what = "seeded rods" if getattr(wfull, "contact", None) is None else "rods (one whole stack, exhaustive contact search)"
             cpu = {"value": rate, "unit": "element-steps/s", "cores": 1, "kind": "oracle",
-                   "sample": f"{ws.n_rods} seeded rods of {a.config} x {a.cpu_sample_steps} steps "
-                             f"({ws.n_elems_total * a.cpu_sample_steps:.3g} element-steps, {secs:.1f} s, 1 thread)"}
+                   "sample": f"{ws.n_rods} {what} of {a.config} x {cs} steps "
+                             f"({ws.n_elems_total * cs:.3g} element-steps, {secs:.1f} s, 1 thread)"}
         out = {
             "metric": "rod element-updates/sec (fp64)", "value": value, "unit": "element-steps/s",
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_max / a.steps,

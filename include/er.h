@@ -284,7 +284,7 @@ typedef enum {
                                   (SURVEY §8 D.3 B_min design).  k > 1: each launch keeps a
                                   rod tile on chip for k steps (temporal blocking, SURVEY §8(f)
                                   NEXT-1); identical results. */
-  ER_OPT_KERNEL = 2            /* 0 (default): fused single-pass step, persistent CTAs with
+  ER_OPT_KERNEL = 2,           /* 0 (default): fused single-pass step, persistent CTAs with
                                   TMA bulk prefetch of the next rod tile.
                                   1: staged three-kernel path (drift / dynamics+kick / drift),
                                   state through HBM between stages (ablation, debugging).
@@ -293,8 +293,21 @@ typedef enum {
                                   3: memory-pipeline probe (measurement aid): the persistent
                                   kernel moves every tile through its TMA stage and back
                                   without computing -- the state and t are left unchanged. */
+  ER_OPT_PHASE_TIMING = 3      /* measurement aid: 1 = er_step records a CUDA event pair (on the
+                                  handle's stream) around every step-kernel launch and every
+                                  contact evaluation, summed into er_get_phase_times; setting
+                                  the option (0 or 1) resets the sums.  Default 0. */
 } er_option;
 er_status er_set_option(er_batch *b, int32_t option, int64_t value);
+
+/* Device time of er_step's phases since ER_OPT_PHASE_TIMING was last set (CUDA events). */
+typedef struct {
+  double step_kernel_ms;        /* the rod step kernel launches (all kinds)                 */
+  int64_t step_kernel_launches;
+  double contact_ms;            /* contact evaluations (broad + narrow phase graphs)        */
+  int64_t contact_evals;
+} er_phase_times;
+er_status er_get_phase_times(const er_batch *b, er_phase_times *out);
 
 /* Measurement aid: when `trace` (DEVICE memory, [grid][64][4] uint64, zeroed by the caller) is
  * non-NULL, the persistent step kernel records for thread 0 of each CTA and its first 64 tiles

@@ -23,7 +23,7 @@ LIB_PATH = os.path.join(_HERE, "lib", "libelasticarod.so")
 ER_OK, ER_EINVAL, ER_EUNSTABLE, ER_EIO, ER_ENOMEM, ER_ECUDA = range(6)
 ER_HOST, ER_DEVICE = 0, 1
 ER_F_NONFINITE, ER_F_DEGENERATE, ER_F_ANTIPODAL, ER_F_OVERSPEED, ER_F_CONTACT = 1, 2, 4, 8, 16
-ER_OPT_STEPS_PER_LAUNCH, ER_OPT_KERNEL = 1, 2
+ER_OPT_STEPS_PER_LAUNCH, ER_OPT_KERNEL, ER_OPT_PHASE_TIMING = 1, 2, 3
 ER_NDIAG = 12
 DIAG_NAMES = ("ke_trans", "ke_rot", "pe_shear", "pe_bend", "pe_grav", "pe_tip",
               "px", "py", "pz", "vmax", "mass", "n_elems")
@@ -84,9 +84,14 @@ class er_contact_stats(C.Structure):
     ]
 
 
+class er_phase_times(C.Structure):
+    _fields_ = [("step_kernel_ms", C.c_double), ("step_kernel_launches", C.c_int64),
+                ("contact_ms", C.c_double), ("contact_evals", C.c_int64)]
+
+
 EXPORTS = ("er_create_batch", "er_set_bc", "er_set_forcing", "er_step", "er_get_state", "er_set_state",
            "er_diagnostics", "er_fault", "er_set_option", "er_set_trace", "er_query", "er_last_error",
-           "er_abi_version", "er_destroy", "er_set_contact", "er_get_contact_stats")
+           "er_abi_version", "er_destroy", "er_set_contact", "er_get_contact_stats", "er_get_phase_times")
 
 
 def _load():
@@ -110,12 +115,13 @@ def _load():
     lib.er_last_error.restype = C.c_char_p
     lib.er_set_contact.argtypes = [h, C.POINTER(er_contact)]
     lib.er_get_contact_stats.argtypes = [h, C.POINTER(er_contact_stats)]
+    lib.er_get_phase_times.argtypes = [h, C.POINTER(er_phase_times)]
     lib.er_abi_version.restype = C.c_int32
     lib.er_destroy.argtypes = [h]
     lib.er_destroy.restype = None
     for name in ("er_create_batch", "er_set_bc", "er_set_forcing", "er_step", "er_get_state",
                  "er_set_state", "er_diagnostics", "er_fault", "er_set_option", "er_set_trace", "er_query",
-                 "er_set_contact", "er_get_contact_stats"):
+                 "er_set_contact", "er_get_contact_stats", "er_get_phase_times"):
         getattr(lib, name).restype = C.c_int
     return lib
 
@@ -199,6 +205,12 @@ def er_set_contact(handle, contact):
 def er_get_contact_stats(handle) -> er_contact_stats:
     out = er_contact_stats()
     _check(handle, lib.er_get_contact_stats(handle, C.byref(out)))
+    return out
+
+
+def er_get_phase_times(handle) -> er_phase_times:
+    out = er_phase_times()
+    _check(handle, lib.er_get_phase_times(handle, C.byref(out)))
     return out
 
 
@@ -346,6 +358,9 @@ class RodBatch:
 
     def contact_stats(self) -> er_contact_stats:
         return er_get_contact_stats(self.handle)
+
+    def phase_times(self) -> er_phase_times:
+        return er_get_phase_times(self.handle)
 
     # -- stepping / state
     def step(self, n_steps: int, dt: float):

@@ -121,6 +121,13 @@ struct er_batch {
   ErContactParams cp{};
   void *sort_tmp = nullptr;
   size_t sort_bytes = 0;
+  // ER_OPT_PHASE_TIMING: event pool, this call's intervals (start, end, phase), running sums
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<int> iv;  // triples
+  double phase_ms[2] = {0.0, 0.0};
+  int64_t phase_n[2] = {0, 0};
   cudaGraphExec_t cgraph = nullptr;  // per-step contact evaluation (conditional build)
   int cgraph_kernels = 0;
   std::vector<double> rod_A0, rod_E0, rod_lmin, rod_lmax;  // host, per rod (contact radius, stiffness, HHG)
@@ -164,7 +171,36 @@ void free_contact(er_batch *b) {
   b->contact_on = false;
 }
 
+// Phase timing: mark() records an event on the stream and returns its index (-1 when off).
+int mark(er_batch *b) {
+  if (!b->timing) return -1;
+  if (b->ev_used == b->ev_pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return -1;
+    b->ev_pool.push_back(e);
+  }
+  const int k = (int)b->ev_used++;
+  cudaEventRecord(b->ev_pool[k], b->stream);
+  return k;
+}
+void interval(er_batch *b, int e0, int e1, int phase) {
+  if (e0 >= 0 && e1 >= 0) { b->iv.push_back(e0); b->iv.push_back(e1); b->iv.push_back(phase); }
+}
+void collect_times(er_batch *b) {  // after the stream was synchronised
+  for (size_t k = 0; k + 2 < b->iv.size(); k += 3) {
+    float ms = 0.0f;
+    if (cudaEventElapsedTime(&ms, b->ev_pool[b->iv[k]], b->ev_pool[b->iv[k + 1]]) == cudaSuccess) {
+      b->phase_ms[b->iv[k + 2]] += ms;
+      b->phase_n[b->iv[k + 2]] += 1;
+    }
+  }
+  b->iv.clear();
+  b->ev_used = 0;
+}
+
 void free_all(er_batch *b) {
+  for (cudaEvent_t e : b->ev_pool) cudaEventDestroy(e);
+  b->ev_pool.clear();
   void *ptrs[] = {b->d_state, b->d_rec, b->d_eoff, b->d_tiles, b->d_gpar, b->d_sigma0, b->d_mag, b->d_musc,
                   b->d_fault, b->d_diag_partial, b->d_diag_out, b->d_valid};
   for (void *p : ptrs)
@@ -716,6 +752,13 @@ er_status er_set_option(er_batch *b, int32_t option, int64_t value) {
     b->steps_per_launch = value;
     return ER_OK;
   }
+  if (option == ER_OPT_PHASE_TIMING) {
+    if (value != 0 && value != 1) { b->last_error = "phase timing must be 0 or 1"; return ER_EINVAL; }
+    b->timing = value == 1;
+    b->phase_ms[0] = b->phase_ms[1] = 0.0;
+    b->phase_n[0] = b->phase_n[1] = 0;
+    return ER_OK;
+  }
   if (option == ER_OPT_KERNEL) {
     if (value < 0 || value > 3) { b->last_error = "kernel must be 0 (fused persistent), 1 (staged), 2 (fused, one tile per CTA) or 3 (memory probe)"; return ER_EINVAL; }
     b->kernel_mode = (int)value;
@@ -739,6 +782,8 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
   if (err.count) { b->last_error = err.msg; return ER_EINVAL; }
   b->fault_rod = -1;
   b->fault_bits = 0;
+  b->iv.clear();
+  b->ev_used = 0;
   if (n_steps == 0 || b->n_rods == 0) return ER_OK;
   CK(cudaSetDevice(b->device), "cudaSetDevice");
   const unsigned long long init[2] = {0ull, ~0ull};
@@ -767,16 +812,23 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
     p.cbuild = b->cp.cbuild;
     p.disp2 = 0.25 * b->cp.skin * b->cp.skin;
     p.rebuild = b->cp.rebuild;
+    int m0 = mark(b);
     CK(er_launch_step(&p, b->block, 1, 15, b->stream), "drift kernel");
     b->launches += 1;
+    int m1 = mark(b);
+    interval(b, m0, m1, 0);
     p.cfc = b->cp.fc;
     p.cfs = b->cp.fs;
     for (int64_t q = 0; q < n_steps; ++q) {
       CK(er_contact_eval(&b->cp, b->sort_tmp, b->sort_bytes, b->cgraph, b->stream, &b->launches, b->cgraph_kernels), "contact");
+      const int m2 = mark(b);
+      interval(b, m1, m2, 1);
       p.t = t;
       p.cnode = q + 1 < n_steps ? b->cp.cnode : nullptr;
       CK(er_launch_step(&p, b->block, 0, feat | FEAT_CONTACT, b->stream), "step kernel");
       b->launches += 1;
+      m1 = mark(b);
+      interval(b, m2, m1, 0);
       const double th = t + 0.5 * dt;
       t = th + 0.5 * dt;
     }
@@ -806,8 +858,10 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
       const int64_t k = std::min<int64_t>(b->steps_per_launch, n_steps - done);
       p.n_steps = (int32_t)k;
       p.t = t;
+      const int m0 = mark(b);
       CK(er_launch_step(&p, b->block, b->kernel_mode == 0 ? 0 : 3, feat, b->stream), "step kernel");
       b->launches += 1;
+      interval(b, m0, mark(b), 0);
       for (int64_t q = 0; q < k; ++q) { const double th = t + 0.5 * dt; t = th + 0.5 * dt; }
       done += k;
     } else {  // staged ablation: drift | dynamics + kick | drift, state through HBM between stages
@@ -826,6 +880,7 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
   unsigned long long fw[2];
   CK(cudaMemcpyAsync(fw, b->d_fault, sizeof fw, cudaMemcpyDeviceToHost, b->stream), "D2H fault");
   CK(cudaStreamSynchronize(b->stream), "cudaStreamSynchronize");
+  collect_times(b);
   if (fw[0]) {
     b->fault_bits = (int32_t)fw[0];
     b->fault_rod = (int64_t)fw[1];
@@ -1033,6 +1088,15 @@ er_status er_diagnostics(er_batch *b, double out[ER_NDIAG]) {
   CK(er_launch_diag(&p, b->block, b->d_diag_out, b->stream), "diag kernel");
   CK(cudaMemcpyAsync(out, b->d_diag_out, sizeof(double) * ER_NDIAG, cudaMemcpyDeviceToHost, b->stream), "D2H diag");
   CK(cudaStreamSynchronize(b->stream), "cudaStreamSynchronize");
+  return ER_OK;
+}
+
+er_status er_get_phase_times(const er_batch *b, er_phase_times *out) {
+  if (!b || !out) return ER_EINVAL;
+  out->step_kernel_ms = b->phase_ms[0];
+  out->step_kernel_launches = b->phase_n[0];
+  out->contact_ms = b->phase_ms[1];
+  out->contact_evals = b->phase_n[1];
   return ER_OK;
 }
 
