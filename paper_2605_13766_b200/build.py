@@ -38,7 +38,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *[f for f in FLAGS if f != "-shared"], *FILE_FLAGS.get(src, []), "-c",
+        extra = os.environ.get("ER_NVCC_EXTRA", "").split()  # experiments only (e.g. -DER_...)
+        cmd = [NVCC, *[f for f in FLAGS if f != "-shared"], *FILE_FLAGS.get(src, []), *extra, "-c",
                "-I", os.path.join(ROOT, "include"), "-I", CSRC, os.path.join(CSRC, src), "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:

@@ -322,7 +322,8 @@ int feat_of(const er_batch *b) {
   int f = 0;
   if (b->any_general) f |= FEAT_GENERAL;
   if (b->has_kappa0) f |= FEAT_KAPPA0;
-  if (b->has_sigma0 || b->d_mag || b->has_act || b->has_musc) f |= FEAT_EXTRA;
+  if (b->has_sigma0 || b->d_mag || b->has_musc) f |= FEAT_EXTRA;
+  else if (b->has_act) f |= FEAT_ACT;  // actuation alone: the lighter kernel
   return f;
 }
 
@@ -760,7 +761,7 @@ er_status er_set_option(er_batch *b, int32_t option, int64_t value) {
     return ER_OK;
   }
   if (option == ER_OPT_KERNEL) {
-    if (value < 0 || value > 3) { b->last_error = "kernel must be 0 (fused persistent), 1 (staged), 2 (fused, one tile per CTA) or 3 (memory probe)"; return ER_EINVAL; }
+    if (value < 0 || value > 4) { b->last_error = "kernel must be 0 (fused persistent), 1 (staged), 2 (fused, one tile per CTA), 3 (memory probe) or 4 (persistent, direct stores)"; return ER_EINVAL; }
     b->kernel_mode = (int)value;
     return ER_OK;
   }
@@ -854,12 +855,13 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
       const double th = t + 0.5 * dt;
       t = th + 0.5 * dt;
       done += 1;
-    } else if (b->kernel_mode == 0 || b->kernel_mode == 2) {
+    } else if (b->kernel_mode == 0 || b->kernel_mode == 2 || b->kernel_mode == 4) {
       const int64_t k = std::min<int64_t>(b->steps_per_launch, n_steps - done);
       p.n_steps = (int32_t)k;
       p.t = t;
       const int m0 = mark(b);
-      CK(er_launch_step(&p, b->block, b->kernel_mode == 0 ? 0 : 3, feat, b->stream), "step kernel");
+      CK(er_launch_step(&p, b->block, b->kernel_mode == 0 ? 0 : b->kernel_mode == 4 ? 5 : 3, feat, b->stream),
+         "step kernel");
       b->launches += 1;
       interval(b, m0, mark(b), 0);
       for (int64_t q = 0; q < k; ++q) { const double th = t + 0.5 * dt; t = th + 0.5 * dt; }

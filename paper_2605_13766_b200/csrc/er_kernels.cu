@@ -110,6 +110,7 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
                                           const double k0s[3], double &t, unsigned &fbits) {
   constexpr bool GEN = (FEAT & FEAT_GENERAL) != 0;
   constexpr bool EXTRA = (FEAT & FEAT_EXTRA) != 0;
+  constexpr bool ACT = (FEAT & (FEAT_EXTRA | FEAT_ACT)) != 0;
   constexpr bool CONTACT = (FEAT & FEAT_CONTACT) != 0;
   const int s = si.s, i = si.i, N = si.N;
   const double h = p.h, hh = 0.5 * p.h;
@@ -197,7 +198,7 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
       const double ieps = Dh * rcp_fast(D);
       const double ieps3 = ieps * ieps * ieps;
       double k0[3] = {k0s[0], k0s[1], k0s[2]};
-      if (EXTRA && (si.fl & FL_ACT)) {
+      if (ACT && (si.fl & FL_ACT)) {
         const double sk = general ? gp(GP_SK) : i * rec[REC_LHAT];
         // A sin(2 pi (s/L - f t)) = A sinpi(2 (s/L - f t))
         const double arg = 2.0 * fma(sk, rec[REC_ACTIL], -rec[REC_ACTF] * t_half);
@@ -426,7 +427,7 @@ __device__ __forceinline__ void issue_tile(const ErStepParams &p, const TileHead
   bulk_g2s(B + SG::TOFF, tile_ptr, (uint32_t)sizeof(ErTile), bar);
 }
 
-template <int BLOCK, int MINB, int FEAT>
+template <int BLOCK, int MINB, int FEAT, bool DSTORE = false>
 __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepParams p) {
   using SG = Stage<BLOCK, FEAT>;
   extern __shared__ __align__(16) double sm[];
@@ -477,7 +478,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
     si.node = T.nbase + tid;
     si.elem = T.ebase + tid - lo;
     si.vor = si.elem - si.rod - 1;
+#ifdef ER_REC_ALIGN
+    const double *rec = static_cast<const double *>(__builtin_assume_aligned(B + SG::RECOFF + lo * ER_REC, 16));
+#else
     const double *rec = B + SG::RECOFF + lo * ER_REC;
+#endif
     si.fl = si.active ? rec_flags(rec) : 0;
     finish_slot(si);
 
@@ -529,6 +534,24 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
     if (fbits) { fbits_all |= fbits; frod = min(frod, si.rod); }
     if (tr) tr[2] = gtimer() & ((1ull << 48) - 1);
 
+    if (DSTORE) {  // ablation: results straight from registers to HBM (coalesced SoA planes)
+      double *G = p.state + boff;
+      if (si.active) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          __stcs(G + c * ns + tid, r[c]);
+          __stcs(G + (3 + c) * ns + tid, v[c]);
+        }
+      }
+      if (si.has_e) {
+#pragma unroll
+        for (int c = 0; c < 9; ++c) __stcs(G + 6 * ns + c * nel + le, Q[c]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) __stcs(G + 6 * ns + (9 + c) * nel + le, w[c]);
+      }
+      if (tr) tr[3] = gtimer() & ((1ull << 48) - 1);
+      continue;
+    }
     // ---- registers -> stage (block layout at OUTOFF) -> HBM with one TMA bulk store
     double *O = B + SG::OUTOFF;
     if (si.active) {
@@ -836,9 +859,9 @@ namespace {
 size_t simple_smem(int block) { return (size_t)er::XPLANES * 8 * block + sizeof(int) * (block / 8 + 4); }
 size_t diag_smem(int block) { return (size_t)12 * 8 * block + 16 * 8 * (block / 32) + sizeof(int) * (block / 8 + 4); }
 
-template <int BLOCK, int MINB, int FEAT>
+template <int BLOCK, int MINB, int FEAT, bool DSTORE = false>
 cudaError_t launch_persistent(const ErStepParams &p, cudaStream_t st) {
-  auto k = er::fused_persistent<BLOCK, MINB, FEAT>;
+  auto k = er::fused_persistent<BLOCK, MINB, FEAT, DSTORE>;
   const size_t sm = er::Stage<BLOCK, FEAT>::bytes();
   static int grid_per_sm[64] = {0};  // per device
   int dev = 0;
@@ -859,26 +882,26 @@ cudaError_t launch_persistent(const ErStepParams &p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// feat: GENERAL | KAPPA0 | CONTACT bits, plus at most one of FEAT_EXTRA / FEAT_ACT (24 kernels)
+template <int BLOCK, int MINB, int X>
+cudaError_t launch_persistent_base(const ErStepParams &p, int base, cudaStream_t st) {
+  switch (base) {
+    case 0: return launch_persistent<BLOCK, MINB, X | 0>(p, st);
+    case 1: return launch_persistent<BLOCK, MINB, X | 1>(p, st);
+    case 2: return launch_persistent<BLOCK, MINB, X | 2>(p, st);
+    case 3: return launch_persistent<BLOCK, MINB, X | 3>(p, st);
+    case 8: return launch_persistent<BLOCK, MINB, X | 8>(p, st);
+    case 9: return launch_persistent<BLOCK, MINB, X | 9>(p, st);
+    case 10: return launch_persistent<BLOCK, MINB, X | 10>(p, st);
+    default: return launch_persistent<BLOCK, MINB, X | 11>(p, st);
+  }
+}
 template <int BLOCK, int MINB>
 cudaError_t launch_persistent_feat(const ErStepParams &p, int feat, cudaStream_t st) {
-  switch (feat & 15) {
-    case 0: return launch_persistent<BLOCK, MINB, 0>(p, st);
-    case 1: return launch_persistent<BLOCK, MINB, 1>(p, st);
-    case 2: return launch_persistent<BLOCK, MINB, 2>(p, st);
-    case 3: return launch_persistent<BLOCK, MINB, 3>(p, st);
-    case 4: return launch_persistent<BLOCK, MINB, 4>(p, st);
-    case 5: return launch_persistent<BLOCK, MINB, 5>(p, st);
-    case 6: return launch_persistent<BLOCK, MINB, 6>(p, st);
-    case 7: return launch_persistent<BLOCK, MINB, 7>(p, st);
-    case 8: return launch_persistent<BLOCK, MINB, 8>(p, st);
-    case 9: return launch_persistent<BLOCK, MINB, 9>(p, st);
-    case 10: return launch_persistent<BLOCK, MINB, 10>(p, st);
-    case 11: return launch_persistent<BLOCK, MINB, 11>(p, st);
-    case 12: return launch_persistent<BLOCK, MINB, 12>(p, st);
-    case 13: return launch_persistent<BLOCK, MINB, 13>(p, st);
-    case 14: return launch_persistent<BLOCK, MINB, 14>(p, st);
-    default: return launch_persistent<BLOCK, MINB, 15>(p, st);
-  }
+  const int base = feat & (FEAT_GENERAL | FEAT_KAPPA0 | FEAT_CONTACT);
+  if (feat & FEAT_EXTRA) return launch_persistent_base<BLOCK, MINB, FEAT_EXTRA>(p, base, st);
+  if (feat & FEAT_ACT) return launch_persistent_base<BLOCK, MINB, FEAT_ACT>(p, base, st);
+  return launch_persistent_base<BLOCK, MINB, 0>(p, base, st);
 }
 
 template <int BLOCK, int MINB, int MODE>
@@ -907,6 +930,7 @@ cudaError_t er_launch_step(const ErStepParams *p, int block, int kind, int feat,
   }
   if (block == 256) {
     if (kind == 0) return launch_persistent_feat<256, 2>(*p, feat, st);
+    if (kind == 5 && feat == 0) return launch_persistent<256, 2, 0, true>(*p, st);  // ablation
     if (kind == 1) return launch_simple<256, 2, er::MODE_DRIFT>(*p, st);
     if (kind == 2) return launch_simple<256, 2, er::MODE_DYN>(*p, st);
     return launch_simple<256, 2, er::MODE_FUSED>(*p, st);

@@ -71,8 +71,10 @@ enum {
 };
 
 // batch-level feature bits (kernel template parameter)
-enum { FEAT_GENERAL = 1, FEAT_KAPPA0 = 2, FEAT_EXTRA = 4 /* sigma0 / magnetization / actuation */,
-       FEAT_CONTACT = 8 /* contact forces from ErStepParams.cfc; launch = kick + drift-2 [+ next drift-1] */ };
+enum { FEAT_GENERAL = 1, FEAT_KAPPA0 = 2,
+       FEAT_EXTRA = 4   /* sigma0 / magnetization / muscle wave (and actuation) */,
+       FEAT_CONTACT = 8 /* contact forces from ErStepParams.cfc; launch = kick + drift-2 [+ next drift-1] */,
+       FEAT_ACT = 16    /* rest-curvature actuation only (a lighter kernel than FEAT_EXTRA) */ };
 
 // canonical fields (er_get_state / er_set_state order)
 enum { FIELD_POS = 0, FIELD_VEL = 1, FIELD_DIR = 2, FIELD_OMEGA = 3, FIELD_KAPPA0 = 4 };
