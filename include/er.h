@@ -292,7 +292,10 @@ typedef enum {
                                   All three give identical results.
                                   3: memory-pipeline probe (measurement aid): the persistent
                                   kernel moves every tile through its TMA stage and back
-                                  without computing -- the state and t are left unchanged. */
+                                  without computing -- the state and t are left unchanged.
+                                  4: as 0 but results go from registers straight to HBM
+                                  (plain coalesced stores instead of the smem stage + TMA
+                                  bulk store; ablation, cfg3-type batches only). */
   ER_OPT_PHASE_TIMING = 3      /* measurement aid: 1 = er_step records a CUDA event pair (on the
                                   handle's stream) around every step-kernel launch and every
                                   contact evaluation, summed into er_get_phase_times; setting

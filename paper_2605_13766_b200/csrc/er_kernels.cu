@@ -923,7 +923,7 @@ extern "C" {
 cudaError_t er_launch_step(const ErStepParams *p, int block, int kind, int feat, cudaStream_t st) {
   if (p->n_tiles <= 0) return cudaSuccess;
   if (block == 128) {
-    if (kind == 0) return launch_persistent_feat<128, 4>(*p, feat, st);
+    if (kind == 0 || kind == 5) return launch_persistent_feat<128, 4>(*p, feat, st);
     if (kind == 1) return launch_simple<128, 4, er::MODE_DRIFT>(*p, st);
     if (kind == 2) return launch_simple<128, 4, er::MODE_DYN>(*p, st);
     return launch_simple<128, 4, er::MODE_FUSED>(*p, st);
@@ -931,11 +931,12 @@ cudaError_t er_launch_step(const ErStepParams *p, int block, int kind, int feat,
   if (block == 256) {
     if (kind == 0) return launch_persistent_feat<256, 2>(*p, feat, st);
     if (kind == 5 && feat == 0) return launch_persistent<256, 2, 0, true>(*p, st);  // ablation
+    if (kind == 5) return launch_persistent_feat<256, 2>(*p, feat, st);
     if (kind == 1) return launch_simple<256, 2, er::MODE_DRIFT>(*p, st);
     if (kind == 2) return launch_simple<256, 2, er::MODE_DYN>(*p, st);
     return launch_simple<256, 2, er::MODE_FUSED>(*p, st);
   }
-  if (kind == 0) return launch_persistent_feat<512, 1>(*p, feat, st);
+  if (kind == 0 || kind == 5) return launch_persistent_feat<512, 1>(*p, feat, st);
   if (kind == 1) return launch_simple<512, 1, er::MODE_DRIFT>(*p, st);
   if (kind == 2) return launch_simple<512, 1, er::MODE_DYN>(*p, st);
   return launch_simple<512, 1, er::MODE_FUSED>(*p, st);
