@@ -18,7 +18,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libelasticarod.so")
+LIB_PATH = os.environ.get("ER_LIB") or os.path.join(_HERE, "lib", "libelasticarod.so")  # ER_LIB: A/B builds
 
 ER_OK, ER_EINVAL, ER_EUNSTABLE, ER_EIO, ER_ENOMEM, ER_ECUDA = range(6)
 ER_HOST, ER_DEVICE = 0, 1
