@@ -5,10 +5,12 @@
 
 One bench "step" = one position-Verlet time step (all SURVEY §8(a) rows A1-A10) over the
 whole batch.  Default workload: BASELINE.json configs[2] ("cfg3": 1,048,576 rods x 16
-elements, the paper's 1024^2-filament strong-scaling size), synthetic and seeded
-(workloads/).  Multi-GPU: one process per GPU (torchrun), rods sharded across ranks with no
-data-path collective; NCCL all-reduces only the scalar diagnostics once after the timed
-region.  Rank 0 prints one JSON line.
+elements, the paper's 1024^2-filament size), synthetic and seeded (workloads/).
+Multi-GPU: one process per GPU (torchrun).  Rods are independent, so the default is weak
+scaling (each rank advances its own 1,048,576-rod cfg3 batch; the job is N x cfg3) with no
+data-path collective; `--scaling strong` instead shards the one cfg3 batch across the ranks
+(the paper's strong-scaling experiment).  NCCL all-reduces only the scalar diagnostics, once,
+after the timed region.  Rank 0 prints one JSON line.
 
 `--impl reference`: there is no reference implementation to install (the paper ships no
 code); the reference arm is the CPU oracle (oracle/, plain C fp64), timed on
@@ -45,7 +47,7 @@ def parse():
     ap.add_argument("--steps-per-launch", type=int, default=1,
                     help="1 = every step streams the state through HBM (the B_min design); "
                          ">1 = temporal blocking (SURVEY NEXT-1)")
-    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--scaling", default="weak", choices=["strong", "weak"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-temporal", action="store_true")
@@ -328,7 +330,7 @@ def main():
         out = {
             "metric": "rod element-updates/sec (fp64)", "value": value, "unit": "element-steps/s",
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_max / a.steps,
-            "higher_is_better": True, "scaling": a.scaling if world > 1 else "strong",
+            "higher_is_better": True, "scaling": a.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, workloads/)",
             "config": {"workload": f"{a.config}: {wfull.n_rods} rods x "
                                    f"{int(wfull.n_elems.min())}-{int(wfull.n_elems.max())} elements "
@@ -337,7 +339,9 @@ def main():
                        "steps_per_launch": a.steps_per_launch,
                        "l2": "inputs larger than L2 (state %.2f GB per GPU vs 126 MB L2)" % (
                            b.info().device_bytes / 1e9),
-                       "parallelism": f"rod shards over {world} GPU(s), NCCL for scalar diagnostics only"},
+                       "parallelism": (f"weak: each of {world} GPU(s) advances its own {a.config} batch"
+                                       if a.scaling == "weak" else f"strong: one {a.config} batch in rod shards over "
+                                       f"{world} GPU(s)") + "; NCCL for scalar diagnostics only"},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
