@@ -116,6 +116,7 @@ struct er_batch {
   int64_t fault_rod = -1;
   int32_t fault_bits = 0;
   std::string last_error;
+  double *upload_stage = nullptr;  // during er_create_batch: one staging buffer for all fields
   // contact (NEXT-4)
   bool contact_on = false;
   ErContactParams cp{};
@@ -199,6 +200,8 @@ void collect_times(er_batch *b) {  // after the stream was synchronised
 }
 
 void free_all(er_batch *b) {
+  if (b->upload_stage) cudaFree(b->upload_stage);
+  b->upload_stage = nullptr;
   for (cudaEvent_t e : b->ev_pool) cudaEventDestroy(e);
   b->ev_pool.clear();
   void *ptrs[] = {b->d_state, b->d_rec, b->d_eoff, b->d_tiles, b->d_gpar, b->d_sigma0, b->d_mag, b->d_musc,
@@ -236,6 +239,19 @@ int field_k(int field) { return field == FIELD_DIR ? 9 : 3; }
 // Canonical AoS array (host or device, or NULL = zeros) -> tile-blocked planes.  With
 // `validate`, non-finite counts (and, for directors, max |QQ^T - I| and |det Q - 1|)
 // accumulate in d_valid.
+// Device alias of a page-locked host pointer (pinned or registered memory is mapped into the
+// device address space under UVA), or nullptr for pageable memory.  er_get_state's layout
+// kernel then writes host memory directly over PCIe (posted writes run at the DMA rate; reads
+// of host memory from a kernel do not, so uploads keep the DMA copy into a staging buffer).
+double *mapped_host(const void *h) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost && a.devicePointer ? static_cast<double *>(a.devicePointer) : nullptr;
+}
+
 er_status upload_field(er_batch *b, const double *src, int src_mem, int field, bool validate) {
   const int64_t n = field_rows(b, field);
   if (n <= 0) return ER_OK;
@@ -247,14 +263,15 @@ er_status upload_field(er_batch *b, const double *src, int src_mem, int field, b
   }
   const double *dsrc = src;
   double *stage = nullptr;
-  if (src_mem == ER_HOST) {
-    CK(cudaMallocAsync((void **)&stage, sizeof(double) * (size_t)(n * k), b->stream), "cudaMallocAsync(stage)");
+  if (src_mem == ER_HOST) {  // DMA into a device staging buffer (the caller's `stage` when given)
+    stage = b->upload_stage;
+    if (!stage) CK(cudaMallocAsync((void **)&stage, sizeof(double) * (size_t)(n * k), b->stream), "cudaMallocAsync(stage)");
     CK(cudaMemcpyAsync(stage, src, sizeof(double) * (size_t)(n * k), cudaMemcpyHostToDevice, b->stream), "H2D");
     dsrc = stage;
   }
   if (validate) CK(er_launch_validate(dsrc, n, k, field == FIELD_DIR, b->d_valid, b->stream), "validate");
   CK(er_launch_canon_tiles(&p, const_cast<double *>(dsrc), field, 1, b->stream), "canon->tiles");
-  if (stage) CK(cudaFreeAsync(stage, b->stream), "cudaFreeAsync");
+  if (stage && stage != b->upload_stage) CK(cudaFreeAsync(stage, b->stream), "cudaFreeAsync");
   return ER_OK;
 }
 
@@ -265,6 +282,10 @@ er_status download_field(er_batch *b, double *dst, int dst_mem, int field) {
   const int k = field_k(field);
   if (dst_mem == ER_DEVICE) {
     CK(er_launch_canon_tiles(&p, dst, field, 0, b->stream), "tiles->canon");
+    return ER_OK;
+  }
+  if (double *hm = mapped_host(dst)) {  // page-locked host array: written directly
+    CK(er_launch_canon_tiles(&p, hm, field, 0, b->stream), "tiles->canon(host)");
     return ER_OK;
   }
   double *stage = nullptr;
@@ -603,11 +624,16 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   tm.mark("alloc + small uploads", b->stream);
   er_status st;
   CK(cudaMemsetAsync(b->d_valid, 0, sizeof(double) * 4, b->stream), "memset");
+  // one staging buffer, sized for the largest field, reused by every host upload
+  CK(cudaMalloc((void **)&b->upload_stage, sizeof(double) * (size_t)std::max<int64_t>(9 * E, 3 * NN) + 64), "cudaMalloc(stage)");
   if ((st = upload_field(b, d->positions, d->src_mem, FIELD_POS, true)) != ER_OK) return fail(st);
   if ((st = upload_field(b, d->velocities, d->src_mem, FIELD_VEL, true)) != ER_OK) return fail(st);
   if ((st = upload_field(b, d->directors, d->src_mem, FIELD_DIR, true)) != ER_OK) return fail(st);
   if ((st = upload_field(b, d->omega, d->src_mem, FIELD_OMEGA, true)) != ER_OK) return fail(st);
   if (b->has_kappa0 && (st = upload_field(b, d->rest_kappa, ER_HOST, FIELD_KAPPA0, false)) != ER_OK) return fail(st);
+  CK(cudaStreamSynchronize(b->stream), "sync");
+  cudaFree(b->upload_stage);
+  b->upload_stage = nullptr;
   if (d->rest_sigma) {
     CK(dalloc(b, &b->d_sigma0, 3 * b->ne), "cudaMalloc(sigma0)");
     if ((st = upload_side_planes(b, d->rest_sigma, b->d_sigma0, E, b->ne)) != ER_OK) return fail(st);

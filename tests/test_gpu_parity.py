@@ -302,6 +302,31 @@ def test_fault_degenerate_and_overspeed(er, orc):
         assert b.fault()[0] == 1 and b.fault()[1] & er.ER_F_OVERSPEED
 
 
+def test_pinned_host_zero_copy_paths(er):
+    """Page-locked host arrays take the zero-copy layout path (the kernels read / write host
+    memory over PCIe); pageable ones the staged copy.  Both give identical states, and the
+    validation still runs on the zero-copy upload."""
+    import torch
+    w = W.make("cfg5", n_rods=40)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    tp = {k: pin(getattr(w, k)) for k in ("positions", "velocities", "directors", "omega")}
+    wp = dataclasses.replace(w, **{k: v.numpy() for k, v in tp.items()})
+    outs = [torch.empty_like(tp[k]).pin_memory() for k in ("positions", "velocities", "directors", "omega")]
+    with er.RodBatch(wp) as b:
+        b.step(7, w.dt)
+        b.get_state_into(*[o.numpy() for o in outs])
+    with er.RodBatch(w) as b:
+        b.step(7, w.dt)
+        ref = b.get_state()[:4]
+    for o, r in zip(outs, ref):
+        assert np.array_equal(o.numpy(), r)
+    bad = tp["directors"].clone().pin_memory()
+    bad[3] *= 1.01
+    with pytest.raises(er.ErError) as ei:
+        er.RodBatch(dataclasses.replace(wp, directors=bad.numpy()))
+    assert "orthonormal" in str(ei.value)
+
+
 def test_validation_collects_all_errors(er):
     w = W.make("cfg2", n_rods=4)
     w.directors[3] *= 1.01
