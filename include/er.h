@@ -229,7 +229,9 @@ er_status er_fault(const er_batch *b, int64_t *rod, int32_t *bits);
  * k = k_n if k_n > 0, else min(E_a r_a, E_b r_b).  With plane_on, every node x with
  * gap = n.x - d - r < 0 receives the same law against the half-space n.x >= d (v_r = its velocity).
  * Contact forces are evaluated once per step at the half-step configuration (after drift-1) with
- * v^n, so er_step runs the staged (synchronous) path while contact is enabled.
+ * v^n (the synchronous protocol): while contact is enabled every er_step step is
+ * one contact evaluation plus one step-kernel launch, ER_OPT_STEPS_PER_LAUNCH does not apply, and
+ * ER_OPT_KERNEL = 1 selects the staged kernels (any other value the fused contact step).
  *  radius      HOST [n_rods] contact radius, or NULL = sqrt(A/pi) of the rod's first element.
  *  cell0       finest HHG cell (m); 0 = auto: 1.25 x the smallest rest capsule extent
  *              (lhat + 2r).  n_levels (1..8); 0 = auto: enough levels of doubling cells for the

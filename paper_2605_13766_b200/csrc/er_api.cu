@@ -830,6 +830,8 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
     CK(cudaStreamSynchronize(b->stream), "cudaStreamSynchronize");
     return ER_OK;
   }
+  // contact: every step needs all rods' half-step positions, so ER_OPT_STEPS_PER_LAUNCH does not
+  // apply; ER_OPT_KERNEL 1 selects the staged path, any other value the fused contact step
   if (b->contact_on && b->kernel_mode != 1) {
     // NEXT-4, fused: drift-1 of the first step (+ node records); then per step the contact
     // evaluation and one persistent launch doing kick + drift-2 + the next step's drift-1

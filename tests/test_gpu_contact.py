@@ -241,3 +241,54 @@ def test_graph_equals_plain_launches(er, monkeypatch):
     assert out[0][1] == out[1][1] > 10
     for x, y in zip(out[0][0], out[1][0]):
         assert np.array_equal(x, y)
+
+
+def edge_case_workload():
+    """Single-element rods (both nodes on one element: the half-space law on two nodes), clamped
+    rods, non-uniform rest lengths and per-rod radii together, against the oracle.  Each rod gets
+    its own height (7.2 mm apart, radii 3-4.5 mm: overlaps below 1.8 mm, so the problem stays
+    well conditioned over the run): crossing rods at the SAME height have intersecting axes, where
+    the contact normal (pa - pb)/|pa - pb| is undefined -- round-off then decides it, on both
+    sides differently (a degenerate configuration of the capsule model, not a parity case)."""
+    rng = np.random.default_rng(5)
+    ws = []
+    for q in range(12):
+        N = [1, 2, 5][q % 3]
+        ang = rng.uniform(0, np.pi)
+        d = np.array([np.cos(ang), np.sin(ang), 0.0])
+        Q = np.stack([[0, 0, 1.0], np.cross(d, [0, 0, 1.0]), d])
+        base = (rng.uniform(-0.02, 0.02) - 0.02 * d[0], rng.uniform(-0.02, 0.02) - 0.02 * d[1], 0.0028 + 0.0072 * q)
+        ws.append(rod(N=N, L=0.04, r=0.004, Q=Q, base=base, clamp=0 if q % 5 == 0 else -1, g=(0, 0, -9.81),
+                      nu=2.0, dt=2e-6))
+    w = concat(ws)
+    lh = w.rest_lengths.copy()
+    lh *= 1.0 + 0.05 * np.sin(np.arange(len(lh)))          # non-uniform rest lengths ("general" rods)
+    w = dataclasses.replace(w, rest_lengths=lh)
+    w.velocities = rng.normal(0, 0.01, w.velocities.shape)
+    w.contact = W.Contact(k_n=500.0, gamma_n=0.1, mu_s=0.4, mu_k=0.3, v_stick=1e-3,
+                          radius=rng.uniform(0.003, 0.0045, w.n_rods), plane_n=np.array([0, 0, 1.0]), plane_d=0.0)
+    return w
+
+
+def test_contact_edge_cases(er, orc):
+    w = edge_case_workload()
+    g, _, st = run_gpu(er, w, 1)
+    o, _ = run_orc(orc, w, 1)
+    assert_parity(w, g, o, TOL_1STEP, raw=("r", "v", "Q"), label="edge cases 1 step")
+    assert st.contacts > 0 and st.plane_contacts > 0
+    g, _, _ = run_gpu(er, w, 500)
+    o, _ = run_orc(orc, w, 500)
+    assert_parity(w, g, o, TOL_1000, raw=("r", "Q"), label="edge cases 500 steps")
+
+
+def test_contact_empty_and_disable(er):
+    w = W.make("fibres", n_rods=16)
+    with er.RodBatch(w) as b:
+        b.step(3, w.dt)
+        b.set_contact(None)                              # back to independent rods
+        b.step(3, w.dt)
+        assert b.contact_stats().contacts == 0
+    e = dataclasses.replace(W.make("fibres", n_rods=16).subset(np.arange(0)), contact=w.contact)
+    with er.RodBatch(e) as b:
+        b.step(5, w.dt)
+        assert b.contact_stats().contacts == 0
