@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <map>
 #include <string>
 #include <thread>
 #include <vector>
@@ -105,8 +106,17 @@ struct er_batch {
   bool has_kappa0 = false, any_general = false, has_sigma0 = false, has_act = false, has_musc = false;
   int musc_comp = 0;
   // host mirrors
-  std::vector<int32_t> n_elems_h;
-  std::vector<int64_t> eoff;
+  // Rods are stored in a packed order (tile order): packed rod p is canonical rod ord[p].  The
+  // order is the identity unless the rod lengths differ, when a best-fit-decreasing packing fills
+  // the tiles.  Per-rod and per-element device arrays are all in packed order; the
+  // API converts at its boundary.
+  std::vector<int32_t> ord;        // packed -> canonical rod
+  bool identity = true;
+  std::vector<int32_t> n_elems_h;  // packed
+  std::vector<int64_t> eoff;       // packed element offsets
+  std::vector<int64_t> eoffc;      // canonical element offsets
+  int32_t *d_ord = nullptr;
+  int64_t *d_eoffc = nullptr;
   std::vector<double> rec;
   std::vector<int32_t> flags;
   double g[3] = {0, 0, 0};
@@ -135,6 +145,56 @@ struct er_batch {
 };
 
 namespace {
+
+// Best-fit-decreasing packing of rods (n + 1 slots each) into tiles of `cap` slots and at most
+// `rmax` rods: rods by decreasing length, each into the fullest tile it still fits; tiles listed
+// by their lowest rod id, rods inside a tile in canonical order.  Returns packed -> canonical.
+std::vector<int32_t> pack_rods(const int32_t *n, int64_t R, int cap, int rmax) {
+  std::vector<int32_t> idx((size_t)R);
+  for (int64_t r = 0; r < R; ++r) idx[r] = (int32_t)r;
+  std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) { return n[a] > n[b]; });
+  std::vector<std::vector<int32_t>> bins;
+  std::vector<int> room;
+  std::multimap<int, int> open;  // remaining slots -> bin
+  for (int32_t r : idx) {
+    const int need = n[r] + 1;
+    auto it = open.lower_bound(need);
+    int bin;
+    if (it == open.end()) {
+      bin = (int)bins.size();
+      bins.emplace_back();
+      room.push_back(cap);
+    } else {
+      bin = it->second;
+      open.erase(it);
+    }
+    bins[bin].push_back(r);
+    room[bin] -= need;
+    if ((int)bins[bin].size() < rmax && room[bin] >= 2) open.emplace(room[bin], bin);
+  }
+  for (auto &bn : bins) std::sort(bn.begin(), bn.end());
+  std::sort(bins.begin(), bins.end(), [](const std::vector<int32_t> &a, const std::vector<int32_t> &b) { return a[0] < b[0]; });
+  std::vector<int32_t> ord;
+  ord.reserve((size_t)R);
+  for (auto &bn : bins) ord.insert(ord.end(), bn.begin(), bn.end());
+  return ord;
+}
+
+// Rows of a canonical per-element (or per-rod) array in packed order (host copy), k doubles/row.
+std::vector<double> pack_rows(const er_batch *b, const double *src, int k, bool per_elem) {
+  std::vector<double> out;
+  if (!src) return out;
+  const int64_t R = b->n_rods;
+  out.resize((size_t)(per_elem ? b->n_elems : R) * k);
+  for (int64_t p = 0; p < R; ++p) {
+    const int32_t r = b->ord[p];
+    if (per_elem)
+      std::memcpy(&out[(size_t)b->eoff[p] * k], src + b->eoffc[r] * k, sizeof(double) * (size_t)(b->n_elems_h[p] * k));
+    else
+      std::memcpy(&out[(size_t)p * k], src + (int64_t)r * k, sizeof(double) * k);
+  }
+  return out;
+}
 
 er_status cuda_fail(er_batch *b, cudaError_t e, const char *what) {
   std::string m = std::string(what) + ": " + cudaGetErrorString(e);
@@ -204,7 +264,7 @@ void free_all(er_batch *b) {
   b->upload_stage = nullptr;
   for (cudaEvent_t e : b->ev_pool) cudaEventDestroy(e);
   b->ev_pool.clear();
-  void *ptrs[] = {b->d_state, b->d_rec, b->d_eoff, b->d_tiles, b->d_gpar, b->d_sigma0, b->d_mag, b->d_musc,
+  void *ptrs[] = {b->d_state, b->d_rec, b->d_eoff, b->d_ord, b->d_eoffc, b->d_tiles, b->d_gpar, b->d_sigma0, b->d_mag, b->d_musc,
                   b->d_fault, b->d_diag_partial, b->d_diag_out, b->d_valid};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -219,6 +279,7 @@ ErStepParams params_of(const er_batch *b) {
   std::memset(&p, 0, sizeof p);
   p.state = b->d_state;
   p.rec = b->d_rec; p.eoff = b->d_eoff; p.tiles = b->d_tiles; p.n_tiles = b->n_tiles;
+  p.ord = b->d_ord; p.eoffc = b->d_eoffc;
   p.gpar = b->d_gpar; p.ng = b->ng; p.sigma0 = b->d_sigma0; p.mag = b->d_mag; p.ne = b->ne;
   p.musc = b->has_musc ? b->d_musc : nullptr;
   p.musc_comp = b->musc_comp;
@@ -371,9 +432,14 @@ er_status apply_forcing(er_batch *b, const er_forcing *f, bool forcing) {
   CK(cudaMemcpyAsync(dflags, b->flags.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, b->stream), "H2D flags");
   p += (n + 1) / 2;
   const double *ddamp = nullptr, *dtip = nullptr, *dA = nullptr, *dF = nullptr, *dL = nullptr;
+  std::vector<std::vector<double>> keep;  // packed-order copies, alive until the final sync
   auto up = [&](const double *src, size_t cnt) -> const double * {
     double *q = p;
     p += cnt;
+    if (!b->identity) {  // caller's canonical per-rod rows -> packed order
+      keep.push_back(pack_rows(b, src, (int)(cnt / n), false));
+      src = keep.back().data();
+    }
     return cudaMemcpyAsync(q, src, sizeof(double) * cnt, cudaMemcpyHostToDevice, b->stream) == cudaSuccess ? q : nullptr;
   };
   if (damp) ddamp = up(f->damping, n);
@@ -454,8 +520,26 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   b->device = d->device;
   b->n_rods = R; b->n_elems = E; b->n_nodes = NN; b->n_vor = NV; b->max_n = max_n;
   b->t = d->t0;
-  b->n_elems_h.assign(d->n_elems, d->n_elems + R);
-  b->eoff = eoff;
+  b->block = d->tile_slots ? d->tile_slots : (max_n + 1 <= 256) ? 256 : 512;
+  {
+    int32_t min_n = max_n;
+    for (int64_t r = 0; r < R; ++r) min_n = std::min(min_n, d->n_elems[r]);
+    b->identity = R <= 1 || min_n == max_n || std::getenv("ER_NO_PACK") != nullptr;
+    if (b->identity) {
+      b->ord.resize((size_t)R);
+      for (int64_t r = 0; r < R; ++r) b->ord[r] = (int32_t)r;
+    } else {
+      b->ord = pack_rods(d->n_elems, R, b->block, b->block / 8);
+    }
+  }
+  b->eoffc = eoff;
+  b->n_elems_h.resize((size_t)R);
+  b->eoff.assign((size_t)R + 1, 0);
+  for (int64_t p = 0; p < R; ++p) {
+    b->n_elems_h[p] = d->n_elems[b->ord[p]];
+    b->eoff[p + 1] = b->eoff[p] + b->n_elems_h[p];
+  }
+  const std::vector<int64_t> &eoffp = b->eoff;
   auto fail = [&](er_status s) { g_create_error = b->last_error; free_all(b); delete b; return s; };
 #undef CK
 #define CK(call, what)                                                 \
@@ -481,7 +565,8 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   std::vector<char> gen_flag((size_t)std::max<int64_t>(R, 1), 0);
   for (auto *v : {&b->rod_A0, &b->rod_E0, &b->rod_lmin, &b->rod_lmax}) v->assign((size_t)std::max<int64_t>(R, 1), 0.0);
   auto rec_range = [&](int64_t ra, int64_t rb) {
-  for (int64_t r = ra; r < rb; ++r) {
+  for (int64_t pr = ra; pr < rb; ++pr) {
+    const int64_t r = b->ord[pr];  // canonical rod of packed rod pr
     const ElemMat m0 = mat_at(r, eoff[r]);
     bool uniform = true;
     if (d->material_per_rod) {  // only the rest lengths can vary along the rod
@@ -494,17 +579,18 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
                   m.ac == m0.ac && m.lh == m0.lh;
       }
     }
-    fill_record(&b->rec[(size_t)r * ER_REC], m0);
-    if (!uniform) gen_flag[r] = 1;
+    fill_record(&b->rec[(size_t)pr * ER_REC], m0);
+    b->rec[(size_t)pr * ER_REC + REC_CANON] = (double)r;
+    if (!uniform) gen_flag[pr] = 1;
     double lmin = d->rest_lengths[eoff[r]], lmax = lmin;
     for (int64_t j = eoff[r] + 1; j < eoff[r + 1]; ++j) {
       lmin = std::min(lmin, d->rest_lengths[j]);
       lmax = std::max(lmax, d->rest_lengths[j]);
     }
-    b->rod_A0[r] = m0.A;
-    b->rod_E0[r] = m0.E;
-    b->rod_lmin[r] = lmin;
-    b->rod_lmax[r] = lmax;
+    b->rod_A0[pr] = m0.A;
+    b->rod_E0[pr] = m0.E;
+    b->rod_lmin[pr] = lmin;
+    b->rod_lmax[pr] = lmax;
   }
   };
   if (R < 65536) rec_range(0, R);
@@ -522,10 +608,11 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   std::vector<double> gpar;
   if (b->any_general) {
     gpar.assign((size_t)ER_GP * b->ng, 0.0);
-    for (int64_t r = 0; r < R; ++r) {
-      if (!(b->flags[r] & FL_GENERAL)) continue;
-      const int32_t N = b->n_elems_h[r];
-      const int64_t n0 = eoff[r] + r;
+    for (int64_t pr = 0; pr < R; ++pr) {
+      if (!(b->flags[pr] & FL_GENERAL)) continue;
+      const int64_t r = b->ord[pr];
+      const int32_t N = b->n_elems_h[pr];
+      const int64_t n0 = eoffp[pr] + pr;
       double sk = 0.0;
       for (int32_t i = 0; i <= N; ++i) {
         auto G = [&](int q) -> double & { return gpar[(size_t)q * b->ng + n0 + i]; };
@@ -560,15 +647,14 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   // ---- rod-aligned tiles (greedy contiguous packing, <= block slots and <= block/8 rods per
   // tile); each tile's state is one contiguous SoA block: 6 node planes x nslots, 12 element
   // planes x nel, [3 Voronoi planes x nvor], padded to an even number of doubles (16 B).
-  b->block = d->tile_slots ? d->tile_slots : (max_n + 1 <= 256) ? 256 : 512;
   std::vector<ErTile> tiles;
   {
     int64_t r = 0, boff = 0;
     while (r < R) {
       ErTile T;
       T.r0 = (int32_t)r;
-      T.nbase = eoff[r] + r;
-      T.ebase = eoff[r];
+      T.nbase = eoffp[r] + r;
+      T.ebase = eoffp[r];
       T.boff = boff;
       int64_t used = 0;
       int32_t nr = 0;
@@ -579,7 +665,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
       }
       T.nr = nr;
       T.nslots = (int32_t)used;
-      T.nel = (int32_t)(eoff[r] - eoff[T.r0]);
+      T.nel = (int32_t)(eoffp[r] - eoffp[T.r0]);
       std::memset(T.smask, 0, sizeof T.smask);
       std::memset(T.pfx, 0, sizeof T.pfx);
       T.pad_ = 0;
@@ -607,10 +693,14 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   CK(dalloc(b, &b->d_diag_out, 16), "cudaMalloc(diag_out)");
   CK(dalloc(b, &b->d_valid, 4), "cudaMalloc(valid)");
   CK(cudaMemsetAsync(b->d_state, 0, sizeof(double) * (b->state_doubles + 64), b->stream), "memset");
+  CK(dalloc(b, &b->d_ord, R + 1), "cudaMalloc(ord)");
+  CK(dalloc(b, &b->d_eoffc, R + 1), "cudaMalloc(eoffc)");
   {
-    std::vector<int64_t> ep(eoff);
-    ep.resize((size_t)R + 4, eoff[R]);
+    std::vector<int64_t> ep(eoffp);
+    ep.resize((size_t)R + 4, eoffp[R]);
     CK(cudaMemcpyAsync(b->d_eoff, ep.data(), sizeof(int64_t) * ep.size(), cudaMemcpyHostToDevice, b->stream), "H2D eoff");
+    if (R > 0) CK(cudaMemcpyAsync(b->d_ord, b->ord.data(), sizeof(int32_t) * R, cudaMemcpyHostToDevice, b->stream), "H2D ord");
+    CK(cudaMemcpyAsync(b->d_eoffc, eoff.data(), sizeof(int64_t) * (R + 1), cudaMemcpyHostToDevice, b->stream), "H2D eoffc");
     if (!tiles.empty())
       CK(cudaMemcpyAsync(b->d_tiles, tiles.data(), sizeof(ErTile) * tiles.size(), cudaMemcpyHostToDevice, b->stream), "H2D tiles");
     if (b->any_general) {
@@ -636,7 +726,8 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   b->upload_stage = nullptr;
   if (d->rest_sigma) {
     CK(dalloc(b, &b->d_sigma0, 3 * b->ne), "cudaMalloc(sigma0)");
-    if ((st = upload_side_planes(b, d->rest_sigma, b->d_sigma0, E, b->ne)) != ER_OK) return fail(st);
+    const std::vector<double> ps = b->identity ? std::vector<double>() : pack_rows(b, d->rest_sigma, 3, true);
+    if ((st = upload_side_planes(b, b->identity ? d->rest_sigma : ps.data(), b->d_sigma0, E, b->ne)) != ER_OK) return fail(st);
   }
   tm.mark("state upload + layout", b->stream);
   // ---- validation of the uploaded state (directors orthonormal within 1e-10, all finite)
@@ -666,10 +757,11 @@ er_status er_set_bc(er_batch *b, const int8_t *clamp_end) {
     for (int64_t r = 0; r < b->n_rods; ++r)
       if (clamp_end[r] < -1 || clamp_end[r] > 1) err.add("clamp_end[%lld] = %d not in {-1, 0, 1}", (long long)r, clamp_end[r]);
   if (err.count) { b->last_error = err.msg; return ER_EINVAL; }
-  for (int64_t r = 0; r < b->n_rods; ++r) {
-    b->flags[r] &= ~FL_CLAMP_MASK;
-    if (clamp_end && clamp_end[r] == 0) b->flags[r] |= 1;
-    if (clamp_end && clamp_end[r] == 1) b->flags[r] |= 2;
+  for (int64_t pr = 0; pr < b->n_rods; ++pr) {
+    const int64_t r = b->ord[pr];
+    b->flags[pr] &= ~FL_CLAMP_MASK;
+    if (clamp_end && clamp_end[r] == 0) b->flags[pr] |= 1;
+    if (clamp_end && clamp_end[r] == 1) b->flags[pr] |= 2;
   }
   CK(cudaSetDevice(b->device), "cudaSetDevice");
   return apply_forcing(b, nullptr, false);
@@ -749,11 +841,12 @@ er_status er_set_forcing(er_batch *b, const er_forcing *f) {
   if (st != ER_OK) return st;
   if (musc && R > 0) {
     std::vector<double> mh((size_t)R * 4);
-    for (int64_t r = 0; r < R; ++r) {
-      mh[4 * r + 0] = f->musc_A[r];
-      mh[4 * r + 1] = 1.0 / f->musc_T[r];
-      mh[4 * r + 2] = 1.0 / f->musc_lambda[r];
-      mh[4 * r + 3] = f->musc_phi[r] / 3.14159265358979323846;
+    for (int64_t pr = 0; pr < R; ++pr) {
+      const int64_t r = b->ord[pr];
+      mh[4 * pr + 0] = f->musc_A[r];
+      mh[4 * pr + 1] = 1.0 / f->musc_T[r];
+      mh[4 * pr + 2] = 1.0 / f->musc_lambda[r];
+      mh[4 * pr + 3] = f->musc_phi[r] / 3.14159265358979323846;
     }
     if (!b->d_musc) CK(dalloc(b, &b->d_musc, 4 * R), "cudaMalloc(musc)");
     CK(cudaMemcpyAsync(b->d_musc, mh.data(), sizeof(double) * mh.size(), cudaMemcpyHostToDevice, b->stream), "H2D musc");
@@ -761,7 +854,9 @@ er_status er_set_forcing(er_batch *b, const er_forcing *f) {
   }
   if (f->magnetization && b->n_elems > 0) {
     if (!b->d_mag) CK(dalloc(b, &b->d_mag, 3 * b->ne), "cudaMalloc(mag)");
-    if ((st = upload_side_planes(b, f->magnetization, b->d_mag, b->n_elems, b->ne)) != ER_OK) return st;
+    const std::vector<double> pm = b->identity ? std::vector<double>() : pack_rows(b, f->magnetization, 3, true);
+    if ((st = upload_side_planes(b, b->identity ? f->magnetization : pm.data(), b->d_mag, b->n_elems, b->ne)) != ER_OK)
+      return st;
   } else if (b->d_mag) {
     CK(cudaStreamSynchronize(b->stream), "sync");
     cudaFree(b->d_mag);
@@ -972,7 +1067,7 @@ er_status er_set_contact(er_batch *b, const er_contact *c) {
   std::vector<double> rad((size_t)std::max<int64_t>(R, 1)), kr((size_t)std::max<int64_t>(R, 1));
   double xmin = 0.0, xmax = 0.0;
   for (int64_t r = 0; r < R; ++r) {
-    rad[r] = c->radius ? c->radius[r] : std::sqrt(b->rod_A0[r] / 3.14159265358979323846);
+    rad[r] = c->radius ? c->radius[b->ord[r]] : std::sqrt(b->rod_A0[r] / 3.14159265358979323846);  // r packed
     kr[r] = b->rod_E0[r] * rad[r];
     const double lo = b->rod_lmin[r] + 2.0 * rad[r], hi = b->rod_lmax[r] + 2.0 * rad[r];
     xmin = r == 0 ? lo : std::min(xmin, lo);
@@ -1021,6 +1116,7 @@ er_status er_set_contact(er_batch *b, const er_contact *c) {
   CA(d_rad, R); CA(d_kr, R); CA(d_erod, E);
   CA(d_nrad, b->n_nodes); CA(d_nkr, b->n_nodes);
   cp.rad = d_rad; cp.kr = d_kr; cp.erod = d_erod; cp.nrad = d_nrad; cp.nkr = d_nkr;
+  cp.ord = b->d_ord;
   CA(cp.cnode, 6 * b->n_nodes); CA(cp.cbuild, 3 * b->n_nodes); CA(cp.rebuild, 1);
   CA(cp.gext, 3 * ER_HHG_MAXLEV); CA(cp.gdim, 4 * ER_HHG_MAXLEV);
   CA(cp.key, E); CA(cp.key_s, E); CA(cp.val, E); CA(cp.val_s, E);

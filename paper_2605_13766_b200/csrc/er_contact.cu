@@ -55,9 +55,9 @@ constexpr unsigned long long F_CONTACT = 16ull;  // ER_F_CONTACT (include/er.h)
 constexpr int CBITS = 20;                        // cell index bits per axis in a cell code
 constexpr int CHALF = 1 << (CBITS - 1);
 
-__device__ __forceinline__ void flag_fault(const ErContactParams &p, int rod) {
+__device__ __forceinline__ void flag_fault(const ErContactParams &p, int rod) {  // rod: packed id
   atomicOr(p.fault, F_CONTACT);
-  atomicMin(p.fault + 1, (unsigned long long)rod);
+  atomicMin(p.fault + 1, (unsigned long long)__ldg(p.ord + rod));
 }
 
 __device__ __forceinline__ uint32_t cell_hash(int cx, int cy, int cz, int l, int hbits) {

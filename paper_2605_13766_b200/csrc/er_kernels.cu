@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
         if (st + 1 < p.n_steps) __syncthreads();  // exchange C is re-used as A by the next step
       }
     }
-    if (fbits) { fbits_all |= fbits; frod = min(frod, si.rod); }
+    if (fbits) { fbits_all |= fbits; frod = min(frod, (int)rec[REC_CANON]); }  // canonical rod id
     if (tr) tr[2] = gtimer() & ((1ull << 48) - 1);
 
     if (DSTORE) {  // ablation: results straight from registers to HBM (coalesced SoA planes)
@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) simple_kernel(const ErStepParams 
 #pragma unroll
     for (int c = 0; c < 3; ++c) __stcs(G + 6 * ns + (9 + c) * nel + le, w[c]);
   }
-  report_fault(p, fbits, si.rod);
+  report_fault(p, fbits, si.active ? (int)rec[REC_CANON] : 0);  // canonical rod id
 }
 
 // --------------------------------------------------------------------------- diagnostics
@@ -785,25 +785,33 @@ __global__ void aos_to_soa(const double *__restrict__ src, double *__restrict__ 
     dst[c * stride + e] = src[q];
   }
 }
-// Canonical AoS [rows][k] <-> tile-blocked planes, one CTA per tile.  canon == nullptr with
-// to_tiles writes zeros.
+// Canonical AoS [rows][k] <-> tile-blocked planes, one CTA per tile, rod by rod: the rods of a tile
+// are consecutive in packed order, and each rod's rows are contiguous in the canonical array (at
+// its canonical offset).  canon == nullptr with to_tiles writes zeros.
 __global__ void canon_tiles(const ErStepParams p, double *canon, int field, int to_tiles) {
   const ErTile T = p.tiles[blockIdx.x];
   const int k = field == FIELD_DIR ? 9 : 3;
-  int64_t base, count, off;
+  int64_t count, off;
+  int shift;  // rows per rod = N + shift
   if (field <= FIELD_VEL) {
-    base = T.nbase; count = T.nslots; off = tile_node_plane(T, field == FIELD_VEL ? 3 : 0);
+    count = T.nslots; off = tile_node_plane(T, field == FIELD_VEL ? 3 : 0); shift = 1;
   } else if (field <= FIELD_OMEGA) {
-    base = T.ebase; count = T.nel; off = tile_elem_plane(T, field == FIELD_OMEGA ? 9 : 0);
+    count = T.nel; off = tile_elem_plane(T, field == FIELD_OMEGA ? 9 : 0); shift = 0;
   } else {
-    base = T.ebase - T.r0; count = T.nel - T.nr; off = tile_vor_plane(T, 0);
+    count = T.nel - T.nr; off = tile_vor_plane(T, 0); shift = -1;
   }
   double *blk = p.state + T.boff + off;
-  for (int64_t q = threadIdx.x; q < count * k; q += blockDim.x) {
-    const int64_t u = q / k;
-    const int c = (int)(q - u * k);
-    if (to_tiles) blk[c * count + u] = canon ? canon[base * k + q] : 0.0;
-    else canon[base * k + q] = blk[c * count + u];
+  for (int q = 0; q < T.nr; ++q) {
+    const int64_t pr = T.r0 + q, cr = p.ord[pr];
+    const int64_t n = p.eoff[pr + 1] - p.eoff[pr] + shift;                     // rows of this rod
+    const int64_t loc = p.eoff[pr] - T.ebase + (int64_t)q * shift;            // first row in the tile
+    const int64_t can = p.eoffc[cr] + cr * shift;                              // first canonical row
+    for (int64_t x = threadIdx.x; x < n * k; x += blockDim.x) {
+      const int64_t u = x / k;
+      const int c = (int)(x - u * k);
+      if (to_tiles) blk[c * count + loc + u] = canon ? canon[can * k + x] : 0.0;
+      else canon[can * k + x] = blk[c * count + loc + u];
+    }
   }
 }
 

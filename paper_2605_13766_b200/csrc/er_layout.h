@@ -11,6 +11,9 @@
 //                   actuation and the flag word -- one 192-byte record read per rod per step
 //  - eoff         : [n_rods+4] int64 element offsets (node offset = eoff + rod); padded so
 //                   16-byte-aligned bulk copies may over-read
+//  - rod order    : rods are stored in a packed (tile) order, ord[p] = canonical id of packed rod
+//                   p -- the identity unless rod lengths differ (best-fit-decreasing tiles); every
+//                   per-rod / per-element / per-node device array is in packed order
 //  - tiles        : [n_tiles] ErTile
 //  - gpar         : optional [ER_GP][ng] per-slot parameters of "general" rods (non-uniform
 //                   rest lengths or per-element material), canonical node index
@@ -49,7 +52,7 @@ enum {
   REC_ACTF,      // actuation frequency f
   REC_ACTIL,     // 1/L of the actuation wave
   REC_FLAGS,     // flag word (int64 bits)
-  REC_PAD,
+  REC_CANON,     // canonical id of the rod (records are stored in packed rod order)
   ER_REC
 };
 
@@ -122,7 +125,8 @@ struct ErContactParams {
   int64_t n_elems, n_nodes, n_rods;
   const double *rad;            // [R] contact radius
   const double *kr;             // [R] E r (pair stiffness scale)
-  const int32_t *erod;          // [E] rod of each element
+  const int32_t *erod;          // [E] rod of each element (packed ids, like every array here)
+  const int32_t *ord;           // [R] packed -> canonical rod (fault reports)
   const double *nrad, *nkr;     // [n_nodes] contact radius / E r of the node's rod
   double *cnode;                // [n_nodes][6] node r, v after drift-1 (AoS: an element's two
                                 //   nodes are 96 contiguous bytes)
@@ -159,7 +163,9 @@ struct ErContactParams {
 struct ErStepParams {
   double *state;          // tile-blocked state
   const double *rec;
-  const int64_t *eoff;
+  const int64_t *eoff;     // [n_rods+4] element offsets in packed rod order
+  const int32_t *ord;      // [n_rods] packed -> canonical rod
+  const int64_t *eoffc;    // [n_rods+1] canonical element offsets
   const ErTile *tiles;
   int64_t n_tiles;
   const double *gpar;     // may be null

@@ -284,6 +284,37 @@ def test_fault_reports_rod(er):
         assert rod_id == 13 and bits & er.ER_F_NONFINITE
 
 
+def test_packed_rod_order(er, monkeypatch):
+    """Ragged batches are stored in a best-fit-decreasing tile order (fewer, fuller tiles); the
+    API stays canonical: the same trajectory bitwise as the identity order, forcing / clamps /
+    fault ids in canonical rod numbering."""
+    w = W.make("cfg5", n_rods=300)
+    tip = np.zeros((w.n_rods, 3))
+    tip[::7, 0] = 1e-4                                       # per-rod forcing in canonical order
+    w = dataclasses.replace(w, tip_force=tip)
+    out, tiles = [], []
+    for pack in (True, False):
+        if not pack:
+            monkeypatch.setenv("ER_NO_PACK", "1")
+        with er.RodBatch(w) as b:
+            tiles.append(b.info().n_tiles)
+            b.step(20, w.dt)
+            out.append(b.get_state())
+    assert tiles[0] < tiles[1]
+    for x, y in zip(out[0], out[1]):
+        assert np.array_equal(x, y)
+    monkeypatch.delenv("ER_NO_PACK")
+    no = w.node_offsets()
+    bad = w.velocities.copy()
+    for r in (250, 77):
+        bad[no[r] + 2, 0] = np.inf
+    with er.RodBatch(w) as b:
+        b.set_state(velocities=bad)
+        with pytest.raises(er.ErError):
+            b.step(2, w.dt)
+        assert b.fault()[0] == 77
+
+
 def test_fault_degenerate_and_overspeed(er, orc):
     w = concat([rod(N=4, L=0.2), rod(N=4, L=0.2), rod(N=4, L=0.2)])
     w.positions[11] = w.positions[10]
