@@ -109,7 +109,8 @@ typedef struct {
   int32_t src_mem; /* er_mem */
   int32_t device;
   void *stream;
-  int32_t tile_slots; /* 0 = auto (256, or 512 when a rod has more than 255 elements);
+  int32_t tile_slots; /* 0 = auto (256; 512 when a rod has more than 255 elements, or when
+                         equal-length rods keep clearly more lanes busy in 512-slot tiles);
                          128, 256 or 512 = slots (threads) per rod tile; must be >= max N + 1 */
 } er_batch_desc;
 
