@@ -15,6 +15,7 @@
 #include <cstring>
 #include <limits>
 #include <map>
+#include <memory>
 #include <string>
 #include <thread>
 #include <vector>
@@ -117,7 +118,8 @@ struct er_batch {
   std::vector<int64_t> eoffc;      // canonical element offsets
   int32_t *d_ord = nullptr;
   int64_t *d_eoffc = nullptr;
-  std::vector<double> rec;
+  std::unique_ptr<double[]> rec;  // host records during create (not value-initialised)
+  size_t rec_n = 0;
   std::vector<int32_t> flags;
   double g[3] = {0, 0, 0};
   double b0[3] = {0, 0, 0}, b1[3] = {0, 0, 0}, b2[3] = {0, 0, 0};  // b(t) = b0 cos + b1 sin + b2
@@ -126,7 +128,8 @@ struct er_batch {
   int64_t fault_rod = -1;
   int32_t fault_bits = 0;
   std::string last_error;
-  double *upload_stage = nullptr;  // during er_create_batch: one staging buffer for all fields
+  double *upload_stage = nullptr;  // during er_create_batch: device staging of the host state arrays
+  double *staged[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // per field, inside upload_stage
   // contact (NEXT-4)
   bool contact_on = false;
   ErContactParams cp{};
@@ -274,6 +277,25 @@ void free_all(er_batch *b) {
 
 bool pos_finite(double x) { return std::isfinite(x) && x > 0.0; }
 
+// First index k < n with !ok(a[k]), or -1; large arrays are scanned by host threads.
+template <class Ok>
+int64_t first_bad(const double *a, int64_t n, Ok ok) {
+  const int nthr = (int)std::max<unsigned>(1u, std::min<unsigned>(16u, std::thread::hardware_concurrency()));
+  auto scan = [&](int64_t lo, int64_t hi) {
+    for (int64_t k = lo; k < hi; ++k)
+      if (!ok(a[k])) return k;
+    return (int64_t)-1;
+  };
+  if (n < (1 << 20) || nthr == 1) return scan(0, n);
+  std::vector<int64_t> res((size_t)nthr, -1);
+  std::vector<std::thread> th;
+  for (int q = 0; q < nthr; ++q) th.emplace_back([&, q] { res[q] = scan(n * q / nthr, n * (q + 1) / nthr); });
+  for (auto &t : th) t.join();
+  for (int64_t x : res)
+    if (x >= 0) return x;
+  return -1;
+}
+
 ErStepParams params_of(const er_batch *b) {
   ErStepParams p;
   std::memset(&p, 0, sizeof p);
@@ -324,15 +346,16 @@ er_status upload_field(er_batch *b, const double *src, int src_mem, int field, b
   }
   const double *dsrc = src;
   double *stage = nullptr;
-  if (src_mem == ER_HOST) {  // DMA into a device staging buffer (the caller's `stage` when given)
-    stage = b->upload_stage;
-    if (!stage) CK(cudaMallocAsync((void **)&stage, sizeof(double) * (size_t)(n * k), b->stream), "cudaMallocAsync(stage)");
+  if (src_mem == ER_HOST && b->staged[field]) {  // copied at the start of er_create_batch
+    dsrc = b->staged[field];
+  } else if (src_mem == ER_HOST) {  // DMA into a temporary device buffer
+    CK(cudaMallocAsync((void **)&stage, sizeof(double) * (size_t)(n * k), b->stream), "cudaMallocAsync(stage)");
     CK(cudaMemcpyAsync(stage, src, sizeof(double) * (size_t)(n * k), cudaMemcpyHostToDevice, b->stream), "H2D");
     dsrc = stage;
   }
   if (validate) CK(er_launch_validate(dsrc, n, k, field == FIELD_DIR, b->d_valid, b->stream), "validate");
   CK(er_launch_canon_tiles(&p, const_cast<double *>(dsrc), field, 1, b->stream), "canon->tiles");
-  if (stage && stage != b->upload_stage) CK(cudaFreeAsync(stage, b->stream), "cudaFreeAsync");
+  if (stage) CK(cudaFreeAsync(stage, b->stream), "cudaFreeAsync");
   return ER_OK;
 }
 
@@ -412,7 +435,7 @@ int feat_of(const er_batch *b) {
 er_status upload_records(er_batch *b) {
   sync_flags(b);
   if (b->n_rods > 0)
-    CK(cudaMemcpyAsync(b->d_rec, b->rec.data(), sizeof(double) * b->rec.size(), cudaMemcpyHostToDevice, b->stream),
+    CK(cudaMemcpyAsync(b->d_rec, b->rec.get(), sizeof(double) * b->rec_n, cudaMemcpyHostToDevice, b->stream),
        "H2D rec");
   return ER_OK;
 }
@@ -487,23 +510,21 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   const char *mnames[7] = {"density", "area", "I1", "I2", "youngs", "shear_mod", "alpha_c"};
   const double *marr[7] = {d->density, d->area, d->I1, d->I2, d->youngs, d->shear_mod, d->alpha_c};
   if (R > 0) {
+    auto fin = [](double x) { return std::isfinite(x); };
     for (int q = 0; q < 7; ++q) {
       if (!marr[q]) { err.add("%s is NULL", mnames[q]); continue; }
-      for (int64_t k = 0; k < nmat; ++k)
-        if (!pos_finite(marr[q][k])) { err.add("%s[%lld] = %g is not positive and finite", mnames[q], (long long)k, marr[q][k]); break; }
+      const int64_t k = first_bad(marr[q], nmat, pos_finite);
+      if (k >= 0) err.add("%s[%lld] = %g is not positive and finite", mnames[q], (long long)k, marr[q][k]);
     }
     if (!d->rest_lengths) err.add("rest_lengths is NULL");
-    else
-      for (int64_t k = 0; k < E; ++k)
-        if (!pos_finite(d->rest_lengths[k])) { err.add("rest_lengths[%lld] = %g is not positive and finite", (long long)k, d->rest_lengths[k]); break; }
+    else if (const int64_t k = first_bad(d->rest_lengths, E, pos_finite); k >= 0)
+      err.add("rest_lengths[%lld] = %g is not positive and finite", (long long)k, d->rest_lengths[k]);
     if (!d->positions) err.add("positions is NULL");
     if (!d->directors) err.add("directors is NULL");
     if (d->rest_sigma)
-      for (int64_t k = 0; k < 3 * E; ++k)
-        if (!std::isfinite(d->rest_sigma[k])) { err.add("rest_sigma[%lld] is not finite", (long long)k); break; }
+      if (const int64_t k = first_bad(d->rest_sigma, 3 * E, fin); k >= 0) err.add("rest_sigma[%lld] is not finite", (long long)k);
     if (d->rest_kappa)
-      for (int64_t k = 0; k < 3 * NV; ++k)
-        if (!std::isfinite(d->rest_kappa[k])) { err.add("rest_kappa[%lld] is not finite", (long long)k); break; }
+      if (const int64_t k = first_bad(d->rest_kappa, 3 * NV, fin); k >= 0) err.add("rest_kappa[%lld] is not finite", (long long)k);
   }
   if (!std::isfinite(d->t0)) err.add("t0 is not finite");
   if (d->tile_slots != 0 && d->tile_slots != 128 && d->tile_slots != 256 && d->tile_slots != 512)
@@ -561,8 +582,35 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   if (d->stream) b->stream = (cudaStream_t)d->stream;
   else { CK(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking), "cudaStreamCreate"); b->own_stream = true; }
 
+  // ---- start the host->device copies of the state now: from page-locked arrays the DMA runs
+  // while the host builds records and tiles below (the layout kernels use the staged copies)
+  {
+    const struct { const double *src; int field; int64_t n; } fs[5] = {
+        {d->src_mem == ER_HOST ? d->positions : nullptr, FIELD_POS, 3 * NN},
+        {d->src_mem == ER_HOST ? d->velocities : nullptr, FIELD_VEL, 3 * NN},
+        {d->src_mem == ER_HOST ? d->directors : nullptr, FIELD_DIR, 9 * E},
+        {d->src_mem == ER_HOST ? d->omega : nullptr, FIELD_OMEGA, 3 * E},
+        {NV > 0 ? d->rest_kappa : nullptr, FIELD_KAPPA0, 3 * NV}};
+    int64_t total = 0;
+    for (const auto &f : fs) total += f.src ? f.n : 0;
+    if (total > 0) {
+      CK(cudaMalloc((void **)&b->upload_stage, sizeof(double) * (size_t)total + 64), "cudaMalloc(stage)");
+      int64_t o = 0;
+      for (const auto &f : fs)
+        if (f.src) {
+          b->staged[f.field] = b->upload_stage + o;
+          CK(cudaMemcpyAsync(b->staged[f.field], f.src, sizeof(double) * (size_t)f.n, cudaMemcpyHostToDevice, b->stream),
+             "H2D state");
+          o += f.n;
+        }
+    }
+  }
+  tm.mark("state copies issued");
+
   // ---- per-rod records; general rods get per-slot parameter planes
-  b->rec.assign((size_t)std::max<int64_t>(R, 1) * ER_REC, 0.0);
+  b->rec_n = (size_t)std::max<int64_t>(R, 1) * ER_REC;
+  b->rec.reset(new double[b->rec_n]);  // every record is fully written below (in parallel)
+  if (R == 0) std::fill_n(b->rec.get(), b->rec_n, 0.0);
   b->flags.assign((size_t)std::max<int64_t>(R, 1), 0);
   auto mat_at = [&](int64_t r, int64_t j) {
     const int64_t k = d->material_per_rod ? r : j;
@@ -589,6 +637,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
                   m.ac == m0.ac && m.lh == m0.lh;
       }
     }
+    std::fill_n(&b->rec[(size_t)pr * ER_REC], ER_REC, 0.0);
     fill_record(&b->rec[(size_t)pr * ER_REC], m0);
     b->rec[(size_t)pr * ER_REC + REC_CANON] = (double)r;
     if (!uniform) gen_flag[pr] = 1;
@@ -695,7 +744,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
 
   // ---- device allocation and upload
   CK(dalloc(b, &b->d_state, b->state_doubles + 64), "cudaMalloc(state)");
-  CK(dalloc(b, &b->d_rec, (int64_t)b->rec.size()), "cudaMalloc(rec)");
+  CK(dalloc(b, &b->d_rec, (int64_t)b->rec_n), "cudaMalloc(rec)");
   CK(dalloc(b, &b->d_eoff, R + 4), "cudaMalloc(eoff)");
   CK(dalloc(b, &b->d_tiles, std::max<int64_t>((int64_t)tiles.size(), 1)), "cudaMalloc(tiles)");
   CK(dalloc(b, &b->d_fault, 2), "cudaMalloc(fault)");
@@ -724,8 +773,6 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   tm.mark("alloc + small uploads", b->stream);
   er_status st;
   CK(cudaMemsetAsync(b->d_valid, 0, sizeof(double) * 4, b->stream), "memset");
-  // one staging buffer, sized for the largest field, reused by every host upload
-  CK(cudaMalloc((void **)&b->upload_stage, sizeof(double) * (size_t)std::max<int64_t>(9 * E, 3 * NN) + 64), "cudaMalloc(stage)");
   if ((st = upload_field(b, d->positions, d->src_mem, FIELD_POS, true)) != ER_OK) return fail(st);
   if ((st = upload_field(b, d->velocities, d->src_mem, FIELD_VEL, true)) != ER_OK) return fail(st);
   if ((st = upload_field(b, d->directors, d->src_mem, FIELD_DIR, true)) != ER_OK) return fail(st);
@@ -734,6 +781,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   CK(cudaStreamSynchronize(b->stream), "sync");
   cudaFree(b->upload_stage);
   b->upload_stage = nullptr;
+  for (auto &sp : b->staged) sp = nullptr;
   if (d->rest_sigma) {
     CK(dalloc(b, &b->d_sigma0, 3 * b->ne), "cudaMalloc(sigma0)");
     const std::vector<double> ps = b->identity ? std::vector<double>() : pack_rows(b, d->rest_sigma, 3, true);
@@ -749,7 +797,8 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   if (vres[1] > 1e-10) err.add("directors not proper rotations: max |det Q - 1| = %.3g", vres[1]);
   if (err.count) { b->last_error = err.msg; return fail(ER_EINVAL); }
 #undef CK
-  std::vector<double>().swap(b->rec);  // the device records are authoritative from here on
+  b->rec.reset();  // the device records are authoritative from here on
+  b->rec_n = 0;
   *out = b;
   return ER_OK;
 }
