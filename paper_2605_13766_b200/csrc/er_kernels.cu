@@ -61,14 +61,12 @@ __device__ __forceinline__ void finish_slot(SlotInfo &si) {
 // Contact force on node i (NEXT-4, DESIGN §3 #27): er_contact.cu left, per element j, the force
 // on its nodes j and j+1 in ErContactParams.fc (half-space forces included); node i collects
 // element i's first and element i-1's second share.
-__device__ __forceinline__ void contact_node_force(const ErStepParams &p, const SlotInfo &si, double F[3]) {
-  if (si.has_e) {
+__device__ __forceinline__ void contact_node_load(const ErStepParams &p, const SlotInfo &si, double f[3]) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) F[c] += __ldg(p.cfc + c * p.cfs + si.elem);
-  }
-  if (si.i >= 1) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) F[c] += __ldg(p.cfc + (3 + c) * p.cfs + si.elem - 1);
+  for (int c = 0; c < 3; ++c) {
+    const double lo = si.has_e ? __ldg(p.cfc + c * p.cfs + si.elem) : 0.0;
+    const double hi = si.active && si.i >= 1 ? __ldg(p.cfc + (3 + c) * p.cfs + si.elem - 1) : 0.0;
+    f[c] = lo + hi;
   }
 }
 
@@ -76,22 +74,25 @@ __device__ __forceinline__ void contact_node_force(const ErStepParams &p, const 
 // kernels read, and the Verlet-list check against the positions of the last list build (a node
 // farther than skin/2 from it raises the rebuild flag).  Called by every thread of the CTA.
 __device__ __forceinline__ void contact_emit(const ErStepParams &p, const SlotInfo &si, const double r[3],
-                                             const double v[3]) {
+                                             const double v[3], const double rb[3]) {
   bool moved = false;
   if (si.active) {
     double *o = p.cnode + 6 * si.node;
-    const double *rb = p.cbuild + 3 * si.node;
     double d2 = 0.0;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       o[c] = r[c];
       o[3 + c] = v[c];
-      const double d = r[c] - __ldg(rb + c);
+      const double d = r[c] - rb[c];
       d2 = fma(d, d, d2);
     }
     moved = !(d2 <= p.disp2);  // also for NaN
   }
   if (__any_sync(0xffffffffu, moved) && (threadIdx.x & 31) == 0) atomicOr(p.rebuild, 1);
+}
+__device__ __forceinline__ void contact_build_pos(const ErStepParams &p, const SlotInfo &si, double rb[3]) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c) rb[c] = si.active ? __ldg(p.cbuild + 3 * si.node + c) : 0.0;
 }
 
 __device__ __forceinline__ int rec_flags(const double *rec) {
@@ -107,7 +108,8 @@ template <int BLOCK, int FEAT, bool DRIFT1, bool DYN, bool DRIFT2>
 __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restrict__ X,
                                           const double *__restrict__ rec, const SlotInfo &si,
                                           double r[3], double v[3], double Q[9], double w[3],
-                                          const double k0s[3], double &t, unsigned &fbits) {
+                                          const double k0s[3], double &t, unsigned &fbits,
+                                          const double *fcon = nullptr) {
   constexpr bool GEN = (FEAT & FEAT_GENERAL) != 0;
   constexpr bool EXTRA = (FEAT & FEAT_EXTRA) != 0;
   constexpr bool ACT = (FEAT & (FEAT_EXTRA | FEAT_ACT)) != 0;
@@ -237,7 +239,10 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
 #pragma unroll
         for (int c = 0; c < 3; ++c) F[c] += rec[REC_TIPX + c];
       }
-      if (CONTACT && p.cfc) contact_node_force(p, si, F);  // NEXT-4: rod-rod + half-space contact
+      if (CONTACT && fcon) {  // NEXT-4: rod-rod + half-space contact force on this node
+#pragma unroll
+        for (int c = 0; c < 3; ++c) F[c] += fcon[c];
+      }
       const double im = general ? gp(GP_IM) : rec[REC_IM] * ((i == 0 || i == N) ? 2.0 : 1.0);
       const double nu = rec[REC_NU];
 #pragma unroll
@@ -507,6 +512,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
 #pragma unroll
       for (int c = 0; c < 3; ++c) k0s[c] = B[6 * ns + 12 * nel + c * nvor + (tid - 2 * lo - 1)];
     }
+    // contact mode: this node's contact force and build position, loaded now so their latency
+    // hides behind the step's first phases
+    double fcon[3] = {0.0, 0.0, 0.0}, rbld[3] = {0.0, 0.0, 0.0};
+    if ((FEAT & FEAT_CONTACT) && p.cfc) contact_node_load(p, si, fcon);
+    if ((FEAT & FEAT_CONTACT) && p.cnode) contact_build_pos(p, si, rbld);
     __syncthreads();  // stage planes consumed: they become this tile's exchange area
     if (tid == 0 && tnext < p.n_tiles) {
       bulk_wait_read_all();  // the bulk store of tile k-1 has finished reading buffer b^1
@@ -520,10 +530,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
       // contact mode: the state arrives after drift-1 (contact forces were evaluated there);
       // kick + drift-2, then -- unless this is the call's last step -- the next step's drift-1
       // and the node records for the next contact evaluation
-      step_body<BLOCK, FEAT, false, true, true>(p, B, rec, si, r, v, Q, w, k0s, t, fbits);
+      step_body<BLOCK, FEAT, false, true, true>(p, B, rec, si, r, v, Q, w, k0s, t, fbits, p.cfc ? fcon : nullptr);
       if (p.cnode) {
         step_body<BLOCK, FEAT, true, false, false>(p, B, rec, si, r, v, Q, w, k0s, t, fbits);
-        contact_emit(p, si, r, v);
+        contact_emit(p, si, r, v, rbld);
       }
     } else {
       for (int st = 0; st < p.n_steps; ++st) {
@@ -636,7 +646,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) simple_kernel(const ErStepParams 
   for (int st = 0; st < nsteps; ++st) {
     if (MODE == MODE_FUSED) step_body<BLOCK, FEAT, true, true, true>(p, sm, rec, si, r, v, Q, w, k0s, t, fbits);
     if (MODE == MODE_DRIFT) step_body<BLOCK, FEAT, true, false, false>(p, sm, rec, si, r, v, Q, w, k0s, t, fbits);
-    if (MODE == MODE_DYN) step_body<BLOCK, FEAT, false, true, false>(p, sm, rec, si, r, v, Q, w, k0s, t, fbits);
+    if (MODE == MODE_DYN) {
+      double fcon[3] = {0.0, 0.0, 0.0};
+      if (p.cfc) contact_node_load(p, si, fcon);
+      step_body<BLOCK, FEAT, false, true, false>(p, sm, rec, si, r, v, Q, w, k0s, t, fbits, p.cfc ? fcon : nullptr);
+    }
     if (MODE == MODE_FUSED && st + 1 < nsteps) __syncthreads();
   }
   if (si.active) {
@@ -646,7 +660,11 @@ __global__ void __launch_bounds__(BLOCK, MINB) simple_kernel(const ErStepParams 
       __stcs(G + (3 + c) * ns + s, v[c]);
     }
   }
-  if (MODE == MODE_DRIFT && p.cnode) contact_emit(p, si, r, v);
+  if (MODE == MODE_DRIFT && p.cnode) {
+    double rb[3];
+    contact_build_pos(p, si, rb);
+    contact_emit(p, si, r, v, rb);
+  }
   if (si.has_e) {
 #pragma unroll
     for (int c = 0; c < 9; ++c) __stcs(G + 6 * ns + c * nel + le, Q[c]);
