@@ -440,7 +440,10 @@ __device__ __forceinline__ unsigned plane_forces(const ErContactParams &p, int64
 // others, which re-run the broad visit of the last build (same order) -- a separate kernel so the
 // common path does not carry the broad visit's registers.
 template <bool LONG>
-__global__ void __launch_bounds__(128, LONG ? 4 : 6) hhg_narrow(const ErContactParams p) {
+#ifndef ER_NARROW_MINB
+#define ER_NARROW_MINB 6
+#endif
+__global__ void __launch_bounds__(128, LONG ? 4 : ER_NARROW_MINB) hhg_narrow(const ErContactParams p) {
   const int64_t ea = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   unsigned n_cont = 0, n_cross = 0, n_plane = 0;
   if (ea < p.n_elems && ((p.cnt[ea] > ER_CAND_K) == LONG)) {
