@@ -518,11 +518,16 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
     if ((FEAT & FEAT_CONTACT) && p.cfc) contact_node_load(p, si, fcon);
     if ((FEAT & FEAT_CONTACT) && p.cnode) contact_build_pos(p, si, rbld);
     __syncthreads();  // stage planes consumed: they become this tile's exchange area
+#ifdef ER_TRACE_FINE
+    if (tr) tr[2] = gtimer() & ((1ull << 48) - 1);
+#endif
     if (tid == 0 && tnext < p.n_tiles) {
       bulk_wait_read_all();  // the bulk store of tile k-1 has finished reading buffer b^1
       issue_tile<BLOCK, FEAT>(p, Tn, p.tiles + tnext, sm + (b ^ 1) * SG::BUFD, &bar[b ^ 1]);
     }
-
+#ifdef ER_TRACE_FINE  // measurement: [2] = after the stage barrier, [3] = prefetch issued
+    if (tr) tr[3] = gtimer() & ((1ull << 48) - 1);
+#endif
     // ---- the steps
     double t = p.t;
     unsigned fbits = 0;
@@ -542,7 +547,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
       }
     }
     if (fbits) { fbits_all |= fbits; frod = min(frod, (int)rec[REC_CANON]); }  // canonical rod id
+#ifndef ER_TRACE_FINE
     if (tr) tr[2] = gtimer() & ((1ull << 48) - 1);
+#endif
 
     if (DSTORE) {  // ablation: results straight from registers to HBM (coalesced SoA planes)
       double *G = p.state + boff;
@@ -559,7 +566,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
 #pragma unroll
         for (int c = 0; c < 3; ++c) __stcs(G + 6 * ns + (9 + c) * nel + le, w[c]);
       }
+#ifndef ER_TRACE_FINE
       if (tr) tr[3] = gtimer() & ((1ull << 48) - 1);
+#endif
       continue;
     }
     // ---- registers -> stage (block layout at OUTOFF) -> HBM with one TMA bulk store
@@ -583,7 +592,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
       bulk_s2g(p.state + boff, O, 8u * (uint32_t)(6 * ns + 12 * nel));
       bulk_commit();
     }
+#ifndef ER_TRACE_FINE
     if (tr) tr[3] = gtimer() & ((1ull << 48) - 1);
+#endif
   }
   if (tid == 0) bulk_wait_all();  // stores complete before the kernel retires
   report_fault(p, fbits_all, frod);

@@ -8,6 +8,6 @@ ER_NVCC_EXTRA="$1" python paper_2605_13766_b200/build.py --force > /dev/null 2>&
 cp paper_2605_13766_b200/lib/libelasticarod.so /tmp/libB.so
 for r in 1 2 3; do
   for v in A B; do
-    echo -n "$v: "; ER_LIB=/tmp/lib$v.so python tools/ab_time.py "$2" "$3" 0 | tail -1
+    echo -n "$v: "; ER_LIB=/tmp/lib$v.so timeout 120 python tools/ab_time.py "$2" "$3" 0 | tail -1
   done
 done
