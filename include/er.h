@@ -71,7 +71,8 @@ typedef enum { ER_HOST = 0, ER_DEVICE = 1 } er_mem;
 
 /* ------------------------------------------------------------------------- er_create_batch
  * A ragged batch of rods with per-rod element counts (north_star "er_create_batch").
- *  n_elems            HOST  [n_rods], each 1 <= n <= ER_MAX_ELEMS_PER_ROD.
+ *  n_elems            HOST  [n_rods], each 1 <= n <= ER_MAX_ELEMS_PER_ROD (rods longer than
+ *                     ER_TILE_MAX_ELEMS: no contact, tile_slots 256 or 512).
  *  material_per_rod   1: the seven material arrays have n_rods entries (one value per rod);
  *                     0: they have n_elems_total entries (one value per element).
  *  density            HOST  rho, volumetric mass density (kg/m^3) (reading DESIGN §3 #6).
@@ -91,7 +92,9 @@ typedef enum { ER_HOST = 0, ER_DEVICE = 1 } er_mem;
  *  tile_slots         rod-tile capacity (see the struct); fixes the device layout.
  * Errors: ER_EINVAL (all problems listed), ER_ENOMEM, ER_ECUDA.  *out is NULL on error.
  */
-#define ER_MAX_ELEMS_PER_ROD 511
+#define ER_MAX_ELEMS_PER_ROD 4095  /* rods up to 511 elements share rod tiles; longer ones are
+                                      advanced by a thread-block cluster of up to 16 CTAs */
+#define ER_TILE_MAX_ELEMS 511
 
 typedef struct {
   int32_t n_rods;

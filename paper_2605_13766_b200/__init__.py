@@ -27,7 +27,8 @@ ER_OPT_STEPS_PER_LAUNCH, ER_OPT_KERNEL, ER_OPT_PHASE_TIMING = 1, 2, 3
 ER_NDIAG = 12
 DIAG_NAMES = ("ke_trans", "ke_rot", "pe_shear", "pe_bend", "pe_grav", "pe_tip",
               "px", "py", "pz", "vmax", "mass", "n_elems")
-ER_MAX_ELEMS_PER_ROD = 511
+ER_MAX_ELEMS_PER_ROD = 4095
+ER_TILE_MAX_ELEMS = 511
 _STATUS = {0: "ER_OK", 1: "ER_EINVAL", 2: "ER_EUNSTABLE", 3: "ER_EIO", 4: "ER_ENOMEM", 5: "ER_ECUDA"}
 
 _dp = C.POINTER(C.c_double)

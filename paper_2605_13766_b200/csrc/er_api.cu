@@ -25,6 +25,7 @@
 
 extern "C" {
 cudaError_t er_launch_step(const ErStepParams *p, int block, int kind, int feat, cudaStream_t st);
+cudaError_t er_launch_long(const ErStepParams *p, int64_t tile0, int64_t n_rods, int nseg, cudaStream_t st);
 cudaError_t er_launch_diag(const ErStepParams *p, int block, double *out, cudaStream_t st);
 cudaError_t er_launch_canon_tiles(const ErStepParams *p, double *canon, int field, int to_tiles, cudaStream_t st);
 cudaError_t er_launch_aos_to_soa(const double *src, double *dst, int64_t n, int k, int64_t stride, cudaStream_t st);
@@ -87,7 +88,10 @@ struct er_batch {
   int64_t n_rods = 0, n_elems = 0, n_nodes = 0, n_vor = 0;
   int32_t max_n = 0;
   int block = 256;
-  int64_t n_tiles = 0;
+  int64_t n_tiles = 0;       // all tiles (layout conversion, diagnostics)
+  int64_t n_tiles_norm = 0;  // tiles of rods with <= 511 elements (the step kernels); long rods'
+  struct LongGroup { int64_t tile0, n_rods; int nseg; };  // segment tiles follow, by cluster size
+  std::vector<LongGroup> long_groups;
   double t = 0.0;
   int64_t steps_per_launch = 1;
   int kernel_mode = 0;
@@ -497,12 +501,14 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   if (err.count) { g_create_error = err.msg; return ER_EINVAL; }
 
   std::vector<int64_t> eoff((size_t)std::max<int64_t>(R, 0) + 1, 0);
-  int32_t max_n = 0;
+  int32_t max_n = 0;       // longest tile rod (<= ER_TILE_MAX_ELEMS elements)
+  int64_t n_long = 0;      // rods longer than that: segments of a thread-block cluster
   for (int64_t r = 0; r < R; ++r) {
     const int32_t n = d->n_elems[r];
     if (n < 1 || n > ER_MAX_ELEMS_PER_ROD) err.add("rod %lld: n_elems = %d outside [1, %d]", (long long)r, n, ER_MAX_ELEMS_PER_ROD);
     eoff[r + 1] = eoff[r] + std::max(n, 0);
-    max_n = std::max(max_n, n);
+    if (n > ER_TILE_MAX_ELEMS) ++n_long;
+    else max_n = std::max(max_n, n);
   }
   const int64_t E = eoff[R];
   const int64_t NN = E + R, NV = E - R;
@@ -531,6 +537,8 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
     err.add("tile_slots = %d not in {0, 128, 256, 512}", d->tile_slots);
   else if (d->tile_slots != 0 && max_n + 1 > d->tile_slots)
     err.add("tile_slots = %d < longest rod's %d slots", d->tile_slots, max_n + 1);
+  else if (d->tile_slots == 128 && n_long > 0)
+    err.add("tile_slots = 128 cannot be combined with rods longer than %d elements", ER_TILE_MAX_ELEMS);
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) err.add("no CUDA device available");
   else if (d->device < 0 || d->device >= ndev) err.add("device %d outside [0, %d)", d->device, ndev);
@@ -540,28 +548,37 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   er_batch *b = new er_batch();
   b->device = d->device;
   b->n_rods = R; b->n_elems = E; b->n_nodes = NN; b->n_vor = NV; b->max_n = max_n;
+  const int64_t Rn = R - n_long;  // tile rods come first in the packed order
   b->t = d->t0;
   b->block = d->tile_slots ? d->tile_slots : (max_n + 1 <= 256) ? 256 : 512;
-  if (!d->tile_slots && b->block == 256 && R > 0) {
+  int32_t min_n = max_n;
+  for (int64_t r = 0; r < R; ++r)
+    if (d->n_elems[r] <= ER_TILE_MAX_ELEMS) min_n = std::min(min_n, d->n_elems[r]);
+  if (!d->tile_slots && b->block == 256 && Rn > 0 && min_n == max_n) {
     // equal-length rods fill a tile with floor(B / (N+1)) of them (<= B/8): take 512-slot tiles
     // when that keeps clearly more lanes busy (65-slot rods: 76% at 256, 89% at 512)
-    int32_t min_n = max_n;
-    for (int64_t r = 0; r < R; ++r) min_n = std::min(min_n, d->n_elems[r]);
-    if (min_n == max_n) {
-      auto fill = [&](int B) { return (double)std::min<int>(B / (max_n + 1), B / 8) * (max_n + 1) / B; };
-      if (R * (int64_t)(max_n + 1) >= 4 * 512 && fill(512) > fill(256) + 0.05) b->block = 512;
-    }
+    auto fill = [&](int B) { return (double)std::min<int>(B / (max_n + 1), B / 8) * (max_n + 1) / B; };
+    if (Rn * (int64_t)(max_n + 1) >= 4 * 512 && fill(512) > fill(256) + 0.05) b->block = 512;
   }
   {
-    int32_t min_n = max_n;
-    for (int64_t r = 0; r < R; ++r) min_n = std::min(min_n, d->n_elems[r]);
-    b->identity = R <= 1 || min_n == max_n || std::getenv("ER_NO_PACK") != nullptr;
-    if (b->identity) {
-      b->ord.resize((size_t)R);
-      for (int64_t r = 0; r < R; ++r) b->ord[r] = (int32_t)r;
-    } else {
-      b->ord = pack_rods(d->n_elems, R, b->block, b->block / 8);
+    // packed order: tile rods (best-fit-decreasing when their lengths differ), then long rods by
+    // cluster size (so each size is one launch), canonical order within
+    std::vector<int32_t> tile_rods, long_rods;
+    for (int64_t r = 0; r < R; ++r) (d->n_elems[r] > ER_TILE_MAX_ELEMS ? long_rods : tile_rods).push_back((int32_t)r);
+    const bool pack = Rn > 1 && min_n != max_n && std::getenv("ER_NO_PACK") == nullptr;
+    if (pack) {
+      std::vector<int32_t> nt(tile_rods.size());
+      for (size_t q = 0; q < tile_rods.size(); ++q) nt[q] = d->n_elems[tile_rods[q]];
+      std::vector<int32_t> o = pack_rods(nt.data(), (int64_t)nt.size(), b->block, b->block / 8);
+      for (auto &x : o) x = tile_rods[x];
+      tile_rods = o;
     }
+    auto nseg = [&](int32_t r) { return (d->n_elems[r] + ER_LONG_SEG) / ER_LONG_SEG; };  // ceil((N+1)/S)
+    std::stable_sort(long_rods.begin(), long_rods.end(), [&](int32_t a, int32_t c) { return nseg(a) < nseg(c); });
+    b->ord = tile_rods;
+    b->ord.insert(b->ord.end(), long_rods.begin(), long_rods.end());
+    b->identity = true;
+    for (int64_t r = 0; r < R; ++r) b->identity = b->identity && b->ord[r] == r;
   }
   b->eoffc = eoff;
   b->n_elems_h.resize((size_t)R);
@@ -709,7 +726,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   std::vector<ErTile> tiles;
   {
     int64_t r = 0, boff = 0;
-    while (r < R) {
+    while (r < Rn) {
       ErTile T;
       T.r0 = (int32_t)r;
       T.nbase = eoffp[r] + r;
@@ -717,7 +734,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
       T.boff = boff;
       int64_t used = 0;
       int32_t nr = 0;
-      while (r < R && nr < b->block / 8 && used + b->n_elems_h[r] + 1 <= b->block) {
+      while (r < Rn && nr < b->block / 8 && used + b->n_elems_h[r] + 1 <= b->block) {
         used += b->n_elems_h[r] + 1;
         ++nr;
         ++r;
@@ -727,15 +744,42 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
       T.nel = (int32_t)(eoffp[r] - eoffp[T.r0]);
       std::memset(T.smask, 0, sizeof T.smask);
       std::memset(T.pfx, 0, sizeof T.pfx);
-      T.pad_ = 0;
+      T.seg = 0;
+      T.nseg = 1;
       for (int32_t q = 0, st = 0; q < nr; ++q) {
         T.smask[st >> 5] |= 1u << (st & 31);
         st += b->n_elems_h[T.r0 + q] + 1;
       }
       for (int wd = 1; wd < 16; ++wd) T.pfx[wd] = (uint8_t)(T.pfx[wd - 1] + __builtin_popcount(T.smask[wd - 1]));
-      int64_t sz = 6 * (int64_t)T.nslots + 12 * (int64_t)T.nel + (b->has_kappa0 ? 3 * (int64_t)(T.nel - T.nr) : 0);
-      boff += (sz + 1) & ~1ll;
+      boff += tile_block_size(T, b->has_kappa0);
       tiles.push_back(T);
+    }
+    b->n_tiles_norm = (int64_t)tiles.size();
+    // long rods: ceil((N+1)/S) segment tiles of S slots each (the last one shorter)
+    for (; r < R; ++r) {
+      const int32_t N = b->n_elems_h[r], K = (N + ER_LONG_SEG) / ER_LONG_SEG;
+      if (b->long_groups.empty() || b->long_groups.back().nseg != K)
+        b->long_groups.push_back({(int64_t)tiles.size(), 0, K});
+      b->long_groups.back().n_rods += 1;
+      for (int32_t k = 0; k < K; ++k) {
+        ErTile T;
+        const int32_t k0 = k * ER_LONG_SEG;
+        T.r0 = (int32_t)r;
+        T.nr = 1;
+        T.nslots = std::min(ER_LONG_SEG, N + 1 - k0);
+        T.nel = std::max(0, std::min(ER_LONG_SEG, N - k0));
+        T.nbase = eoffp[r] + r + k0;
+        T.ebase = eoffp[r] + k0;
+        T.boff = boff;
+        std::memset(T.smask, 0, sizeof T.smask);
+        std::memset(T.pfx, 0, sizeof T.pfx);
+        T.smask[0] = 1u;  // one rod, starting at slot 0 (slot s is node k0 + s of the rod)
+        for (int wd = 1; wd < 16; ++wd) T.pfx[wd] = 1;
+        T.seg = k;
+        T.nseg = K;
+        boff += tile_block_size(T, b->has_kappa0);
+        tiles.push_back(T);
+      }
     }
     b->state_doubles = boff;
   }
@@ -971,9 +1015,23 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
   CK(cudaMemcpyAsync(b->d_fault, init, sizeof init, cudaMemcpyHostToDevice, b->stream), "H2D fault");
   ErStepParams p = params_of(b);
   p.h = dt;
+  p.n_tiles = b->n_tiles_norm;  // long rods: er_launch_long below
   int64_t done = 0;
   double t = b->t;
   const int feat = feat_of(b);
+  // long rods advance k steps from time t (all step kinds give the same trajectory)
+  auto launch_long = [&](int64_t k, double t0) -> cudaError_t {
+    ErStepParams q = p;
+    q.n_tiles = b->n_tiles;
+    q.n_steps = (int32_t)k;
+    q.t = t0;
+    for (const auto &g : b->long_groups) {
+      cudaError_t e = er_launch_long(&q, g.tile0, g.n_rods, g.nseg, b->stream);
+      if (e != cudaSuccess) return e;
+      b->launches += 1;
+    }
+    return cudaSuccess;
+  };
   if (b->kernel_mode == 3) {  // memory-pipeline probe: n_steps passes of load + store, no physics
     p.n_steps = 0;
     p.t = t;
@@ -1046,6 +1104,7 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
          "step kernel");
       b->launches += 1;
       interval(b, m0, mark(b), 0);
+      CK(launch_long(k, t), "long-rod kernel");
       for (int64_t q = 0; q < k; ++q) { const double th = t + 0.5 * dt; t = th + 0.5 * dt; }
       done += k;
     } else {  // staged ablation: drift | dynamics + kick | drift, state through HBM between stages
@@ -1055,6 +1114,7 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
       CK(er_launch_step(&p, b->block, 2, 7, b->stream), "dyn kernel");
       CK(er_launch_step(&p, b->block, 1, 7, b->stream), "drift kernel");
       b->launches += 3;
+      CK(launch_long(1, t), "long-rod kernel");
       const double th = t + 0.5 * dt;
       t = th + 0.5 * dt;
       done += 1;
@@ -1111,6 +1171,7 @@ er_status er_set_contact(er_batch *b, const er_contact *c) {
     for (int64_t r = 0; r < R; ++r)
       if (!pos_finite(c->radius[r])) { err.add("radius[%lld] = %g must be positive and finite", (long long)r, c->radius[r]); break; }
   if (E >= (1ll << 30)) err.add("contact supports < 2^30 elements per batch (got %lld)", (long long)E);
+  if (!b->long_groups.empty()) err.add("contact does not support rods longer than %d elements", ER_TILE_MAX_ELEMS);
   if (err.count) { b->last_error = err.msg; return ER_EINVAL; }
   CK(cudaSetDevice(b->device), "cudaSetDevice");
   CK(cudaStreamSynchronize(b->stream), "sync");

@@ -27,6 +27,7 @@
 //  simple_kernel    : one tile per CTA, plain loads; MODE_FUSED (ablation), MODE_DRIFT /
 //                     MODE_DYN (the staged three-launch path).
 //  diag_kernel      : per-tile partial sums of the energy functional, deterministic.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -104,12 +105,17 @@ __device__ __forceinline__ int rec_flags(const double *rec) {
 // smem exchange area (XPLANES planes of stride BLOCK); rec points at the rod record (smem in
 // the persistent kernel, global in the simple one).  k0s: static rest curvature of the slot's
 // Voronoi domain (FEAT_KAPPA0).
-template <int BLOCK, int FEAT, bool DRIFT1, bool DYN, bool DRIFT2>
+// Exchange barrier of one CTA (tiles); long rods pass a cluster-wide one that also fills the halos.
+struct CtaSync {
+  __device__ __forceinline__ void operator()(int) const { __syncthreads(); }
+};
+
+template <int BLOCK, int FEAT, bool DRIFT1, bool DYN, bool DRIFT2, int XS = BLOCK, class XSync = CtaSync>
 __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restrict__ X,
                                           const double *__restrict__ rec, const SlotInfo &si,
                                           double r[3], double v[3], double Q[9], double w[3],
                                           const double k0s[3], double &t, unsigned &fbits,
-                                          const double *fcon = nullptr) {
+                                          const double *fcon = nullptr, XSync xsync = XSync()) {
   constexpr bool GEN = (FEAT & FEAT_GENERAL) != 0;
   constexpr bool EXTRA = (FEAT & FEAT_EXTRA) != 0;
   constexpr bool ACT = (FEAT & (FEAT_EXTRA | FEAT_ACT)) != 0;
@@ -131,11 +137,11 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
     // ---- exchange A
     if (si.active) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) { X[(XR + c) * BLOCK + s] = r[c]; X[(XV + c) * BLOCK + s] = v[c]; }
+      for (int c = 0; c < 3; ++c) { X[(XR + c) * XS + s] = r[c]; X[(XV + c) * XS + s] = v[c]; }
 #pragma unroll
-      for (int c = 0; c < 9; ++c) X[(XQ + c) * BLOCK + s] = Q[c];
+      for (int c = 0; c < 9; ++c) X[(XQ + c) * XS + s] = Q[c];
     }
-    __syncthreads();
+    xsync(0);
 
     // ---- A4-A5 edge i: kinematics, shear/stretch strain, stress
     double Ql[3] = {0.0, 0.0, 0.0}, nb[3] = {0.0, 0.0, 0.0}, n[3] = {0.0, 0.0, 0.0};
@@ -146,8 +152,8 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
       double ell[3], dv[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        ell[c] = X[(XR + c) * BLOCK + s + 1] - r[c];
-        dv[c] = X[(XV + c) * BLOCK + s + 1] - v[c];
+        ell[c] = X[(XR + c) * XS + s + 1] - r[c];
+        dv[c] = X[(XV + c) * XS + s + 1] - v[c];
       }
       const double l2 = dot3(ell, ell);
       const double il = rsqrt_fast(l2);
@@ -177,17 +183,17 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
     if (si.has_v) {
       double Qp[9], cth, s2;
 #pragma unroll
-      for (int c = 0; c < 9; ++c) Qp[c] = X[(XQ + c) * BLOCK + s - 1];
+      for (int c = 0; c < 9; ++c) Qp[c] = X[(XQ + c) * XS + s - 1];
       logrot_pair(Q, Qp, kap, cth, s2);
       if (cth < 0.0 && s2 <= 1e-12 * cth * cth) fbits |= 4u;  // ER_F_ANTIPODAL: theta >= pi - 1e-6
     }
     // ---- exchange B
     if (si.has_e) {
-      X[XL * BLOCK + s] = l;
+      X[XL * XS + s] = l;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) X[(XN + c) * BLOCK + s] = n[c];
+      for (int c = 0; c < 3; ++c) X[(XN + c) * XS + s] = n[c];
     }
-    __syncthreads();
+    xsync(1);
 
     // ---- A6 bending moment and its averaged cross term
     double mb[3] = {0.0, 0.0, 0.0}, be[3] = {0.0, 0.0, 0.0};
@@ -196,7 +202,7 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
       const double iDh = general ? 1.0 / Dh : rec[REC_ILHAT];
 #pragma unroll
       for (int c = 0; c < 3; ++c) kap[c] *= iDh;
-      const double D = 0.5 * (X[XL * BLOCK + s - 1] + l);
+      const double D = 0.5 * (X[XL * XS + s - 1] + l);
       const double ieps = Dh * rcp_fast(D);
       const double ieps3 = ieps * ieps * ieps;
       double k0[3] = {k0s[0], k0s[1], k0s[2]};
@@ -234,7 +240,7 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
     if (si.active) {
       double F[3];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) F[c] = n[c] - (i >= 1 ? X[(XN + c) * BLOCK + s - 1] : 0.0);
+      for (int c = 0; c < 3; ++c) F[c] = n[c] - (i >= 1 ? X[(XN + c) * XS + s - 1] : 0.0);
       if ((si.fl & FL_TIP) && i == ((si.fl & FL_CLAMP_MASK) == 2 ? 0 : N)) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) F[c] += rec[REC_TIPX + c];
@@ -254,16 +260,16 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
     // ---- exchange C (aliases A; every A read happened before the B barrier)
     if (si.active) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) { X[(XM + c) * BLOCK + s] = mb[c]; X[(XB + c) * BLOCK + s] = be[c]; }
+      for (int c = 0; c < 3; ++c) { X[(XM + c) * XS + s] = mb[c]; X[(XB + c) * XS + s] = be[c]; }
     }
-    __syncthreads();
+    xsync(2);
 
     // ---- A8 + A9 element couple, angular acceleration, kick
     if (si.has_e) {
       double C[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c)
-        C[c] = (X[(XM + c) * BLOCK + s + 1] - mb[c]) + 0.5 * (X[(XB + c) * BLOCK + s + 1] + be[c]);
+        C[c] = (X[(XM + c) * XS + s + 1] - mb[c]) + 0.5 * (X[(XB + c) * XS + s + 1] + be[c]);
       C[0] += Ql[1] * nb[2] - Ql[2] * nb[1];  // shear torque lhat (Q t) x S(sigma - sigma0) == (Q l) x nbar
       C[1] += Ql[2] * nb[0] - Ql[0] * nb[2];
       C[2] += Ql[0] * nb[1] - Ql[1] * nb[0];
@@ -508,7 +514,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
 #pragma unroll
     for (int c = 0; c < 3; ++c) w[c] = si.has_e ? B[6 * ns + (9 + c) * nel + le] : 0.0;
     if ((FEAT & FEAT_KAPPA0) && si.has_v) {
-      const int nvor = nel - T.nr;
+      const int nvor = tile_nvor(T);
 #pragma unroll
       for (int c = 0; c < 3; ++c) k0s[c] = B[6 * ns + 12 * nel + c * nvor + (tid - 2 * lo - 1)];
     }
@@ -685,6 +691,102 @@ __global__ void __launch_bounds__(BLOCK, MINB) simple_kernel(const ErStepParams 
   report_fault(p, fbits, si.active ? (int)rec[REC_CANON] : 0);  // canonical rod id
 }
 
+// ------------------------------------------------------------------------------------------
+// Long rods (more than 511 elements): the rod's nseg segments of ER_LONG_SEG slots are the CTAs
+// of one thread-block cluster.  The step is step_body with an exchange area that has a halo
+// slot on each side; at every exchange barrier the boundary slots also write their values into
+// the neighbouring segments' halos through distributed shared memory, then the whole cluster
+// synchronises (barrier.cluster, release / acquire).  Plain coalesced loads / stores.
+namespace cgx = cooperative_groups;
+
+template <int BLOCK, int XS>
+struct ClusterSync {
+  double *X;  // this CTA's exchange area: plane c at X[c * XS + s], halos at s = -1 and s = BLOCK
+  int s, nslots, seg, nseg;
+  __device__ __forceinline__ void operator()(int phase) const {
+    cgx::cluster_group cl = cgx::this_cluster();
+    const int p0 = phase == 1 ? XL : 0, np = phase == 0 ? 15 : phase == 1 ? 4 : 6;
+    if (s == 0 && seg > 0) {  // my first slot -> the previous segment's right halo
+      double *R = cl.map_shared_rank(X, seg - 1);
+      for (int c = 0; c < np; ++c) R[(p0 + c) * XS + BLOCK] = X[(p0 + c) * XS];
+    }
+    if (s == nslots - 1 && seg < nseg - 1) {  // my last slot -> the next segment's left halo
+      double *L = cl.map_shared_rank(X, seg + 1);
+      for (int c = 0; c < np; ++c) L[(p0 + c) * XS - 1] = X[(p0 + c) * XS + s];
+    }
+    cl.sync();
+  }
+};
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) long_kernel(const ErStepParams p, int64_t tile0) {
+  constexpr int FEAT = FEAT_GENERAL | FEAT_KAPPA0 | FEAT_EXTRA;
+  constexpr int XS = BLOCK + 2;
+  extern __shared__ __align__(16) double sm[];
+  double *X = sm + 1;
+  cgx::cluster_group cl = cgx::this_cluster();
+  const ErTile T = p.tiles[tile0 + blockIdx.x];
+  const int s = threadIdx.x;
+  SlotInfo si;
+  si.s = s;
+  si.q = 0;
+  si.rod = T.r0;
+  si.N = (int)(p.eoff[T.r0 + 1] - p.eoff[T.r0]);
+  si.i = T.seg * BLOCK + s;
+  si.active = s < T.nslots;
+  si.node = T.nbase + s;
+  si.elem = T.ebase + s;
+  si.vor = si.elem - si.rod - 1;
+  const double *rec = p.rec + (int64_t)si.rod * ER_REC;
+  si.fl = si.active ? rec_flags(rec) : 0;
+  finish_slot(si);
+  double r[3] = {0, 0, 0}, v[3] = {0, 0, 0}, Q[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, w[3] = {0, 0, 0};
+  double k0s[3] = {0.0, 0.0, 0.0};
+  double *G = p.state + T.boff;
+  const int ns = T.nslots, nel = T.nel;
+  if (si.active) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      r[c] = __ldcs(G + c * ns + s);
+      v[c] = __ldcs(G + (3 + c) * ns + s);
+    }
+  }
+  if (si.has_e) {
+#pragma unroll
+    for (int c = 0; c < 9; ++c) Q[c] = __ldcs(G + 6 * ns + c * nel + s);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) w[c] = __ldcs(G + 6 * ns + (9 + c) * nel + s);
+  }
+  if (p.has_kappa0 && si.has_v) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) k0s[c] = __ldg(G + tile_vor_plane(T, c) + (s - (T.seg == 0 ? 1 : 0)));
+  }
+  cl.sync();  // every segment of the cluster is resident before any distributed-smem access
+  const ClusterSync<BLOCK, XS> xs{X, s, T.nslots, T.seg, T.nseg};
+  double t = p.t;
+  unsigned fbits = 0;
+  for (int st = 0; st < p.n_steps; ++st) {
+    step_body<BLOCK, FEAT, true, true, true, XS, ClusterSync<BLOCK, XS>>(p, X, rec, si, r, v, Q, w, k0s, t, fbits,
+                                                                        nullptr, xs);
+    if (st + 1 < p.n_steps) cl.sync();  // the next step's exchange A re-uses these planes
+  }
+  if (si.active) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      __stcs(G + c * ns + s, r[c]);
+      __stcs(G + (3 + c) * ns + s, v[c]);
+    }
+  }
+  if (si.has_e) {
+#pragma unroll
+    for (int c = 0; c < 9; ++c) __stcs(G + 6 * ns + c * nel + s, Q[c]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) __stcs(G + 6 * ns + (9 + c) * nel + s, w[c]);
+  }
+  report_fault(p, fbits, si.active ? (int)rec[REC_CANON] : 0);
+  cl.sync();  // no CTA leaves while a neighbour may still access its shared memory
+}
+
 // --------------------------------------------------------------------------- diagnostics
 // Per-tile partial sums of the energy functional at time p.t; deterministic.
 template <int BLOCK>
@@ -733,7 +835,12 @@ __global__ void __launch_bounds__(BLOCK) diag_kernel(const ErStepParams p) {
     const double lh = general ? gp(GP_LHAT) : rec[REC_LHAT];
     const double ilh = general ? gp(GP_ILHAT) : rec[REC_ILHAT];
     double ell[3];
-    for (int c = 0; c < 3; ++c) ell[c] = xr[c * BLOCK + s + 1] - r[c];
+    if (s + 1 == T.nslots && T.seg + 1 < T.nseg) {  // long rod: next node is slot 0 of the next segment
+      const ErTile Tn = p.tiles[blockIdx.x + 1];
+      for (int c = 0; c < 3; ++c) ell[c] = p.state[Tn.boff + c * Tn.nslots] - r[c];
+    } else {
+      for (int c = 0; c < 3; ++c) ell[c] = xr[c * BLOCK + s + 1] - r[c];
+    }
     const double l = sqrt(dot3(ell, ell));
     const double e = l * ilh;
     double sg[3] = {dot3(Q, ell) * ilh, dot3(Q + 3, ell) * ilh, dot3(Q + 6, ell) * ilh - 1.0};
@@ -749,11 +856,17 @@ __global__ void __launch_bounds__(BLOCK) diag_kernel(const ErStepParams p) {
   }
   if (si.has_v) {
     double Qp[9], kap[3], cth, s2;
-    for (int c = 0; c < 9; ++c) Qp[c] = xQ[c * BLOCK + s - 1];
+    if (s == 0) {  // long rod segment: previous element is the last of the previous segment
+      const ErTile Tp = p.tiles[blockIdx.x - 1];
+      for (int c = 0; c < 9; ++c) Qp[c] = p.state[Tp.boff + 6 * Tp.nslots + c * Tp.nel + Tp.nel - 1];
+    } else {
+      for (int c = 0; c < 9; ++c) Qp[c] = xQ[c * BLOCK + s - 1];
+    }
     logrot_pair(Q, Qp, kap, cth, s2);
     const double Dh = general ? gp(GP_DH) : rec[REC_LHAT];
     double k0[3] = {0, 0, 0};
-    if (p.has_kappa0) for (int c = 0; c < 3; ++c) k0[c] = G[tile_vor_plane(T, c) + (s - 2 * si.q - 1)];
+    const int lv = T.nseg > 1 ? s - (T.seg == 0 ? 1 : 0) : s - 2 * si.q - 1;  // local Voronoi index
+    if (p.has_kappa0) for (int c = 0; c < 3; ++c) k0[c] = G[tile_vor_plane(T, c) + lv];
     if (si.fl & FL_ACT) {
       const double sk = general ? gp(GP_SK) : i * rec[REC_LHAT];
       const double act = rec[REC_ACTA] * sinpi(2.0 * (sk * rec[REC_ACTIL] - rec[REC_ACTF] * p.t));
@@ -827,14 +940,20 @@ __global__ void canon_tiles(const ErStepParams p, double *canon, int field, int 
   } else if (field <= FIELD_OMEGA) {
     count = T.nel; off = tile_elem_plane(T, field == FIELD_OMEGA ? 9 : 0); shift = 0;
   } else {
-    count = T.nel - T.nr; off = tile_vor_plane(T, 0); shift = -1;
+    count = tile_nvor(T); off = tile_vor_plane(T, 0); shift = -1;
   }
   double *blk = p.state + T.boff + off;
   for (int q = 0; q < T.nr; ++q) {
     const int64_t pr = T.r0 + q, cr = p.ord[pr];
-    const int64_t n = p.eoff[pr + 1] - p.eoff[pr] + shift;                     // rows of this rod
-    const int64_t loc = p.eoff[pr] - T.ebase + (int64_t)q * shift;            // first row in the tile
-    const int64_t can = p.eoffc[cr] + cr * shift;                              // first canonical row
+    int64_t n = p.eoff[pr + 1] - p.eoff[pr] + shift;                           // rows of this rod
+    int64_t loc = p.eoff[pr] - T.ebase + (int64_t)q * shift;                  // first row in the tile
+    int64_t can = p.eoffc[cr] + cr * shift;                                    // first canonical row
+    if (T.nseg > 1) {  // long rod: this segment's rows only
+      const int64_t k0 = (int64_t)T.seg * ER_LONG_SEG;
+      n = count;
+      loc = 0;
+      can += shift < 0 ? (T.seg == 0 ? 0 : k0 - 1) : k0;
+    }
     for (int64_t x = threadIdx.x; x < n * k; x += blockDim.x) {
       const int64_t u = x / k;
       const int c = (int)(x - u * k);
@@ -977,6 +1096,32 @@ cudaError_t er_launch_step(const ErStepParams *p, int block, int kind, int feat,
   if (kind == 1) return launch_simple<512, 1, er::MODE_DRIFT>(*p, st);
   if (kind == 2) return launch_simple<512, 1, er::MODE_DYN>(*p, st);
   return launch_simple<512, 1, er::MODE_FUSED>(*p, st);
+}
+
+// Long rods: `n_rods` rods of `nseg` segments each, tiles [tile0, tile0 + n_rods * nseg), one
+// cluster of nseg CTAs per rod.
+cudaError_t er_launch_long(const ErStepParams *p, int64_t tile0, int64_t n_rods, int nseg, cudaStream_t st) {
+  if (n_rods <= 0) return cudaSuccess;
+  constexpr int B = ER_LONG_SEG;
+  auto k = er::long_kernel<B>;
+  const size_t sm = (size_t)er::XPLANES * (B + 2) * 8 + 16;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e == cudaSuccess && nseg > 8) e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(n_rods * nseg), 1, 1);
+  cfg.blockDim = dim3(B, 1, 1);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)nseg;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, k, *p, tile0);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t er_launch_diag(const ErStepParams *p, int block, double *out, cudaStream_t st) {

@@ -95,8 +95,11 @@ struct __align__(16) ErTile {
   int64_t boff;    // offset of the tile's state block (doubles, even)
   uint32_t smask[16];
   uint8_t pfx[16];
-  int64_t pad_;
+  int32_t seg;     // long rods (> 511 elements): segment k of the rod's nseg tiles of
+  int32_t nseg;    //   ER_LONG_SEG slots each, advanced by a thread-block cluster; else 0 / 1
 };
+#define ER_LONG_SEG 256     // slots per segment of a long rod (one CTA of the cluster)
+#define ER_LONG_MAXSEG 16   // cluster size limit (non-portable 16 on sm_100a): N + 1 <= 4096
 
 // Contact law (DESIGN §3 #27): penalty normal force with damping, regularised
 // Coulomb friction, optional half-space n.x >= d.
@@ -205,11 +208,14 @@ __host__ __device__ inline int64_t tile_node_plane(const ErTile &T, int c) { ret
 __host__ __device__ inline int64_t tile_elem_plane(const ErTile &T, int c) {
   return 6 * (int64_t)T.nslots + (int64_t)c * T.nel;
 }
+// Voronoi domains of a tile: one per element except each rod's first (a long rod's first
+// element is in its segment 0)
+__host__ __device__ inline int32_t tile_nvor(const ErTile &T) { return T.nel - (T.seg == 0 ? T.nr : 0); }
 __host__ __device__ inline int64_t tile_vor_plane(const ErTile &T, int c) {
-  return 6 * (int64_t)T.nslots + 12 * (int64_t)T.nel + (int64_t)c * (T.nel - T.nr);
+  return 6 * (int64_t)T.nslots + 12 * (int64_t)T.nel + (int64_t)c * tile_nvor(T);
 }
 __host__ __device__ inline int64_t tile_block_size(const ErTile &T, int has_kappa0) {
-  const int64_t sz = 6 * (int64_t)T.nslots + 12 * (int64_t)T.nel + (has_kappa0 ? 3 * (int64_t)(T.nel - T.nr) : 0);
+  const int64_t sz = 6 * (int64_t)T.nslots + 12 * (int64_t)T.nel + (has_kappa0 ? 3 * (int64_t)tile_nvor(T) : 0);
   return (sz + 1) & ~1ll;
 }
 static_assert(sizeof(ErTile) == 128, "ErTile must stay 128 bytes (bulk-copied)");

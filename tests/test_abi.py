@@ -75,7 +75,7 @@ int main(void) {
 def test_host_validation_collects_all_errors(er):
     """Pure host-side validation (runs before any device work): every problem is listed."""
     d = er.er_batch_desc()
-    n = np.array([3, 0, 600], np.int32)
+    n = np.array([3, 0, 5000], np.int32)
     mat = np.array([1.0, -2.0, 1.0])
     d.n_rods = 3
     d.n_elems = n.ctypes.data_as(C.POINTER(C.c_int32))
@@ -87,7 +87,7 @@ def test_host_validation_collects_all_errors(er):
         er.er_create_batch(d)
     msg = str(ei.value)
     assert ei.value.status == er.ER_EINVAL
-    assert "rod 1: n_elems = 0" in msg and "rod 2: n_elems = 600" in msg
+    assert "rod 1: n_elems = 0" in msg and "rod 2: n_elems = 5000" in msg
 
 
 def test_null_arguments_are_rejected(er):
