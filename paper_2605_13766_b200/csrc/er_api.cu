@@ -25,7 +25,7 @@
 
 extern "C" {
 cudaError_t er_launch_step(const ErStepParams *p, int block, int kind, int feat, cudaStream_t st);
-cudaError_t er_launch_long(const ErStepParams *p, int64_t tile0, int64_t n_rods, int nseg, cudaStream_t st);
+cudaError_t er_launch_long(const ErStepParams *p, int64_t tile0, int64_t n_rods, int nseg, int feat, cudaStream_t st);
 cudaError_t er_launch_diag(const ErStepParams *p, int block, double *out, cudaStream_t st);
 cudaError_t er_launch_canon_tiles(const ErStepParams *p, double *canon, int field, int to_tiles, cudaStream_t st);
 cudaError_t er_launch_aos_to_soa(const double *src, double *dst, int64_t n, int k, int64_t stride, cudaStream_t st);
@@ -1026,7 +1026,7 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
     q.n_steps = (int32_t)k;
     q.t = t0;
     for (const auto &g : b->long_groups) {
-      cudaError_t e = er_launch_long(&q, g.tile0, g.n_rods, g.nseg, b->stream);
+      cudaError_t e = er_launch_long(&q, g.tile0, g.n_rods, g.nseg, feat, b->stream);
       if (e != cudaSuccess) return e;
       b->launches += 1;
     }

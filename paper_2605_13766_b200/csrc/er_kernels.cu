@@ -718,9 +718,11 @@ struct ClusterSync {
   }
 };
 
-template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) long_kernel(const ErStepParams p, int64_t tile0) {
-  constexpr int FEAT = FEAT_GENERAL | FEAT_KAPPA0 | FEAT_EXTRA;
+#ifndef ER_LONG_MINB
+#define ER_LONG_MINB 2
+#endif
+template <int BLOCK, int FEAT>
+__global__ void __launch_bounds__(BLOCK, ER_LONG_MINB) long_kernel(const ErStepParams p, int64_t tile0) {
   constexpr int XS = BLOCK + 2;
   extern __shared__ __align__(16) double sm[];
   double *X = sm + 1;
@@ -1100,10 +1102,11 @@ cudaError_t er_launch_step(const ErStepParams *p, int block, int kind, int feat,
 
 // Long rods: `n_rods` rods of `nseg` segments each, tiles [tile0, tile0 + n_rods * nseg), one
 // cluster of nseg CTAs per rod.
-cudaError_t er_launch_long(const ErStepParams *p, int64_t tile0, int64_t n_rods, int nseg, cudaStream_t st) {
+cudaError_t er_launch_long(const ErStepParams *p, int64_t tile0, int64_t n_rods, int nseg, int feat, cudaStream_t st) {
   if (n_rods <= 0) return cudaSuccess;
   constexpr int B = ER_LONG_SEG;
-  auto k = er::long_kernel<B>;
+  // plain rods get the lean instantiation; any feature takes the general one
+  auto k = feat == 0 ? er::long_kernel<B, 0> : er::long_kernel<B, FEAT_GENERAL | FEAT_KAPPA0 | FEAT_EXTRA>;
   const size_t sm = (size_t)er::XPLANES * (B + 2) * 8 + 16;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e == cudaSuccess && nseg > 8) e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
