@@ -11,7 +11,8 @@
  * discretised on N+1 nodes / N elements / N-1 Voronoi domains per rod and advanced by
  * position Verlet, drift(h/2) - kick(h) - drift(h/2), with kinematic constraints after
  * every stage.  The discrete readings are DESIGN.md §3 (= SURVEY.md §8 C.3-C.4).
- * Rods do not interact: every rod of a batch is advanced independently.
+ * Rods do not interact (every rod of a batch is advanced independently) unless contact is
+ * enabled with er_set_contact.
  *
  * Conventions shared by every call
  *  - fp64 throughout.  Lab-frame vectors: positions, velocities, tip forces, gravity, b(t).
