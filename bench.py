@@ -204,8 +204,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # ER_BENCH_SHARE_GPU=1: functional test of the multi-rank path on a one-GPU box (ranks share
+    # GPU 0 and reduce over gloo) -- never a measurement
+    share = os.environ.get("ER_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % torch.cuda.device_count()
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     import paper_2605_13766_b200 as er
 
