@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--no-temporal", action="store_true")
     ap.add_argument("--no-contact", action="store_true")
     ap.add_argument("--cpu-sample-rods", type=int, default=8192)
-    ap.add_argument("--cpu-sample-steps", type=int, default=300)
+    ap.add_argument("--cpu-sample-steps", type=int, default=400)
     return ap.parse_args()
 
 
