@@ -31,6 +31,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "er_layout.h"
 #include "er_math.cuh"
 
@@ -391,14 +394,15 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 // Stage geometry of the persistent kernel: per buffer the tile's state block (<= 18 or 21
 // planes of <= BLOCK doubles; the exchange area of XPLANES x BLOCK reuses it), then the rod
 // records (RMAX x ER_REC) and the tile's element offsets (RMAX + 4 int64).
-template <int BLOCK, int FEAT>
+template <int BLOCK, int FEAT, bool LONG = false>
 struct Stage {
   static constexpr int NPL = (FEAT & FEAT_KAPPA0) ? 21 : 18;
   static constexpr int RMAX = BLOCK / 8;
+  static constexpr int XS = LONG ? BLOCK + 2 : BLOCK;  // exchange plane stride (long rods: halos)
   // the results of a tile are written at OUTOFF (clear of the exchange-C planes 0-5, which other
   // warps may still read) and bulk-stored from there
-  static constexpr int OUTOFF = 6 * BLOCK;
-  static constexpr int PLANES = 24 * BLOCK + 8;
+  static constexpr int OUTOFF = 6 * XS;
+  static constexpr int PLANES = 24 * XS + 8;
   static constexpr int RECOFF = PLANES;
   static constexpr int EOFF = RECOFF + RMAX * ER_REC;
   static constexpr int TOFF = EOFF + RMAX + 4;   // staged ErTile (16 doubles)
@@ -411,22 +415,23 @@ struct Stage {
 // block, its rod records and its element offsets -- three TMA 1-D bulk copies.
 struct TileHead {  // the descriptor fields the issuing thread needs
   int64_t boff;
-  int32_t r0, nr, nslots, nel;
+  int32_t r0, nr, nslots, nel, nvor;
 };
 __device__ __forceinline__ TileHead load_head(const ErTile *t) {
   TileHead h;
   h.boff = __ldg(&t->boff);
   const int4 v = __ldg(reinterpret_cast<const int4 *>(&t->r0));
   h.r0 = v.x; h.nr = v.y; h.nslots = v.z; h.nel = v.w;
+  h.nvor = h.nel - (__ldg(&t->seg) == 0 ? h.nr : 0);  // see tile_nvor
   return h;
 }
 
-template <int BLOCK, int FEAT>
+template <int BLOCK, int FEAT, bool LONG = false>
 __device__ __forceinline__ void issue_tile(const ErStepParams &p, const TileHead &T, const ErTile *tile_ptr, double *B,
                                            uint64_t *bar) {
-  using SG = Stage<BLOCK, FEAT>;
+  using SG = Stage<BLOCK, FEAT, LONG>;
   const int64_t sz = 6 * (int64_t)T.nslots + 12 * (int64_t)T.nel +
-                     (((FEAT & FEAT_KAPPA0) && p.has_kappa0) ? 3 * (int64_t)(T.nel - T.nr) : 0);
+                     (((FEAT & FEAT_KAPPA0) && p.has_kappa0) ? 3 * (int64_t)T.nvor : 0);
   const uint32_t cs = (uint32_t)((sz + 1) & ~1ll);
   const int64_t ra = T.r0 & ~1ll;
   const uint32_t ceo = (uint32_t)(((T.r0 + T.nr + 2) & ~1ll) - ra);
@@ -789,6 +794,114 @@ __global__ void __launch_bounds__(BLOCK, ER_LONG_MINB) long_kernel(const ErStepP
   cl.sync();  // no CTA leaves while a neighbour may still access its shared memory
 }
 
+// Persistent long-rod kernel: clusters of K CTAs walk the group's rods (one segment tile per CTA)
+// with the tile kernel's TMA double-buffered pipeline; a cluster barrier replaces the stage
+// barrier (a neighbour's halo writes land in this CTA's stage area).
+template <int BLOCK, int FEAT>
+__global__ void __launch_bounds__(BLOCK, 2) long_persistent(const ErStepParams p, int64_t tile0, int64_t n_rods) {
+  using SG = Stage<BLOCK, FEAT, true>;
+  constexpr int XS = SG::XS;
+  extern __shared__ __align__(16) double sm[];
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sm + 2 * SG::BUFD);
+  cgx::cluster_group cl = cgx::this_cluster();
+  const int tid = threadIdx.x;
+  const int K = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  const int64_t ncl = gridDim.x / K;
+  auto tile_of = [&](int64_t rr) { return tile0 + rr * K + rank; };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  int64_t rod = blockIdx.x / K;
+  if (tid == 0 && rod < n_rods)
+    issue_tile<BLOCK, FEAT, true>(p, load_head(p.tiles + tile_of(rod)), p.tiles + tile_of(rod), sm, &bar[0]);
+  cl.sync();  // every CTA of the cluster resident before any distributed-smem access
+  uint32_t phase = 0;
+  unsigned fbits_all = 0;
+  int frod = 0x7fffffff;
+  for (int k = 0; rod < n_rods; rod += ncl, ++k) {
+    const int b = k & 1;
+    double *B = sm + b * SG::BUFD;
+    const int64_t rnext = rod + ncl;
+    TileHead Tn;
+    if (tid == 0 && rnext < n_rods) Tn = load_head(p.tiles + tile_of(rnext));
+    mbar_wait(&bar[b], (phase >> b) & 1u);
+    phase ^= 1u << b;
+    const ErTile &T = *reinterpret_cast<const ErTile *>(B + SG::TOFF);
+    const int64_t *eo = reinterpret_cast<const int64_t *>(B + SG::EOFF) + (T.r0 & 1);
+    const double *rec = B + SG::RECOFF;
+    SlotInfo si;
+    si.s = tid;
+    si.q = 0;
+    si.rod = T.r0;
+    si.N = (int)(eo[1] - eo[0]);
+    si.i = T.seg * BLOCK + tid;
+    si.active = tid < T.nslots;
+    si.node = T.nbase + tid;
+    si.elem = T.ebase + tid;
+    si.vor = si.elem - si.rod - 1;
+    si.fl = si.active ? rec_flags(rec) : 0;
+    finish_slot(si);
+    const int ns = T.nslots, nel = T.nel, seg = T.seg, nseg = T.nseg;
+    const int64_t boff = T.boff;
+    double r[3], v[3], Q[9], w[3], k0s[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      r[c] = si.active ? B[c * ns + tid] : 0.0;
+      v[c] = si.active ? B[(3 + c) * ns + tid] : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < 9; ++c) Q[c] = si.has_e ? B[6 * ns + c * nel + tid] : 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) w[c] = si.has_e ? B[6 * ns + (9 + c) * nel + tid] : 0.0;
+    if ((FEAT & FEAT_KAPPA0) && p.has_kappa0 && si.has_v) {
+      const int nvor = tile_nvor(T);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) k0s[c] = B[6 * ns + 12 * nel + c * nvor + (tid - (seg == 0 ? 1 : 0))];
+    }
+    cl.sync();  // all segments consumed their stage: exchange areas and halos are free
+    if (tid == 0 && rnext < n_rods) {
+      bulk_wait_read_all();  // the bulk store of the previous rod has read buffer b^1
+      issue_tile<BLOCK, FEAT, true>(p, Tn, p.tiles + tile_of(rnext), sm + (b ^ 1) * SG::BUFD, &bar[b ^ 1]);
+    }
+    double *X = B + 1;
+    const ClusterSync<BLOCK, XS> xs{X, tid, ns, seg, nseg};
+    double t = p.t;
+    unsigned fbits = 0;
+    for (int st = 0; st < p.n_steps; ++st) {
+      step_body<BLOCK, FEAT, true, true, true, XS, ClusterSync<BLOCK, XS>>(p, X, rec, si, r, v, Q, w, k0s, t, fbits,
+                                                                          nullptr, xs);
+      if (st + 1 < p.n_steps) cl.sync();
+    }
+    if (fbits) { fbits_all |= fbits; frod = min(frod, (int)rec[REC_CANON]); }
+    double *O = B + SG::OUTOFF;
+    if (si.active) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        O[c * ns + tid] = r[c];
+        O[(3 + c) * ns + tid] = v[c];
+      }
+    }
+    if (si.has_e) {
+#pragma unroll
+      for (int c = 0; c < 9; ++c) O[6 * ns + c * nel + tid] = Q[c];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) O[6 * ns + (9 + c) * nel + tid] = w[c];
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      bulk_s2g(p.state + boff, O, 8u * (uint32_t)(6 * ns + 12 * nel));
+      bulk_commit();
+    }
+  }
+  if (tid == 0) bulk_wait_all();
+  report_fault(p, fbits_all, frod);
+  cl.sync();  // no CTA leaves while a neighbour may still access its shared memory
+}
+
 // --------------------------------------------------------------------------- diagnostics
 // Per-tile partial sums of the energy functional at time p.t; deterministic.
 template <int BLOCK>
@@ -1072,6 +1185,35 @@ cudaError_t launch_simple(const ErStepParams &p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <int FEAT>
+cudaError_t launch_long_persistent(const ErStepParams *p, int64_t tile0, int64_t n_rods, int nseg, cudaStream_t st) {
+  constexpr int B = ER_LONG_SEG;
+  auto k = er::long_persistent<B, FEAT>;
+  const size_t sm = er::Stage<B, FEAT, true>::bytes();
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e == cudaSuccess && nseg > 8) e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(B, 1, 1);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)nseg;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3((unsigned)nseg, 1, 1);
+  int ncl = 0;
+  e = cudaOccupancyMaxActiveClusters(&ncl, k, &cfg);
+  if (e != cudaSuccess) return e;
+  ncl = (int)std::max<int64_t>(1, std::min<int64_t>(n_rods, ncl));
+  cfg.gridDim = dim3((unsigned)(ncl * nseg), 1, 1);
+  e = cudaLaunchKernelEx(&cfg, k, *p, tile0, n_rods);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 }  // namespace
 
 extern "C" {
@@ -1104,6 +1246,9 @@ cudaError_t er_launch_step(const ErStepParams *p, int block, int kind, int feat,
 // cluster of nseg CTAs per rod.
 cudaError_t er_launch_long(const ErStepParams *p, int64_t tile0, int64_t n_rods, int nseg, int feat, cudaStream_t st) {
   if (n_rods <= 0) return cudaSuccess;
+  if (!std::getenv("ER_LONG_SIMPLE"))  // persistent, TMA-pipelined clusters (default)
+    return feat == 0 ? launch_long_persistent<0>(p, tile0, n_rods, nseg, st)
+                     : launch_long_persistent<FEAT_GENERAL | FEAT_KAPPA0 | FEAT_EXTRA>(p, tile0, n_rods, nseg, st);
   constexpr int B = ER_LONG_SEG;
   // plain rods get the lean instantiation; any feature takes the general one
   auto k = feat == 0 ? er::long_kernel<B, 0> : er::long_kernel<B, FEAT_GENERAL | FEAT_KAPPA0 | FEAT_EXTRA>;

@@ -89,9 +89,9 @@ def test_long_rod_loads_and_bcs(er, orc):
     assert_parity(w, g[:4], o, TOL_1000, raw=("r", "Q"), label="loads 200 steps")
 
 
-def test_long_rod_layout_and_modes(er):
-    """Create / get_state round trip bitwise; temporal blocking and the staged kernel mode give
-    the same trajectory bitwise (long rods always run in their cluster kernel)."""
+def test_long_rod_layout_and_modes(er, monkeypatch):
+    """Create / get_state round trip bitwise; temporal blocking, the staged kernel mode and the
+    non-persistent cluster kernel (ER_LONG_SIMPLE) give the same trajectory bitwise."""
     w = perturbed([1500, 40, 513, 3])
     with er.RodBatch(w) as b:
         pos, vel, dirs, om, _ = b.get_state()
@@ -105,6 +105,10 @@ def test_long_rod_layout_and_modes(er):
             out = b.get_state()
         for x, y in zip(out[:4], ref[:4]):
             assert np.array_equal(x, y)
+    monkeypatch.setenv("ER_LONG_SIMPLE", "1")
+    out = run_gpu(er, w, 24)
+    for x, y in zip(out[:4], ref[:4]):
+        assert np.array_equal(x, y)
 
 
 def test_long_rod_diagnostics(er, orc):
