@@ -1020,13 +1020,13 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
   double t = b->t;
   const int feat = feat_of(b);
   // long rods advance k steps from time t (all step kinds give the same trajectory)
-  auto launch_long = [&](int64_t k, double t0) -> cudaError_t {
+  auto launch_long = [&](int64_t k, double t0, int lfeat = -1) -> cudaError_t {
     ErStepParams q = p;
     q.n_tiles = b->n_tiles;
     q.n_steps = (int32_t)k;
     q.t = t0;
     for (const auto &g : b->long_groups) {
-      cudaError_t e = er_launch_long(&q, g.tile0, g.n_rods, g.nseg, feat, b->stream);
+      cudaError_t e = er_launch_long(&q, g.tile0, g.n_rods, g.nseg, lfeat < 0 ? feat : lfeat, b->stream);
       if (e != cudaSuccess) return e;
       b->launches += 1;
     }
@@ -1054,7 +1054,9 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
     p.disp2 = 0.25 * b->cp.skin * b->cp.skin;
     p.rebuild = b->cp.rebuild;
     int m0 = mark(b);
+    p.n_tiles = b->n_tiles;  // the drift kernel handles long-rod segment tiles too (no exchange)
     CK(er_launch_step(&p, b->block, 1, 15, b->stream), "drift kernel");
+    p.n_tiles = b->n_tiles_norm;
     b->launches += 1;
     int m1 = mark(b);
     interval(b, m0, m1, 0);
@@ -1068,6 +1070,7 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
       p.cnode = q + 1 < n_steps ? b->cp.cnode : nullptr;
       CK(er_launch_step(&p, b->block, 0, feat | FEAT_CONTACT, b->stream), "step kernel");
       b->launches += 1;
+      CK(launch_long(1, t, feat | FEAT_CONTACT), "long-rod kernel");
       m1 = mark(b);
       interval(b, m2, m1, 0);
       const double th = t + 0.5 * dt;
@@ -1083,12 +1086,15 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
       p.cbuild = b->cp.cbuild;
       p.disp2 = 0.25 * b->cp.skin * b->cp.skin;
       p.rebuild = b->cp.rebuild;
+      p.n_tiles = b->n_tiles;  // drift-1 + node records for long-rod segments too
       CK(er_launch_step(&p, b->block, 1, 15, b->stream), "drift kernel");
+      p.n_tiles = b->n_tiles_norm;
       p.cnode = nullptr;
       CK(er_contact_eval(&b->cp, b->sort_tmp, b->sort_bytes, b->cgraph, b->stream, &b->launches, b->cgraph_kernels), "contact");
       p.cfc = b->cp.fc;
       p.cfs = b->cp.fs;
       CK(er_launch_step(&p, b->block, 2, 7, b->stream), "dyn kernel");
+      CK(launch_long(1, t, feat | FEAT_CONTACT), "long-rod kernel");  // kick + drift-2 (cnode unset)
       p.cfc = nullptr;
       CK(er_launch_step(&p, b->block, 1, 7, b->stream), "drift kernel");
       b->launches += 3;
@@ -1171,7 +1177,6 @@ er_status er_set_contact(er_batch *b, const er_contact *c) {
     for (int64_t r = 0; r < R; ++r)
       if (!pos_finite(c->radius[r])) { err.add("radius[%lld] = %g must be positive and finite", (long long)r, c->radius[r]); break; }
   if (E >= (1ll << 30)) err.add("contact supports < 2^30 elements per batch (got %lld)", (long long)E);
-  if (!b->long_groups.empty()) err.add("contact does not support rods longer than %d elements", ER_TILE_MAX_ELEMS);
   if (err.count) { b->last_error = err.msg; return ER_EINVAL; }
   CK(cudaSetDevice(b->device), "cudaSetDevice");
   CK(cudaStreamSynchronize(b->stream), "sync");

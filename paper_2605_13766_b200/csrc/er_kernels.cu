@@ -660,7 +660,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) simple_kernel(const ErStepParams 
   }
   if (p.has_kappa0 && si.has_v) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) k0s[c] = __ldg(G + tile_vor_plane(T, c) + (s - 2 * si.q - 1));
+    for (int c = 0; c < 3; ++c)
+      k0s[c] = __ldg(G + tile_vor_plane(T, c) + (T.nseg > 1 ? s - (T.seg == 0 ? 1 : 0) : s - 2 * si.q - 1));
   }
   double t = p.t;
   unsigned fbits = 0;
@@ -861,6 +862,9 @@ __global__ void __launch_bounds__(BLOCK, 2) long_persistent(const ErStepParams p
 #pragma unroll
       for (int c = 0; c < 3; ++c) k0s[c] = B[6 * ns + 12 * nel + c * nvor + (tid - (seg == 0 ? 1 : 0))];
     }
+    double fcon[3] = {0.0, 0.0, 0.0}, rbld[3] = {0.0, 0.0, 0.0};  // contact mode, as in fused_persistent
+    if ((FEAT & FEAT_CONTACT) && p.cfc) contact_node_load(p, si, fcon);
+    if ((FEAT & FEAT_CONTACT) && p.cnode) contact_build_pos(p, si, rbld);
     cl.sync();  // all segments consumed their stage: exchange areas and halos are free
     if (tid == 0 && rnext < n_rods) {
       bulk_wait_read_all();  // the bulk store of the previous rod has read buffer b^1
@@ -870,10 +874,19 @@ __global__ void __launch_bounds__(BLOCK, 2) long_persistent(const ErStepParams p
     const ClusterSync<BLOCK, XS> xs{X, tid, ns, seg, nseg};
     double t = p.t;
     unsigned fbits = 0;
-    for (int st = 0; st < p.n_steps; ++st) {
-      step_body<BLOCK, FEAT, true, true, true, XS, ClusterSync<BLOCK, XS>>(p, X, rec, si, r, v, Q, w, k0s, t, fbits,
-                                                                          nullptr, xs);
-      if (st + 1 < p.n_steps) cl.sync();
+    if (FEAT & FEAT_CONTACT) {  // state after drift-1: kick + drift-2 [+ next drift-1 + node records]
+      step_body<BLOCK, FEAT, false, true, true, XS, ClusterSync<BLOCK, XS>>(p, X, rec, si, r, v, Q, w, k0s, t, fbits,
+                                                                           p.cfc ? fcon : nullptr, xs);
+      if (p.cnode) {
+        step_body<BLOCK, FEAT, true, false, false>(p, X, rec, si, r, v, Q, w, k0s, t, fbits);
+        contact_emit(p, si, r, v, rbld);
+      }
+    } else {
+      for (int st = 0; st < p.n_steps; ++st) {
+        step_body<BLOCK, FEAT, true, true, true, XS, ClusterSync<BLOCK, XS>>(p, X, rec, si, r, v, Q, w, k0s, t, fbits,
+                                                                            nullptr, xs);
+        if (st + 1 < p.n_steps) cl.sync();
+      }
     }
     if (fbits) { fbits_all |= fbits; frod = min(frod, (int)rec[REC_CANON]); }
     double *O = B + SG::OUTOFF;
@@ -1246,9 +1259,13 @@ cudaError_t er_launch_step(const ErStepParams *p, int block, int kind, int feat,
 // cluster of nseg CTAs per rod.
 cudaError_t er_launch_long(const ErStepParams *p, int64_t tile0, int64_t n_rods, int nseg, int feat, cudaStream_t st) {
   if (n_rods <= 0) return cudaSuccess;
+  constexpr int ALL = FEAT_GENERAL | FEAT_KAPPA0 | FEAT_EXTRA;
+  if (feat & FEAT_CONTACT)  // contact mode: always the persistent kernel
+    return (feat & ~FEAT_CONTACT) == 0 ? launch_long_persistent<FEAT_CONTACT>(p, tile0, n_rods, nseg, st)
+                                       : launch_long_persistent<ALL | FEAT_CONTACT>(p, tile0, n_rods, nseg, st);
   if (!std::getenv("ER_LONG_SIMPLE"))  // persistent, TMA-pipelined clusters (default)
     return feat == 0 ? launch_long_persistent<0>(p, tile0, n_rods, nseg, st)
-                     : launch_long_persistent<FEAT_GENERAL | FEAT_KAPPA0 | FEAT_EXTRA>(p, tile0, n_rods, nseg, st);
+                     : launch_long_persistent<ALL>(p, tile0, n_rods, nseg, st);
   constexpr int B = ER_LONG_SEG;
   // plain rods get the lean instantiation; any feature takes the general one
   auto k = feat == 0 ? er::long_kernel<B, 0> : er::long_kernel<B, FEAT_GENERAL | FEAT_KAPPA0 | FEAT_EXTRA>;

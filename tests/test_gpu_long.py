@@ -126,13 +126,45 @@ def test_long_rod_diagnostics(er, orc):
     assert np.isclose(d[9], ref[9], rtol=1e-12) and np.isclose(d[10], ref[10], rtol=1e-13) and d[11] == ref[11]
 
 
-def test_longest_rod_and_contact_refused(er):
+def test_longest_rod(er):
     w = perturbed([er.ER_MAX_ELEMS_PER_ROD])                      # 16 segments: the largest cluster
     g = run_gpu(er, w, 2)
     assert all(np.all(np.isfinite(x)) for x in g[:4])
-    w.contact = W.Contact(k_n=1e3)
-    with pytest.raises(er.ErError):
-        er.RodBatch(w)
     too_long = perturbed([er.ER_MAX_ELEMS_PER_ROD + 1])
     with pytest.raises(er.ErError):
         er.RodBatch(too_long)
+
+
+def test_long_rods_in_contact(er, orc):
+    """A 700-element rod lying across short rods on a floor: contact forces reach the long rod's
+    segments (cluster kernel, contact mode) exactly as the oracle's exhaustive search says; the
+    fused and staged contact paths agree bitwise."""
+    N, lh, r = 700, 0.002, 0.004
+    L = N * lh
+    ws = [rod(N=N, L=L, r=r, Q=np.array([[0, 0, -1.0], [0, 1.0, 0], [1.0, 0, 0]]), base=(-L / 2, 0.0, 3 * r - 2e-6),
+              g=(0, 0, -9.81), nu=1.0, dt=2e-6)]
+    for k in range(6):                                   # short rods along y, under the long rod
+        x = -0.5 + 0.2 * k
+        ws.append(rod(N=10, L=0.1, r=r, Q=np.array([[1.0, 0, 0], [0, 0, -1.0], [0, 1.0, 0]]),
+                      base=(x, -0.05, r - 1e-6), g=(0, 0, -9.81), nu=1.0, dt=2e-6))
+    w = concat(ws)
+    w.velocities = np.random.default_rng(2).normal(0, 1e-3, w.velocities.shape)
+    w.contact = W.Contact(k_n=2e3, gamma_n=0.05, mu_s=0.3, mu_k=0.3, v_stick=1e-3,
+                          plane_n=np.array([0, 0, 1.0]), plane_d=0.0)
+    with er.RodBatch(w) as b:
+        b.step(1, w.dt)
+        g1 = b.get_state()
+        st = b.contact_stats()
+    assert st.contacts >= 6 and st.plane_contacts > 0
+    o, _ = run_orc(orc, w, 1)
+    assert_parity(w, g1[:4], o, TOL_1STEP, raw=("r", "v", "Q"), label="long rod contact 1 step")
+    out = []
+    for kernel in (0, 1):
+        with er.RodBatch(w) as b:
+            b.set_option(er.ER_OPT_KERNEL, kernel)
+            b.step(150, w.dt)
+            out.append(b.get_state())
+    for x, y in zip(out[0][:4], out[1][:4]):
+        assert np.array_equal(x, y)
+    o, _ = run_orc(orc, w, 150)
+    assert_parity(w, out[0][:4], o, TOL_1000, raw=("r", "Q"), label="long rod contact 150 steps")
