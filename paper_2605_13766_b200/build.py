@@ -35,19 +35,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     objdir = os.path.join(os.path.dirname(OUT), "obj")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
-    for src in SOURCES:
+    objs, procs = [], []
+    extra = os.environ.get("ER_NVCC_EXTRA", "").split()  # experiments only (e.g. -DER_...)
+    for src in SOURCES:  # the translation units compile concurrently
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        extra = os.environ.get("ER_NVCC_EXTRA", "").split()  # experiments only (e.g. -DER_...)
         cmd = [NVCC, *[f for f in FLAGS if f != "-shared"], *FILE_FLAGS.get(src, []), *extra, "-c",
                "-I", os.path.join(ROOT, "include"), "-I", CSRC, os.path.join(CSRC, src), "-o", obj]
-        res = subprocess.run(cmd, capture_output=True, text=True)
-        if res.returncode != 0:
-            sys.stderr.write(res.stdout + res.stderr)
+        procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+        objs.append(obj)
+    for src, pr in procs:
+        out, err = pr.communicate()
+        if pr.returncode != 0:
+            sys.stderr.write(out + err)
             raise RuntimeError(f"nvcc failed compiling {src}")
         if verbose:
-            sys.stderr.write(res.stderr)
-        objs.append(obj)
+            sys.stderr.write(err)
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", OUT + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
