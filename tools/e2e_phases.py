@@ -1,3 +1,4 @@
+"""Time the phases of one end-to-end cfg3 job (create from pinned host arrays, 1000 steps, state back to pinned host)."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch, dataclasses

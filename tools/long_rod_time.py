@@ -1,3 +1,4 @@
+"""Device timing of long rods (16,384 rods x 1000 elements: thread-block clusters), 1 and 10 steps per launch."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch

@@ -1,3 +1,4 @@
+"""Raw pinned-host <-> device copy bandwidth (the PCIe ceiling of the e2e path)."""
 import torch, time
 n = 1 << 28  # 2 GiB of fp64
 h = torch.empty(n, dtype=torch.float64).pin_memory()
