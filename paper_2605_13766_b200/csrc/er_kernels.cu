@@ -494,11 +494,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
     si.node = T.nbase + tid;
     si.elem = T.ebase + tid - lo;
     si.vor = si.elem - si.rod - 1;
-#ifdef ER_REC_ALIGN
-    const double *rec = static_cast<const double *>(__builtin_assume_aligned(B + SG::RECOFF + lo * ER_REC, 16));
-#else
     const double *rec = B + SG::RECOFF + lo * ER_REC;
-#endif
     si.fl = si.active ? rec_flags(rec) : 0;
     finish_slot(si);
 
