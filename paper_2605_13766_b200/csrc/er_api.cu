@@ -41,6 +41,8 @@ cudaError_t er_contact_graph(const ErContactParams *p, void *tmp, size_t tmp_byt
 
 #include <chrono>
 
+#define ER_GRAPH_LAUNCHES 32  // step launches per CUDA-graph launch (even: the time ping-pong)
+
 namespace {
 
 thread_local std::string g_create_error;
@@ -143,10 +145,16 @@ struct er_batch {
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
-  std::vector<int> iv;  // triples
+  std::vector<int> iv;  // (start event, end event, phase, launches) quadruples
   double phase_ms[2] = {0.0, 0.0};
   int64_t phase_n[2] = {0, 0};
   cudaGraphExec_t cgraph = nullptr;  // per-step contact evaluation (conditional build)
+  // streaming steps as a CUDA graph of ER_GRAPH_LAUNCHES step launches (no host launch per step);
+  // the launch time lives in tdev (ping-pong); rebuilt when its parameters change
+  cudaGraphExec_t sgraph = nullptr;
+  int64_t sgraph_key = -1;
+  double *tdev = nullptr;
+  int64_t forcing_version = 0;
   int cgraph_kernels = 0;
   std::vector<double> rod_A0, rod_E0, rod_lmin, rod_lmax;  // host, per rod (contact radius, stiffness, HHG)
 };
@@ -251,22 +259,31 @@ int mark(er_batch *b) {
   cudaEventRecord(b->ev_pool[k], b->stream);
   return k;
 }
-void interval(er_batch *b, int e0, int e1, int phase) {
-  if (e0 >= 0 && e1 >= 0) { b->iv.push_back(e0); b->iv.push_back(e1); b->iv.push_back(phase); }
+void interval(er_batch *b, int e0, int e1, int phase, int launches = 1) {
+  if (e0 >= 0 && e1 >= 0) { b->iv.push_back(e0); b->iv.push_back(e1); b->iv.push_back(phase); b->iv.push_back(launches); }
 }
 void collect_times(er_batch *b) {  // after the stream was synchronised
-  for (size_t k = 0; k + 2 < b->iv.size(); k += 3) {
+  for (size_t k = 0; k + 3 < b->iv.size(); k += 4) {
     float ms = 0.0f;
     if (cudaEventElapsedTime(&ms, b->ev_pool[b->iv[k]], b->ev_pool[b->iv[k + 1]]) == cudaSuccess) {
       b->phase_ms[b->iv[k + 2]] += ms;
-      b->phase_n[b->iv[k + 2]] += 1;
+      b->phase_n[b->iv[k + 2]] += b->iv[k + 3];
     }
   }
   b->iv.clear();
   b->ev_used = 0;
 }
 
+void free_step_graph(er_batch *b) {
+  if (b->sgraph) cudaGraphExecDestroy(b->sgraph);
+  b->sgraph = nullptr;
+  b->sgraph_key = -1;
+}
+
 void free_all(er_batch *b) {
+  free_step_graph(b);
+  if (b->tdev) cudaFree(b->tdev);
+  b->tdev = nullptr;
   if (b->upload_stage) cudaFree(b->upload_stage);
   b->upload_stage = nullptr;
   for (cudaEvent_t e : b->ev_pool) cudaEventDestroy(e);
@@ -872,6 +889,7 @@ er_status er_set_bc(er_batch *b, const int8_t *clamp_end) {
 
 er_status er_set_forcing(er_batch *b, const er_forcing *f) {
   if (!b || !f) { if (b) b->last_error = "forcing is NULL"; return ER_EINVAL; }
+  b->forcing_version += 1;  // step-graph parameters (gravity, field, features) may change
   Errors err;
   const int64_t R = b->n_rods;
   for (int c = 0; c < 3; ++c) {
@@ -996,6 +1014,7 @@ er_status er_set_option(er_batch *b, int32_t option, int64_t value) {
 er_status er_set_trace(er_batch *b, void *trace) {
   if (!b) return ER_EINVAL;
   b->trace = reinterpret_cast<unsigned long long *>(trace);
+  b->forcing_version += 1;
   return ER_OK;
 }
 
@@ -1077,6 +1096,48 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
       t = th + 0.5 * dt;
     }
     done = n_steps;
+  }
+  // Streaming steps as CUDA-graph launches of ER_GRAPH_LAUNCHES step launches each (the time is
+  // carried on the device between launches); the rest as plain launches below.
+  const int64_t spl = b->steps_per_launch;
+  if (!b->contact_on && b->kernel_mode == 0 && n_steps - done >= ER_GRAPH_LAUNCHES * spl &&
+      !std::getenv("ER_NO_STEP_GRAPH")) {
+    const int64_t key = ((b->forcing_version * 32 + feat) << 31) + spl;
+    if (!b->tdev) CK(dalloc(b, &b->tdev, 2), "cudaMalloc(tdev)");
+    if (b->sgraph_key != key) {
+      free_step_graph(b);
+      cudaStream_t cs;
+      CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "cudaStreamCreate");
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed);  // launchers query attributes
+      for (int j = 0; e == cudaSuccess && j < ER_GRAPH_LAUNCHES; ++j) {
+        ErStepParams q = p;
+        q.n_steps = (int32_t)spl;
+        q.tdev = b->tdev;
+        q.tpar = j & 1;
+        e = er_launch_step(&q, b->block, 0, feat, cs);
+        q.n_tiles = b->n_tiles;
+        for (const auto &gr : b->long_groups)
+          if (e == cudaSuccess) e = er_launch_long(&q, gr.tile0, gr.n_rods, gr.nseg, feat, cs);
+      }
+      cudaError_t e2 = cudaStreamEndCapture(cs, &g);
+      if (e == cudaSuccess) e = e2;
+      if (e == cudaSuccess) e = cudaGraphInstantiate(&b->sgraph, g, 0);
+      if (g) cudaGraphDestroy(g);
+      cudaStreamDestroy(cs);
+      CK(e, "step graph");
+      b->sgraph_key = key;
+    }
+    const double t_host = t;  // pageable 8-byte copy: staged before cudaMemcpyAsync returns
+    CK(cudaMemcpyAsync(b->tdev, &t_host, sizeof(double), cudaMemcpyHostToDevice, b->stream), "H2D t");
+    while (n_steps - done >= ER_GRAPH_LAUNCHES * spl) {
+      const int m0 = mark(b);
+      CK(cudaGraphLaunch(b->sgraph, b->stream), "step graph launch");
+      interval(b, m0, mark(b), 0, ER_GRAPH_LAUNCHES);
+      b->launches += ER_GRAPH_LAUNCHES * (1 + (int64_t)b->long_groups.size());
+      for (int64_t q = 0; q < ER_GRAPH_LAUNCHES * spl; ++q) { const double th = t + 0.5 * dt; t = th + 0.5 * dt; }
+      done += ER_GRAPH_LAUNCHES * spl;
+    }
   }
   while (done < n_steps) {
     if (b->contact_on) {  // NEXT-4 staged: drift | contact (broad + narrow phase) | dynamics + kick | drift

@@ -320,6 +320,18 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
   }
 }
 
+// Start time of a launch: the host's value, or (graph launches) the device copy the previous launch
+// advanced; block 0 advances it for the next launch with the host's arithmetic.
+__device__ __forceinline__ double launch_t0(const ErStepParams &p) { return p.tdev ? p.tdev[p.tpar] : p.t; }
+__device__ __forceinline__ void advance_tdev(const ErStepParams &p, double t0) {
+  if (!p.tdev || blockIdx.x != 0 || threadIdx.x != 0) return;
+  for (int st = 0; st < p.n_steps; ++st) {
+    const double th = t0 + 0.5 * p.h;
+    t0 = th + 0.5 * p.h;
+  }
+  p.tdev[p.tpar ^ 1] = t0;
+}
+
 __device__ __forceinline__ void report_fault(const ErStepParams &p, unsigned bits, int rod) {
   if (__ballot_sync(0xffffffffu, bits != 0) == 0) return;
   if (bits) {
@@ -457,6 +469,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
   __syncthreads();
   int64_t tile = blockIdx.x;
   if (tid == 0 && tile < p.n_tiles) issue_tile<BLOCK, FEAT>(p, load_head(p.tiles + tile), p.tiles + tile, sm, &bar[0]);
+  const double t0 = launch_t0(p);
   uint32_t phase = 0;  // bit b = load parity of buffer b
   unsigned fbits_all = 0;
   int frod = 0x7fffffff;
@@ -536,7 +549,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
     if (tr) tr[3] = gtimer() & ((1ull << 48) - 1);
 #endif
     // ---- the steps
-    double t = p.t;
+    double t = t0;
     unsigned fbits = 0;
     if (FEAT & FEAT_CONTACT) {
       // contact mode: the state arrives after drift-1 (contact forces were evaluated there);
@@ -604,6 +617,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
 #endif
   }
   if (tid == 0) bulk_wait_all();  // stores complete before the kernel retires
+  advance_tdev(p, t0);
   report_fault(p, fbits_all, frod);
 }
 
@@ -767,7 +781,8 @@ __global__ void __launch_bounds__(BLOCK, ER_LONG_MINB) long_kernel(const ErStepP
   }
   cl.sync();  // every segment of the cluster is resident before any distributed-smem access
   const ClusterSync<BLOCK, XS> xs{X, s, T.nslots, T.seg, T.nseg};
-  double t = p.t;
+  const double t0 = launch_t0(p);
+  double t = t0;
   unsigned fbits = 0;
   for (int st = 0; st < p.n_steps; ++st) {
     step_body<BLOCK, FEAT, true, true, true, XS, ClusterSync<BLOCK, XS>>(p, X, rec, si, r, v, Q, w, k0s, t, fbits,
@@ -788,6 +803,7 @@ __global__ void __launch_bounds__(BLOCK, ER_LONG_MINB) long_kernel(const ErStepP
     for (int c = 0; c < 3; ++c) __stcs(G + 6 * ns + (9 + c) * nel + s, w[c]);
   }
   report_fault(p, fbits, si.active ? (int)rec[REC_CANON] : 0);
+  advance_tdev(p, t0);
   cl.sync();  // no CTA leaves while a neighbour may still access its shared memory
 }
 
@@ -815,6 +831,7 @@ __global__ void __launch_bounds__(BLOCK, 2) long_persistent(const ErStepParams p
   if (tid == 0 && rod < n_rods)
     issue_tile<BLOCK, FEAT, true>(p, load_head(p.tiles + tile_of(rod)), p.tiles + tile_of(rod), sm, &bar[0]);
   cl.sync();  // every CTA of the cluster resident before any distributed-smem access
+  const double t0 = launch_t0(p);
   uint32_t phase = 0;
   unsigned fbits_all = 0;
   int frod = 0x7fffffff;
@@ -868,7 +885,7 @@ __global__ void __launch_bounds__(BLOCK, 2) long_persistent(const ErStepParams p
     }
     double *X = B + 1;
     const ClusterSync<BLOCK, XS> xs{X, tid, ns, seg, nseg};
-    double t = p.t;
+    double t = t0;
     unsigned fbits = 0;
     if (FEAT & FEAT_CONTACT) {  // state after drift-1: kick + drift-2 [+ next drift-1 + node records]
       step_body<BLOCK, FEAT, false, true, true, XS, ClusterSync<BLOCK, XS>>(p, X, rec, si, r, v, Q, w, k0s, t, fbits,
@@ -907,6 +924,7 @@ __global__ void __launch_bounds__(BLOCK, 2) long_persistent(const ErStepParams p
     }
   }
   if (tid == 0) bulk_wait_all();
+  advance_tdev(p, t0);
   report_fault(p, fbits_all, frod);
   cl.sync();  // no CTA leaves while a neighbour may still access its shared memory
 }

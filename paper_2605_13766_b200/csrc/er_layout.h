@@ -187,8 +187,9 @@ struct ErStepParams {
   double b2[3];
   double b_omega;
   int32_t n_steps;        // steps in this launch
-  int32_t pad_;
-  double t;               // time at the start of the launch
+  int32_t tpar;           // with tdev: the launch reads tdev[tpar], block 0 writes tdev[tpar ^ 1]
+  double t;               // time at the start of the launch (when tdev is null)
+  double *tdev;           // CUDA-graph step launches: [2] device time, ping-pong
   double h;               // dt
   unsigned long long *fault;  // [0] = OR of bits, [1] = min rod id
   double *diag_partial;   // diagnostics: [n_tiles][16]

@@ -424,3 +424,20 @@ def test_cilia_farm_sampled(er, orc):
     o, to = run_orc(orc, ws, 200)
     assert t == to
     assert_parity(ws, (pos[nidx], vel[nidx], dirs[eidx], om[eidx]), o, TOL_1000, raw=("r", "Q"), label="farm")
+
+
+def test_step_graph_bitwise(er, monkeypatch):
+    """Runs of >= 32 launches go through a CUDA graph (time carried on the device): bitwise the
+    same as plain launches, for tile rods, ragged rods, long rods and temporal blocking."""
+    w = W.make("cfg5", n_rods=40)
+    out = []
+    for plain in (False, True):
+        if plain:
+            monkeypatch.setenv("ER_NO_STEP_GRAPH", "1")
+        with er.RodBatch(w) as b:
+            b.step(70, w.dt)                                  # 2 graph launches + 6 plain steps
+            b.set_option(er.ER_OPT_STEPS_PER_LAUNCH, 3)
+            b.step(100, w.dt)                                 # 1 graph launch (96 steps) + 4
+            out.append(b.get_state())
+    for x, y in zip(out[0], out[1]):
+        assert np.array_equal(np.asarray(x), np.asarray(y))
