@@ -1160,7 +1160,11 @@ size_t diag_smem(int block) { return (size_t)12 * 8 * block + 16 * 8 * (block / 
 template <int BLOCK, int MINB, int FEAT, bool DSTORE = false>
 cudaError_t launch_persistent(const ErStepParams &p, cudaStream_t st) {
   auto k = er::fused_persistent<BLOCK, MINB, FEAT, DSTORE>;
+#ifdef ER_ONE_CTA_PER_SM  // measurement: request enough smem that only one CTA fits per SM
+  const size_t sm = 160 * 1024;
+#else
   const size_t sm = er::Stage<BLOCK, FEAT>::bytes();
+#endif
   static int grid_per_sm[64] = {0};  // per device
   int dev = 0;
   cudaGetDevice(&dev);
