@@ -57,7 +57,7 @@ class _Problem(C.Structure):
         ("act_component", C.c_int32), ("magnetization", _dp), ("b_field", C.c_double * 3),
         ("b_omega", C.c_double), ("b_axis", C.c_double * 3),
         ("musc_A", _dp), ("musc_T", _dp), ("musc_lambda", _dp), ("musc_phi", _dp), ("musc_component", C.c_int32),
-        ("contact", C.POINTER(_Contact)),
+        ("contact", C.POINTER(_Contact)), ("ext_force", _dp), ("ext_couple", _dp),
     ]
 
 
@@ -142,6 +142,8 @@ class Problem:
             c.plane_d = float(ct.plane_d)
             self._keep.append(c)
             p.contact = C.pointer(c)
+        p.ext_force = _ptr(k(getattr(w, "ext_force", None)))
+        p.ext_couple = _ptr(k(getattr(w, "ext_couple", None)))
         self.c = p
 
 

@@ -332,7 +332,7 @@ static int rod_dynamics(const orc_problem *P, int32_t rod, rod_ctx *c, const dou
     v_cross(c->kap + 3 * k, c->mbar + 3 * k, c->beta + 3 * k);
     for (int q = 0; q < 3; ++q) c->beta[3 * k + q] *= c->Dh[k];
   }
-  /* 5. forces: F_i = n_i - n_{i-1} (zero padded) + m_i g + tip; a_i = F_i/m_i - nu v_i */
+  /* 5. forces: F_i = n_i - n_{i-1} (zero padded) + m_i g + contact + tip + f_i; a_i = F_i/m_i - nu v_i */
   for (int32_t i = 0; i <= N; ++i) {
     for (int q = 0; q < 3; ++q) {
       double f = 0.0;
@@ -341,6 +341,7 @@ static int rod_dynamics(const orc_problem *P, int32_t rod, rod_ctx *c, const dou
       f += c->m[i] * P->gravity[q];
       if (Fext) f += Fext[3 * i + q];                       /* contact forces (NEXT-4) */
       if (P->tip_force && i == c->tip_node) f += P->tip_force[3 * rod + q];
+      if (P->ext_force) f += P->ext_force[3 * (c->n0 + i) + q];   /* f of Eq. (1a) */
       c->F[3 * i + q] = f;
       c->a[3 * i + q] = f / c->m[i] - c->nu * v[3 * i + q];
     }
@@ -379,6 +380,8 @@ static int rod_dynamics(const orc_problem *P, int32_t rod, rod_ctx *c, const dou
       v_cross(P->magnetization + 3 * (c->e0 + j), Qb, mb);
       for (int q = 0; q < 3; ++q) Cj[q] += c->lhat[j] * mb[q];
     }
+    if (P->ext_couple)                                      /* c-bar of Eq. (1b) */
+      for (int q = 0; q < 3; ++q) Cj[q] += P->ext_couple[3 * (c->e0 + j) + q];
     for (int q = 0; q < 3; ++q) {
       c->C[3 * j + q] = Cj[q];
       c->al[3 * j + q] = c->e[j] / c->J[3 * j + q] * Cj[q] - c->nu * w[3 * j + q];

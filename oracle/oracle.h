@@ -57,6 +57,11 @@ typedef struct {
   const double *musc_A, *musc_T, *musc_lambda, *musc_phi; /* [R] muscular torque wave, or NULL */
   int32_t musc_component;          /* local axis of the muscle couple (0 = d1)           */
   const orc_contact *contact;      /* NULL = rods do not interact                        */
+  /* User external loads f and c-bar of Eqs. (1a)-(1b), discrete (DESIGN §3 #30):
+   * a force per node [n_nodes*3] lab frame (N) and a couple per element [E*3] local frame (N m),
+   * constant in time, added to F_i and C_j; NULL = none. */
+  const double *ext_force;
+  const double *ext_couple;
 } orc_problem;
 
 enum { ORC_OK = 0, ORC_EINVAL = 1, ORC_EUNSTABLE = 2 };

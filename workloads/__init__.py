@@ -93,6 +93,8 @@ class Workload:
     musc_phi: Optional[np.ndarray] = None       # f64 [R]
     musc_component: int = 0
     contact: Optional[Contact] = None           # NEXT-4: rods interact through contact
+    ext_force: Optional[np.ndarray] = None      # [n_nodes, 3] lab, N: f of Eq. (1a) per node
+    ext_couple: Optional[np.ndarray] = None     # [n_elems, 3] local, N m: c-bar of Eq. (1b) per element
 
     # ---- layout helpers (integer bookkeeping only) ----
     @property
