@@ -168,6 +168,23 @@ typedef struct {
 
 er_status er_set_forcing(er_batch *b, const er_forcing *f);
 
+/* ------------------------------------------------------------------------- er_set_external_loads
+ * User external loads: the distributed force f of Eq. (1a) and couple c-bar of Eq. (1b)
+ * (PAPER.md:252), e.g. the hydrodynamic loads an external flow solver returns every step
+ * (reading DESIGN §3 #30).  Discrete and already integrated:
+ *  node_force   [n_nodes_total*3] lab-frame force on each node (N), canonical node order
+ *               (rod by rod, N_r + 1 nodes each), added to F_i; or NULL for none.
+ *  elem_couple  [n_elems_total*3] local-frame (director basis) couple on each element (N m),
+ *               added to C_j; or NULL for none.
+ * src_mem says where both arrays live (ER_DEVICE: device pointers on the batch's device, read
+ * stream-ordered, no host synchronisation, so a solver can update them every step).  Values are
+ * copied; they stay in force, constant in time, until the next call (NULL clears that array).
+ * Independent of er_set_forcing.  Not validated: non-finite loads surface as ER_F_NONFINITE at the
+ * next er_step.  They do no work in the diagnostics' potential energies (non-conservative).
+ * Errors: ER_EINVAL (bad src_mem), ER_ECUDA.
+ */
+er_status er_set_external_loads(er_batch *b, int32_t src_mem, const double *node_force, const double *elem_couple);
+
 /* ------------------------------------------------------------------------- er_step
  * Advance every rod by n_steps >= 0 position-Verlet steps of size dt > 0 (north_star
  * "er_step(n_steps, dt)").  Stream-ordered; returns after the work completed and one 16-byte

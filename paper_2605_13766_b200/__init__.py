@@ -92,7 +92,8 @@ class er_phase_times(C.Structure):
 
 EXPORTS = ("er_create_batch", "er_set_bc", "er_set_forcing", "er_step", "er_get_state", "er_set_state",
            "er_diagnostics", "er_fault", "er_set_option", "er_set_trace", "er_query", "er_last_error",
-           "er_abi_version", "er_destroy", "er_set_contact", "er_get_contact_stats", "er_get_phase_times")
+           "er_abi_version", "er_destroy", "er_set_contact", "er_get_contact_stats", "er_get_phase_times",
+           "er_set_external_loads")
 
 
 def _load():
@@ -117,12 +118,13 @@ def _load():
     lib.er_set_contact.argtypes = [h, C.POINTER(er_contact)]
     lib.er_get_contact_stats.argtypes = [h, C.POINTER(er_contact_stats)]
     lib.er_get_phase_times.argtypes = [h, C.POINTER(er_phase_times)]
+    lib.er_set_external_loads.argtypes = [h, C.c_int32, C.c_void_p, C.c_void_p]
     lib.er_abi_version.restype = C.c_int32
     lib.er_destroy.argtypes = [h]
     lib.er_destroy.restype = None
     for name in ("er_create_batch", "er_set_bc", "er_set_forcing", "er_step", "er_get_state",
                  "er_set_state", "er_diagnostics", "er_fault", "er_set_option", "er_set_trace", "er_query",
-                 "er_set_contact", "er_get_contact_stats", "er_get_phase_times"):
+                 "er_set_contact", "er_get_contact_stats", "er_get_phase_times", "er_set_external_loads"):
         getattr(lib, name).restype = C.c_int
     return lib
 
@@ -201,6 +203,10 @@ def er_query(handle) -> er_info:
 
 def er_set_contact(handle, contact):
     _check(handle, lib.er_set_contact(handle, None if contact is None else C.byref(contact)))
+
+
+def er_set_external_loads(handle, src_mem, node_force, elem_couple):
+    _check(handle, lib.er_set_external_loads(handle, src_mem, node_force, elem_couple))
 
 
 def er_get_contact_stats(handle) -> er_contact_stats:
@@ -294,6 +300,8 @@ class RodBatch:
             self.set_forcing_from(w)
             if getattr(w, "contact", None) is not None:
                 self.set_contact(w.contact)
+            if getattr(w, "ext_force", None) is not None or getattr(w, "ext_couple", None) is not None:
+                self.set_external_loads(getattr(w, "ext_force", None), getattr(w, "ext_couple", None))
 
     # -- boundary conditions / forcing
     def set_bc(self, clamp_end=None):
@@ -320,6 +328,21 @@ class RodBatch:
         f.musc_lambda, f.musc_phi = k.host(musc_lambda), k.host(musc_phi)
         f.musc_component = int(musc_component)
         er_set_forcing(self.handle, f)
+
+    def set_external_loads(self, node_force=None, elem_couple=None):
+        """er_set_external_loads: node_force [n_nodes, 3] lab (N), elem_couple [n_elems, 3] local
+        (N m), canonical order; numpy (host) or torch CUDA tensors (device), both the same kind;
+        None clears that array."""
+        k = _Keep()
+        pf, mf = k.any(node_force)
+        pc, mc = k.any(elem_couple)
+        mems = {m for m in (mf, mc) if m is not None}
+        if len(mems) > 1:
+            raise ValueError("node_force and elem_couple must both be host or both be device")
+        for a, rows in ((node_force, self.n_nodes_total), (elem_couple, self.n_elems_total)):
+            if a is not None and tuple(a.shape) != (rows, 3):
+                raise ValueError(f"external load of shape {tuple(a.shape)}, expected ({rows}, 3)")
+        er_set_external_loads(self.handle, mems.pop() if mems else ER_HOST, pf, pc)
 
     def set_forcing_from(self, w):
         self.set_forcing(gravity=getattr(w, "gravity", (0, 0, 0)), damping=getattr(w, "damping", None),

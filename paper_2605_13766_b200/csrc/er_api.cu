@@ -29,6 +29,8 @@ cudaError_t er_launch_long(const ErStepParams *p, int64_t tile0, int64_t n_rods,
 cudaError_t er_launch_diag(const ErStepParams *p, int block, double *out, cudaStream_t st);
 cudaError_t er_launch_canon_tiles(const ErStepParams *p, double *canon, int field, int to_tiles, cudaStream_t st);
 cudaError_t er_launch_aos_to_soa(const double *src, double *dst, int64_t n, int k, int64_t stride, cudaStream_t st);
+cudaError_t er_launch_pack_planes(const double *src, double *dst, int64_t stride, const int64_t *eoffp,
+                                  const int32_t *ord, const int64_t *eoffc, int64_t n_rods, int nodes, cudaStream_t st);
 cudaError_t er_launch_validate(const double *aos, int64_t n, int k, int orth, double *out, cudaStream_t st);
 cudaError_t er_launch_apply_forcing(double *rec, int64_t n_rods, const int32_t *flags, const double *damping,
                                     double damping_all, const double *tip, const double *actA, const double *actF,
@@ -107,6 +109,7 @@ struct er_batch {
   int64_t *d_eoff = nullptr;
   ErTile *d_tiles = nullptr;
   double *d_gpar = nullptr, *d_sigma0 = nullptr, *d_mag = nullptr, *d_musc = nullptr;
+  double *d_fext = nullptr, *d_cext = nullptr;  // user external loads (er_set_external_loads)
   unsigned long long *d_fault = nullptr;
   unsigned long long *trace = nullptr;  // caller-owned, optional
   double *d_diag_partial = nullptr, *d_diag_out = nullptr, *d_valid = nullptr;
@@ -289,6 +292,7 @@ void free_all(er_batch *b) {
   for (cudaEvent_t e : b->ev_pool) cudaEventDestroy(e);
   b->ev_pool.clear();
   void *ptrs[] = {b->d_state, b->d_rec, b->d_eoff, b->d_ord, b->d_eoffc, b->d_tiles, b->d_gpar, b->d_sigma0, b->d_mag, b->d_musc,
+                  b->d_fext, b->d_cext,
                   b->d_fault, b->d_diag_partial, b->d_diag_out, b->d_valid};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -324,6 +328,7 @@ ErStepParams params_of(const er_batch *b) {
   p.rec = b->d_rec; p.eoff = b->d_eoff; p.tiles = b->d_tiles; p.n_tiles = b->n_tiles;
   p.ord = b->d_ord; p.eoffc = b->d_eoffc;
   p.gpar = b->d_gpar; p.ng = b->ng; p.sigma0 = b->d_sigma0; p.mag = b->d_mag; p.ne = b->ne;
+  p.fext = b->d_fext; p.cext = b->d_cext;
   p.musc = b->has_musc ? b->d_musc : nullptr;
   p.musc_comp = b->musc_comp;
   p.has_kappa0 = b->has_kappa0 ? 1 : 0;
@@ -448,7 +453,7 @@ int feat_of(const er_batch *b) {
   int f = 0;
   if (b->any_general) f |= FEAT_GENERAL;
   if (b->has_kappa0) f |= FEAT_KAPPA0;
-  if (b->has_sigma0 || b->d_mag || b->has_musc) f |= FEAT_EXTRA;
+  if (b->has_sigma0 || b->d_mag || b->has_musc || b->d_fext || b->d_cext) f |= FEAT_EXTRA;
   else if (b->has_act) f |= FEAT_ACT;  // actuation alone: the lighter kernel
   return f;
 }
@@ -985,6 +990,52 @@ er_status er_set_forcing(er_batch *b, const er_forcing *f) {
     b->d_mag = nullptr;
   }
   CK(cudaStreamSynchronize(b->stream), "sync");
+  return ER_OK;
+}
+
+// One external-load array: canonical AoS [rows][3] (host or device) -> planes in packed rod order.
+// NULL frees the planes.  Returns whether the plane pointer changed (step graphs capture it).
+static er_status set_ext_planes(er_batch *b, int32_t src_mem, const double *src, double **planes, int64_t stride,
+                         int64_t rows, int nodes, bool *changed) {
+  if (!src) {
+    if (*planes) {
+      CK(cudaStreamSynchronize(b->stream), "sync");
+      cudaFree(*planes);
+      b->device_bytes -= (int64_t)sizeof(double) * 3 * stride;
+      *planes = nullptr;
+      *changed = true;
+    }
+    return ER_OK;
+  }
+  if (!*planes) {
+    CK(dalloc(b, planes, 3 * stride), "cudaMalloc(ext)");
+    CK(cudaMemsetAsync(*planes, 0, sizeof(double) * 3 * (size_t)stride, b->stream), "memset(ext)");
+    *changed = true;
+  }
+  if (rows <= 0) return ER_OK;
+  const double *dsrc = src;
+  double *stage = nullptr;
+  if (src_mem == ER_HOST) {
+    CK(cudaMallocAsync((void **)&stage, sizeof(double) * 3 * (size_t)rows, b->stream), "cudaMallocAsync(stage)");
+    CK(cudaMemcpyAsync(stage, src, sizeof(double) * 3 * (size_t)rows, cudaMemcpyHostToDevice, b->stream), "H2D ext");
+    dsrc = stage;
+  }
+  CK(er_launch_pack_planes(dsrc, *planes, stride, b->d_eoff, b->d_ord, b->d_eoffc, b->n_rods, nodes, b->stream),
+     "pack_planes");
+  if (stage) CK(cudaFreeAsync(stage, b->stream), "cudaFreeAsync");
+  return ER_OK;
+}
+
+er_status er_set_external_loads(er_batch *b, int32_t src_mem, const double *node_force, const double *elem_couple) {
+  if (!b) return ER_EINVAL;
+  if (src_mem != ER_HOST && src_mem != ER_DEVICE) { b->last_error = "src_mem must be ER_HOST or ER_DEVICE"; return ER_EINVAL; }
+  CK(cudaSetDevice(b->device), "cudaSetDevice");
+  bool changed = false;
+  er_status st = set_ext_planes(b, src_mem, node_force, &b->d_fext, b->ng, b->n_nodes, 1, &changed);
+  if (st != ER_OK) return st;
+  if ((st = set_ext_planes(b, src_mem, elem_couple, &b->d_cext, b->ne, b->n_elems, 0, &changed)) != ER_OK) return st;
+  if (changed) b->forcing_version += 1;  // new plane pointers / kernel features: recapture step graphs
+  if (src_mem == ER_HOST) CK(cudaStreamSynchronize(b->stream), "sync");  // caller may reuse its buffers
   return ER_OK;
 }
 

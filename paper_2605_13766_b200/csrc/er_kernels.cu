@@ -252,6 +252,10 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
 #pragma unroll
         for (int c = 0; c < 3; ++c) F[c] += fcon[c];
       }
+      if (EXTRA && p.fext) {  // user external force f of Eq. (1a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) F[c] += __ldg(p.fext + c * p.ng + si.node);
+      }
       const double im = general ? gp(GP_IM) : rec[REC_IM] * ((i == 0 || i == N) ? 2.0 : 1.0);
       const double nu = rec[REC_NU];
 #pragma unroll
@@ -289,6 +293,10 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
         C[0] += lh * (m[1] * Qb[2] - m[2] * Qb[1]);
         C[1] += lh * (m[2] * Qb[0] - m[0] * Qb[2]);
         C[2] += lh * (m[0] * Qb[1] - m[1] * Qb[0]);
+      }
+      if (EXTRA && p.cext) {  // user external couple c-bar of Eq. (1b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) C[c] += __ldg(p.cext + c * p.ne + si.elem);
       }
       const double nu = rec[REC_NU];
       const double rate = edot * inv_e - nu;
@@ -1069,6 +1077,24 @@ __global__ void aos_to_soa(const double *__restrict__ src, double *__restrict__ 
     dst[c * stride + e] = src[q];
   }
 }
+// Canonical AoS [rows][3] -> 3 planes in packed rod order (user external loads): one warp per
+// packed rod, lanes stride over the rod's contiguous canonical rows (coalesced reads).
+// nodes = 1: node rows (N_r + 1 per rod, offset eoff + rod); 0: element rows.
+__global__ void pack_planes(const double *__restrict__ src, double *__restrict__ dst, int64_t stride,
+                            const int64_t *__restrict__ eoffp, const int32_t *__restrict__ ord,
+                            const int64_t *__restrict__ eoffc, int64_t n_rods, int nodes) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t pr = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; pr < n_rods; pr += nw) {
+    const int64_t r = ord[pr];
+    const int64_t c0 = eoffc[r] + (nodes ? r : 0), p0 = eoffp[pr] + (nodes ? pr : 0);
+    const int64_t cnt = 3 * (eoffc[r + 1] - eoffc[r] + nodes);
+    for (int64_t q = lane; q < cnt; q += 32) {
+      const int64_t row = q / 3;
+      dst[(q - 3 * row) * stride + p0 + row] = src[3 * c0 + q];
+    }
+  }
+}
 // Canonical AoS [rows][k] <-> tile-blocked planes, one CTA per tile, rod by rod: the rods of a tile
 // are consecutive in packed order, and each rod's rows are contiguous in the canonical array (at
 // its canonical offset).  canon == nullptr with to_tiles writes zeros.
@@ -1330,6 +1356,12 @@ cudaError_t er_launch_diag(const ErStepParams *p, int block, double *out, cudaSt
 cudaError_t er_launch_aos_to_soa(const double *src, double *dst, int64_t n, int k, int64_t stride, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   er::aos_to_soa<<<148 * 8, 256, 0, st>>>(src, dst, n, k, stride);
+  return cudaGetLastError();
+}
+cudaError_t er_launch_pack_planes(const double *src, double *dst, int64_t stride, const int64_t *eoffp,
+                                  const int32_t *ord, const int64_t *eoffc, int64_t n_rods, int nodes, cudaStream_t st) {
+  if (n_rods <= 0) return cudaSuccess;
+  er::pack_planes<<<148 * 8, 256, 0, st>>>(src, dst, stride, eoffp, ord, eoffc, n_rods, nodes);
   return cudaGetLastError();
 }
 cudaError_t er_launch_canon_tiles(const ErStepParams *p, double *canon, int field, int to_tiles, cudaStream_t st) {

@@ -17,7 +17,8 @@
 //  - tiles        : [n_tiles] ErTile
 //  - gpar         : optional [ER_GP][ng] per-slot parameters of "general" rods (non-uniform
 //                   rest lengths or per-element material), canonical node index
-//  - sigma0, mag  : optional [3][ne] canonical element planes
+//  - sigma0, mag  : optional [3][ne] element planes (packed rod order)
+//  - fext / cext  : optional user external loads, [3][ng] node / [3][ne] element planes
 // Ghost nodes exist only in shared memory, never in HBM.
 #pragma once
 #include <stdint.h>
@@ -176,6 +177,8 @@ struct ErStepParams {
   const double *sigma0;   // may be null, planes stride ne
   const double *mag;      // may be null, planes stride ne
   const double *musc;     // may be null: [n_rods][4] = A, 1/T, 1/lambda, phi/pi
+  const double *fext;     // may be null: user node forces f (lab), planes stride ng
+  const double *cext;     // may be null: user element couples c-bar (local), planes stride ne
   int64_t ne;
   int32_t has_kappa0;     // static kappa0 planes present in the tile blocks
   int32_t act_comp;

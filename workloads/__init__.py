@@ -156,6 +156,7 @@ class Workload:
             rest_sigma=gather(eo, self.rest_sigma), rest_kappa=gather(vo, self.rest_kappa),
             act_A=per_rod(self.act_A), act_f=per_rod(self.act_f), act_L=per_rod(self.act_L),
             magnetization=gather(eo, self.magnetization),
+            ext_force=gather(no, self.ext_force), ext_couple=gather(eo, self.ext_couple),
             musc_A=per_rod(self.musc_A), musc_T=per_rod(self.musc_T),
             musc_lambda=per_rod(self.musc_lambda), musc_phi=per_rod(self.musc_phi),
             contact=None if self.contact is None else dataclasses.replace(
