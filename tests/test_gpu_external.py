@@ -10,6 +10,7 @@ import pytest
 import workloads as W
 from parity import TOL_1000, TOL_1STEP, assert_parity
 from test_gpu_long import perturbed
+from test_gpu_parity import RAW, RAW_1000
 
 pytestmark = pytest.mark.gpu
 
@@ -70,9 +71,9 @@ def tup(st):
 def test_parity(er, orc, name, n):
     w = W.make(name, n_rods=n) if name != "cfg5" else W.make(name).subset(W.sample_rods(W.make(name), n, seed=3))
     w = with_loads(w, seed=1)
-    assert_parity(w, run_gpu(er, w, 1), tup(run_orc(orc, w, 1)), TOL_1STEP, raw=("r", "v", "Q", "w"),
+    assert_parity(w, run_gpu(er, w, 1), tup(run_orc(orc, w, 1)), TOL_1STEP, raw=RAW[name],
                   label=f"{name} loads 1 step")
-    assert_parity(w, run_gpu(er, w, 1000), tup(run_orc(orc, w, 1000)), TOL_1000, raw=("r", "Q"),
+    assert_parity(w, run_gpu(er, w, 1000), tup(run_orc(orc, w, 1000)), TOL_1000, raw=RAW_1000[name],
                   label=f"{name} loads 1000 steps")
 
 
