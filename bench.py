@@ -65,13 +65,16 @@ def peaks():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
-def b_min_per_el_step(w) -> float:
-    """16 [6(N+1) + 12 N] + P + 24 (N-1) chi_kappa0 bytes per rod-step, / N.
+def b_min_per_el_step(w, q_planes: float = 9.0) -> float:
+    """SURVEY §8 D.3 with the stored director form (DESIGN §4 "Director storage"): the state is
+    r, v per node and d1, d2, w per element (d3 = d1 x d2 is rebuilt on chip), so
+    16 [6(N+1) + 9 N] + P + 24 (N-1) chi_kappa0 bytes per rod-step, / N (SURVEY's 12 N counts
+    the full 3x3 Q; `b_min_survey_3x3` below keeps that figure for reference).
     Contact mode (NEXT-4) adds, for the step kernel: the contact force on each element's
     two nodes read (48 B per element), the node records for the next contact evaluation written
     (48 B per node) and the build positions read for the Verlet check (24 B per node)."""
     N = w.n_elems.astype(np.float64)
-    per_rod = 16.0 * (6.0 * (N + 1) + 12.0 * N) + 128.0 + (24.0 * (N - 1) if w.rest_kappa is not None else 0.0)
+    per_rod = 16.0 * (6.0 * (N + 1) + q_planes * N) + 128.0 + (24.0 * (N - 1) if w.rest_kappa is not None else 0.0)
     if getattr(w, "contact", None) is not None:
         per_rod = per_rod + 48.0 * N + 72.0 * (N + 1)
     return float(per_rod.sum() / N.sum())
@@ -283,6 +286,7 @@ def main():
             traffic = None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "peak_source": peak_src, "bytes_per_el_step": bmin,
+            "b_min_survey_3x3": b_min_per_el_step(w, 12.0),
             "kernel": "er::fused_persistent<256,2,FEAT> (fused single-pass step, TMA bulk load/store pipeline)",
             "kernel_ms_per_launch": launch_ms, "kernel_share_of_step": ph.step_kernel_ms / ms if ms > 0 else None}
     if ph.contact_evals:

@@ -1483,9 +1483,9 @@ er_status er_query(const er_batch *b, er_info *info) {
   info->launches = b->launches;
   info->device_bytes = b->device_bytes;
   info->t = b->t;
-  // bytes one fused step moves: state read + written once (r, v: 6 per node; Q, w: 12 per
-  // element), the 192-byte rod record read once, static kappa0 read once
-  double bytes = 16.0 * (6.0 * b->n_nodes + 12.0 * b->n_elems) + 8.0 * ER_REC * b->n_rods;
+  // bytes one fused step moves: state read + written once (r, v: 6 per node; d1, d2, w: ER_EPL
+  // per element), the 192-byte rod record read once, static kappa0 read once
+  double bytes = 16.0 * (6.0 * b->n_nodes + (double)ER_EPL * b->n_elems) + 8.0 * ER_REC * b->n_rods;
   if (b->has_kappa0) bytes += 24.0 * b->n_vor;
   info->bytes_per_step = bytes;
   return ER_OK;

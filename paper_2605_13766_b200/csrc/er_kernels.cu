@@ -416,13 +416,14 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 // records (RMAX x ER_REC) and the tile's element offsets (RMAX + 4 int64).
 template <int BLOCK, int FEAT, bool LONG = false>
 struct Stage {
-  static constexpr int NPL = (FEAT & FEAT_KAPPA0) ? 21 : 18;
+  static constexpr int NPL = 6 + ER_EPL + ((FEAT & FEAT_KAPPA0) ? 3 : 0);  // staged input planes
   static constexpr int RMAX = BLOCK / 8;
   static constexpr int XS = LONG ? BLOCK + 2 : BLOCK;  // exchange plane stride (long rods: halos)
   // the results of a tile are written at OUTOFF (clear of the exchange-C planes 0-5, which other
   // warps may still read) and bulk-stored from there
   static constexpr int OUTOFF = 6 * XS;
-  static constexpr int PLANES = 24 * XS + 8;
+  static constexpr int NP0 = NPL > XPLANES ? NPL : XPLANES;
+  static constexpr int PLANES = (NP0 > 6 + 6 + ER_EPL ? NP0 : 6 + 6 + ER_EPL) * XS + 8;
   static constexpr int RECOFF = PLANES;
   static constexpr int EOFF = RECOFF + RMAX * ER_REC;
   static constexpr int TOFF = EOFF + RMAX + 4;   // staged ErTile (16 doubles)
@@ -450,7 +451,7 @@ template <int BLOCK, int FEAT, bool LONG = false>
 __device__ __forceinline__ void issue_tile(const ErStepParams &p, const TileHead &T, const ErTile *tile_ptr, double *B,
                                            uint64_t *bar) {
   using SG = Stage<BLOCK, FEAT, LONG>;
-  const int64_t sz = 6 * (int64_t)T.nslots + 12 * (int64_t)T.nel +
+  const int64_t sz = 6 * (int64_t)T.nslots + ER_EPL * (int64_t)T.nel +
                      (((FEAT & FEAT_KAPPA0) && p.has_kappa0) ? 3 * (int64_t)T.nvor : 0);
   const uint32_t cs = (uint32_t)((sz + 1) & ~1ll);
   const int64_t ra = T.r0 & ~1ll;
@@ -532,13 +533,14 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
     // a rod's last node owns no element: its Q, w stay 0 (le would index past the element planes,
     // into stale stage contents that the non-finite check would otherwise see)
 #pragma unroll
-    for (int c = 0; c < 9; ++c) Q[c] = si.has_e ? B[6 * ns + c * nel + le] : 0.0;
+    for (int c = 0; c < ER_QST; ++c) Q[c] = si.has_e ? B[6 * ns + c * nel + le] : 0.0;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) w[c] = si.has_e ? B[6 * ns + (9 + c) * nel + le] : 0.0;
+    for (int c = 0; c < 3; ++c) w[c] = si.has_e ? B[6 * ns + (ER_QST + c) * nel + le] : 0.0;
+    complete_d3(Q);
     if ((FEAT & FEAT_KAPPA0) && si.has_v) {
       const int nvor = tile_nvor(T);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) k0s[c] = B[6 * ns + 12 * nel + c * nvor + (tid - 2 * lo - 1)];
+      for (int c = 0; c < 3; ++c) k0s[c] = B[6 * ns + ER_EPL * nel + c * nvor + (tid - 2 * lo - 1)];
     }
     // contact mode: this node's contact force and build position, loaded now so their latency
     // hides behind the step's first phases
@@ -590,9 +592,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
       }
       if (si.has_e) {
 #pragma unroll
-        for (int c = 0; c < 9; ++c) __stcs(G + 6 * ns + c * nel + le, Q[c]);
+        for (int c = 0; c < ER_QST; ++c) __stcs(G + 6 * ns + c * nel + le, Q[c]);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) __stcs(G + 6 * ns + (9 + c) * nel + le, w[c]);
+        for (int c = 0; c < 3; ++c) __stcs(G + 6 * ns + (ER_QST + c) * nel + le, w[c]);
       }
 #ifndef ER_TRACE_FINE
       if (tr) tr[3] = gtimer() & ((1ull << 48) - 1);
@@ -610,15 +612,19 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
     }
     if (si.has_e) {
 #pragma unroll
-      for (int c = 0; c < 9; ++c) O[6 * ns + c * nel + le] = Q[c];
+      for (int c = 0; c < ER_QST; ++c) O[6 * ns + c * nel + le] = Q[c];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) O[6 * ns + (9 + c) * nel + le] = w[c];
+      for (int c = 0; c < 3; ++c) O[6 * ns + (ER_QST + c) * nel + le] = w[c];
     }
     fence_proxy_async();  // this thread's generic smem writes -> visible to the async proxy
     __syncthreads();
     if (tid == 0) {
-      bulk_s2g(p.state + boff, O, 8u * (uint32_t)(6 * ns + 12 * nel));
+      // bulk copies move multiples of 16 bytes; with an odd element count the block's last
+      // double (d1, d2, w planes: 9 nel doubles) goes with a plain store
+      const uint32_t tot = (uint32_t)(6 * ns + ER_EPL * nel);
+      bulk_s2g(p.state + boff, O, 8u * (tot & ~1u));
       bulk_commit();
+      if (tot & 1u) p.state[boff + tot - 1] = O[tot - 1];
     }
 #ifndef ER_TRACE_FINE
     if (tr) tr[3] = gtimer() & ((1ull << 48) - 1);
@@ -672,9 +678,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) simple_kernel(const ErStepParams 
   }
   if (si.has_e) {
 #pragma unroll
-    for (int c = 0; c < 9; ++c) Q[c] = __ldcs(G + 6 * ns + c * nel + le);
+    for (int c = 0; c < ER_QST; ++c) Q[c] = __ldcs(G + 6 * ns + c * nel + le);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) w[c] = __ldcs(G + 6 * ns + (9 + c) * nel + le);
+    for (int c = 0; c < 3; ++c) w[c] = __ldcs(G + 6 * ns + (ER_QST + c) * nel + le);
+    complete_d3(Q);
   }
   if (p.has_kappa0 && si.has_v) {
 #pragma unroll
@@ -708,9 +715,9 @@ __global__ void __launch_bounds__(BLOCK, MINB) simple_kernel(const ErStepParams 
   }
   if (si.has_e) {
 #pragma unroll
-    for (int c = 0; c < 9; ++c) __stcs(G + 6 * ns + c * nel + le, Q[c]);
+    for (int c = 0; c < ER_QST; ++c) __stcs(G + 6 * ns + c * nel + le, Q[c]);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) __stcs(G + 6 * ns + (9 + c) * nel + le, w[c]);
+    for (int c = 0; c < 3; ++c) __stcs(G + 6 * ns + (ER_QST + c) * nel + le, w[c]);
   }
   report_fault(p, fbits, si.active ? (int)rec[REC_CANON] : 0);  // canonical rod id
 }
@@ -779,9 +786,10 @@ __global__ void __launch_bounds__(BLOCK, ER_LONG_MINB) long_kernel(const ErStepP
   }
   if (si.has_e) {
 #pragma unroll
-    for (int c = 0; c < 9; ++c) Q[c] = __ldcs(G + 6 * ns + c * nel + s);
+    for (int c = 0; c < ER_QST; ++c) Q[c] = __ldcs(G + 6 * ns + c * nel + s);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) w[c] = __ldcs(G + 6 * ns + (9 + c) * nel + s);
+    for (int c = 0; c < 3; ++c) w[c] = __ldcs(G + 6 * ns + (ER_QST + c) * nel + s);
+    complete_d3(Q);
   }
   if (p.has_kappa0 && si.has_v) {
 #pragma unroll
@@ -806,9 +814,9 @@ __global__ void __launch_bounds__(BLOCK, ER_LONG_MINB) long_kernel(const ErStepP
   }
   if (si.has_e) {
 #pragma unroll
-    for (int c = 0; c < 9; ++c) __stcs(G + 6 * ns + c * nel + s, Q[c]);
+    for (int c = 0; c < ER_QST; ++c) __stcs(G + 6 * ns + c * nel + s, Q[c]);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) __stcs(G + 6 * ns + (9 + c) * nel + s, w[c]);
+    for (int c = 0; c < 3; ++c) __stcs(G + 6 * ns + (ER_QST + c) * nel + s, w[c]);
   }
   report_fault(p, fbits, si.active ? (int)rec[REC_CANON] : 0);
   advance_tdev(p, t0);
@@ -875,13 +883,14 @@ __global__ void __launch_bounds__(BLOCK, 2) long_persistent(const ErStepParams p
       v[c] = si.active ? B[(3 + c) * ns + tid] : 0.0;
     }
 #pragma unroll
-    for (int c = 0; c < 9; ++c) Q[c] = si.has_e ? B[6 * ns + c * nel + tid] : 0.0;
+    for (int c = 0; c < ER_QST; ++c) Q[c] = si.has_e ? B[6 * ns + c * nel + tid] : 0.0;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) w[c] = si.has_e ? B[6 * ns + (9 + c) * nel + tid] : 0.0;
+    for (int c = 0; c < 3; ++c) w[c] = si.has_e ? B[6 * ns + (ER_QST + c) * nel + tid] : 0.0;
+    complete_d3(Q);
     if ((FEAT & FEAT_KAPPA0) && p.has_kappa0 && si.has_v) {
       const int nvor = tile_nvor(T);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) k0s[c] = B[6 * ns + 12 * nel + c * nvor + (tid - (seg == 0 ? 1 : 0))];
+      for (int c = 0; c < 3; ++c) k0s[c] = B[6 * ns + ER_EPL * nel + c * nvor + (tid - (seg == 0 ? 1 : 0))];
     }
     double fcon[3] = {0.0, 0.0, 0.0}, rbld[3] = {0.0, 0.0, 0.0};  // contact mode, as in fused_persistent
     if ((FEAT & FEAT_CONTACT) && p.cfc) contact_node_load(p, si, fcon);
@@ -920,15 +929,19 @@ __global__ void __launch_bounds__(BLOCK, 2) long_persistent(const ErStepParams p
     }
     if (si.has_e) {
 #pragma unroll
-      for (int c = 0; c < 9; ++c) O[6 * ns + c * nel + tid] = Q[c];
+      for (int c = 0; c < ER_QST; ++c) O[6 * ns + c * nel + tid] = Q[c];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) O[6 * ns + (9 + c) * nel + tid] = w[c];
+      for (int c = 0; c < 3; ++c) O[6 * ns + (ER_QST + c) * nel + tid] = w[c];
     }
     fence_proxy_async();
     __syncthreads();
     if (tid == 0) {
-      bulk_s2g(p.state + boff, O, 8u * (uint32_t)(6 * ns + 12 * nel));
+      // bulk copies move multiples of 16 bytes; with an odd element count the block's last
+      // double (d1, d2, w planes: 9 nel doubles) goes with a plain store
+      const uint32_t tot = (uint32_t)(6 * ns + ER_EPL * nel);
+      bulk_s2g(p.state + boff, O, 8u * (tot & ~1u));
       bulk_commit();
+      if (tot & 1u) p.state[boff + tot - 1] = O[tot - 1];
     }
   }
   if (tid == 0) bulk_wait_all();
@@ -959,9 +972,10 @@ __global__ void __launch_bounds__(BLOCK) diag_kernel(const ErStepParams p) {
   double r[3] = {0, 0, 0}, v[3] = {0, 0, 0}, Q[9], w[3] = {0, 0, 0};
   for (int c = 0; c < 3; ++c) {
     if (si.active) { r[c] = G[c * ns + s]; v[c] = G[(3 + c) * ns + s]; }
-    if (si.has_e) w[c] = G[6 * ns + (9 + c) * nel + le];
+    if (si.has_e) w[c] = G[6 * ns + (ER_QST + c) * nel + le];
   }
-  for (int c = 0; c < 9; ++c) Q[c] = si.has_e ? G[6 * ns + c * nel + le] : 0.0;
+  for (int c = 0; c < ER_QST; ++c) Q[c] = si.has_e ? G[6 * ns + c * nel + le] : 0.0;
+  complete_d3(Q);
   if (si.active) {
     for (int c = 0; c < 3; ++c) xr[c * BLOCK + s] = r[c];
     for (int c = 0; c < 9; ++c) xQ[c * BLOCK + s] = Q[c];
@@ -1008,7 +1022,8 @@ __global__ void __launch_bounds__(BLOCK) diag_kernel(const ErStepParams p) {
     double Qp[9], kap[3], cth, s2;
     if (s == 0) {  // long rod segment: previous element is the last of the previous segment
       const ErTile Tp = p.tiles[blockIdx.x - 1];
-      for (int c = 0; c < 9; ++c) Qp[c] = p.state[Tp.boff + 6 * Tp.nslots + c * Tp.nel + Tp.nel - 1];
+      for (int c = 0; c < ER_QST; ++c) Qp[c] = p.state[Tp.boff + 6 * Tp.nslots + c * Tp.nel + Tp.nel - 1];
+      complete_d3(Qp);
     } else {
       for (int c = 0; c < 9; ++c) Qp[c] = xQ[c * BLOCK + s - 1];
     }
@@ -1098,6 +1113,9 @@ __global__ void pack_planes(const double *__restrict__ src, double *__restrict__
 // Canonical AoS [rows][k] <-> tile-blocked planes, one CTA per tile, rod by rod: the rods of a tile
 // are consecutive in packed order, and each rod's rows are contiguous in the canonical array (at
 // its canonical offset).  canon == nullptr with to_tiles writes zeros.
+//
+// Directors: the canonical rows hold all 9 components; the tiles store d1, d2 (er_layout.h), so
+// to_tiles drops d3 and the way back rebuilds it with complete_d3, the bits every kernel uses.
 __global__ void canon_tiles(const ErStepParams p, double *canon, int field, int to_tiles) {
   const ErTile T = p.tiles[blockIdx.x];
   const int k = field == FIELD_DIR ? 9 : 3;
@@ -1106,7 +1124,7 @@ __global__ void canon_tiles(const ErStepParams p, double *canon, int field, int 
   if (field <= FIELD_VEL) {
     count = T.nslots; off = tile_node_plane(T, field == FIELD_VEL ? 3 : 0); shift = 1;
   } else if (field <= FIELD_OMEGA) {
-    count = T.nel; off = tile_elem_plane(T, field == FIELD_OMEGA ? 9 : 0); shift = 0;
+    count = T.nel; off = tile_elem_plane(T, field == FIELD_OMEGA ? ER_QST : 0); shift = 0;
   } else {
     count = tile_nvor(T); off = tile_vor_plane(T, 0); shift = -1;
   }
@@ -1121,6 +1139,20 @@ __global__ void canon_tiles(const ErStepParams p, double *canon, int field, int 
       n = count;
       loc = 0;
       can += shift < 0 ? (T.seg == 0 ? 0 : k0 - 1) : k0;
+    }
+    if (field == FIELD_DIR) {  // one thread per element row
+      for (int64_t u = threadIdx.x; u < n; u += blockDim.x) {
+        double *row = canon + (can + u) * 9;
+        if (to_tiles) {
+          for (int c = 0; c < ER_QST; ++c) blk[c * count + loc + u] = canon ? row[c] : 0.0;
+        } else {
+          double Q[9];
+          for (int c = 0; c < ER_QST; ++c) Q[c] = blk[c * count + loc + u];
+          complete_d3(Q);
+          for (int c = 0; c < 9; ++c) row[c] = Q[c];
+        }
+      }
+      continue;
     }
     for (int64_t x = threadIdx.x; x < n * k; x += blockDim.x) {
       const int64_t u = x / k;

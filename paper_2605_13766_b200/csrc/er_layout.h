@@ -3,9 +3,12 @@
 // HBM layout:
 //  - state        : tile-blocked SoA.  The rods are packed into rod-aligned tiles (<= BLOCK
 //                   slots, <= BLOCK/8 rods); tile T owns one contiguous block at T.boff:
-//                   6 node planes [rx ry rz vx vy vz] x nslots, then 12 element planes
-//                   [Q00..Q22 wx wy wz] x nel, then (static kappa0 only) 3 Voronoi planes x nvor,
-//                   padded to 16 bytes.  SoA per component inside the block, so every warp
+//                   6 node planes [rx ry rz vx vy vz] x nslots, then ER_EPL = 9 element planes
+//                   [d1 (Q00..Q02), d2 (Q10..Q12), wx wy wz] x nel, then (static kappa0 only) 3
+//                   Voronoi planes x nvor, padded to 16 bytes.  The third director is not stored:
+//                   d3 = d1 x d2 is rebuilt on every load and after every rotation (complete_d3),
+//                   so it is the same function of (d1, d2) everywhere (DESIGN §4 "Director
+//                   storage"); 48 of the 302 bytes per element-step the 3x3 form would move.  SoA per component inside the block, so every warp
 //                   access is coalesced, and one TMA bulk copy moves a whole tile.
 //  - rod records  : [n_rods][ER_REC] fp64: derived constants, damping, v_max^2, tip force,
 //                   actuation and the flag word -- one 192-byte record read per rod per step
@@ -23,6 +26,9 @@
 #pragma once
 #include <stdint.h>
 #include <vector_types.h>
+
+#define ER_QST 6  // stored director components per element (rows d1, d2 of Q)
+#define ER_EPL 9  // stored element planes per tile: d1, d2, w
 
 #ifndef __CUDACC__
 #define __host__
@@ -216,10 +222,10 @@ __host__ __device__ inline int64_t tile_elem_plane(const ErTile &T, int c) {
 // element is in its segment 0)
 __host__ __device__ inline int32_t tile_nvor(const ErTile &T) { return T.nel - (T.seg == 0 ? T.nr : 0); }
 __host__ __device__ inline int64_t tile_vor_plane(const ErTile &T, int c) {
-  return 6 * (int64_t)T.nslots + 12 * (int64_t)T.nel + (int64_t)c * tile_nvor(T);
+  return 6 * (int64_t)T.nslots + ER_EPL * (int64_t)T.nel + (int64_t)c * tile_nvor(T);
 }
 __host__ __device__ inline int64_t tile_block_size(const ErTile &T, int has_kappa0) {
-  const int64_t sz = 6 * (int64_t)T.nslots + 12 * (int64_t)T.nel + (has_kappa0 ? 3 * (int64_t)tile_nvor(T) : 0);
+  const int64_t sz = 6 * (int64_t)T.nslots + ER_EPL * (int64_t)T.nel + (has_kappa0 ? 3 * (int64_t)tile_nvor(T) : 0);
   return (sz + 1) & ~1ll;
 }
 static_assert(sizeof(ErTile) == 128, "ErTile must stay 128 bytes (bulk-copied)");

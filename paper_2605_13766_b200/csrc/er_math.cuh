@@ -66,8 +66,18 @@ __device__ __forceinline__ double rsqrt_fast(double x) {
   return fma(y, e, y);
 }
 
+// d3 = d1 x d2: the third director row, rebuilt from the two stored rows (er_layout.h).  Written
+// with explicit fma so every kernel (and er_get_state) computes the same bits.
+__device__ __forceinline__ void complete_d3(double Q[9]) {
+  Q[6] = fma(Q[1], Q[5], -Q[2] * Q[4]);
+  Q[7] = fma(Q[2], Q[3], -Q[0] * Q[5]);
+  Q[8] = fma(Q[0], Q[4], -Q[1] * Q[3]);
+}
+
 // Q <- rot(v) Q with rot(v) = exp(-[v]x) = I - a [v]x + b [v]x^2 (Rodrigues; the in-place SO(3)
-// rotation of PAPER.md:30).  Rows of Q are the directors.  v = 0 leaves Q bit-identical.
+// rotation of PAPER.md:30).  Rows of Q are the directors.  Rows d1, d2 are rotated, d3 is rebuilt
+// as d1 x d2 (equal in exact arithmetic for a proper rotation).  v = 0 leaves Q bit-identical
+// when it already holds d3 = complete_d3(d1, d2), which every kernel maintains.
 __device__ __forceinline__ void rotate_inplace(double Q[9], double vx, double vy, double vz) {
   const double x = fma(vx, vx, fma(vy, vy, vz * vz));
   double a, b;
@@ -88,13 +98,14 @@ __device__ __forceinline__ void rotate_inplace(double Q[9], double vx, double vy
   const double R01 = s01 + az, R10 = s01 - az;
   const double R02 = s02 - ay, R20 = s02 + ay;
   const double R12 = s12 + ax, R21 = s12 - ax;
+  (void)R20; (void)R21; (void)R22;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     const double q0 = Q[c], q1 = Q[3 + c], q2 = Q[6 + c];
     Q[c] = fma(R00, q0, fma(R01, q1, R02 * q2));
     Q[3 + c] = fma(R10, q0, fma(R11, q1, R12 * q2));
-    Q[6 + c] = fma(R20, q0, fma(R21, q1, R22 * q2));
   }
+  complete_d3(Q);
 }
 
 __device__ __forceinline__ double dot3(const double *a, const double *b) {

@@ -54,3 +54,12 @@ def assert_parity(w, gpu, orc, tol, dt=None, raw=(), label=""):
     badr = {k: e[k + "_raw"] for k in raw if not (e[k + "_raw"] <= tol)}
     assert not badr, f"{label} raw parity > {tol}: {e}"
     return e
+
+
+def assert_directors_round_trip(out, inp):
+    """Directors come back from the tile layout with d1, d2 bitwise and d3 rebuilt as d1 x d2
+    (the stored form, DESIGN §4 "Director storage"): within round-off of the input's d3."""
+    out, inp = np.asarray(out), np.asarray(inp)
+    assert np.array_equal(out[:, :2, :], inp[:, :2, :])
+    assert np.max(np.abs(out[:, 2, :] - inp[:, 2, :]), initial=0.0) <= 1e-15
+    assert np.max(np.abs(out[:, 2, :] - np.cross(out[:, 0, :], out[:, 1, :])), initial=0.0) <= 4.5e-16
