@@ -41,9 +41,9 @@ namespace er {
 
 enum { MODE_FUSED = 0, MODE_DRIFT = 1, MODE_DYN = 2 };
 
-// exchange planes (stride BLOCK): A = r(0-2) v(3-5) Q(6-14); B = l(15) n(16-18); C aliases A:
-// mbar(0-2) beta(3-5).  19 planes.
-enum { XR = 0, XV = 3, XQ = 6, XL = 15, XN = 16, XM = 0, XB = 3, XPLANES = 19 };
+// exchange planes (stride BLOCK): A = r(0-2) v(3-5) d1 d2 (6-11; the reader rebuilds d3);
+// B = l(12) n(13-15); C aliases A: mbar(0-2) beta(3-5).  16 planes.
+enum { XR = 0, XV = 3, XQ = 6, XL = 6 + ER_QST, XN = 7 + ER_QST, XM = 0, XB = 3, XPLANES = 10 + ER_QST };
 
 struct SlotInfo {
   int s;            // slot (thread) index in the tile
@@ -142,7 +142,7 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
 #pragma unroll
       for (int c = 0; c < 3; ++c) { X[(XR + c) * XS + s] = r[c]; X[(XV + c) * XS + s] = v[c]; }
 #pragma unroll
-      for (int c = 0; c < 9; ++c) X[(XQ + c) * XS + s] = Q[c];
+      for (int c = 0; c < ER_QST; ++c) X[(XQ + c) * XS + s] = Q[c];  // d3 is rebuilt by the reader
     }
     xsync(0);
 
@@ -186,7 +186,8 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
     if (si.has_v) {
       double Qp[9], cth, s2;
 #pragma unroll
-      for (int c = 0; c < 9; ++c) Qp[c] = X[(XQ + c) * XS + s - 1];
+      for (int c = 0; c < ER_QST; ++c) Qp[c] = X[(XQ + c) * XS + s - 1];
+      complete_d3(Qp);  // the bits the neighbour holds in its registers
       logrot_pair(Q, Qp, kap, cth, s2);
       if (cth < 0.0 && s2 <= 1e-12 * cth * cth) fbits |= 4u;  // ER_F_ANTIPODAL: theta >= pi - 1e-6
     }
@@ -736,7 +737,7 @@ struct ClusterSync {
   int s, nslots, seg, nseg;
   __device__ __forceinline__ void operator()(int phase) const {
     cgx::cluster_group cl = cgx::this_cluster();
-    const int p0 = phase == 1 ? XL : 0, np = phase == 0 ? 15 : phase == 1 ? 4 : 6;
+    const int p0 = phase == 1 ? XL : 0, np = phase == 0 ? XL : phase == 1 ? 4 : 6;
     if (s == 0 && seg > 0) {  // my first slot -> the previous segment's right halo
       double *R = cl.map_shared_rank(X, seg - 1);
       for (int c = 0; c < np; ++c) R[(p0 + c) * XS + BLOCK] = X[(p0 + c) * XS];
@@ -1140,16 +1141,15 @@ __global__ void canon_tiles(const ErStepParams p, double *canon, int field, int 
       loc = 0;
       can += shift < 0 ? (T.seg == 0 ? 0 : k0 - 1) : k0;
     }
-    if (field == FIELD_DIR) {  // one thread per element row
-      for (int64_t u = threadIdx.x; u < n; u += blockDim.x) {
-        double *row = canon + (can + u) * 9;
+    if (field == FIELD_DIR) {  // consecutive threads on consecutive canonical doubles (coalesced)
+      for (int64_t x = threadIdx.x; x < n * 9; x += blockDim.x) {
+        const int64_t u = x / 9;
+        const int c = (int)(x - u * 9);
+        const double *q = blk + loc + u;  // this element's stored components, plane stride count
         if (to_tiles) {
-          for (int c = 0; c < ER_QST; ++c) blk[c * count + loc + u] = canon ? row[c] : 0.0;
+          if (c < ER_QST) blk[c * count + loc + u] = canon ? canon[can * 9 + x] : 0.0;
         } else {
-          double Q[9];
-          for (int c = 0; c < ER_QST; ++c) Q[c] = blk[c * count + loc + u];
-          complete_d3(Q);
-          for (int c = 0; c < 9; ++c) row[c] = Q[c];
+          canon[can * 9 + x] = c < ER_QST ? q[c * count] : d3_component(c - ER_QST, q, count);
         }
       }
       continue;

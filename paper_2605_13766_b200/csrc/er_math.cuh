@@ -74,6 +74,13 @@ __device__ __forceinline__ void complete_d3(double Q[9]) {
   Q[8] = fma(Q[0], Q[4], -Q[1] * Q[3]);
 }
 
+// One component of complete_d3 from components strided by st (layout conversion); the same
+// expressions, so the same bits.
+__device__ __forceinline__ double d3_component(int j, const double *q, int64_t st) {
+  const double q0 = q[0], q1 = q[st], q2 = q[2 * st], q3 = q[3 * st], q4 = q[4 * st], q5 = q[5 * st];
+  return j == 0 ? fma(q1, q5, -q2 * q4) : j == 1 ? fma(q2, q3, -q0 * q5) : fma(q0, q4, -q1 * q3);
+}
+
 // Q <- rot(v) Q with rot(v) = exp(-[v]x) = I - a [v]x + b [v]x^2 (Rodrigues; the in-place SO(3)
 // rotation of PAPER.md:30).  Rows of Q are the directors.  Rows d1, d2 are rotated, d3 is rebuilt
 // as d1 x d2 (equal in exact arithmetic for a proper rotation).  v = 0 leaves Q bit-identical
