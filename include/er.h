@@ -72,8 +72,11 @@ typedef enum { ER_HOST = 0, ER_DEVICE = 1 } er_mem;
 
 /* ------------------------------------------------------------------------- er_create_batch
  * A ragged batch of rods with per-rod element counts (north_star "er_create_batch").
- *  n_elems            HOST  [n_rods], each 1 <= n <= ER_MAX_ELEMS_PER_ROD (rods longer than
- *                     ER_TILE_MAX_ELEMS run in thread-block clusters; tile_slots 256 or 512).
+ *  n_elems            HOST  [n_rods], each 1 <= n <= ER_MAX_ELEMS_PER_ROD.  Rods longer than
+ *                     the tile capacity minus one run in thread-block clusters of 256-slot
+ *                     segments: > ER_TILE_MAX_ELEMS with 512-slot tiles, > 255 with 256-slot
+ *                     tiles (tile_slots 256, or automatically for ragged batches whose rods of
+ *                     256..511 elements hold <= 2% of the elements); not with tile_slots 128.
  *  material_per_rod   1: the seven material arrays have n_rods entries (one value per rod);
  *                     0: they have n_elems_total entries (one value per element).
  *  density            HOST  rho, volumetric mass density (kg/m^3) (reading DESIGN §3 #6).

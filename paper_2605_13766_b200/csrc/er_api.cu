@@ -523,13 +523,32 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   if (err.count) { g_create_error = err.msg; return ER_EINVAL; }
 
   std::vector<int64_t> eoff((size_t)std::max<int64_t>(R, 0) + 1, 0);
-  int32_t max_n = 0;       // longest tile rod (<= ER_TILE_MAX_ELEMS elements)
-  int64_t n_long = 0;      // rods longer than that: segments of a thread-block cluster
   for (int64_t r = 0; r < R; ++r) {
     const int32_t n = d->n_elems[r];
     if (n < 1 || n > ER_MAX_ELEMS_PER_ROD) err.add("rod %lld: n_elems = %d outside [1, %d]", (long long)r, n, ER_MAX_ELEMS_PER_ROD);
     eoff[r + 1] = eoff[r] + std::max(n, 0);
-    if (n > ER_TILE_MAX_ELEMS) ++n_long;
+  }
+  // Longest rod that shares rod tiles (lmax); longer rods run as thread-block clusters.  512-slot
+  // tiles (1 CTA per SM) only when rods of 256..511 elements carry a real share of the work;
+  // otherwise 256-slot tiles (2 CTAs per SM overlap each other's staging) and those few rods go
+  // to 2-segment clusters (DESIGN §4 "Tile size").
+  int32_t lmax = ER_TILE_MAX_ELEMS;
+  if (d->tile_slots == 256 || d->tile_slots == 128) lmax = d->tile_slots - 1;
+  if (d->tile_slots == 0 && R > 0) {
+    int64_t mid = 0;  // elements in rods of 256..511 elements
+    int32_t lo = ER_MAX_ELEMS_PER_ROD, hi = 0;
+    for (int64_t r = 0; r < R; ++r) {
+      const int32_t n = d->n_elems[r];
+      if (n >= 256 && n <= ER_TILE_MAX_ELEMS) mid += n;
+      if (n <= ER_TILE_MAX_ELEMS) { lo = std::min(lo, n); hi = std::max(hi, n); }
+    }
+    if (mid > 0 && lo != hi && (double)mid <= 0.02 * (double)eoff[R] && !std::getenv("ER_NO_MID_CLUSTERS")) lmax = 255;
+  }
+  int32_t max_n = 0;       // longest tile rod (<= lmax elements)
+  int64_t n_long = 0;      // rods longer than that: segments of a thread-block cluster
+  for (int64_t r = 0; r < R; ++r) {
+    const int32_t n = d->n_elems[r];
+    if (n > lmax) ++n_long;
     else max_n = std::max(max_n, n);
   }
   const int64_t E = eoff[R];
@@ -560,7 +579,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   else if (d->tile_slots != 0 && max_n + 1 > d->tile_slots)
     err.add("tile_slots = %d < longest rod's %d slots", d->tile_slots, max_n + 1);
   else if (d->tile_slots == 128 && n_long > 0)
-    err.add("tile_slots = 128 cannot be combined with rods longer than %d elements", ER_TILE_MAX_ELEMS);
+    err.add("tile_slots = 128 cannot be combined with rods longer than 127 elements");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) err.add("no CUDA device available");
   else if (d->device < 0 || d->device >= ndev) err.add("device %d outside [0, %d)", d->device, ndev);
@@ -575,7 +594,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   b->block = d->tile_slots ? d->tile_slots : (max_n + 1 <= 256) ? 256 : 512;
   int32_t min_n = max_n;
   for (int64_t r = 0; r < R; ++r)
-    if (d->n_elems[r] <= ER_TILE_MAX_ELEMS) min_n = std::min(min_n, d->n_elems[r]);
+    if (d->n_elems[r] <= lmax) min_n = std::min(min_n, d->n_elems[r]);
   if (!d->tile_slots && b->block == 256 && Rn > 0 && min_n == max_n) {
     // equal-length rods fill a tile with floor(B / (N+1)) of them (<= B/8): take 512-slot tiles
     // when that keeps clearly more lanes busy (65-slot rods: 76% at 256, 89% at 512)
@@ -586,7 +605,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
     // packed order: tile rods (best-fit-decreasing when their lengths differ), then long rods by
     // cluster size (so each size is one launch), canonical order within
     std::vector<int32_t> tile_rods, long_rods;
-    for (int64_t r = 0; r < R; ++r) (d->n_elems[r] > ER_TILE_MAX_ELEMS ? long_rods : tile_rods).push_back((int32_t)r);
+    for (int64_t r = 0; r < R; ++r) (d->n_elems[r] > lmax ? long_rods : tile_rods).push_back((int32_t)r);
     const bool pack = Rn > 1 && min_n != max_n && std::getenv("ER_NO_PACK") == nullptr;
     if (pack) {
       std::vector<int32_t> nt(tile_rods.size());

@@ -23,5 +23,5 @@ for spl in (1, 10):
     e0.record(st); b.step(200, w.dt); e1.record(st); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 200
     el = R * N
-    bmin = (16 * (6 * (N + 1) + 12 * N) + 128) / N
+    bmin = (16 * (6 * (N + 1) + 9 * N) + 128) / N  # stored state: r, v, d1, d2, w
     print(f"spl={spl}: {ms:.4f} ms/step  {el / (ms * 1e-3):.3e} el-steps/s  {bmin * el / (ms * 1e-3) / 1e9:.0f} GB/s (B_min)")
