@@ -316,6 +316,15 @@ def main():
         temporal = {"steps_per_launch": spl, "ms_per_step": float(tms.item()) / a.steps,
                     "value": float(el_total.item()) * a.steps / (float(tms.item()) * 1e-3),
                     "note": "SURVEY NEXT-1: state crosses HBM once per launch; FP64/issue-bound"}
+        tpath = os.path.join(ROOT, "profiles", "temporal.json")
+        try:  # the FP64-pipe share SURVEY NEXT-1 asks for, from the committed ncu capture
+            tj = json.load(open(tpath)).get(f"{a.config}_spl{spl}")
+            if tj:
+                temporal["fp64_pipe_pct_of_peak"] = tj["fp64_pipe_pct_of_peak"]
+                temporal["issue_active_pct"] = tj["issue_active_pct"]
+                temporal["fp64_source"] = tj["source"]
+        except Exception:
+            pass
 
     # NEXT-4 context: the contact workload (fibres: 65,536 rods x 16 elements in crossed layers,
     # HHG broad phase + Verlet lists + narrow phase every step), same timing protocol
@@ -408,9 +417,12 @@ def e2e_run(er, w, steps, dt, local, world):
         dist.barrier()
     t0 = time.perf_counter()
     b = er.RodBatch(wp, device=local)                  # H2D of the inputs (pinned host)
+    t1 = time.perf_counter()
     b.step(steps, dt)
+    t2 = time.perf_counter()
     b.get_state_into(outp.numpy(), outv.numpy(), outd.numpy(), outo.numpy())  # D2H of the result
-    secs = time.perf_counter() - t0
+    t3 = time.perf_counter()
+    secs = t3 - t0
     b.close()
     tt = torch.tensor([secs], dtype=torch.float64, device=f"cuda:{local}")
     el = torch.tensor([float(w.n_elems_total)], dtype=torch.float64, device=f"cuda:{local}")
@@ -423,6 +435,7 @@ def e2e_run(er, w, steps, dt, local, world):
     return {"value": float(el.item()) * steps / float(tt.item()), "unit": "element-steps/s",
             "h2d_bytes_per_step": (state_bytes + param_bytes) / steps, "d2h_bytes_per_step": state_bytes / steps,
             "seconds": float(tt.item()),
+            "phases_s": {"create": t1 - t0, "step": t2 - t1, "get_state": t3 - t2},
             "what": f"er_create_batch from pinned host arrays + er_step({steps}) + er_get_state to pinned host, "
                     "wall clock (max over ranks); transfer bytes are per job / steps"}
 
