@@ -49,6 +49,7 @@ def parse():
                          ">1 = temporal blocking (SURVEY NEXT-1)")
     ap.add_argument("--scaling", default="weak", choices=["strong", "weak"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-fanout", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-temporal", action="store_true")
     ap.add_argument("--no-contact", action="store_true")
@@ -161,6 +162,31 @@ def oracle_rate(w, n_rods, n_steps, seed=3):
     st, s, _, _ = oracle.step(ws, n_steps=n_steps)
     dt = time.perf_counter() - t0
     return ws.n_elems_total * n_steps / dt, dt, ws
+
+
+def _fanout_worker(args):
+    ws, n_steps = args
+    import oracle
+    t0 = time.perf_counter()
+    oracle.step(ws, n_steps=n_steps)
+    return ws.n_elems_total * n_steps, time.perf_counter() - t0
+
+
+def oracle_fanout_rate(w, rods_per_proc, n_steps, seed=5):
+    """SURVEY §8(d) whole-host fan-out: the oracle as it stands in one process per host core,
+    each on its own seeded rod shard (rods are independent).  Rate = all element-steps / the
+    slowest process's time."""
+    import multiprocessing as mp
+    n_proc = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    rods = W.sample_rods(w, min(w.n_rods, rods_per_proc * n_proc), seed=seed)
+    shards = [w.subset(np.sort(part)) for part in np.array_split(rods, n_proc) if len(part)]
+    with mp.get_context("spawn").Pool(len(shards)) as pool:
+        res = pool.map(_fanout_worker, [(x, n_steps) for x in shards])
+    work = sum(r[0] for r in res)
+    slow = max(r[1] for r in res)
+    return {"value": work / slow, "unit": "element-steps/s", "cores": len(shards), "kind": "oracle, one process per core",
+            "sample": f"{len(rods)} seeded rods of the workload in {len(shards)} shards x {n_steps} steps "
+                      f"({work:.3g} element-steps, slowest process {slow:.1f} s)"}
 
 
 def run_reference(a):
@@ -348,6 +374,11 @@ def main():
             cpu = {"value": rate, "unit": "element-steps/s", "cores": 1, "kind": "oracle",
                    "sample": f"{ws.n_rods} {what} of {a.config} x {cs} steps "
                              f"({ws.n_elems_total * cs:.3g} element-steps, {secs:.1f} s, 1 thread)"}
+            if not a.no_cpu_fanout and getattr(wfull, "contact", None) is None:
+                try:
+                    cpu["fanout"] = oracle_fanout_rate(wfull, 512, a.cpu_sample_steps)
+                except Exception as ex:  # the single-thread figure stands on its own
+                    cpu["fanout"] = {"unavailable": str(ex)[:200]}
         out = {
             "metric": "rod element-updates/sec (fp64)", "value": value, "unit": "element-steps/s",
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_max / a.steps,
