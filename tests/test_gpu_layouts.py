@@ -1,0 +1,91 @@
+"""Layout choices must not change results: the tile size (256-slot tiles with mid-length rods as
+2-segment clusters vs 512-slot tiles), the packed rod order and temporal blocking give the same
+trajectory bitwise, with every load type including user external loads; and the mid-length
+cluster path is in parity with the oracle."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import workloads as W
+from parity import TOL_1000, TOL_1STEP, assert_parity
+from rodkit import concat, rod
+from test_gpu_external import loads
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def er():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2605_13766_b200 as er
+    return er
+
+
+def mixed_batch(n_short=1000, seed=7):
+    """n_short rods of 20-60 elements plus rods of 256 and 300 elements (about 1.4% of the
+    elements: the automatic rule takes 256-slot tiles and runs the two as 2-segment clusters),
+    random orientations, perturbed directors, random rates, clamps, tip loads, gravity, damping."""
+    rng = np.random.default_rng(seed)
+    ns = list(rng.integers(20, 61, n_short)) + [256, 300]
+    ws = []
+    for q, N in enumerate(ns):
+        Q0 = W.uniform_so3(rng, 1)[0]
+        ws.append(rod(N=int(N), L=0.004 * N, r=0.002, E=1e6, Q=Q0, base=tuple(rng.uniform(-1, 1, 3)),
+                      clamp=int(rng.integers(-1, 2)), nu=0.3, g=(0, 0, -9.81), dt=2e-6,
+                      tip=tuple(rng.normal(0, 1e-6, 3))))
+    w = concat(ws)
+    w.tip_force = np.stack([x.tip_force[0] for x in ws])
+    E = w.n_elems_total
+    R = W.quat_to_rows(W.axis_angle_quat(rng.standard_normal((E, 3)), rng.uniform(0, 0.03, E)))
+    w.directors = np.einsum("eab,ebc->eac", R, w.directors)
+    w.velocities = rng.normal(0, 1e-3, w.velocities.shape)
+    w.omega = rng.normal(0, 1e-2, w.omega.shape)
+    return w
+
+
+def run(er, w, n_steps, spl=1):
+    with er.RodBatch(w) as b:
+        if spl > 1:
+            b.set_option(er.ER_OPT_STEPS_PER_LAUNCH, spl)
+        b.step(n_steps, w.dt)
+        return b.get_state()[:4], b.info().tile_slots
+
+
+def test_mid_length_clusters_match_512_tiles(er, orc, monkeypatch):
+    w = mixed_batch()
+    a, slots_a = run(er, w, 40)
+    monkeypatch.setenv("ER_NO_MID_CLUSTERS", "1")
+    b, slots_b = run(er, w, 40)
+    assert (slots_a, slots_b) == (256, 512)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    monkeypatch.delenv("ER_NO_MID_CLUSTERS")
+    st, s, _, _ = orc.step(w, n_steps=1)
+    assert s == 0
+    g, _ = run(er, w, 1)
+    assert_parity(w, g, (st.positions, st.velocities, st.directors, st.omega), TOL_1STEP, raw=("r", "Q"),
+                  label="mid-length clusters 1 step")
+    st, s, _, _ = orc.step(w, n_steps=300)
+    g, _ = run(er, w, 300)
+    assert_parity(w, g, (st.positions, st.velocities, st.directors, st.omega), TOL_1000, raw=("r", "Q"),
+                  label="mid-length clusters 300 steps")
+
+
+def test_external_loads_invariant_to_layout(er, monkeypatch):
+    """External loads (packed into the device order) with temporal blocking and without the
+    packed rod order: the same trajectory bitwise."""
+    w = mixed_batch(n_short=300, seed=3)
+    f, c = loads(w, seed=9)
+    w = dataclasses.replace(w, ext_force=f, ext_couple=c, act_A=np.full(w.n_rods, 0.5),
+                            act_f=np.full(w.n_rods, 3.0), act_L=0.004 * w.n_elems.astype(float))
+    ref, _ = run(er, w, 24)
+    for out in (run(er, w, 24, spl=8)[0],):
+        for x, y in zip(out, ref):
+            assert np.array_equal(x, y)
+    monkeypatch.setenv("ER_NO_PACK", "1")
+    out, _ = run(er, w, 24)
+    for x, y in zip(out, ref):
+        assert np.array_equal(x, y)
