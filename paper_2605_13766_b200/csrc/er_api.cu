@@ -553,6 +553,59 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   }
   const int64_t E = eoff[R];
   const int64_t NN = E + R, NV = E - R;
+
+  // ---- the device, the batch and the host->device copies of the state come first: from
+  // page-locked arrays the DMA then runs under all the host work below (validation, records,
+  // tiles); the layout kernels later read the staged copies
+  {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) err.add("no CUDA device available");
+    else if (d->device < 0 || d->device >= ndev) err.add("device %d outside [0, %d)", d->device, ndev);
+  }
+  er_batch *b = nullptr;
+  if (err.count == 0) {  // (with errors already found: collect the rest, then report them all)
+    b = new er_batch();
+    b->device = d->device;
+    auto early = [&](cudaError_t e, const char *what) {
+      cuda_fail(nullptr, e, what);
+      free_all(b);
+      delete b;
+      return e == cudaErrorMemoryAllocation ? ER_ENOMEM : ER_ECUDA;
+    };
+#undef CK
+#define CK(call, what)                              \
+  do {                                              \
+    cudaError_t e_ = (call);                        \
+    if (e_ != cudaSuccess) return early(e_, what);  \
+  } while (0)
+    CK(cudaSetDevice(d->device), "cudaSetDevice");
+    if (d->stream) b->stream = (cudaStream_t)d->stream;
+    else { CK(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking), "cudaStreamCreate"); b->own_stream = true; }
+    // ---- start the host->device copies of the state now: from page-locked arrays the DMA runs
+    // while the host builds records and tiles below (the layout kernels use the staged copies)
+    {
+      const struct { const double *src; int field; int64_t n; } fs[5] = {
+          {d->src_mem == ER_HOST ? d->positions : nullptr, FIELD_POS, 3 * NN},
+          {d->src_mem == ER_HOST ? d->velocities : nullptr, FIELD_VEL, 3 * NN},
+          {d->src_mem == ER_HOST ? d->directors : nullptr, FIELD_DIR, 9 * E},
+          {d->src_mem == ER_HOST ? d->omega : nullptr, FIELD_OMEGA, 3 * E},
+          {NV > 0 ? d->rest_kappa : nullptr, FIELD_KAPPA0, 3 * NV}};
+      int64_t total = 0;
+      for (const auto &f : fs) total += f.src ? f.n : 0;
+      if (total > 0) {
+        CK(cudaMalloc((void **)&b->upload_stage, sizeof(double) * (size_t)total + 64), "cudaMalloc(stage)");
+        int64_t o = 0;
+        for (const auto &f : fs)
+          if (f.src) {
+            b->staged[f.field] = b->upload_stage + o;
+            CK(cudaMemcpyAsync(b->staged[f.field], f.src, sizeof(double) * (size_t)f.n, cudaMemcpyHostToDevice, b->stream),
+               "H2D state");
+            o += f.n;
+          }
+      }
+    }
+    tm.mark("state copies issued");
+  }
   const int64_t nmat = d->material_per_rod ? R : E;
   const char *mnames[7] = {"density", "area", "I1", "I2", "youngs", "shear_mod", "alpha_c"};
   const double *marr[7] = {d->density, d->area, d->I1, d->I2, d->youngs, d->shear_mod, d->alpha_c};
@@ -580,14 +633,13 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
     err.add("tile_slots = %d < longest rod's %d slots", d->tile_slots, max_n + 1);
   else if (d->tile_slots == 128 && n_long > 0)
     err.add("tile_slots = 128 cannot be combined with rods longer than 127 elements");
-  int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) err.add("no CUDA device available");
-  else if (d->device < 0 || d->device >= ndev) err.add("device %d outside [0, %d)", d->device, ndev);
-  if (err.count) { g_create_error = err.msg; return ER_EINVAL; }
+  if (err.count) {
+    g_create_error = err.msg;
+    if (b) { free_all(b); delete b; }
+    return ER_EINVAL;
+  }
 
   tm.mark("host validation");
-  er_batch *b = new er_batch();
-  b->device = d->device;
   b->n_rods = R; b->n_elems = E; b->n_nodes = NN; b->n_vor = NV; b->max_n = max_n;
   const int64_t Rn = R - n_long;  // tile rods come first in the packed order
   b->t = d->t0;
@@ -636,34 +688,6 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
     cudaError_t e_ = (call);                                           \
     if (e_ != cudaSuccess) { cuda_fail(b, e_, what); return fail(e_ == cudaErrorMemoryAllocation ? ER_ENOMEM : ER_ECUDA); } \
   } while (0)
-  CK(cudaSetDevice(d->device), "cudaSetDevice");
-  if (d->stream) b->stream = (cudaStream_t)d->stream;
-  else { CK(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking), "cudaStreamCreate"); b->own_stream = true; }
-
-  // ---- start the host->device copies of the state now: from page-locked arrays the DMA runs
-  // while the host builds records and tiles below (the layout kernels use the staged copies)
-  {
-    const struct { const double *src; int field; int64_t n; } fs[5] = {
-        {d->src_mem == ER_HOST ? d->positions : nullptr, FIELD_POS, 3 * NN},
-        {d->src_mem == ER_HOST ? d->velocities : nullptr, FIELD_VEL, 3 * NN},
-        {d->src_mem == ER_HOST ? d->directors : nullptr, FIELD_DIR, 9 * E},
-        {d->src_mem == ER_HOST ? d->omega : nullptr, FIELD_OMEGA, 3 * E},
-        {NV > 0 ? d->rest_kappa : nullptr, FIELD_KAPPA0, 3 * NV}};
-    int64_t total = 0;
-    for (const auto &f : fs) total += f.src ? f.n : 0;
-    if (total > 0) {
-      CK(cudaMalloc((void **)&b->upload_stage, sizeof(double) * (size_t)total + 64), "cudaMalloc(stage)");
-      int64_t o = 0;
-      for (const auto &f : fs)
-        if (f.src) {
-          b->staged[f.field] = b->upload_stage + o;
-          CK(cudaMemcpyAsync(b->staged[f.field], f.src, sizeof(double) * (size_t)f.n, cudaMemcpyHostToDevice, b->stream),
-             "H2D state");
-          o += f.n;
-        }
-    }
-  }
-  tm.mark("state copies issued");
 
   // ---- per-rod records; general rods get per-slot parameter planes
   b->rec_n = (size_t)std::max<int64_t>(R, 1) * ER_REC;
