@@ -342,7 +342,8 @@ er_status er_get_phase_times(const er_batch *b, er_phase_times *out);
 /* Measurement aid: when `trace` (DEVICE memory, [grid][64][4] uint64, zeroed by the caller) is
  * non-NULL, the persistent step kernel records for thread 0 of each CTA and its first 64 tiles
  * the low 48 bits of %globaltimer at: wait start (bits 56-63 = SM id), data arrival, compute
- * end, stores issued.  NULL disables it. */
+ * end, stores issued.  NULL disables it.  Compiled in only with -DER_TRACE=1 (a measurement
+ * build, ER_NVCC_EXTRA); otherwise a non-NULL trace returns ER_EINVAL. */
 er_status er_set_trace(er_batch *b, void *trace);
 
 typedef struct {

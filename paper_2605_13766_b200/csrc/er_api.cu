@@ -1107,6 +1107,7 @@ er_status er_set_option(er_batch *b, int32_t option, int64_t value) {
 
 er_status er_set_trace(er_batch *b, void *trace) {
   if (!b) return ER_EINVAL;
+  if (trace && !ER_TRACE) { b->last_error = "the timeline needs a build with -DER_TRACE=1 (ER_NVCC_EXTRA)"; return ER_EINVAL; }
   b->trace = reinterpret_cast<unsigned long long *>(trace);
   b->forcing_version += 1;
   return ER_OK;

@@ -363,15 +363,18 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef ER_MBAR_SUSPEND_NS
+#define ER_MBAR_SUSPEND_NS 20000  // try_wait may suspend the warp up to this long (it wakes on the phase flip)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
       "@!P1 bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
+      "r"(phase), "n"(ER_MBAR_SUSPEND_NS)
       : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
@@ -494,8 +497,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
     const int64_t tnext = tile + gridDim.x;
     TileHead Tn;
     if (tid == 0 && tnext < p.n_tiles) Tn = load_head(p.tiles + tnext);  // overlaps the wait
+#if ER_TRACE  // measurement builds only (ER_NVCC_EXTRA=-DER_TRACE=1): the per-tile timeline
     unsigned long long *tr = (p.trace && tid == 0 && k < ER_TRACE_ITERS)
                                  ? p.trace + ((int64_t)blockIdx.x * ER_TRACE_ITERS + k) * 4 : nullptr;
+#else
+    constexpr unsigned long long *tr = nullptr;
+#endif
     if (tr) tr[0] = (gtimer() & ((1ull << 48) - 1)) | ((unsigned long long)smid() << 56);
     mbar_wait(&bar[b], (phase >> b) & 1u);
     phase ^= 1u << b;

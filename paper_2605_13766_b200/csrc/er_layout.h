@@ -212,6 +212,9 @@ struct ErStepParams {
   int32_t *rebuild;       // ... sets this flag
 };
 #define ER_TRACE_ITERS 64
+#ifndef ER_TRACE
+#define ER_TRACE 0  // per-tile timeline compiled in (measurement builds: -DER_TRACE=1)
+#endif
 
 // offsets inside a tile block (doubles)
 __host__ __device__ inline int64_t tile_node_plane(const ErTile &T, int c) { return (int64_t)c * T.nslots; }
