@@ -538,10 +538,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
       r[c] = B[c * ns + tid];
       v[c] = B[(3 + c) * ns + tid];
     }
-    // a rod's last node owns no element: its Q, w stay 0 (le would index past the element planes,
-    // into stale stage contents that the non-finite check would otherwise see)
+    // a rod's last node owns no element: its w stays 0 (le would index past the element planes,
+    // into stale stage contents that the non-finite check would otherwise see); its Q is loaded
+    // unguarded (a neighbouring in-buffer value) because nothing reads it: rotations, kinematics
+    // and stores are per element, and no slot reads Q from a rod's last node
 #pragma unroll
-    for (int c = 0; c < ER_QST; ++c) Q[c] = si.has_e ? B[6 * ns + c * nel + le] : 0.0;
+    for (int c = 0; c < ER_QST; ++c) Q[c] = B[6 * ns + c * nel + le];
 #pragma unroll
     for (int c = 0; c < 3; ++c) w[c] = si.has_e ? B[6 * ns + (ER_QST + c) * nel + le] : 0.0;
     complete_d3(Q);
