@@ -367,6 +367,18 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 #define ER_MBAR_SUSPEND_NS 20000  // try_wait may suspend the warp up to this long (it wakes on the phase flip)
 #endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+#if ER_MBAR_SUSPEND_NS == 0
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+  return;
+#endif
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
