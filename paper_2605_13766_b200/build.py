@@ -30,13 +30,16 @@ def _deps():
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(p) for p in _deps()):
+    extra = os.environ.get("ER_NVCC_EXTRA", "").split()  # experiments only (e.g. -DER_...)
+    stamp = OUT + ".flags"  # the extra flags the library was built with: a change forces a rebuild
+    same_flags = os.path.exists(stamp) and open(stamp).read() == " ".join(extra)
+    if (not force and same_flags and os.path.exists(OUT)
+            and os.path.getmtime(OUT) >= max(os.path.getmtime(p) for p in _deps())):
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     objdir = os.path.join(os.path.dirname(OUT), "obj")
     os.makedirs(objdir, exist_ok=True)
     objs, procs = [], []
-    extra = os.environ.get("ER_NVCC_EXTRA", "").split()  # experiments only (e.g. -DER_...)
     for src in SOURCES:  # the translation units compile concurrently
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
         cmd = [NVCC, *[f for f in FLAGS if f != "-shared"], *FILE_FLAGS.get(src, []), *extra, "-c",
@@ -56,6 +59,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed linking libelasticarod.so")
     os.replace(OUT + ".tmp", OUT)
+    with open(stamp, "w") as f:
+        f.write(" ".join(extra))
     return OUT
 
 
