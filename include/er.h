@@ -179,8 +179,9 @@ er_status er_set_forcing(er_batch *b, const er_forcing *f);
  *               (rod by rod, N_r + 1 nodes each), added to F_i; or NULL for none.
  *  elem_couple  [n_elems_total*3] local-frame (director basis) couple on each element (N m),
  *               added to C_j; or NULL for none.
- * src_mem says where both arrays live (ER_DEVICE: device pointers on the batch's device, read
- * stream-ordered, no host synchronisation, so a solver can update them every step).  Values are
+ * src_mem says where both arrays live (ER_DEVICE: device pointers on the batch's device, read on
+ * the batch's stream (er_query().stream) without host synchronisation, so a solver can update
+ * them every step; the caller orders their producer before the call -- same stream or an event).  Values are
  * copied; they stay in force, constant in time, until the next call (NULL clears that array).
  * Independent of er_set_forcing.  Not validated: non-finite loads surface as ER_F_NONFINITE at the
  * next er_step.  They do no work in the diagnostics' potential energies (non-conservative).
@@ -205,7 +206,8 @@ er_status er_get_state(er_batch *b, int32_t dst_mem, double *positions, double *
 
 /* ------------------------------------------------------------------------- er_set_state
  * Overwrite the state (resume from a snapshot taken with er_get_state, or inject a state).
- * src_mem says where the arrays live; any pointer may be NULL to keep that quantity; t may be
+ * src_mem says where the arrays live (ER_DEVICE arrays are read on the batch's stream: the caller
+ * orders their producer before the call); any pointer may be NULL to keep that quantity; t may be
  * NULL to keep the time.  Deliberately NOT validated (no orthonormality / finiteness check):
  * a bad state surfaces as ER_EUNSTABLE at the next er_step.  Clamped poses are unchanged
  * (call er_set_bc again to re-pose).   Errors: ER_EINVAL (bad src_mem), ER_ECUDA.

@@ -290,6 +290,10 @@ class RodBatch:
         d.device = int(device)
         d.stream = None if stream is None else C.c_void_p(int(getattr(stream, "cuda_stream", stream)))
         d.tile_slots = int(tile_slots)
+        if d.src_mem == ER_DEVICE:  # the library reads the arrays on its own stream: finish their producers
+            import torch
+            torch.cuda.current_stream(int(device)).synchronize()
+        self.device = int(device)
         self.handle = er_create_batch(d)
         self.n_rods = d.n_rods
         info = er_query(self.handle)
@@ -342,7 +346,10 @@ class RodBatch:
         for a, rows in ((node_force, self.n_nodes_total), (elem_couple, self.n_elems_total)):
             if a is not None and tuple(a.shape) != (rows, 3):
                 raise ValueError(f"external load of shape {tuple(a.shape)}, expected ({rows}, 3)")
-        er_set_external_loads(self.handle, mems.pop() if mems else ER_HOST, pf, pc)
+        mem = mems.pop() if mems else ER_HOST
+        if mem == ER_DEVICE:
+            self._after_torch()
+        er_set_external_loads(self.handle, mem, pf, pc)
 
     def set_forcing_from(self, w):
         self.set_forcing(gravity=getattr(w, "gravity", (0, 0, 0)), damping=getattr(w, "damping", None),
@@ -409,12 +416,22 @@ class RodBatch:
         ptrs = [None if b is None else (b.data_ptr() if _is_torch(b) else b.ctypes.data) for b in bufs]
         return er_get_state(self.handle, ER_DEVICE if dev else ER_HOST, *ptrs)
 
+    def _after_torch(self):
+        """Order the batch's stream after torch's current stream (device tensors handed to the
+        library are read on the batch's stream)."""
+        import torch
+        cur = torch.cuda.current_stream(self.device)
+        if cur.cuda_stream != (self.info().stream or 0):
+            torch.cuda.ExternalStream(self.info().stream, device=self.device).wait_stream(cur)
+
     def set_state(self, positions=None, velocities=None, directors=None, omega=None, t=None):
         """Overwrite (parts of) the state; numpy -> host source, torch CUDA tensors -> device."""
         k = _Keep()
         bufs = [positions, velocities, directors, omega]
         dev = any(x is not None and _is_torch(x) and x.is_cuda for x in bufs)
         ptrs = [k.any(x)[0] if dev else k.host(x) for x in bufs]
+        if dev:
+            self._after_torch()
         er_set_state(self.handle, ER_DEVICE if dev else ER_HOST, *ptrs, t=t)
 
     def diagnostics(self) -> np.ndarray:

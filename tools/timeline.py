@@ -1,4 +1,6 @@
-"""Per-CTA timeline of the persistent kernel (globaltimer stamps) for one launch."""
+"""Per-CTA timeline of the persistent kernel (globaltimer stamps) for one launch.  Needs a
+measurement build: ER_NVCC_EXTRA=-DER_TRACE=1 python paper_2605_13766_b200/build.py (the
+production kernel has no timeline code; er_set_trace returns ER_EINVAL there)."""
 import os, sys, json, collections
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
