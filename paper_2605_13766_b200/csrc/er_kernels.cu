@@ -32,6 +32,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "er_layout.h"
@@ -1318,6 +1319,9 @@ cudaError_t launch_long_persistent(const ErStepParams *p, int64_t tile0, int64_t
   int ncl = 0;
   e = cudaOccupancyMaxActiveClusters(&ncl, k, &cfg);
   if (e != cudaSuccess) return e;
+  if (std::getenv("ER_DEBUG_LONG"))
+    fprintf(stderr, "[long_persistent] nseg %d: %d clusters resident (%d CTAs), %lld rods\n", nseg, ncl, ncl * nseg,
+            (long long)n_rods);
   ncl = (int)std::max<int64_t>(1, std::min<int64_t>(n_rods, ncl));
   cfg.gridDim = dim3((unsigned)(ncl * nseg), 1, 1);
   e = cudaLaunchKernelEx(&cfg, k, *p, tile0, n_rods);
