@@ -149,18 +149,36 @@ def shard(w, rank, world, scaling):
     return w.subset(np.arange(cuts[rank], cuts[rank + 1]))
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def oracle_rate(w, n_rods, n_steps, seed=3):
     """The oracle as it stands (single-threaded C), on a seeded rod sample (for contact workloads:
-    the first whole stack, an independent sub-problem)."""
+    the first whole stack, an independent sub-problem), pinned to one host core while it runs
+    (taskset)."""
     import oracle
     if getattr(w, "contact", None) is not None:
         rods = np.arange(min(w.n_rods, W.FIBRES["layers"] * W.FIBRES["per_layer"]))
     else:
         rods = W.sample_rods(w, n_rods, seed=seed)
     ws = w.subset(rods)
-    t0 = time.perf_counter()
-    st, s, _, _ = oracle.step(ws, n_steps=n_steps)
-    dt = time.perf_counter() - t0
+    aff = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
+    if aff:
+        os.sched_setaffinity(0, {min(aff)})
+    try:
+        t0 = time.perf_counter()
+        st, s, _, _ = oracle.step(ws, n_steps=n_steps)
+        dt = time.perf_counter() - t0
+    finally:
+        if aff:
+            os.sched_setaffinity(0, aff)
     return ws.n_elems_total * n_steps / dt, dt, ws
 
 
@@ -371,9 +389,9 @@ def main():
             cs = a.cpu_sample_steps if getattr(wfull, "contact", None) is None else max(5, a.cpu_sample_steps // 6)
             rate, secs, ws = oracle_rate(wfull, a.cpu_sample_rods, cs)
             what = "seeded rods" if getattr(wfull, "contact", None) is None else "rods (one whole stack, exhaustive contact search)"
-            cpu = {"value": rate, "unit": "element-steps/s", "cores": 1, "kind": "oracle",
+            cpu = {"value": rate, "unit": "element-steps/s", "cores": 1, "kind": "oracle", "cpu": cpu_model(),
                    "sample": f"{ws.n_rods} {what} of {a.config} x {cs} steps "
-                             f"({ws.n_elems_total * cs:.3g} element-steps, {secs:.1f} s, 1 thread)"}
+                             f"({ws.n_elems_total * cs:.3g} element-steps, {secs:.1f} s, 1 thread pinned to one core)"}
             if not a.no_cpu_fanout and getattr(wfull, "contact", None) is None:
                 try:
                     cpu["fanout"] = oracle_fanout_rate(wfull, 512, a.cpu_sample_steps)
