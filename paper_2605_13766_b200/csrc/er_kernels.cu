@@ -776,7 +776,7 @@ struct ClusterSync {
 #define ER_LONG_MINB 2
 #endif
 template <int BLOCK, int FEAT>
-__global__ void __launch_bounds__(BLOCK, ER_LONG_MINB) long_kernel(const ErStepParams p, int64_t tile0) {
+__global__ void __launch_bounds__(BLOCK, BLOCK > 256 ? 1 : ER_LONG_MINB) long_kernel(const ErStepParams p, int64_t tile0) {
   constexpr int XS = BLOCK + 2;
   extern __shared__ __align__(16) double sm[];
   double *X = sm + 1;
@@ -850,7 +850,7 @@ __global__ void __launch_bounds__(BLOCK, ER_LONG_MINB) long_kernel(const ErStepP
 // with the tile kernel's TMA double-buffered pipeline; a cluster barrier replaces the stage
 // barrier (a neighbour's halo writes land in this CTA's stage area).
 template <int BLOCK, int FEAT>
-__global__ void __launch_bounds__(BLOCK, 2) long_persistent(const ErStepParams p, int64_t tile0, int64_t n_rods) {
+__global__ void __launch_bounds__(BLOCK, BLOCK > 256 ? 1 : 2) long_persistent(const ErStepParams p, int64_t tile0, int64_t n_rods) {
   using SG = Stage<BLOCK, FEAT, true>;
   constexpr int XS = SG::XS;
   extern __shared__ __align__(16) double sm[];

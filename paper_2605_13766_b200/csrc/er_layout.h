@@ -105,7 +105,9 @@ struct __align__(16) ErTile {
   int32_t seg;     // long rods (> 511 elements): segment k of the rod's nseg tiles of
   int32_t nseg;    //   ER_LONG_SEG slots each, advanced by a thread-block cluster; else 0 / 1
 };
+#ifndef ER_LONG_SEG
 #define ER_LONG_SEG 256     // slots per segment of a long rod (one CTA of the cluster)
+#endif
 #define ER_LONG_MAXSEG 16   // cluster size limit (non-portable 16 on sm_100a): N + 1 <= 4096
 
 // Contact law (DESIGN §3 #27): penalty normal force with damping, regularised
