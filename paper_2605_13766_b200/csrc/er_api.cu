@@ -326,6 +326,7 @@ ErStepParams params_of(const er_batch *b) {
   std::memset(&p, 0, sizeof p);
   p.state = b->d_state;
   p.rec = b->d_rec; p.eoff = b->d_eoff; p.tiles = b->d_tiles; p.n_tiles = b->n_tiles;
+  p.state_doubles = b->state_doubles;
   p.ord = b->d_ord; p.eoffc = b->d_eoffc;
   p.gpar = b->d_gpar; p.ng = b->ng; p.sigma0 = b->d_sigma0; p.mag = b->d_mag; p.ne = b->ne;
   p.fext = b->d_fext; p.cext = b->d_cext;

@@ -474,6 +474,8 @@ __device__ __forceinline__ void issue_tile(const ErStepParams &p, const TileHead
   const int64_t ra = T.r0 & ~1ll;
   const uint32_t ceo = (uint32_t)(((T.r0 + T.nr + 2) & ~1ll) - ra);
   const uint32_t bytes = 8u * cs + (uint32_t)T.nr * ER_REC * 8u + 8u * ceo + (uint32_t)sizeof(ErTile);
+  ER_CHECK(cs <= (uint32_t)SG::PLANES && T.nr <= SG::RMAX && ceo <= (uint32_t)SG::RMAX + 4);
+  ER_CHECK(T.boff >= 0 && T.boff + cs <= p.state_doubles + 64);
   mbar_expect_tx(bar, bytes);
   bulk_g2s(B, p.state + T.boff, 8u * cs, bar);
   bulk_g2s(B + SG::RECOFF, p.rec + (int64_t)T.r0 * ER_REC, (uint32_t)T.nr * ER_REC * 8u, bar);
@@ -544,6 +546,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
     // ---- stage -> registers (tile-local SoA planes)
     const int ns = T.nslots, nel = T.nel;
     const int le = tid - lo;
+    ER_CHECK(6 * ns + (ER_EPL - 1) * nel + le < SG::BUFD && (!si.has_e || (le >= 0 && le < nel)));
     const int64_t boff = T.boff;
     double r[3], v[3], Q[9], w[3], k0s[3] = {0.0, 0.0, 0.0};
 #pragma unroll
@@ -645,6 +648,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
       // bulk copies move multiples of 16 bytes; with an odd element count the block's last
       // double (d1, d2, w planes: 9 nel doubles) goes with a plain store
       const uint32_t tot = (uint32_t)(6 * ns + ER_EPL * nel);
+      ER_CHECK(boff + tot <= p.state_doubles && SG::OUTOFF + tot <= (uint32_t)SG::PLANES);
       bulk_s2g(p.state + boff, O, 8u * (tot & ~1u));
       bulk_commit();
       if (tot & 1u) p.state[boff + tot - 1] = O[tot - 1];
@@ -962,6 +966,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCK > 256 ? 1 : 2) long_persistent(co
       // bulk copies move multiples of 16 bytes; with an odd element count the block's last
       // double (d1, d2, w planes: 9 nel doubles) goes with a plain store
       const uint32_t tot = (uint32_t)(6 * ns + ER_EPL * nel);
+      ER_CHECK(boff + tot <= p.state_doubles && SG::OUTOFF + tot <= (uint32_t)SG::PLANES);
       bulk_s2g(p.state + boff, O, 8u * (tot & ~1u));
       bulk_commit();
       if (tot & 1u) p.state[boff + tot - 1] = O[tot - 1];
@@ -1127,6 +1132,7 @@ __global__ void pack_planes(const double *__restrict__ src, double *__restrict__
     const int64_t r = ord[pr];
     const int64_t c0 = eoffc[r] + (nodes ? r : 0), p0 = eoffp[pr] + (nodes ? pr : 0);
     const int64_t cnt = 3 * (eoffc[r + 1] - eoffc[r] + nodes);
+    ER_CHECK(p0 + cnt / 3 <= stride);
     for (int64_t q = lane; q < cnt; q += 32) {
       const int64_t row = q / 3;
       dst[(q - 3 * row) * stride + p0 + row] = src[3 * c0 + q];
@@ -1152,6 +1158,7 @@ __global__ void canon_tiles(const ErStepParams p, double *canon, int field, int 
     count = tile_nvor(T); off = tile_vor_plane(T, 0); shift = -1;
   }
   double *blk = p.state + T.boff + off;
+  ER_CHECK(T.boff + off + (int64_t)(field == FIELD_DIR ? ER_QST : 3) * count <= p.state_doubles);
   for (int q = 0; q < T.nr; ++q) {
     const int64_t pr = T.r0 + q, cr = p.ord[pr];
     int64_t n = p.eoff[pr + 1] - p.eoff[pr] + shift;                           // rows of this rod

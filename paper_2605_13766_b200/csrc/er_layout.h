@@ -180,6 +180,7 @@ struct ErStepParams {
   const int64_t *eoffc;    // [n_rods+1] canonical element offsets
   const ErTile *tiles;
   int64_t n_tiles;
+  int64_t state_doubles;  // size of `state` (bounds checks of -DER_CHECK_BOUNDS=1 builds)
   const double *gpar;     // may be null
   int64_t ng;             // gpar plane stride
   const double *sigma0;   // may be null, planes stride ne
@@ -217,6 +218,16 @@ struct ErStepParams {
 #ifndef ER_TRACE
 #define ER_TRACE 0  // per-tile timeline compiled in (measurement builds: -DER_TRACE=1)
 #endif
+#ifndef ER_CHECK_BOUNDS
+#define ER_CHECK_BOUNDS 0  // debug builds (-DER_CHECK_BOUNDS=1): index checks that trap (the pool has no sanitizer)
+#endif
+#define ER_CHECK(cond)                                                      \
+  do {                                                                      \
+    if (ER_CHECK_BOUNDS && !(cond)) {                                       \
+      printf("ER_CHECK failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);   \
+      __trap();                                                             \
+    }                                                                       \
+  } while (0)
 
 // offsets inside a tile block (doubles)
 __host__ __device__ inline int64_t tile_node_plane(const ErTile &T, int c) { return (int64_t)c * T.nslots; }
