@@ -9,7 +9,11 @@ in the local frame, constant until changed).
 - a uniform couple about the local d3 spins a straight free rod rigidly: omega_3 = c t / J3 with
   J3 = rho lhat (I1 + I2), rotation angle c t^2 / (2 J3) (position Verlet is exact for a constant
   angular acceleration), with d3 along lab x so that a lab-frame reading of c-bar fails;
-- all-zero loads are the same trajectory, bitwise, as no loads.
+- all-zero loads are the same trajectory, bitwise, as no loads;
+- beam theory: a uniform distributed force q on a cantilever (node shares q lhat, ends q lhat/2)
+  deflects the tip by q L^4/(8EI) + q L^2/(2 ac G A), and a uniform distributed couple c about
+  the local d1 rotates the tip by c L^2/(2EI) toward -y (right-handed), both at the effective
+  length L - lhat/2 of the element-0 clamp (DESIGN §3 #15) to < 0.1%.
 """
 import dataclasses
 
@@ -85,3 +89,39 @@ def test_zero_loads_are_no_loads(orc):
     for x, y in ((a.positions, b.positions), (a.velocities, b.velocities), (a.directors, b.directors),
                  (a.omega, b.omega)):
         assert np.array_equal(x, y)
+
+
+def _relaxed(orc, w):
+    st, s, _, _ = orc.step(w, n_steps=250000, dt=1e-4)
+    assert s == 0 and np.max(np.abs(st.velocities)) < 1e-5
+    return st
+
+
+def test_distributed_force_cantilever(orc):
+    N, L, q = 100, 1.0, 1e-3
+    lh = L / N
+    w = rod(N=N, L=L, r=0.01, clamp=0, nu=1.2)
+    f = np.zeros((N + 1, 3))
+    f[1:N, 0] = q * lh
+    f[0, 0] = f[N, 0] = q * lh / 2
+    st = _relaxed(orc, dataclasses.replace(w, ext_force=f))
+    E, I, A, G, ac = w.youngs[0], w.I1[0], w.area[0], w.shear_mod[0], w.alpha_c[0]
+    Le = L - lh / 2
+    expect = q * Le ** 4 / (8 * E * I) + q * Le ** 2 / (2 * ac * G * A)
+    assert abs(st.positions[-1, 0] / expect - 1) < 1e-3, st.positions[-1, 0] / expect - 1
+    assert abs(st.positions[-1, 1]) < 1e-12
+
+
+def test_distributed_couple_cantilever(orc):
+    N, L, c = 100, 1.0, 2e-4
+    lh = L / N
+    w = rod(N=N, L=L, r=0.01, clamp=0, nu=1.2)
+    C = np.zeros((N, 3))
+    C[:, 0] = c * lh                                 # about the local d1 (= lab x here)
+    st = _relaxed(orc, dataclasses.replace(w, ext_couple=C))
+    E, I = w.youngs[0], w.I1[0]
+    d3r, d3t = st.directors[0, 2], st.directors[-1, 2]
+    theta = np.arccos(np.clip(d3r @ d3t, -1.0, 1.0))
+    expect = c * (L - lh / 2) ** 2 / (2 * E * I)
+    assert abs(theta / expect - 1) < 1e-3, theta / expect - 1
+    assert d3t[1] < 0 and st.positions[-1, 1] < 0 and abs(st.positions[-1, 0]) < 1e-12
