@@ -160,3 +160,27 @@ def test_clear_restores_load_free_path(er):
     with er.RodBatch(w) as b:
         with pytest.raises(ValueError):
             b.set_external_loads(f[:-1], None)
+
+
+def test_distributed_load_cantilever_statics(er):
+    """A cantilever under a uniform distributed force (node shares q lhat, ends q lhat/2) relaxes
+    on the GPU (temporal blocking, 250,000 steps) to the beam-theory tip deflection
+    q L^4/(8EI) + q L^2/(2 ac G A) at the clamp's effective length -- the oracle pin of
+    tests/test_oracle_external.py, reached by the CUDA path."""
+    from rodkit import rod
+    N, L, q = 100, 1.0, 1e-3
+    lh = L / N
+    w = rod(N=N, L=L, r=0.01, clamp=0, nu=1.2, dt=1e-4)
+    f = np.zeros((N + 1, 3))
+    f[1:N, 0] = q * lh
+    f[0, 0] = f[N, 0] = q * lh / 2
+    w = dataclasses.replace(w, ext_force=f)
+    with er.RodBatch(w) as b:
+        b.set_option(er.ER_OPT_STEPS_PER_LAUNCH, 1000)
+        b.step(250000, w.dt)
+        pos, vel, _, _, _ = b.get_state()
+    assert np.max(np.abs(vel)) < 1e-5
+    E, I, A, G, ac = w.youngs[0], w.I1[0], w.area[0], w.shear_mod[0], w.alpha_c[0]
+    Le = L - lh / 2
+    expect = q * Le ** 4 / (8 * E * I) + q * Le ** 2 / (2 * ac * G * A)
+    assert abs(pos[-1, 0] / expect - 1) < 1e-3, pos[-1, 0] / expect - 1
