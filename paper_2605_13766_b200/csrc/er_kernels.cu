@@ -426,6 +426,8 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
 // Stage geometry of the persistent kernel: per buffer the tile's state block (<= 18 or 21
@@ -495,6 +497,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
     fence_mbar_init();
   }
   __syncthreads();
+  griddep_wait();  // (programmatic launch) the previous kernel's results are complete and visible
   int64_t tile = blockIdx.x;
   if (tid == 0 && tile < p.n_tiles) issue_tile<BLOCK, FEAT>(p, load_head(p.tiles + tile), p.tiles + tile, sm, &bar[0]);
   const double t0 = launch_t0(p);
@@ -512,6 +515,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
     const int64_t tnext = tile + gridDim.x;
     TileHead Tn;
     if (tid == 0 && tnext < p.n_tiles) Tn = load_head(p.tiles + tnext);  // overlaps the wait
+    if (tnext >= p.n_tiles) griddep_launch_dependents();  // this CTA's last tile: the next step's grid may launch
 #if ER_TRACE  // measurement builds only (ER_NVCC_EXTRA=-DER_TRACE=1): the per-tile timeline
     unsigned long long *tr = (p.trace && tid == 0 && k < ER_TRACE_ITERS)
                                  ? p.trace + ((int64_t)blockIdx.x * ER_TRACE_ITERS + k) * 4 : nullptr;
@@ -1267,8 +1271,22 @@ cudaError_t launch_persistent(const ErStepParams &p, cudaStream_t st) {
   int n_sm = 148;
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
   const int64_t g = std::min<int64_t>(p.n_tiles, (int64_t)n_sm * grid_per_sm[dev]);
-  k<<<(unsigned)g, BLOCK, sm, st>>>(p);
-  return cudaGetLastError();
+  // programmatic dependent launch: this grid's CTAs may start (and set up their stage barriers)
+  // while the previous kernel on the stream drains; they read no global memory before
+  // griddepcontrol.wait (which waits for the previous grids to complete and flush)
+  static const bool pdl = std::getenv("ER_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)g, 1, 1);
+  cfg.blockDim = dim3(BLOCK, 1, 1);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k, p);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // feat: GENERAL | KAPPA0 | CONTACT bits, plus at most one of FEAT_EXTRA / FEAT_ACT (24 kernels)
