@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg3", choices=list(W.CONFIG_NAMES) + list(W.EXTRA_CONFIGS))
+    ap.add_argument("--sweeps", type=int, default=0,
+                    help="ER_OPT_SWEEPS_PER_LAUNCH (0 = the library default)")
     ap.add_argument("--steps-per-launch", type=int, default=1,
                     help="1 = every step streams the state through HBM (the B_min design); "
                          ">1 = temporal blocking (SURVEY NEXT-1)")
@@ -270,6 +272,8 @@ def main():
     b = er.RodBatch(w, device=local, stream=stream)
     if a.steps_per_launch > 1:
         b.set_option(er.ER_OPT_STEPS_PER_LAUNCH, a.steps_per_launch)
+    if a.sweeps > 0:
+        b.set_option(er.ER_OPT_SWEEPS_PER_LAUNCH, a.sweeps)
     dt = w.dt
 
     # warm-up (untimed)
@@ -407,6 +411,7 @@ def main():
                                    f"({wfull.n_elems_total} elements), dt={wfull.dt}",
                        "rods_per_gpu": w.n_rods, "elements_per_gpu": w.n_elems_total,
                        "steps_per_launch": a.steps_per_launch,
+                       "sweeps_per_launch": a.sweeps or er.ER_DEFAULT_SWEEPS,
                        "l2": "inputs larger than L2 (state %.2f GB per GPU vs 126 MB L2)" % (
                            b.info().device_bytes / 1e9),
                        "parallelism": (f"weak: each of {world} GPU(s) advances its own {a.config} batch"

@@ -325,11 +325,19 @@ typedef enum {
                                   4: as 0 but results go from registers straight to HBM
                                   (plain coalesced stores instead of the smem stage + TMA
                                   bulk store; ablation, cfg3-type batches only). */
-  ER_OPT_PHASE_TIMING = 3      /* measurement aid: 1 = er_step records a CUDA event pair (on the
+  ER_OPT_PHASE_TIMING = 3,     /* measurement aid: 1 = er_step records a CUDA event pair (on the
                                   handle's stream) around every step-kernel launch and every
-                                  contact evaluation, summed into er_get_phase_times; setting
-                                  the option (0 or 1) resets the sums.  Default 0. */
+                                  contact evaluation, summed into er_get_phase_times (a launch
+                                  of S sweeps counts as S launches); setting the option (0 or 1)
+                                  resets the sums.  Default 0. */
+  ER_OPT_SWEEPS_PER_LAUNCH = 4 /* S >= 1: without contact, one persistent launch streams all rod
+                                  tiles through HBM S times (S steps, each of ER_OPT_STEPS_PER_
+                                  LAUNCH on-chip steps) -- the work of S launches without their
+                                  boundaries or host submissions; identical results.  1 = one
+                                  launch per step (CUDA-graph replays of 32).  Default
+                                  ER_DEFAULT_SWEEPS. */
 } er_option;
+#define ER_DEFAULT_SWEEPS 128
 er_status er_set_option(er_batch *b, int32_t option, int64_t value);
 
 /* Device time of er_step's phases since ER_OPT_PHASE_TIMING was last set (CUDA events). */

@@ -98,6 +98,7 @@ struct er_batch {
   std::vector<LongGroup> long_groups;
   double t = 0.0;
   int64_t steps_per_launch = 1;
+  int64_t sweeps = ER_DEFAULT_SWEEPS;  // ER_OPT_SWEEPS_PER_LAUNCH
   int kernel_mode = 0;
   int64_t launches = 0;
   int64_t device_bytes = 0;
@@ -327,6 +328,7 @@ ErStepParams params_of(const er_batch *b) {
   p.state = b->d_state;
   p.rec = b->d_rec; p.eoff = b->d_eoff; p.tiles = b->d_tiles; p.n_tiles = b->n_tiles;
   p.state_doubles = b->state_doubles;
+  p.sweeps = 1;
   p.ord = b->d_ord; p.eoffc = b->d_eoffc;
   p.gpar = b->d_gpar; p.ng = b->ng; p.sigma0 = b->d_sigma0; p.mag = b->d_mag; p.ne = b->ne;
   p.fext = b->d_fext; p.cext = b->d_cext;
@@ -1090,6 +1092,11 @@ er_status er_set_option(er_batch *b, int32_t option, int64_t value) {
     b->steps_per_launch = value;
     return ER_OK;
   }
+  if (option == ER_OPT_SWEEPS_PER_LAUNCH) {
+    if (value < 1 || value > (1 << 20)) { b->last_error = "sweeps_per_launch must be in [1, 2^20]"; return ER_EINVAL; }
+    b->sweeps = value;
+    return ER_OK;
+  }
   if (option == ER_OPT_PHASE_TIMING) {
     if (value != 0 && value != 1) { b->last_error = "phase timing must be 0 or 1"; return ER_EINVAL; }
     b->timing = value == 1;
@@ -1193,9 +1200,27 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
     }
     done = n_steps;
   }
+  const int64_t spl = b->steps_per_launch;
+  // Sweeps: one persistent launch streams every tile through HBM S times (S steps of spl on-chip
+  // steps each); long-rod clusters advance the same steps in their own launch.
+  if (!b->contact_on && b->kernel_mode == 0 && b->sweeps > 1) {
+    while (n_steps - done >= spl) {
+      const int64_t S = std::min<int64_t>(b->sweeps, (n_steps - done) / spl);
+      p.n_steps = (int32_t)spl;
+      p.sweeps = (int32_t)S;
+      p.t = t;
+      const int m0 = mark(b);
+      CK(er_launch_step(&p, b->block, 0, feat, b->stream), "step kernel");
+      b->launches += 1;
+      interval(b, m0, mark(b), 0, (int)S);
+      CK(launch_long(spl * S, t), "long-rod kernel");
+      for (int64_t q = 0; q < spl * S; ++q) { const double th = t + 0.5 * dt; t = th + 0.5 * dt; }
+      done += spl * S;
+    }
+    p.sweeps = 1;
+  }
   // Streaming steps as CUDA-graph launches of ER_GRAPH_LAUNCHES step launches each (the time is
   // carried on the device between launches); the rest as plain launches below.
-  const int64_t spl = b->steps_per_launch;
   if (!b->contact_on && b->kernel_mode == 0 && n_steps - done >= ER_GRAPH_LAUNCHES * spl &&
       !std::getenv("ER_NO_STEP_GRAPH")) {
     const int64_t key = ((b->forcing_version * 32 + feat) << 31) + spl;

@@ -335,7 +335,8 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
 __device__ __forceinline__ double launch_t0(const ErStepParams &p) { return p.tdev ? p.tdev[p.tpar] : p.t; }
 __device__ __forceinline__ void advance_tdev(const ErStepParams &p, double t0) {
   if (!p.tdev || blockIdx.x != 0 || threadIdx.x != 0) return;
-  for (int st = 0; st < p.n_steps; ++st) {
+  const int64_t n = (int64_t)p.n_steps * (p.sweeps > 1 ? p.sweeps : 1);
+  for (int64_t st = 0; st < n; ++st) {
     const double th = t0 + 0.5 * p.h;
     t0 = th + 0.5 * p.h;
   }
@@ -425,6 +426,8 @@ __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t by
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all_but_newest() { asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
@@ -509,13 +512,26 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
   //   read b^1, load tile k+1 into b^1] -> steps (exchange in b) -> barrier -> results to b ->
   //   barrier -> [t0: bulk store b -> HBM].  Loads and stores are TMA bulk copies, so no warp
   //   ever waits on HBM except for the (prefetched) load of its next tile.
-  for (int k = 0; tile < p.n_tiles; tile += gridDim.x, ++k) {
+  // Sweeps (p.sweeps > 1): the launch streams its tiles through the pipeline that many times, one
+  // step (p.n_steps on-chip steps) per pass and the state through HBM every pass -- the work of
+  // that many launches without their boundaries.  The prefetch wraps to the CTA's first tile:
+  // that tile's store (a pass ago) must have completed first (all store groups but the newest),
+  // or, for a CTA with a single tile, the reload waits for the tile's own store.
+  const int sweeps = (!DSTORE && p.sweeps > 1) ? p.sweeps : 1;
+  const int64_t m_tiles = (p.n_tiles - (int64_t)blockIdx.x + gridDim.x - 1) / gridDim.x;  // per pass
+  int sw = 0;
+  double t_sw = t0;  // time at the start of this pass
+  for (int k = 0; tile < p.n_tiles; ++k) {
     const int b = k & 1;
     double *B = sm + b * SG::BUFD;
-    const int64_t tnext = tile + gridDim.x;
+    int64_t tnext = tile + gridDim.x;
+    int swn = sw;
+    if (tnext >= p.n_tiles) { tnext = blockIdx.x; swn = sw + 1; }
+    const bool has_next = swn < sweeps;
+    const bool defer = has_next && tnext == tile;  // one tile per CTA: reload after its own store
     TileHead Tn;
-    if (tid == 0 && tnext < p.n_tiles) Tn = load_head(p.tiles + tnext);  // overlaps the wait
-    if (tnext >= p.n_tiles) griddep_launch_dependents();  // this CTA's last tile: the next step's grid may launch
+    if (tid == 0 && has_next) Tn = load_head(p.tiles + tnext);  // overlaps the wait
+    if (!has_next) griddep_launch_dependents();  // this CTA's last tile: the next step's grid may launch
 #if ER_TRACE  // measurement builds only (ER_NVCC_EXTRA=-DER_TRACE=1): the per-tile timeline
     unsigned long long *tr = (p.trace && tid == 0 && k < ER_TRACE_ITERS)
                                  ? p.trace + ((int64_t)blockIdx.x * ER_TRACE_ITERS + k) * 4 : nullptr;
@@ -581,7 +597,12 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
 #ifdef ER_TRACE_FINE
     if (tr) tr[2] = gtimer() & ((1ull << 48) - 1);
 #endif
-    if (tid == 0 && tnext < p.n_tiles) {
+    if (tid == 0 && has_next && !defer) {
+      if (swn != sw) {  // wrapping to the next pass: the first tile's store must have landed
+        if (m_tiles <= 2) bulk_wait_all();   // it is the newest store group
+        else bulk_wait_all_but_newest();     // the newest group is tile k-1's
+        fence_proxy_async_all();             // (and the odd-tail plain store) before the reload
+      }
       bulk_wait_read_all();  // the bulk store of tile k-1 has finished reading buffer b^1
       issue_tile<BLOCK, FEAT>(p, Tn, p.tiles + tnext, sm + (b ^ 1) * SG::BUFD, &bar[b ^ 1]);
     }
@@ -589,7 +610,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
     if (tr) tr[3] = gtimer() & ((1ull << 48) - 1);
 #endif
     // ---- the steps
-    double t = t0;
+    double t = t_sw;
     unsigned fbits = 0;
     if (FEAT & FEAT_CONTACT) {
       // contact mode: the state arrives after drift-1 (contact forces were evaluated there);
@@ -629,8 +650,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
 #ifndef ER_TRACE_FINE
       if (tr) tr[3] = gtimer() & ((1ull << 48) - 1);
 #endif
-      continue;
-    }
+    } else {
     // ---- registers -> stage (block layout at OUTOFF) -> HBM with one TMA bulk store
     double *O = B + SG::OUTOFF;
     if (si.active) {
@@ -660,6 +680,20 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
 #ifndef ER_TRACE_FINE
     if (tr) tr[3] = gtimer() & ((1ull << 48) - 1);
 #endif
+    }
+    if (tid == 0 && defer) {  // single-tile CTA: its next pass reads what this pass just stored
+      bulk_wait_all();
+      fence_proxy_async_all();
+      issue_tile<BLOCK, FEAT>(p, Tn, p.tiles + tnext, sm + (b ^ 1) * SG::BUFD, &bar[b ^ 1]);
+    }
+    if (swn != sw)  // next pass: one step later (the arithmetic of step_body's time update)
+      for (int st = 0; st < p.n_steps; ++st) {
+        const double th = t_sw + 0.5 * p.h;
+        t_sw = th + 0.5 * p.h;
+      }
+    sw = swn;
+    tile = tnext;
+    if (!has_next) break;
   }
   if (tid == 0) bulk_wait_all();  // stores complete before the kernel retires
   advance_tdev(p, t0);

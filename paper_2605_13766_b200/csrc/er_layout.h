@@ -200,6 +200,8 @@ struct ErStepParams {
   double b_omega;
   int32_t n_steps;        // steps in this launch
   int32_t tpar;           // with tdev: the launch reads tdev[tpar], block 0 writes tdev[tpar ^ 1]
+  int32_t sweeps;         // tile kernel: passes over all tiles in this launch (one step each), >= 1
+  int32_t pad3_;
   double t;               // time at the start of the launch (when tdev is null)
   double *tdev;           // CUDA-graph step launches: [2] device time, ping-pong
   double h;               // dt

@@ -106,3 +106,17 @@ def test_no_oracle_in_product_path():
                 s = open(os.path.join(dirpath, f)).read()
                 for pat in ("import oracle", "from oracle", "liboracle", "oracle.h", "orc_"):
                     assert pat not in s, (f, pat)
+
+
+def test_binding_constants_mirror_header(er):
+    """Every `#define ER_*` number and `ER_OPT_*` / `ER_F_*` / `ER_D_*` enumerator the binding
+    exposes equals the header's value."""
+    src = open(HEADER).read()
+    consts = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define\s+(ER_\w+)\s+(\d+)\b", src)}
+    consts.update({m.group(1): int(m.group(2)) for m in re.finditer(r"\b(ER_(?:OPT|D|F)_\w+)\s*=\s*(\d+)", src)})
+    checked = 0
+    for name, value in consts.items():
+        if hasattr(er, name):
+            assert getattr(er, name) == value, name
+            checked += 1
+    assert checked >= 8 and er.ER_DEFAULT_SWEEPS == consts["ER_DEFAULT_SWEEPS"]

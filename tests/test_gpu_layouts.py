@@ -89,3 +89,43 @@ def test_external_loads_invariant_to_layout(er, monkeypatch):
     out, _ = run(er, w, 24)
     for x, y in zip(out, ref):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("case", ["one_tile", "two_tiles", "many_tiles", "ragged_long_loads"])
+def test_sweeps_bitwise(er, case):
+    """ER_OPT_SWEEPS_PER_LAUNCH: one launch streams all tiles S times (the reload of a CTA's first
+    tile waits for its store: one, two and more tiles per CTA) -- bitwise the trajectory of one
+    launch per step, also with long-rod clusters, external loads, actuation and on-chip steps."""
+    if case == "one_tile":
+        w = W.make("cfg2", n_rods=4)
+    elif case == "two_tiles":
+        w = W.make("cfg3", n_rods=6000)          # 400 tiles on 296 CTAs: one or two per CTA
+    elif case == "many_tiles":
+        w = W.make("cfg3", n_rods=15000)
+    else:
+        w = mixed_batch(n_short=800, seed=5)
+        f, c = loads(w, seed=3)
+        w = dataclasses.replace(w, ext_force=f, ext_couple=c, act_A=np.full(w.n_rods, 0.5),
+                                act_f=np.full(w.n_rods, 3.0), act_L=0.004 * w.n_elems.astype(float))
+    with er.RodBatch(w) as b:                   # one launch per step (CUDA-graph replays)
+        b.set_option(er.ER_OPT_SWEEPS_PER_LAUNCH, 1)
+        b.step(37, w.dt)
+        ref = b.get_state()[:4]
+    for sweeps, spl in ((8, 1), (37, 1), (5, 3), (128, 1)):
+        with er.RodBatch(w) as b:
+            b.set_option(er.ER_OPT_SWEEPS_PER_LAUNCH, sweeps)
+            if spl > 1:
+                b.set_option(er.ER_OPT_STEPS_PER_LAUNCH, spl)
+            b.step(37, w.dt)
+            out = b.get_state()
+        assert out[4] == b_t(w, 37)
+        for x, y in zip(out[:4], ref):
+            assert np.array_equal(x, y), (case, sweeps, spl)
+
+
+def b_t(w, n):
+    t = float(getattr(w, "t0", 0.0))
+    for _ in range(n):
+        th = t + 0.5 * w.dt
+        t = th + 0.5 * w.dt
+    return t

@@ -436,6 +436,7 @@ def test_step_graph_bitwise(er, monkeypatch):
         if plain:
             monkeypatch.setenv("ER_NO_STEP_GRAPH", "1")
         with er.RodBatch(w) as b:
+            b.set_option(er.ER_OPT_SWEEPS_PER_LAUNCH, 1)      # one launch per step (graphs)
             b.step(70, w.dt)                                  # 2 graph launches + 6 plain steps
             b.set_option(er.ER_OPT_STEPS_PER_LAUNCH, 3)
             b.step(100, w.dt)                                 # 1 graph launch (96 steps) + 4

@@ -12,6 +12,8 @@ kernels = [int(k) for k in sys.argv[3:]] or [0]
 w = W.make(name)
 stream = torch.cuda.Stream()
 b = er.RodBatch(w, stream=stream, tile_slots=int(os.environ.get("ER_TILE", "0")))
+if os.environ.get("ER_SWEEPS"):
+    b.set_option(er.ER_OPT_SWEEPS_PER_LAUNCH, int(os.environ["ER_SWEEPS"]))
 for rep in range(3):
     for k in kernels:
         b.set_option(er.ER_OPT_KERNEL, k)

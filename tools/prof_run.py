@@ -8,6 +8,7 @@ name = sys.argv[1]; spl = int(sys.argv[2]); launches = int(sys.argv[3]); tile = 
 w = W.make(name)
 with er.RodBatch(w, tile_slots=tile) as b:
     b.set_option(er.ER_OPT_STEPS_PER_LAUNCH, spl)
+    b.set_option(er.ER_OPT_SWEEPS_PER_LAUNCH, 1)  # one launch per step: the launches ncu captures
     b.step(spl * launches, w.dt)
     torch.cuda.synchronize()
 print("ok")
