@@ -518,7 +518,6 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
   // that tile's store (a pass ago) must have completed first (all store groups but the newest),
   // or, for a CTA with a single tile, the reload waits for the tile's own store.
   const int sweeps = (!DSTORE && p.sweeps > 1) ? p.sweeps : 1;
-  const int64_t m_tiles = (p.n_tiles - (int64_t)blockIdx.x + gridDim.x - 1) / gridDim.x;  // per pass
   int sw = 0;
   double t_sw = t0;  // time at the start of this pass
   for (int k = 0; tile < p.n_tiles; ++k) {
@@ -599,7 +598,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
 #endif
     if (tid == 0 && has_next && !defer) {
       if (swn != sw) {  // wrapping to the next pass: the first tile's store must have landed
-        if (m_tiles <= 2) bulk_wait_all();   // it is the newest store group
+        if (p.n_tiles - (int64_t)blockIdx.x <= 2 * (int64_t)gridDim.x) bulk_wait_all();  // newest group
         else bulk_wait_all_but_newest();     // the newest group is tile k-1's
         fence_proxy_async_all();             // (and the odd-tail plain store) before the reload
       }
