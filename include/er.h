@@ -334,10 +334,11 @@ typedef enum {
                                   tiles through HBM S times (S steps, each of ER_OPT_STEPS_PER_
                                   LAUNCH on-chip steps) -- the work of S launches without their
                                   boundaries or host submissions; identical results.  1 = one
-                                  launch per step (CUDA-graph replays of 32).  Default
-                                  ER_DEFAULT_SWEEPS. */
+                                  launch per step (CUDA-graph replays of 32).  0 (default,
+                                  ER_DEFAULT_SWEEPS): 128 for small batches (at most 4 tiles per
+                                  CTA of the grid), else 1. */
 } er_option;
-#define ER_DEFAULT_SWEEPS 128
+#define ER_DEFAULT_SWEEPS 0
 er_status er_set_option(er_batch *b, int32_t option, int64_t value);
 
 /* Device time of er_step's phases since ER_OPT_PHASE_TIMING was last set (CUDA events). */

@@ -24,7 +24,7 @@ ER_OK, ER_EINVAL, ER_EUNSTABLE, ER_EIO, ER_ENOMEM, ER_ECUDA = range(6)
 ER_HOST, ER_DEVICE = 0, 1
 ER_F_NONFINITE, ER_F_DEGENERATE, ER_F_ANTIPODAL, ER_F_OVERSPEED, ER_F_CONTACT = 1, 2, 4, 8, 16
 ER_OPT_STEPS_PER_LAUNCH, ER_OPT_KERNEL, ER_OPT_PHASE_TIMING, ER_OPT_SWEEPS_PER_LAUNCH = 1, 2, 3, 4
-ER_DEFAULT_SWEEPS = 128  # include/er.h
+ER_DEFAULT_SWEEPS = 0  # include/er.h: automatic (128 for small batches, else 1)
 ER_NDIAG = 12
 DIAG_NAMES = ("ke_trans", "ke_rot", "pe_shear", "pe_bend", "pe_grav", "pe_tip",
               "px", "py", "pz", "vmax", "mass", "n_elems")

@@ -1093,7 +1093,7 @@ er_status er_set_option(er_batch *b, int32_t option, int64_t value) {
     return ER_OK;
   }
   if (option == ER_OPT_SWEEPS_PER_LAUNCH) {
-    if (value < 1 || value > (1 << 20)) { b->last_error = "sweeps_per_launch must be in [1, 2^20]"; return ER_EINVAL; }
+    if (value < 0 || value > (1 << 20)) { b->last_error = "sweeps_per_launch must be in [0 (auto), 2^20]"; return ER_EINVAL; }
     b->sweeps = value;
     return ER_OK;
   }
@@ -1203,9 +1203,14 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
   const int64_t spl = b->steps_per_launch;
   // Sweeps: one persistent launch streams every tile through HBM S times (S steps of spl on-chip
   // steps each); long-rod clusters advance the same steps in their own launch.
-  if (!b->contact_on && b->kernel_mode == 0 && b->sweeps > 1) {
+  // Default (0): sweeps only for small batches -- a few tiles per CTA, where launch boundaries
+  // dominate (cfg1/cfg2); large batches keep one launch per step (graph replays), which measured
+  // faster there.
+  const int64_t grid = 148 * (b->block <= 128 ? 4 : b->block <= 256 ? 2 : 1);
+  const int64_t sweeps = b->sweeps > 0 ? b->sweeps : (b->n_tiles_norm <= 4 * grid ? 128 : 1);
+  if (!b->contact_on && b->kernel_mode == 0 && sweeps > 1) {
     while (n_steps - done >= spl) {
-      const int64_t S = std::min<int64_t>(b->sweeps, (n_steps - done) / spl);
+      const int64_t S = std::min<int64_t>(sweeps, (n_steps - done) / spl);
       p.n_steps = (int32_t)spl;
       p.sweeps = (int32_t)S;
       p.t = t;

@@ -333,10 +333,10 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
 // Start time of a launch: the host's value, or (graph launches) the device copy the previous launch
 // advanced; block 0 advances it for the next launch with the host's arithmetic.
 __device__ __forceinline__ double launch_t0(const ErStepParams &p) { return p.tdev ? p.tdev[p.tpar] : p.t; }
-__device__ __forceinline__ void advance_tdev(const ErStepParams &p, double t0) {
+__device__ __forceinline__ void advance_tdev(const ErStepParams &p, double t0, int passes = 1) {
   if (!p.tdev || blockIdx.x != 0 || threadIdx.x != 0) return;
-  const int64_t n = (int64_t)p.n_steps * (p.sweeps > 1 ? p.sweeps : 1);
-  for (int64_t st = 0; st < n; ++st) {
+  const int n = p.n_steps * passes;
+  for (int st = 0; st < n; ++st) {
     const double th = t0 + 0.5 * p.h;
     t0 = th + 0.5 * p.h;
   }
@@ -488,7 +488,7 @@ __device__ __forceinline__ void issue_tile(const ErStepParams &p, const TileHead
   bulk_g2s(B + SG::TOFF, tile_ptr, (uint32_t)sizeof(ErTile), bar);
 }
 
-template <int BLOCK, int MINB, int FEAT, bool DSTORE = false>
+template <int BLOCK, int MINB, int FEAT, bool DSTORE = false, bool SWEEP = false>
 __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepParams p) {
   using SG = Stage<BLOCK, FEAT>;
   extern __shared__ __align__(16) double sm[];
@@ -501,36 +501,42 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
   }
   __syncthreads();
   griddep_wait();  // (programmatic launch) the previous kernel's results are complete and visible
-  int64_t tile = blockIdx.x;
-  if (tid == 0 && tile < p.n_tiles) issue_tile<BLOCK, FEAT>(p, load_head(p.tiles + tile), p.tiles + tile, sm, &bar[0]);
   const double t0 = launch_t0(p);
   uint32_t phase = 0;  // bit b = load parity of buffer b
   unsigned fbits_all = 0;
   int frod = 0x7fffffff;
+  // Sweeps (p.sweeps > 1): the launch streams its tiles through the pipeline that many times, one
+  // step (p.n_steps on-chip steps) per pass and the state through HBM every pass -- the work of
+  // that many launches without their boundaries.  Between passes thread 0 lets this CTA's stores
+  // land (and fences the odd-tail plain store against the async proxy) before reloading.
+  // (a separate instantiation: the pass loop alone costs the one-pass kernel 2-5% -- DESIGN §4)
+  const int sweeps = (SWEEP && !DSTORE && p.sweeps > 1) ? p.sweeps : 1;
+  double t_pass = t0;
+  for (int sw = 0; sw < sweeps; ++sw) {
+  if (sw > 0) {
+    if (tid == 0) fence_proxy_async_all();  // the pass's stores landed (wait at its end); the odd-tail plain store too
+    for (int st = 0; st < p.n_steps; ++st) {  // step_body's own time arithmetic
+      const double th = t_pass + 0.5 * p.h;
+      t_pass = th + 0.5 * p.h;
+    }
+  }
+  const bool last_pass = sw + 1 == sweeps;
+  // every pass starts in buffer 0: every thread is past the previous pass's last epilogue barrier
+  // and thread 0 has waited for its stores, so both buffers are free (mbarrier phases carry on)
+  int64_t tile = blockIdx.x;
+  if (tid == 0 && tile < p.n_tiles) issue_tile<BLOCK, FEAT>(p, load_head(p.tiles + tile), p.tiles + tile, sm, &bar[0]);
   // Pipeline per tile k in buffer b (the other buffer b^1 held tile k-1):
   //   wait load(k) -> stage to registers -> barrier -> [t0: once the bulk store of tile k-1 has
   //   read b^1, load tile k+1 into b^1] -> steps (exchange in b) -> barrier -> results to b ->
   //   barrier -> [t0: bulk store b -> HBM].  Loads and stores are TMA bulk copies, so no warp
   //   ever waits on HBM except for the (prefetched) load of its next tile.
-  // Sweeps (p.sweeps > 1): the launch streams its tiles through the pipeline that many times, one
-  // step (p.n_steps on-chip steps) per pass and the state through HBM every pass -- the work of
-  // that many launches without their boundaries.  The prefetch wraps to the CTA's first tile:
-  // that tile's store (a pass ago) must have completed first (all store groups but the newest),
-  // or, for a CTA with a single tile, the reload waits for the tile's own store.
-  const int sweeps = (!DSTORE && p.sweeps > 1) ? p.sweeps : 1;
-  int sw = 0;
-  double t_sw = t0;  // time at the start of this pass
-  for (int k = 0; tile < p.n_tiles; ++k) {
+  for (int k = 0; tile < p.n_tiles; tile += gridDim.x, ++k) {
     const int b = k & 1;
     double *B = sm + b * SG::BUFD;
-    int64_t tnext = tile + gridDim.x;
-    int swn = sw;
-    if (tnext >= p.n_tiles) { tnext = blockIdx.x; swn = sw + 1; }
-    const bool has_next = swn < sweeps;
-    const bool defer = has_next && tnext == tile;  // one tile per CTA: reload after its own store
+    const int64_t tnext = tile + gridDim.x;
     TileHead Tn;
-    if (tid == 0 && has_next) Tn = load_head(p.tiles + tnext);  // overlaps the wait
-    if (!has_next) griddep_launch_dependents();  // this CTA's last tile: the next step's grid may launch
+    if (tid == 0 && tnext < p.n_tiles) Tn = load_head(p.tiles + tnext);  // overlaps the wait
+    if (last_pass && tnext >= p.n_tiles) griddep_launch_dependents();  // last tile: the next grid may launch
 #if ER_TRACE  // measurement builds only (ER_NVCC_EXTRA=-DER_TRACE=1): the per-tile timeline
     unsigned long long *tr = (p.trace && tid == 0 && k < ER_TRACE_ITERS)
                                  ? p.trace + ((int64_t)blockIdx.x * ER_TRACE_ITERS + k) * 4 : nullptr;
@@ -596,12 +602,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
 #ifdef ER_TRACE_FINE
     if (tr) tr[2] = gtimer() & ((1ull << 48) - 1);
 #endif
-    if (tid == 0 && has_next && !defer) {
-      if (swn != sw) {  // wrapping to the next pass: the first tile's store must have landed
-        if (p.n_tiles - (int64_t)blockIdx.x <= 2 * (int64_t)gridDim.x) bulk_wait_all();  // newest group
-        else bulk_wait_all_but_newest();     // the newest group is tile k-1's
-        fence_proxy_async_all();             // (and the odd-tail plain store) before the reload
-      }
+    if (tid == 0 && tnext < p.n_tiles) {
       bulk_wait_read_all();  // the bulk store of tile k-1 has finished reading buffer b^1
       issue_tile<BLOCK, FEAT>(p, Tn, p.tiles + tnext, sm + (b ^ 1) * SG::BUFD, &bar[b ^ 1]);
     }
@@ -609,7 +610,7 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
     if (tr) tr[3] = gtimer() & ((1ull << 48) - 1);
 #endif
     // ---- the steps
-    double t = t_sw;
+    double t = t_pass;
     unsigned fbits = 0;
     if (FEAT & FEAT_CONTACT) {
       // contact mode: the state arrives after drift-1 (contact forces were evaluated there);
@@ -649,7 +650,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
 #ifndef ER_TRACE_FINE
       if (tr) tr[3] = gtimer() & ((1ull << 48) - 1);
 #endif
-    } else {
+      continue;
+    }
     // ---- registers -> stage (block layout at OUTOFF) -> HBM with one TMA bulk store
     double *O = B + SG::OUTOFF;
     if (si.active) {
@@ -679,23 +681,10 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
 #ifndef ER_TRACE_FINE
     if (tr) tr[3] = gtimer() & ((1ull << 48) - 1);
 #endif
-    }
-    if (tid == 0 && defer) {  // single-tile CTA: its next pass reads what this pass just stored
-      bulk_wait_all();
-      fence_proxy_async_all();
-      issue_tile<BLOCK, FEAT>(p, Tn, p.tiles + tnext, sm + (b ^ 1) * SG::BUFD, &bar[b ^ 1]);
-    }
-    if (swn != sw)  // next pass: one step later (the arithmetic of step_body's time update)
-      for (int st = 0; st < p.n_steps; ++st) {
-        const double th = t_sw + 0.5 * p.h;
-        t_sw = th + 0.5 * p.h;
-      }
-    sw = swn;
-    tile = tnext;
-    if (!has_next) break;
   }
   if (tid == 0) bulk_wait_all();  // stores complete before the kernel retires
-  advance_tdev(p, t0);
+  }  // passes
+  advance_tdev(p, t0, sweeps);
   report_fault(p, fbits_all, frod);
 }
 
@@ -1281,15 +1270,15 @@ namespace {
 size_t simple_smem(int block) { return (size_t)er::XPLANES * 8 * block + sizeof(int) * (block / 8 + 4); }
 size_t diag_smem(int block) { return (size_t)12 * 8 * block + 16 * 8 * (block / 32) + sizeof(int) * (block / 8 + 4); }
 
-template <int BLOCK, int MINB, int FEAT, bool DSTORE = false>
+template <int BLOCK, int MINB, int FEAT, bool DSTORE = false, bool SWEEP = false>
 cudaError_t launch_persistent(const ErStepParams &p, cudaStream_t st) {
-  auto k = er::fused_persistent<BLOCK, MINB, FEAT, DSTORE>;
+  auto k = er::fused_persistent<BLOCK, MINB, FEAT, DSTORE, SWEEP>;
 #ifdef ER_ONE_CTA_PER_SM  // measurement: request enough smem that only one CTA fits per SM
   const size_t sm = 160 * 1024;
 #else
   const size_t sm = er::Stage<BLOCK, FEAT>::bytes();
 #endif
-  static int grid_per_sm[64] = {0};  // per device
+  static int grid_per_sm[64] = {0};  // per device (and instantiation)
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 64) return cudaErrorInvalidDevice;
@@ -1326,10 +1315,10 @@ cudaError_t launch_persistent(const ErStepParams &p, cudaStream_t st) {
 template <int BLOCK, int MINB, int X>
 cudaError_t launch_persistent_base(const ErStepParams &p, int base, cudaStream_t st) {
   switch (base) {
-    case 0: return launch_persistent<BLOCK, MINB, X | 0>(p, st);
-    case 1: return launch_persistent<BLOCK, MINB, X | 1>(p, st);
-    case 2: return launch_persistent<BLOCK, MINB, X | 2>(p, st);
-    case 3: return launch_persistent<BLOCK, MINB, X | 3>(p, st);
+    case 0: return p.sweeps > 1 ? launch_persistent<BLOCK, MINB, X | 0, false, true>(p, st) : launch_persistent<BLOCK, MINB, X | 0>(p, st);
+    case 1: return p.sweeps > 1 ? launch_persistent<BLOCK, MINB, X | 1, false, true>(p, st) : launch_persistent<BLOCK, MINB, X | 1>(p, st);
+    case 2: return p.sweeps > 1 ? launch_persistent<BLOCK, MINB, X | 2, false, true>(p, st) : launch_persistent<BLOCK, MINB, X | 2>(p, st);
+    case 3: return p.sweeps > 1 ? launch_persistent<BLOCK, MINB, X | 3, false, true>(p, st) : launch_persistent<BLOCK, MINB, X | 3>(p, st);
     case 8: return launch_persistent<BLOCK, MINB, X | 8>(p, st);
     case 9: return launch_persistent<BLOCK, MINB, X | 9>(p, st);
     case 10: return launch_persistent<BLOCK, MINB, X | 10>(p, st);

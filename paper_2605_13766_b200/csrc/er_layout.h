@@ -200,8 +200,6 @@ struct ErStepParams {
   double b_omega;
   int32_t n_steps;        // steps in this launch
   int32_t tpar;           // with tdev: the launch reads tdev[tpar], block 0 writes tdev[tpar ^ 1]
-  int32_t sweeps;         // tile kernel: passes over all tiles in this launch (one step each), >= 1
-  int32_t pad3_;
   double t;               // time at the start of the launch (when tdev is null)
   double *tdev;           // CUDA-graph step launches: [2] device time, ping-pong
   double h;               // dt
@@ -215,6 +213,8 @@ struct ErStepParams {
   const double *cbuild;   // [n_nodes][3] positions at the last contact-list build
   double disp2;           // (skin/2)^2: a larger squared displacement since the build ...
   int32_t *rebuild;       // ... sets this flag
+  int32_t sweeps;         // tile kernel: passes over all tiles in this launch (one step each), >= 1
+  int32_t pad3_;
 };
 #define ER_TRACE_ITERS 64
 #ifndef ER_TRACE
