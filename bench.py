@@ -95,10 +95,37 @@ class ClockSampler:
         self.rows = []
         self.proc = None
 
+    def _nvml_loop(self, period):
+        import pynvml as N
+        h = N.nvmlDeviceGetHandleByIndex(self.index)
+        mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        bits = [N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+                N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap]
+        while not self.stop.is_set():
+            sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+            ev = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.rows.append([str(self.index), str(sm), str(mx), "", hex(ev)]
+                             + ["Active" if ev & b else "Not Active" for b in bits])
+            self.stop.wait(period)
+
     def __enter__(self):
         try:
+            if os.environ.get("ER_BENCH_NO_CLOCKS"):  # measurement of the sampler's own effect
+                raise RuntimeError("clock sampling disabled")
+            if os.environ.get("ER_BENCH_CLOCKS", "nvml") == "nvml":
+                # in-process NVML (clock + event-reason queries only): an nvidia-smi query process
+                # stalled the host's kernel submissions for ~70 ms now and then
+                import pynvml as N
+                N.nvmlInit()
+                self.stop = threading.Event()
+                self.th = threading.Thread(target=self._nvml_loop,
+                                           args=(float(os.environ.get("ER_BENCH_CLOCK_MS", "100")) / 1e3,), daemon=True)
+                self.th.start()
+                self.nvml = True
+                return self
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms",
+                                          os.environ.get("ER_BENCH_CLOCK_MS", "100")],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
@@ -111,6 +138,9 @@ class ClockSampler:
             self.rows.append([x.strip() for x in line.split(",")])
 
     def __exit__(self, *a):
+        if getattr(self, "nvml", False):
+            self.stop.set()
+            self.th.join(timeout=5)
         if self.proc:
             self.proc.terminate()
             try:

@@ -157,6 +157,8 @@ struct er_batch {
   // the launch time lives in tdev (ping-pong); rebuilt when its parameters change
   cudaGraphExec_t sgraph = nullptr;
   int64_t sgraph_key = -1;
+  bool sgraph_while = false;    // sgraph repeats its 32 launches in a device-side WHILE loop
+  long long *d_loop = nullptr;  // its iteration counter
   double *tdev = nullptr;
   int64_t forcing_version = 0;
   int cgraph_kernels = 0;
@@ -278,6 +280,12 @@ void collect_times(er_batch *b) {  // after the stream was synchronised
   b->ev_used = 0;
 }
 
+// WHILE-loop control of the step graph: one more pass of its 32 launches while the counter lasts.
+__global__ void er_step_loop_ctl(long long *counter, cudaGraphConditionalHandle h) {
+  const long long left = --*counter;
+  cudaGraphSetConditional(h, left > 0 ? 1u : 0u);
+}
+
 void free_step_graph(er_batch *b) {
   if (b->sgraph) cudaGraphExecDestroy(b->sgraph);
   b->sgraph = nullptr;
@@ -286,6 +294,8 @@ void free_step_graph(er_batch *b) {
 
 void free_all(er_batch *b) {
   free_step_graph(b);
+  if (b->d_loop) cudaFree(b->d_loop);
+  b->d_loop = nullptr;
   if (b->tdev) cudaFree(b->tdev);
   b->tdev = nullptr;
   if (b->upload_stage) cudaFree(b->upload_stage);
@@ -1232,37 +1242,93 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
     if (!b->tdev) CK(dalloc(b, &b->tdev, 2), "cudaMalloc(tdev)");
     if (b->sgraph_key != key) {
       free_step_graph(b);
+      if (!b->d_loop) CK(dalloc(b, &b->d_loop, 1), "cudaMalloc(loop)");
       cudaStream_t cs;
       CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "cudaStreamCreate");
+      auto capture_launches = [&](cudaStream_t s_) -> cudaError_t {
+        cudaError_t e_ = cudaSuccess;
+        for (int j = 0; e_ == cudaSuccess && j < ER_GRAPH_LAUNCHES; ++j) {
+          ErStepParams q = p;
+          q.n_steps = (int32_t)spl;
+          q.tdev = b->tdev;
+          q.tpar = j & 1;
+          e_ = er_launch_step(&q, b->block, 0, feat, s_);
+          q.n_tiles = b->n_tiles;
+          for (const auto &gr : b->long_groups)
+            if (e_ == cudaSuccess) e_ = er_launch_long(&q, gr.tile0, gr.n_rods, gr.nseg, feat, s_);
+        }
+        return e_;
+      };
+      // Preferred: a WHILE node whose body is the 32 launches plus a loop-control kernel, so one
+      // cudaGraphLaunch runs every full chunk of an er_step call with no host submissions in
+      // between (host-side stalls -- a monitoring query holding the driver -- cannot starve the
+      // GPU).  Fallback: the 32 launches as a plain graph, launched once per chunk.
       cudaGraph_t g = nullptr;
-      cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed);  // launchers query attributes
-      for (int j = 0; e == cudaSuccess && j < ER_GRAPH_LAUNCHES; ++j) {
-        ErStepParams q = p;
-        q.n_steps = (int32_t)spl;
-        q.tdev = b->tdev;
-        q.tpar = j & 1;
-        e = er_launch_step(&q, b->block, 0, feat, cs);
-        q.n_tiles = b->n_tiles;
-        for (const auto &gr : b->long_groups)
-          if (e == cudaSuccess) e = er_launch_long(&q, gr.tile0, gr.n_rods, gr.nseg, feat, cs);
+      cudaError_t e = std::getenv("ER_NO_WHILE_GRAPH") ? cudaErrorNotSupported : cudaGraphCreate(&g, 0);
+      cudaGraphConditionalHandle h;
+      if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+      cudaGraphNodeParams np = {};
+      cudaGraphNode_t wnode;
+      if (e == cudaSuccess) {
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.handle = h;
+        np.conditional.type = cudaGraphCondTypeWhile;
+        np.conditional.size = 1;
+        e = cudaGraphAddNode(&wnode, g, nullptr, 0, &np);
       }
-      cudaError_t e2 = cudaStreamEndCapture(cs, &g);
-      if (e == cudaSuccess) e = e2;
+      if (e == cudaSuccess) {
+        cudaGraph_t body = np.conditional.phGraph_out[0];
+        e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+        if (e == cudaSuccess) {
+          cudaError_t eb = capture_launches(cs);
+          if (eb == cudaSuccess) {
+            er_step_loop_ctl<<<1, 1, 0, cs>>>(b->d_loop, h);
+            eb = cudaGetLastError();
+          }
+          e = cudaStreamEndCapture(cs, &body);
+          if (eb != cudaSuccess) e = eb;
+        }
+      }
       if (e == cudaSuccess) e = cudaGraphInstantiate(&b->sgraph, g, 0);
       if (g) cudaGraphDestroy(g);
+      b->sgraph_while = e == cudaSuccess;
+      if (e != cudaSuccess) {
+        cudaGetLastError();  // clear a sticky-free failure of the WHILE path
+        b->sgraph = nullptr;
+        g = nullptr;
+        e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed);  // launchers query attributes
+        if (e == cudaSuccess) {
+          cudaError_t eb = capture_launches(cs);
+          e = cudaStreamEndCapture(cs, &g);
+          if (eb != cudaSuccess) e = eb;
+        }
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&b->sgraph, g, 0);
+        if (g) cudaGraphDestroy(g);
+      }
       cudaStreamDestroy(cs);
       CK(e, "step graph");
       b->sgraph_key = key;
     }
     const double t_host = t;  // pageable 8-byte copy: staged before cudaMemcpyAsync returns
     CK(cudaMemcpyAsync(b->tdev, &t_host, sizeof(double), cudaMemcpyHostToDevice, b->stream), "H2D t");
-    while (n_steps - done >= ER_GRAPH_LAUNCHES * spl) {
+    const int64_t chunk = ER_GRAPH_LAUNCHES * spl;
+    if (b->sgraph_while) {  // every full chunk in one launch: the device counts the iterations
+      const long long iters = (long long)((n_steps - done) / chunk);
+      CK(cudaMemcpyAsync(b->d_loop, &iters, sizeof iters, cudaMemcpyHostToDevice, b->stream), "H2D loop");
+      const int m0 = mark(b);
+      CK(cudaGraphLaunch(b->sgraph, b->stream), "step graph launch");
+      interval(b, m0, mark(b), 0, (int)(ER_GRAPH_LAUNCHES * iters));
+      b->launches += ER_GRAPH_LAUNCHES * iters * (1 + (int64_t)b->long_groups.size());
+      for (int64_t q = 0; q < chunk * iters; ++q) { const double th = t + 0.5 * dt; t = th + 0.5 * dt; }
+      done += chunk * iters;
+    }
+    while (n_steps - done >= chunk) {
       const int m0 = mark(b);
       CK(cudaGraphLaunch(b->sgraph, b->stream), "step graph launch");
       interval(b, m0, mark(b), 0, ER_GRAPH_LAUNCHES);
       b->launches += ER_GRAPH_LAUNCHES * (1 + (int64_t)b->long_groups.size());
-      for (int64_t q = 0; q < ER_GRAPH_LAUNCHES * spl; ++q) { const double th = t + 0.5 * dt; t = th + 0.5 * dt; }
-      done += ER_GRAPH_LAUNCHES * spl;
+      for (int64_t q = 0; q < chunk; ++q) { const double th = t + 0.5 * dt; t = th + 0.5 * dt; }
+      done += chunk;
     }
   }
   while (done < n_steps) {
