@@ -112,9 +112,10 @@ class ClockSampler:
         try:
             if os.environ.get("ER_BENCH_NO_CLOCKS"):  # measurement of the sampler's own effect
                 raise RuntimeError("clock sampling disabled")
-            if os.environ.get("ER_BENCH_CLOCKS", "nvml") == "nvml":
-                # in-process NVML (clock + event-reason queries only): an nvidia-smi query process
-                # stalled the host's kernel submissions for ~70 ms now and then
+            if os.environ.get("ER_BENCH_CLOCKS", "smi") == "nvml":
+                # ER_BENCH_CLOCKS=nvml: in-process NVML (clock + event-reason queries only) instead of
+                # the recipe's nvidia-smi loop; both stall the GPU's kernel launches now and then
+                # (DESIGN §4 "Monitoring stalls")
                 import pynvml as N
                 N.nvmlInit()
                 self.stop = threading.Event()
