@@ -129,3 +129,31 @@ def b_t(w, n):
         th = t + 0.5 * w.dt
         t = th + 0.5 * w.dt
     return t
+
+
+def test_while_graph_equals_chunked_graphs(er, monkeypatch):
+    """The device-side WHILE step graph (one launch per er_step call) and its fallback (one graph
+    launch per 32 steps) give the same trajectory bitwise, with long-rod clusters in the graph."""
+    w = mixed_batch(n_short=300, seed=11)
+    out = []
+    for plain in (False, True):
+        if plain:
+            monkeypatch.setenv("ER_NO_WHILE_GRAPH", "1")
+        with er.RodBatch(w) as b:
+            b.set_option(er.ER_OPT_SWEEPS_PER_LAUNCH, 1)
+            b.step(100, w.dt)                       # 3 chunks of 32 + 4 plain launches
+            b.step(64, w.dt)                        # 2 chunks
+            out.append(b.get_state())
+    for x, y in zip(out[0], out[1]):
+        assert np.array_equal(np.asarray(x), np.asarray(y))
+
+
+def test_option_validation(er):
+    w = W.make("cfg2", n_rods=4)
+    with er.RodBatch(w) as b:
+        for opt, bad in ((er.ER_OPT_SWEEPS_PER_LAUNCH, -1), (er.ER_OPT_STEPS_PER_LAUNCH, 0),
+                         (er.ER_OPT_KERNEL, 9), (er.ER_OPT_PHASE_TIMING, 2), (99, 1)):
+            with pytest.raises(er.ErError):
+                b.set_option(opt, bad)
+        b.set_option(er.ER_OPT_SWEEPS_PER_LAUNCH, 0)   # automatic
+        b.step(3, w.dt)
