@@ -702,107 +702,14 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
     if (e_ != cudaSuccess) { cuda_fail(b, e_, what); return fail(e_ == cudaErrorMemoryAllocation ? ER_ENOMEM : ER_ECUDA); } \
   } while (0)
 
-  // ---- per-rod records; general rods get per-slot parameter planes
-  b->rec_n = (size_t)std::max<int64_t>(R, 1) * ER_REC;
-  b->rec.reset(new double[b->rec_n]);  // every record is fully written below (in parallel)
-  if (R == 0) std::fill_n(b->rec.get(), b->rec_n, 0.0);
-  b->flags.assign((size_t)std::max<int64_t>(R, 1), 0);
-  auto mat_at = [&](int64_t r, int64_t j) {
-    const int64_t k = d->material_per_rod ? r : j;
-    ElemMat m{d->density[k], d->area[k], d->I1[k], d->I2[k], d->youngs[k], d->shear_mod[k], d->alpha_c[k], d->rest_lengths[j]};
-    return m;
-  };
-  // per-rod records in parallel over host threads (independent rods)
-  const int nthr = (int)std::max<unsigned>(1u, std::min<unsigned>(16u, std::thread::hardware_concurrency()));
-  std::vector<std::thread> pool;
-  std::vector<char> gen_flag((size_t)std::max<int64_t>(R, 1), 0);
-  for (auto *v : {&b->rod_A0, &b->rod_E0, &b->rod_lmin, &b->rod_lmax}) v->assign((size_t)std::max<int64_t>(R, 1), 0.0);
-  auto rec_range = [&](int64_t ra, int64_t rb) {
-  for (int64_t pr = ra; pr < rb; ++pr) {
-    const int64_t r = b->ord[pr];  // canonical rod of packed rod pr
-    const ElemMat m0 = mat_at(r, eoff[r]);
-    bool uniform = true;
-    if (d->material_per_rod) {  // only the rest lengths can vary along the rod
-      const double *lh = d->rest_lengths;
-      for (int64_t j = eoff[r] + 1; j < eoff[r + 1]; ++j) uniform &= lh[j] == m0.lh;
-    } else {
-      for (int64_t j = eoff[r] + 1; j < eoff[r + 1] && uniform; ++j) {
-        const ElemMat m = mat_at(r, j);
-        uniform = m.rho == m0.rho && m.A == m0.A && m.I1 == m0.I1 && m.I2 == m0.I2 && m.E == m0.E && m.G == m0.G &&
-                  m.ac == m0.ac && m.lh == m0.lh;
-      }
-    }
-    std::fill_n(&b->rec[(size_t)pr * ER_REC], ER_REC, 0.0);
-    fill_record(&b->rec[(size_t)pr * ER_REC], m0);
-    b->rec[(size_t)pr * ER_REC + REC_CANON] = (double)r;
-    if (!uniform) gen_flag[pr] = 1;
-    double lmin = d->rest_lengths[eoff[r]], lmax = lmin;
-    for (int64_t j = eoff[r] + 1; j < eoff[r + 1]; ++j) {
-      lmin = std::min(lmin, d->rest_lengths[j]);
-      lmax = std::max(lmax, d->rest_lengths[j]);
-    }
-    b->rod_A0[pr] = m0.A;
-    b->rod_E0[pr] = m0.E;
-    b->rod_lmin[pr] = lmin;
-    b->rod_lmax[pr] = lmax;
-  }
-  };
-  if (R < 65536) rec_range(0, R);
-  else {
-    for (int q = 0; q < nthr; ++q) pool.emplace_back(rec_range, R * q / nthr, R * (q + 1) / nthr);
-    for (auto &th : pool) th.join();
-  }
-  for (int64_t r = 0; r < R; ++r)
-    if (gen_flag[r]) { b->flags[r] |= FL_GENERAL; b->any_general = true; }
-  tm.mark("records");
-  b->has_sigma0 = d->rest_sigma != nullptr;
-  b->has_kappa0 = d->rest_kappa != nullptr && NV > 0;
-  b->ng = pad_to(NN, 32);
-  b->ne = pad_to(E, 32);
-  std::vector<double> gpar;
-  if (b->any_general) {
-    gpar.assign((size_t)ER_GP * b->ng, 0.0);
-    for (int64_t pr = 0; pr < R; ++pr) {
-      if (!(b->flags[pr] & FL_GENERAL)) continue;
-      const int64_t r = b->ord[pr];
-      const int32_t N = b->n_elems_h[pr];
-      const int64_t n0 = eoffp[pr] + pr;
-      double sk = 0.0;
-      for (int32_t i = 0; i <= N; ++i) {
-        auto G = [&](int q) -> double & { return gpar[(size_t)q * b->ng + n0 + i]; };
-        double mass = 0.0;
-        if (i < N) {
-          const ElemMat m = mat_at(r, eoff[r] + i);
-          double tmp[ER_REC];
-          fill_record(tmp, m);
-          G(GP_LHAT) = tmp[REC_LHAT]; G(GP_ILHAT) = tmp[REC_ILHAT]; G(GP_S1) = tmp[REC_S1]; G(GP_S3) = tmp[REC_S3];
-          for (int c = 0; c < 3; ++c) { G(GP_IJ1 + c) = tmp[REC_IJ1 + c]; G(GP_KJ1 + c) = tmp[REC_KJ1 + c]; }
-          mass += 0.5 * m.rho * m.A * m.lh;
-        }
-        if (i > 0) {
-          const ElemMat m = mat_at(r, eoff[r] + i - 1);
-          mass += 0.5 * m.rho * m.A * m.lh;
-        }
-        G(GP_IM) = 1.0 / mass;
-        G(GP_SK) = sk;
-        if (i >= 1 && i < N) {
-          const ElemMat ml = mat_at(r, eoff[r] + i - 1), mr = mat_at(r, eoff[r] + i);
-          const double Dh = 0.5 * (ml.lh + mr.lh);
-          const double Bl[3] = {ml.E * ml.I1, ml.E * ml.I2, ml.G * (ml.I1 + ml.I2)};
-          const double Br[3] = {mr.E * mr.I1, mr.E * mr.I2, mr.G * (mr.I1 + mr.I2)};
-          G(GP_DH) = Dh;
-          for (int c = 0; c < 3; ++c) G(GP_BV1 + c) = (Bl[c] * ml.lh + Br[c] * mr.lh) / (2.0 * Dh);
-        }
-        if (i < N) sk += d->rest_lengths[eoff[r] + i];
-      }
-    }
-  }
-
   // ---- rod-aligned tiles (greedy contiguous packing, <= block slots and <= block/8 rods per
-  // tile); each tile's state is one contiguous SoA block: 6 node planes x nslots, 12 element
-  // planes x nel, [3 Voronoi planes x nvor], padded to an even number of doubles (16 B).
+  // tile); each tile's state is one contiguous SoA block: 6 node planes x nslots, ER_EPL element
+  // planes x nel, [3 Voronoi planes x nvor], padded to an even number of doubles (16 B).  Built
+  // on a host thread of its own while the records are built (they share no data).
   std::vector<ErTile> tiles;
-  {
+  b->has_kappa0 = d->rest_kappa != nullptr && NV > 0;
+  std::thread tile_thread([&]() {
+    tiles.reserve((size_t)(Rn / std::max(1, b->block / std::max<int32_t>(max_n + 1, 1))) + (size_t)(R - Rn) * 16 + 64);
     int64_t r = 0, boff = 0;
     while (r < Rn) {
       ErTile T;
@@ -860,7 +767,103 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
       }
     }
     b->state_doubles = boff;
+  });
+  // ---- per-rod records; general rods get per-slot parameter planes
+  b->rec_n = (size_t)std::max<int64_t>(R, 1) * ER_REC;
+  b->rec.reset(new double[b->rec_n]);  // every record is fully written below (in parallel)
+  if (R == 0) std::fill_n(b->rec.get(), b->rec_n, 0.0);
+  b->flags.assign((size_t)std::max<int64_t>(R, 1), 0);
+  auto mat_at = [&](int64_t r, int64_t j) {
+    const int64_t k = d->material_per_rod ? r : j;
+    ElemMat m{d->density[k], d->area[k], d->I1[k], d->I2[k], d->youngs[k], d->shear_mod[k], d->alpha_c[k], d->rest_lengths[j]};
+    return m;
+  };
+  // per-rod records in parallel over host threads (independent rods)
+  const int nthr = (int)std::max<unsigned>(1u, std::min<unsigned>(16u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> pool;
+  std::vector<char> gen_flag((size_t)std::max<int64_t>(R, 1), 0);
+  for (auto *v : {&b->rod_A0, &b->rod_E0, &b->rod_lmin, &b->rod_lmax}) v->assign((size_t)std::max<int64_t>(R, 1), 0.0);
+  auto rec_range = [&](int64_t ra, int64_t rb) {
+  for (int64_t pr = ra; pr < rb; ++pr) {
+    const int64_t r = b->ord[pr];  // canonical rod of packed rod pr
+    const ElemMat m0 = mat_at(r, eoff[r]);
+    bool uniform = true;
+    if (d->material_per_rod) {  // only the rest lengths can vary along the rod
+      const double *lh = d->rest_lengths;
+      for (int64_t j = eoff[r] + 1; j < eoff[r + 1]; ++j) uniform &= lh[j] == m0.lh;
+    } else {
+      for (int64_t j = eoff[r] + 1; j < eoff[r + 1] && uniform; ++j) {
+        const ElemMat m = mat_at(r, j);
+        uniform = m.rho == m0.rho && m.A == m0.A && m.I1 == m0.I1 && m.I2 == m0.I2 && m.E == m0.E && m.G == m0.G &&
+                  m.ac == m0.ac && m.lh == m0.lh;
+      }
+    }
+    std::fill_n(&b->rec[(size_t)pr * ER_REC], ER_REC, 0.0);
+    fill_record(&b->rec[(size_t)pr * ER_REC], m0);
+    b->rec[(size_t)pr * ER_REC + REC_CANON] = (double)r;
+    if (!uniform) gen_flag[pr] = 1;
+    double lmin = d->rest_lengths[eoff[r]], lmax = lmin;
+    for (int64_t j = eoff[r] + 1; j < eoff[r + 1]; ++j) {
+      lmin = std::min(lmin, d->rest_lengths[j]);
+      lmax = std::max(lmax, d->rest_lengths[j]);
+    }
+    b->rod_A0[pr] = m0.A;
+    b->rod_E0[pr] = m0.E;
+    b->rod_lmin[pr] = lmin;
+    b->rod_lmax[pr] = lmax;
   }
+  };
+  if (R < 65536) rec_range(0, R);
+  else {
+    for (int q = 0; q < nthr; ++q) pool.emplace_back(rec_range, R * q / nthr, R * (q + 1) / nthr);
+    for (auto &th : pool) th.join();
+  }
+  for (int64_t r = 0; r < R; ++r)
+    if (gen_flag[r]) { b->flags[r] |= FL_GENERAL; b->any_general = true; }
+  tm.mark("records");
+  b->has_sigma0 = d->rest_sigma != nullptr;
+  b->ng = pad_to(NN, 32);
+  b->ne = pad_to(E, 32);
+  std::vector<double> gpar;
+  if (b->any_general) {
+    gpar.assign((size_t)ER_GP * b->ng, 0.0);
+    for (int64_t pr = 0; pr < R; ++pr) {
+      if (!(b->flags[pr] & FL_GENERAL)) continue;
+      const int64_t r = b->ord[pr];
+      const int32_t N = b->n_elems_h[pr];
+      const int64_t n0 = eoffp[pr] + pr;
+      double sk = 0.0;
+      for (int32_t i = 0; i <= N; ++i) {
+        auto G = [&](int q) -> double & { return gpar[(size_t)q * b->ng + n0 + i]; };
+        double mass = 0.0;
+        if (i < N) {
+          const ElemMat m = mat_at(r, eoff[r] + i);
+          double tmp[ER_REC];
+          fill_record(tmp, m);
+          G(GP_LHAT) = tmp[REC_LHAT]; G(GP_ILHAT) = tmp[REC_ILHAT]; G(GP_S1) = tmp[REC_S1]; G(GP_S3) = tmp[REC_S3];
+          for (int c = 0; c < 3; ++c) { G(GP_IJ1 + c) = tmp[REC_IJ1 + c]; G(GP_KJ1 + c) = tmp[REC_KJ1 + c]; }
+          mass += 0.5 * m.rho * m.A * m.lh;
+        }
+        if (i > 0) {
+          const ElemMat m = mat_at(r, eoff[r] + i - 1);
+          mass += 0.5 * m.rho * m.A * m.lh;
+        }
+        G(GP_IM) = 1.0 / mass;
+        G(GP_SK) = sk;
+        if (i >= 1 && i < N) {
+          const ElemMat ml = mat_at(r, eoff[r] + i - 1), mr = mat_at(r, eoff[r] + i);
+          const double Dh = 0.5 * (ml.lh + mr.lh);
+          const double Bl[3] = {ml.E * ml.I1, ml.E * ml.I2, ml.G * (ml.I1 + ml.I2)};
+          const double Br[3] = {mr.E * mr.I1, mr.E * mr.I2, mr.G * (mr.I1 + mr.I2)};
+          G(GP_DH) = Dh;
+          for (int c = 0; c < 3; ++c) G(GP_BV1 + c) = (Bl[c] * ml.lh + Br[c] * mr.lh) / (2.0 * Dh);
+        }
+        if (i < N) sk += d->rest_lengths[eoff[r] + i];
+      }
+    }
+  }
+
+  tile_thread.join();
   b->n_tiles = (int64_t)tiles.size();
   tm.mark("gpar + tiles");
 

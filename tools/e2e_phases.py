@@ -8,7 +8,7 @@ pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
 hp, hv, hd, ho = pin(w.positions), pin(w.velocities), pin(w.directors), pin(w.omega)
 wp = dataclasses.replace(w, positions=hp.numpy(), velocities=hv.numpy(), directors=hd.numpy(), omega=ho.numpy())
 outs = [torch.empty_like(x).pin_memory() for x in (hp, hv, hd, ho)]
-for rep in range(2):
+for rep in range(int(os.environ.get("REPS", "2"))):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     b = er.RodBatch(wp)
