@@ -91,7 +91,7 @@ def test_cfg1_full_run(er, orc):
     assert_parity(w, g, o, 1e-7, label="cfg1 20000 steps")
 
 
-@pytest.mark.parametrize("name,n_steps", [("cfg3", 1), ("cfg3", 1000), ("cfg5", 1), ("cfg4", 1)])
+@pytest.mark.parametrize("name,n_steps", [("cfg3", 1), ("cfg3", 1000), ("cfg5", 1), ("cfg5", 1000), ("cfg4", 1), ("cfg4", 1000), ("cfg2", 1000)])
 def test_full_size_sampled(er, orc, name, n_steps):
     """Full BASELINE size on the GPU, in bench.py's launch configuration; the oracle re-runs
     a seeded sample of rods (first, last and random ones) and we compare those rods."""
