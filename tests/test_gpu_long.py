@@ -169,3 +169,27 @@ def test_long_rods_in_contact(er, orc):
         assert np.array_equal(x, y)
     o, _ = run_orc(orc, w, 150)
     assert_parity(w, out[0][:4], o, TOL_1000, raw=("r", "Q"), label="long rod contact 150 steps")
+
+
+def test_long_rod_batch_full_size_sampled(er, orc):
+    """16,384 rods x 1000 elements (the long-rod timing workload of tools/long_rod_time.py, 16.4 M
+    elements: 4-CTA clusters), 200 steps on the GPU; the oracle re-runs 8 sampled rods."""
+    R, N = 16384, 1000
+    n = np.full(R, N, np.int32)
+    lh = np.full(R, 0.00625)
+    mat = W._rod_material(R, 1e-3, 1e6)
+    rng = np.random.default_rng(0)
+    Q0 = W.uniform_so3(rng, R)
+    pos = W.straight_rods(n, lh, np.zeros((R, 3)), Q0[:, 2, :])
+    w = W.Workload("long", n, W._expand(lh, n), **mat, positions=pos, velocities=np.zeros_like(pos),
+                   directors=W._expand(Q0, n), omega=np.zeros((R * N, 3)), clamp=np.zeros(R, np.int8),
+                   gravity=np.zeros(3), damping=np.full(R, 0.1), tip_force=rng.normal(0, 1e-6, (R, 3)), dt=1e-6)
+    g = run_gpu(er, w, 200)
+    rods = np.array([0, 1, 777, 5000, 9999, 12345, R - 2, R - 1])
+    ws = w.subset(rods)
+    no, eo = w.node_offsets(), w.elem_offsets()
+    nidx = np.concatenate([np.arange(no[r], no[r + 1]) for r in rods])
+    eidx = np.concatenate([np.arange(eo[r], eo[r + 1]) for r in rods])
+    o, _ = run_orc(orc, ws, 200)
+    assert_parity(ws, (g[0][nidx], g[1][nidx], g[2][eidx], g[3][eidx]), o, TOL_1000, raw=("r", "Q"),
+                  label="16384 x 1000 sampled, 200 steps")
