@@ -228,6 +228,8 @@ def oracle_fanout_rate(w, rods_per_proc, n_steps, seed=5):
     each on its own seeded rod shard (rods are independent).  Rate = all element-steps / the
     slowest process's time."""
     import multiprocessing as mp
+    import oracle
+    oracle.build()            # once, in the parent: the spawned workers only dlopen it
     n_proc = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     rods = W.sample_rods(w, min(w.n_rods, rods_per_proc * n_proc), seed=seed)
     shards = [w.subset(np.sort(part)) for part in np.array_split(rods, n_proc) if len(part)]

@@ -26,12 +26,23 @@ F_NONFINITE, F_DEGENERATE, F_ANTIPODAL, F_OVERSPEED = 1, 2, 4, 8
 SYNC, ASYNC = 0, 1
 
 
-def build(force: bool = False) -> str:
-    """Compile liboracle.so with gcc (plain C, no FMA contraction)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
-            os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
-        subprocess.check_call(["gcc", *CFLAGS, "-o", _LIB, _SRC, "-lm"])
-    return _LIB
+def build(force: bool = False, src: str = _SRC, out: str = _LIB) -> str:
+    """Compile liboracle.so with gcc (plain C, no FMA contraction).
+
+    The library is compiled to a per-process temporary file and renamed into place, so that
+    concurrent builders (bench.py's cpu_baseline fan-out, pytest-xdist workers) never dlopen a
+    half-written file: each sees either the old complete library or the new one."""
+    hdr = os.path.join(os.path.dirname(src), "oracle.h")
+    if force or not os.path.exists(out) or os.path.getmtime(out) < max(
+            os.path.getmtime(src), os.path.getmtime(hdr)):
+        tmp = f"{out}.tmp.{os.getpid()}"
+        try:
+            subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, src, "-lm"])
+            os.replace(tmp, out)
+        finally:
+            if os.path.exists(tmp):
+                os.unlink(tmp)
+    return out
 
 
 _dp = C.POINTER(C.c_double)
@@ -67,7 +78,8 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        _lib = C.CDLL(build())
+        # ER_ORACLE_LIB: a prebuilt oracle library (tools/oracle_mutants.py loads mutated builds)
+        _lib = C.CDLL(os.environ.get("ER_ORACLE_LIB") or build())
         _lib.orc_rot.argtypes = [_dp, _dp]
         _lib.orc_logrot.argtypes = [_dp, _dp]
         _lib.orc_logrot.restype = C.c_int

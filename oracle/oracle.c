@@ -175,7 +175,10 @@ static void ctx_free(rod_ctx *c) { free(c->lhat); }
 /* Derived constants (PAPER.md:239 with the hat convention of C.4 #5):
  * S_j = diag(alpha_c G A, alpha_c G A, E A); B_j = diag(E I1, E I2, G(I1+I2));
  * J_j = rho lhat_j diag(I1, I2, I1+I2); m_i = (rho A lhat)_{i-1}/2 + (rho A lhat)_i/2 (C.4 #10);
- * Dh_k = (lhat_{k-1}+lhat_k)/2; Bv_k = (B_{k-1} lhat_{k-1} + B_k lhat_k)/(2 Dh_k) (C.4 #9). */
+ * Dh_k = (lhat_{k-1}+lhat_k)/2 (distance of the element centres);
+ * Bv_k = 2 Dh_k / (lhat_{k-1}/B_{k-1} + lhat_k/B_k): the Voronoi domain's two half elements act in
+ * series under a uniform moment, so its stiffness is the compliance mean (DESIGN §3 #9; equals B for
+ * a uniform rod, i.e. in every BASELINE config). */
 static void ctx_setup(const orc_problem *P, int32_t rod, int64_t e0, rod_ctx *c) {
   int32_t N = P->n_elems[rod];
   c->N = N;
@@ -204,7 +207,7 @@ static void ctx_setup(const orc_problem *P, int32_t rod, int64_t e0, rod_ctx *c)
   for (int32_t k = 1; k < N; ++k) {
     c->Dh[k] = 0.5 * (c->lhat[k - 1] + c->lhat[k]);
     for (int q = 0; q < 3; ++q)
-      c->Bv[3 * k + q] = (c->B[3 * (k - 1) + q] * c->lhat[k - 1] + c->B[3 * k + q] * c->lhat[k]) / (2.0 * c->Dh[k]);
+      c->Bv[3 * k + q] = (2.0 * c->Dh[k]) / (c->lhat[k - 1] / c->B[3 * (k - 1) + q] + c->lhat[k] / c->B[3 * k + q]);
   }
   c->nu = P->damping ? P->damping[rod] : 0.0;
   {

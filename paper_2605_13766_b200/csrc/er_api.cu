@@ -856,7 +856,9 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
           const double Bl[3] = {ml.E * ml.I1, ml.E * ml.I2, ml.G * (ml.I1 + ml.I2)};
           const double Br[3] = {mr.E * mr.I1, mr.E * mr.I2, mr.G * (mr.I1 + mr.I2)};
           G(GP_DH) = Dh;
-          for (int c = 0; c < 3; ++c) G(GP_BV1 + c) = (Bl[c] * ml.lh + Br[c] * mr.lh) / (2.0 * Dh);
+          // Voronoi stiffness = series (compliance) mean over the domain's two half elements, the
+          // exact stiffness of a composite segment under a uniform moment (DESIGN §3 #9)
+          for (int c = 0; c < 3; ++c) G(GP_BV1 + c) = (2.0 * Dh) / (ml.lh / Bl[c] + mr.lh / Br[c]);
         }
         if (i < N) sk += d->rest_lengths[eoff[r] + i];
       }

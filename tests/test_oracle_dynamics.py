@@ -273,3 +273,22 @@ def test_instability_detected(orc):
     w.positions[7:] = w.positions[5] + (w.positions[7:] - w.positions[6])
     st, s, bad, bits = orc.step(w, n_steps=1, dt=1e-9)
     assert s == 2 and bad == 1 and bits & orc.F_DEGENERATE
+
+
+def test_actuation_wave_travels_toward_tip(orc):
+    """kappa0_x = A sin(2 pi (s/L - f t)) (BASELINE configs[3]) is a wave travelling toward +s at
+    speed L f: after dt_shift = lhat / (L f) the rest-curvature pattern -- and with it the couple a
+    straight rod at rest feels -- has moved by exactly one element."""
+    N, L, A, f = 16, 0.8, 1.5, 0.7
+    w = rod(N=N, L=L, r=0.004)
+    w = dataclasses.replace(w, act_A=np.array([A]), act_f=np.array([f]), act_L=np.array([L]),
+                            act_component=0)
+    t0 = 0.123
+    shift = (L / N) / (L * f)
+    c0 = orc.rod_loads(w, 0, w.positions, w.velocities, w.directors, w.omega, t0)["C"]
+    c1 = orc.rod_loads(w, 0, w.positions, w.velocities, w.directors, w.omega, t0 + shift)["C"]
+    scale = np.max(np.abs(c0))
+    assert scale > 0
+    # interior elements whose two Voronoi neighbours both exist at both times
+    assert np.max(np.abs(c1[2:N - 1] - c0[1:N - 2])) <= 1e-9 * scale
+    assert np.max(np.abs(c1[2:N - 1] - c0[3:N])) > 1e-2 * scale   # not a wave toward -s

@@ -107,3 +107,22 @@ def test_cilia_metachronal_phase_lag(orc):
     lag = np.angle(np.exp(1j * np.diff(phase)))
     assert np.all(amp > 1e-4)
     assert np.all(np.abs(lag - 2 * np.pi / 8) < 0.05 * 2 * np.pi), lag
+
+
+def test_couple_equals_rotated_lab_dipole_torque(orc):
+    """For a rotated element the couple is the lab-frame dipole torque (Q^T m) x b of the element's
+    moment lhat m (a local vector, lab form Q^T m), expressed in the local frame (v_local = Q v_lab,
+    PAPER.md:236-237): the field enters as Q b, never as b or Q^T b."""
+    import scipy.linalg as sla
+    rng = np.random.default_rng(1)
+    N, L = 4, 0.4
+    K = lambda v: np.array([[0, -v[2], v[1]], [v[2], 0, -v[0]], [-v[1], v[0], 0.0]])
+    Q = sla.expm(K([0.7, -1.2, 0.4]))
+    w = rod(N=N, L=L, Q=Q)
+    m = rng.standard_normal((N, 3))
+    b = np.array([0.3, 0.1, -0.6])
+    w = dataclasses.replace(w, magnetization=m, b_field=b, b_omega=0.0)
+    out = orc.rod_loads(w, 0, w.positions, w.velocities, w.directors, w.omega, 0.0)
+    for j in range(N):
+        tau_lab = np.cross(Q.T @ (0.1 * m[j]), b)
+        assert np.allclose(out["C"][j], Q @ tau_lab, rtol=0, atol=1e-14)   # + rest-state round-off
