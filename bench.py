@@ -6,11 +6,14 @@
 One bench "step" = one position-Verlet time step (all SURVEY §8(a) rows A1-A10) over the
 whole batch.  Default workload: BASELINE.json configs[2] ("cfg3": 1,048,576 rods x 16
 elements, the paper's 1024^2-filament size), synthetic and seeded (workloads/).
-Multi-GPU: one process per GPU (torchrun).  Rods are independent, so the default is weak
-scaling (each rank advances its own 1,048,576-rod cfg3 batch; the job is N x cfg3) with no
-data-path collective; `--scaling strong` instead shards the one cfg3 batch across the ranks
-(the paper's strong-scaling experiment).  NCCL all-reduces only the scalar diagnostics, once,
-after the timed region.  Rank 0 prints one JSON line.
+Multi-GPU: one process per GPU, launched by torchrun or, when `--gpus N` is given without a
+torchrun environment (no WORLD_SIZE), spawned by bench.py itself (N ranks, NCCL, rendezvous on
+127.0.0.1).  The default is strong scaling -- the one cfg3 batch of 1,048,576 rods sharded into
+slot-balanced contiguous rod ranges (BASELINE configs[2] "sharded over 1/2/4/8 GPUs", the paper's
+strong-scaling experiment); `--scaling weak` gives every rank its own full batch.
+Rods are independent, so there is no data-path collective: NCCL all-reduces only the scalar
+diagnostics, once, after the timed region.  Rank 0 prints one JSON line with the per-rank times
+and shard sizes.
 
 `--impl reference`: there is no reference implementation to install (the paper ships no
 code); the reference arm is the CPU oracle (oracle/, plain C fp64), timed on
@@ -49,7 +52,7 @@ def parse():
     ap.add_argument("--steps-per-launch", type=int, default=1,
                     help="1 = every step streams the state through HBM (the B_min design); "
                          ">1 = temporal blocking (SURVEY NEXT-1)")
-    ap.add_argument("--scaling", default="weak", choices=["strong", "weak"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-fanout", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -275,10 +278,38 @@ def run_reference(a):
     }), flush=True)
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _spawned_rank(rank, world, port, argv):
+    """Child process of `bench.py --gpus N` run without torchrun: the torchrun environment, then
+    the ordinary per-rank path."""
+    os.environ.update(RANK=str(rank), LOCAL_RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.argv = argv
+    main()
+
+
+def spawn_ranks(a):
+    """`--gpus N` without a torchrun environment: start N ranks here (one process per GPU)."""
+    import torch.multiprocessing as mp
+    os.environ.setdefault("NCCL_DEBUG", "INFO")             # communicator init (nranks) in the log
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    mp.start_processes(_spawned_rank, args=(a.gpus, _free_port(), list(sys.argv)), nprocs=a.gpus,
+                       join=True, start_method="spawn")
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+        return
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(a)
         return
     import torch
     import torch.distributed as dist
@@ -286,6 +317,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus and rank == 0:
+        print(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}; measuring {world} rank(s)", file=sys.stderr)
     # ER_BENCH_SHARE_GPU=1: functional test of the multi-rank path on a one-GPU box (ranks share
     # GPU 0 and reduce over gloo) -- never a measurement
     share = os.environ.get("ER_BENCH_SHARE_GPU") == "1"
@@ -334,6 +367,12 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
+    per_rank = [{"rank": rank, "ms_per_step": ms / a.steps, "rods": w.n_rods, "elements": w.n_elems_total,
+                 "device": local}]
+    if world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, per_rank[0])
+        per_rank = gathered
     el_local = w.n_elems_total
     el_total = torch.tensor([float(el_local)], dtype=torch.float64, device=f"cuda:{local}")
     # scalar diagnostics: the only cross-GPU exchange (NCCL all-reduce of ~12 fp64)
@@ -454,6 +493,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
+            "per_rank": per_rank,
             "temporal_blocking": temporal,
             "contact": contact,
             "clocks": clk.summary(),

@@ -157,6 +157,7 @@ struct er_batch {
   // the launch time lives in tdev (ping-pong); rebuilt when its parameters change
   cudaGraphExec_t sgraph = nullptr;
   int64_t sgraph_key = -1;
+  uint64_t sgraph_h_bits = 0;   // the step size captured into sgraph (ErStepParams.h, by value)
   bool sgraph_while = false;    // sgraph repeats its 32 launches in a device-side WHILE loop
   long long *d_loop = nullptr;  // its iteration counter
   double *tdev = nullptr;
@@ -1244,8 +1245,11 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
   if (!b->contact_on && b->kernel_mode == 0 && n_steps - done >= ER_GRAPH_LAUNCHES * spl &&
       !std::getenv("ER_NO_STEP_GRAPH")) {
     const int64_t key = ((b->forcing_version * 32 + feat) << 31) + spl;
+    uint64_t h_bits;
+    std::memcpy(&h_bits, &dt, sizeof h_bits);
     if (!b->tdev) CK(dalloc(b, &b->tdev, 2), "cudaMalloc(tdev)");
-    if (b->sgraph_key != key) {
+    // the graph holds ErStepParams by value, including h = dt: a call with another dt recaptures
+    if (b->sgraph_key != key || b->sgraph_h_bits != h_bits) {
       free_step_graph(b);
       if (!b->d_loop) CK(dalloc(b, &b->d_loop, 1), "cudaMalloc(loop)");
       cudaStream_t cs;
@@ -1313,6 +1317,7 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
       cudaStreamDestroy(cs);
       CK(e, "step graph");
       b->sgraph_key = key;
+      b->sgraph_h_bits = h_bits;
     }
     const double t_host = t;  // pageable 8-byte copy: staged before cudaMemcpyAsync returns
     CK(cudaMemcpyAsync(b->tdev, &t_host, sizeof(double), cudaMemcpyHostToDevice, b->stream), "H2D t");

@@ -9,6 +9,10 @@ import numpy as np
 TOL_1STEP = 1e-12
 TOL_1000 = 1e-8
 
+# every measured parity (label, tol, errors), printed by tests/conftest.py at the end of the session
+# so that the margins are visible, not only the pass/fail
+MEASURED = []
+
 
 def floors(w, dt=None):
     h = w.dt if dt is None else dt
@@ -49,6 +53,7 @@ def assert_parity(w, gpu, orc, tol, dt=None, raw=(), label=""):
     """Floored metric on all four quantities; additionally the raw ratio on `raw` keys
     (the quantities that are non-degenerate for the config, C.6)."""
     e = errors(w, gpu, orc, dt)
+    MEASURED.append((label, tol, dict(e), tuple(raw)))
     bad = {k: v for k, v in e.items() if not k.endswith("_raw") and not (v <= tol)}
     assert not bad, f"{label} parity > {tol}: {e}"
     badr = {k: e[k + "_raw"] for k in raw if not (e[k + "_raw"] <= tol)}

@@ -17,6 +17,13 @@ def perturbed_run(orc, w, n, seed=0):
     return errors(w, (a.positions, a.velocities, a.directors, a.omega), (b.positions, b.velocities, b.directors, b.omega))
 
 
+def _subset(name, n):
+    if name == "cfg5":
+        w = W.make(name)
+        return w.subset(W.sample_rods(w, n, seed=1))
+    return W.make(name, n_rods=n)
+
+
 def test_oracle_self_conditioning_cfg4(orc):
     w = W.make("cfg4", n_rods=24)
     e1 = perturbed_run(orc, w, 1)
@@ -26,5 +33,22 @@ def test_oracle_self_conditioning_cfg4(orc):
     e = perturbed_run(orc, w, 1000)
     # floored metric stays well inside the 1e-8 gate ...
     assert all(e[k] < TOL_1000 / 5 for k in ("r", "v", "Q", "w")), e
-    # ... while the raw rate ratios are at/above it: an ulp of input moves them by ~1e-8
-    assert max(e["v_raw"], e["w_raw"]) > 2e-9, e
+    # ... while the raw rate ratios are above it: an ulp of input moves them by > 1e-8
+    # (measured: v 1.3e-8, w 2.5e-8), so tests/test_gpu_parity.py RAW_1000 gates r and Q only
+    assert max(e["v_raw"], e["w_raw"]) > TOL_1000, e
+
+
+def test_oracle_self_conditioning_cfg3(orc):
+    """cfg3 starts at rest: interior rates are round-off of the cancellation sigma = e Q t - e3, so
+    after 1000 steps an ulp of input moves raw w by > 1e-8 (measured 1.7e-8; v 7.7e-9): raw rate
+    gates would test the problem's conditioning, not the implementation (RAW_1000: r and Q)."""
+    e = perturbed_run(orc, _subset("cfg3", 48), 1000)
+    assert all(e[k] < TOL_1000 / 5 for k in ("r", "v", "Q", "w")), e
+    assert max(e["v_raw"], e["w_raw"]) > TOL_1000, e
+
+
+def test_oracle_self_conditioning_cfg5(orc):
+    """cfg5 (ragged, gravity, rest curvature) is well conditioned: an ulp of input moves the raw rates
+    by < 1e-9 after 1000 steps (measured v 7.8e-11, w 5.4e-11), so its rates are gated raw."""
+    e = perturbed_run(orc, _subset("cfg5", 24), 1000)
+    assert max(e["v_raw"], e["w_raw"], e["r_raw"], e["Q_raw"]) < TOL_1000 / 10, e

@@ -46,11 +46,11 @@ def run_orc(orc, w, n_steps):
 RAW = {"cfg1": ("r", "Q"), "cfg2": ("r", "v", "Q", "w"), "cfg3": ("r", "Q"), "cfg4": ("r", "Q", "w"),
        "cfg5": ("r", "Q", "w")}
 # After 1000 steps the raw ratio of the rates is bounded by the problem's own conditioning:
-# the oracle perturbed by half an ulp moves raw v/w by ~2e-8..3e-8 on cfg4
-# (tests/test_conditioning.py), so raw is gated on r and Q only there; the floored metric
-# (C.6) gates all four quantities.
+# the oracle perturbed by half an ulp moves raw v/w by > 1e-8 on cfg3 and cfg4
+# (tests/test_conditioning.py), so raw is gated on r and Q only there; cfg5 is well conditioned
+# (< 1e-9) and gated raw on all four; the floored metric (C.6) gates all four everywhere.
 RAW_1000 = {"cfg1": ("r", "Q"), "cfg2": ("r", "v", "Q", "w"), "cfg3": ("r", "Q"), "cfg4": ("r", "Q"),
-            "cfg5": ("r", "Q")}
+            "cfg5": ("r", "v", "Q", "w")}
 SMALL = {"cfg1": None, "cfg2": 200, "cfg3": 600, "cfg4": 96, "cfg5": 120}
 
 
@@ -443,3 +443,69 @@ def test_step_graph_bitwise(er, monkeypatch):
             out.append(b.get_state())
     for x, y in zip(out[0], out[1]):
         assert np.array_equal(np.asarray(x), np.asarray(y))
+
+
+def test_fault_antipodal(er, orc):
+    """Adjacent elements rotated by nearly pi against each other (SPEC.md:113 reading, ER_F_ANTIPODAL):
+    the kernel flags the rod id; a rotation safely below the threshold is not flagged; the oracle
+    agrees in both cases."""
+    import scipy.linalg as sla
+    K = lambda v: np.array([[0, -v[2], v[1]], [v[2], 0, -v[0]], [-v[1], v[0], 0.0]])
+    for angle, flagged in ((np.pi - 1e-8, True), (np.pi - 1e-4, False)):
+        parts = [rod(N=5, L=0.05, r=0.002) for _ in range(3)]
+        a = np.array([0.3, 1.0, -0.4])
+        a /= np.linalg.norm(a)
+        R = sla.expm(angle * K(a))
+        w = concat(parts)
+        eo = w.elem_offsets()
+        w.directors[eo[2] + 3:eo[3]] = R @ w.directors[eo[2] + 3]   # rod 2: elements 3.. turned by R
+        with er.RodBatch(w) as b:
+            if flagged:
+                with pytest.raises(er.ErError) as ei:
+                    b.step(1, 1e-9)
+                assert ei.value.status == er.ER_EUNSTABLE
+                rod_id, bits = b.fault()
+                assert rod_id == 2 and bits & er.ER_F_ANTIPODAL, (rod_id, bits)
+            else:
+                b.step(1, 1e-9)
+                assert b.fault()[1] & er.ER_F_ANTIPODAL == 0
+        st, s, bad, bits = orc.step(w, n_steps=1, dt=1e-9)
+        assert (bad == 2 and bits & orc.F_ANTIPODAL) if flagged else not (bits & orc.F_ANTIPODAL)
+
+
+def test_step_graph_follows_dt_change(er, monkeypatch):
+    """er_step may change dt between calls: the captured step graph holds the step size by value, so
+    a call with a new dt must recapture it.  A batch large enough for one launch per
+    step (no sweeps) and runs of >= 32 launches take the graph path; the result must equal plain
+    launches bitwise and the oracle within the 1000-step gate."""
+    w = W.make("cfg3").subset(np.arange(148 * 2 * 16 * 5))     # > 4 tiles per CTA: no sweeps
+    out = []
+    for plain in (False, True):
+        if plain:
+            monkeypatch.setenv("ER_NO_STEP_GRAPH", "1")
+        with er.RodBatch(w) as b:
+            b.step(64, w.dt)
+            b.step(64, w.dt / 2)
+            b.step(64, w.dt * 3)
+            out.append(b.get_state())
+    for x, y in zip(out[0], out[1]):
+        assert np.array_equal(np.asarray(x), np.asarray(y))
+
+
+def test_temporal_blocking_full_size_vs_oracle(er, orc):
+    """bench.py's temporal-blocking configuration (full cfg3, 100 steps per launch) against the
+    oracle on sampled rods after 1000 steps (it was only checked transitively)."""
+    w = W.make("cfg3")
+    with er.RodBatch(w) as b:
+        b.set_option(er.ER_OPT_STEPS_PER_LAUNCH, 100)
+        b.step(1000, w.dt)
+        pos, vel, dirs, om, t = b.get_state()
+    rods = W.sample_rods(w, 48, seed=7)
+    ws = w.subset(rods)
+    no, eo = w.node_offsets(), w.elem_offsets()
+    nidx = np.concatenate([np.arange(no[r], no[r + 1]) for r in rods])
+    eidx = np.concatenate([np.arange(eo[r], eo[r + 1]) for r in rods])
+    o, to = run_orc(orc, ws, 1000)
+    assert t == to
+    assert_parity(ws, (pos[nidx], vel[nidx], dirs[eidx], om[eidx]), o, TOL_1000, raw=RAW_1000["cfg3"],
+                  label="cfg3 full x 1000, 100 steps per launch")
