@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define ER_ABI_VERSION 1
+#define ER_ABI_VERSION 2
 
 typedef struct er_batch er_batch; /* opaque handle; owns device memory */
 
@@ -367,6 +367,10 @@ typedef struct {
   int64_t device_bytes;    /* device memory owned by the handle                */
   double t;                /* current time                                     */
   double bytes_per_step;   /* algorithmic HBM bytes of one step    */
+  int32_t warp_rod_elems;  /* > 0: streaming steps run the warp-local kernel  */
+                           /* (equal-length rods of this many elements, one   */
+                           /* rod per <= 32 lanes); 0: tile kernel */
+  int32_t warp_buffers;    /* its stage buffers per CTA (0 if not used)       */
 } er_info;
 er_status er_query(const er_batch *b, er_info *info);
 

@@ -64,6 +64,7 @@ class er_info(C.Structure):
         ("n_voronoi_total", C.c_int64), ("n_tiles", C.c_int64), ("tile_slots", C.c_int32),
         ("device", C.c_int32), ("stream", C.c_void_p), ("launches", C.c_int64),
         ("device_bytes", C.c_int64), ("t", C.c_double), ("bytes_per_step", C.c_double),
+        ("warp_rod_elems", C.c_int32), ("warp_buffers", C.c_int32),
     ]
 
 

@@ -14,11 +14,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "lib", "libelasticarod.so")
-SOURCES = ["er_api.cu", "er_kernels.cu", "er_contact.cu"]
+SOURCES = ["er_api.cu", "er_kernels.cu", "er_warp.cu", "er_contact.cu"]
 # per-file flags: the contact narrow phase takes its branch decisions on IEEE-rounded products
 # and sums in the order written (no FMA contraction; DESIGN §3 #27)
 FILE_FLAGS = {"er_contact.cu": ["-fmad=false"]}
-HEADERS = ["er_layout.h", "er_math.cuh"]
+HEADERS = ["er_layout.h", "er_math.cuh", "er_tma.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]

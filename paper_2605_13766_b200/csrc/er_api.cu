@@ -25,6 +25,7 @@
 
 extern "C" {
 cudaError_t er_launch_step(const ErStepParams *p, int block, int kind, int feat, cudaStream_t st);
+cudaError_t er_launch_warp(const ErStepParams *p, int feat, cudaStream_t st);
 cudaError_t er_launch_long(const ErStepParams *p, int64_t tile0, int64_t n_rods, int nseg, int feat, cudaStream_t st);
 cudaError_t er_launch_diag(const ErStepParams *p, int block, double *out, cudaStream_t st);
 cudaError_t er_launch_canon_tiles(const ErStepParams *p, double *canon, int field, int to_tiles, cudaStream_t st);
@@ -92,6 +93,10 @@ struct er_batch {
   int64_t n_rods = 0, n_elems = 0, n_nodes = 0, n_vor = 0;
   int32_t max_n = 0;
   int block = 256;
+  // warp kernel (er_warp.cu): equal-length rods of ER_WARP_MIN_N..32 elements; 0 = not used
+  int32_t wN = 0, wR = 0, wnb = 0, wbufd = 0, wrec = 0, wdesc = 0;
+  int32_t wrt = 0, wch = 0;    // per-warp streaming variant (0: the tile-pipelined warp kernel)
+  int64_t wcs = 0, wrods = 0;
   int64_t n_tiles = 0;       // all tiles (layout conversion, diagnostics)
   int64_t n_tiles_norm = 0;  // tiles of rods with <= 511 elements (the step kernels); long rods'
   struct LongGroup { int64_t tile0, n_rods; int nseg; };  // segment tiles follow, by cluster size
@@ -350,6 +355,12 @@ ErStepParams params_of(const er_batch *b) {
   p.b_omega = b->b_omega; p.act_comp = b->act_comp;
   p.fault = b->d_fault; p.diag_partial = b->d_diag_partial;
   p.trace = b->trace;
+  p.wN = b->wN; p.wR = b->wR; p.wnb = b->wnb; p.wbufd = b->wbufd; p.wrec = b->wrec; p.wdesc = b->wdesc;
+  p.wrt = b->wrt; p.wch = b->wch; p.wcs = b->wcs; p.wrods = b->wrods;
+  {
+    static const int l2pf = std::getenv("ER_WARP_L2PF") ? std::atoi(std::getenv("ER_WARP_L2PF")) : 0;
+    p.wl2pf = l2pf;
+  }
   return p;
 }
 
@@ -667,6 +678,21 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
     auto fill = [&](int B) { return (double)std::min<int>(B / (max_n + 1), B / 8) * (max_n + 1) / B; };
     if (Rn * (int64_t)(max_n + 1) >= 4 * 512 && fill(512) > fill(256) + 0.05) b->block = 512;
   }
+  // Warp kernel: every rod has the same N in [ER_WARP_MIN_N, 32] elements (no long rods); tiles then
+  // hold 8 warps x floor(32/N) rods (ER_WARP_TILE_RODS overrides, measurement), and the tile kernels
+  // that still run on them (staged ablations, contact mode, sweeps of small batches, diagnostics)
+  // take the block size those tiles need.
+  int32_t wtile_rods = 0;
+  if (!d->tile_slots && n_long == 0 && R > 0 && min_n == max_n && max_n >= ER_WARP_MIN_N && max_n <= 32 &&
+      std::getenv("ER_NO_WARP") == nullptr) {
+    b->wN = max_n;
+    b->wR = 32 / max_n;
+    // default: warp-sized tiles (wR rods, one contiguous block per warp) for the per-warp streaming
+    // kernel; ER_WARP_TMA=1: tiles of 8 warps for the tile-pipelined warp kernel
+    wtile_rods = std::getenv("ER_WARP_TMA") ? 8 * b->wR : b->wR;
+    if (const char *e = std::getenv("ER_WARP_TILE_RODS")) wtile_rods = std::max(1, std::min(8 * b->wR, std::atoi(e)));
+    b->block = (int64_t)wtile_rods * (max_n + 1) <= 256 && wtile_rods <= 32 ? 256 : 512;
+  }
   {
     // packed order: tile rods (best-fit-decreasing when their lengths differ), then long rods by
     // cluster size (so each size is one launch), canonical order within
@@ -720,7 +746,8 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
       T.boff = boff;
       int64_t used = 0;
       int32_t nr = 0;
-      while (r < Rn && nr < b->block / 8 && used + b->n_elems_h[r] + 1 <= b->block) {
+      const int32_t rmax = wtile_rods ? wtile_rods : b->block / 8;
+      while (r < Rn && nr < rmax && used + b->n_elems_h[r] + 1 <= b->block) {
         used += b->n_elems_h[r] + 1;
         ++nr;
         ++r;
@@ -867,6 +894,32 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   }
 
   tile_thread.join();
+  if (b->wN > 0) {
+    // warp-kernel stage buffer: the largest tile block | its rod records | the descriptor; as many
+    // buffers (2..4) as keep two 256-thread CTAs per SM within the 228 KB of shared memory
+    int64_t cs = 0, nr = 0;
+    for (int64_t k = 0; k < b->n_tiles_norm; ++k) {
+      cs = std::max(cs, tile_block_size(tiles[(size_t)k], b->has_kappa0));
+      nr = std::max<int64_t>(nr, tiles[(size_t)k].nr);
+    }
+    b->wrec = (int32_t)cs;
+    b->wdesc = (int32_t)(cs + nr * ER_REC);
+    b->wbufd = b->wdesc + 16;
+    const int64_t per_cta = 113 * 1024 - 64;
+    b->wnb = (int32_t)std::max<int64_t>(2, std::min<int64_t>(4, per_cta / (8 * (int64_t)b->wbufd + 12)));
+    if (const char *e = std::getenv("ER_WARP_BUFFERS")) b->wnb = std::max(1, std::min(8, std::atoi(e)));
+    if (std::getenv("ER_WARP_TMA") == nullptr && b->n_tiles_norm > 0 && wtile_rods == b->wR) {
+      // per-warp streaming (default): uniform tiles (every rod N elements, identity order), a ring
+      // of 2..4 slots of one warp chunk (wR rods: node, element, kappa0 planes, records) per warp
+      const int32_t N = b->wN, Rw = b->wR;
+      b->wrt = wtile_rods;
+      b->wcs = tile_block_size(tiles[0], b->has_kappa0);
+      b->wrods = Rn;
+      b->wch = (int32_t)(b->wcs + Rw * ER_REC);  // block | records (both even: 16-byte copies)
+      b->wnb = (int32_t)std::max<int64_t>(2, std::min<int64_t>(4, (113 * 1024 - 64) / (8 * 8 * (int64_t)b->wch)));
+      if (const char *e = std::getenv("ER_WARP_BUFFERS")) b->wnb = std::max(2, std::min(4, std::atoi(e)));
+    }
+  }
   b->n_tiles = (int64_t)tiles.size();
   tm.mark("gpar + tiles");
 
@@ -1223,7 +1276,8 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
   // dominate (cfg1/cfg2); large batches keep one launch per step (graph replays), which measured
   // faster there.
   const int64_t grid = 148 * (b->block <= 128 ? 4 : b->block <= 256 ? 2 : 1);
-  const int64_t sweeps = b->sweeps > 0 ? b->sweeps : (b->n_tiles_norm <= 4 * grid ? 128 : 1);
+  // (the warp kernel's batches keep one launch per step: its tiles are warp-sized)
+  const int64_t sweeps = b->sweeps > 0 ? b->sweeps : (b->wN == 0 && b->n_tiles_norm <= 4 * grid ? 128 : 1);
   if (!b->contact_on && b->kernel_mode == 0 && sweeps > 1) {
     while (n_steps - done >= spl) {
       const int64_t S = std::min<int64_t>(sweeps, (n_steps - done) / spl);
@@ -1408,6 +1462,75 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
   return ER_OK;
 }
 
+// A warp-layout batch (warp-sized tiles of the warp kernel, er_warp.cu) -> the tile kernels' layout
+// (rod-aligned tiles of <= 256 slots): contact mode runs the tile kernels.  Equal-length rods in the
+// identity order, so only the tiles and the state blocks change; the state moves through canonical
+// device arrays (d1, d2 exactly; d3 is rebuilt as everywhere).
+er_status relayout_to_tiles(er_batch *b) {
+  if (b->wN <= 0) return ER_OK;
+  CK(cudaStreamSynchronize(b->stream), "sync");
+  const int fields[5] = {FIELD_POS, FIELD_VEL, FIELD_DIR, FIELD_OMEGA, FIELD_KAPPA0};
+  const int nf = b->has_kappa0 ? 5 : 4;
+  double *tmp[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  for (int f = 0; f < nf; ++f) {
+    const int64_t n = field_rows(b, fields[f]) * field_k(fields[f]);
+    CK(cudaMalloc((void **)&tmp[f], sizeof(double) * (size_t)std::max<int64_t>(n, 1)), "cudaMalloc(relayout)");
+    er_status st = download_field(b, tmp[f], ER_DEVICE, fields[f]);
+    if (st != ER_OK) return st;
+  }
+  const int32_t N = b->wN;
+  const int64_t R = b->n_rods;
+  b->block = 256;
+  const int32_t rmax = std::min<int32_t>(b->block / 8, b->block / (N + 1));
+  std::vector<ErTile> tiles;
+  tiles.reserve((size_t)(R / rmax + 1));
+  int64_t boff = 0;
+  for (int64_t r = 0; r < R;) {
+    ErTile T;
+    const int32_t nr = (int32_t)std::min<int64_t>(rmax, R - r);
+    T.r0 = (int32_t)r;
+    T.nr = nr;
+    T.nslots = nr * (N + 1);
+    T.nel = nr * N;
+    T.nbase = r * (N + 1);
+    T.ebase = r * N;
+    T.boff = boff;
+    std::memset(T.smask, 0, sizeof T.smask);
+    std::memset(T.pfx, 0, sizeof T.pfx);
+    T.seg = 0;
+    T.nseg = 1;
+    for (int32_t q = 0, st = 0; q < nr; ++q, st += N + 1) T.smask[st >> 5] |= 1u << (st & 31);
+    for (int wd = 1; wd < 16; ++wd) T.pfx[wd] = (uint8_t)(T.pfx[wd - 1] + __builtin_popcount(T.smask[wd - 1]));
+    boff += tile_block_size(T, b->has_kappa0);
+    tiles.push_back(T);
+    r += nr;
+  }
+  free_step_graph(b);
+  cudaFree(b->d_state);
+  cudaFree(b->d_tiles);
+  cudaFree(b->d_diag_partial);
+  b->device_bytes -= (int64_t)sizeof(double) * (b->state_doubles + 64) + (int64_t)sizeof(ErTile) * std::max<int64_t>(b->n_tiles, 1) +
+                     (int64_t)sizeof(double) * std::max<int64_t>(b->n_tiles, 1) * 16;
+  b->state_doubles = boff;
+  b->n_tiles = b->n_tiles_norm = (int64_t)tiles.size();
+  CK(dalloc(b, &b->d_state, b->state_doubles + 64), "cudaMalloc(state)");
+  CK(dalloc(b, &b->d_tiles, std::max<int64_t>(b->n_tiles, 1)), "cudaMalloc(tiles)");
+  CK(dalloc(b, &b->d_diag_partial, std::max<int64_t>(b->n_tiles, 1) * 16), "cudaMalloc(diag)");
+  CK(cudaMemsetAsync(b->d_state, 0, sizeof(double) * (b->state_doubles + 64), b->stream), "memset");
+  if (!tiles.empty())
+    CK(cudaMemcpyAsync(b->d_tiles, tiles.data(), sizeof(ErTile) * tiles.size(), cudaMemcpyHostToDevice, b->stream), "H2D tiles");
+  b->wN = b->wR = b->wnb = b->wbufd = b->wrec = b->wdesc = b->wrt = b->wch = 0;
+  b->wcs = b->wrods = 0;
+  for (int f = 0; f < nf; ++f) {
+    er_status st = upload_field(b, tmp[f], ER_DEVICE, fields[f], false);
+    if (st != ER_OK) return st;
+  }
+  CK(cudaStreamSynchronize(b->stream), "sync");  // the host tile vector is freed at scope exit
+  for (int f = 0; f < nf; ++f) cudaFree(tmp[f]);
+  b->forcing_version += 1;
+  return ER_OK;
+}
+
 er_status er_set_contact(er_batch *b, const er_contact *c) {
   if (!b) return ER_EINVAL;
   if (!c || !c->enable) {
@@ -1444,6 +1567,10 @@ er_status er_set_contact(er_batch *b, const er_contact *c) {
   CK(cudaSetDevice(b->device), "cudaSetDevice");
   CK(cudaStreamSynchronize(b->stream), "sync");
   free_contact(b);
+  if (b->wN > 0) {  // contact runs the tile kernels: warp-sized tiles -> rod-aligned 256-slot tiles
+    er_status st = relayout_to_tiles(b);
+    if (st != ER_OK) return st;
+  }
   ErContactParams &cp = b->cp;
   ErContactLaw &L = cp.law;
   L.k_n = c->k_n; L.gamma_n = c->gamma_n; L.mu_s = c->mu_s; L.mu_k = c->mu_k; L.v_stick = c->v_stick;
@@ -1629,6 +1756,8 @@ er_status er_query(const er_batch *b, er_info *info) {
   info->n_voronoi_total = b->n_vor;
   info->n_tiles = b->n_tiles;
   info->tile_slots = b->block;
+  info->warp_rod_elems = b->wN;
+  info->warp_buffers = b->wnb;
   info->device = b->device;
   info->stream = (void *)b->stream;
   info->launches = b->launches;

@@ -215,7 +215,24 @@ struct ErStepParams {
   int32_t *rebuild;       // ... sets this flag
   int32_t sweeps;         // tile kernel: passes over all tiles in this launch (one step each), >= 1
   int32_t pad3_;
+  // warp-local kernel (er_warp.cu): uniform rods of ER_WARP_MIN_N..32 elements, each rod on N lanes
+  // of one warp (lane = element; the rod's last lane also owns node N), wR rods per warp, 8 warps
+  // per tile; neighbour values move by warp shuffles, warps never wait for each other
+  int32_t wN;             // elements per rod (0: the batch does not use the warp kernel)
+  int32_t wR;             // rods per warp (floor(32 / wN))
+  int32_t wnb;            // stage buffers per CTA
+  int32_t wbufd;          // doubles per stage buffer (state block | rod records | tile descriptor)
+  int32_t wrec;           // offset of the rod records in a buffer (doubles)
+  int32_t wdesc;          // offset of the tile descriptor in a buffer (doubles)
+  // per-warp streaming variant (warp_stream): uniform tiles of wrt rods, blocks of wcs doubles
+  int32_t wrt;            // rods per tile (all tiles but the last are full)
+  int32_t wch;            // doubles per warp stage slot (node | element | kappa0 planes | records)
+  int64_t wcs;            // doubles per full tile block (tile t starts at t * wcs)
+  int64_t wrods;          // rods in the tile part of the batch
+  int32_t wl2pf;          // warp_bulk: L2 prefetch distance in tiles beyond the slot ring (0 = none)
+  int32_t pad4_;
 };
+#define ER_WARP_MIN_N 4     // warp kernel: <= 8 rods per warp, <= 64 per tile (the record staging)
 #define ER_TRACE_ITERS 64
 #ifndef ER_TRACE
 #define ER_TRACE 0  // per-tile timeline compiled in (measurement builds: -DER_TRACE=1)

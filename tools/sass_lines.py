@@ -29,7 +29,7 @@ si, ie, ss = h.index("Source"), h.index("Instructions Executed"), h.index("Warp 
 body = [r for r in rows[2:] if len(r) > ie]
 assert len(body) == len(seq), (len(body), len(seq))
 files = {}
-for f in ("er_kernels.cu", "er_math.cuh"):
+for f in ("er_kernels.cu", "er_math.cuh", "er_warp.cu", "er_tma.cuh"):
     files[f] = open(os.path.join(ROOT, "paper_2605_13766_b200", "csrc", f)).read().split("\n")
 agg, inst, ops = collections.Counter(), collections.Counter(), collections.Counter()
 tots = sum(int(r[ss] or 0) for r in body)
