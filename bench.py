@@ -407,7 +407,10 @@ def main():
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "peak_source": peak_src, "bytes_per_el_step": bmin,
             "b_min_survey_3x3": b_min_per_el_step(w, 12.0),
-            "kernel": "er::fused_persistent<256,2,FEAT> (fused single-pass step, TMA bulk load/store pipeline)",
+            "kernel": (f"er::warp_bulk<FEAT,{b.info().warp_buffers},{b.info().warp_rod_elems}> (warp-local step: lane = "
+                       "element, shuffle exchanges, per-warp TMA bulk load/store ring)" if b.info().warp_rod_elems
+                       else f"er::fused_persistent<{b.info().tile_slots},MINB,FEAT> (tile step, CTA-level TMA bulk "
+                            "load/store pipeline)"),
             "kernel_ms_per_launch": launch_ms, "kernel_share_of_step": ph.step_kernel_ms / ms if ms > 0 else None}
     if ph.contact_evals:
         roof["contact_ms_per_step"] = ph.contact_ms / ph.contact_evals

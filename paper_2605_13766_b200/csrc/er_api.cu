@@ -736,6 +736,50 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   std::vector<ErTile> tiles;
   b->has_kappa0 = d->rest_kappa != nullptr && NV > 0;
   std::thread tile_thread([&]() {
+    if (wtile_rods > 0) {
+      // warp layout: equal rods in the identity order, every tile but the last full -- each tile's
+      // descriptor is a function of its index, filled by host threads in parallel (cfg3: 524,288
+      // warp-sized tiles)
+      const int32_t N = max_n;
+      const int64_t nt = (Rn + wtile_rods - 1) / wtile_rods;
+      tiles.resize((size_t)nt);
+      ErTile full;
+      std::memset(&full, 0, sizeof full);
+      full.nr = (int32_t)std::min<int64_t>(wtile_rods, Rn);
+      full.nslots = full.nr * (N + 1);
+      full.nel = full.nr * N;
+      full.nseg = 1;
+      for (int32_t q = 0, st = 0; q < full.nr; ++q, st += N + 1) full.smask[st >> 5] |= 1u << (st & 31);
+      for (int wd = 1; wd < 16; ++wd) full.pfx[wd] = (uint8_t)(full.pfx[wd - 1] + __builtin_popcount(full.smask[wd - 1]));
+      const int64_t bsz = tile_block_size(full, b->has_kappa0);
+      auto fill = [&](int64_t t0, int64_t t1) {
+        for (int64_t t = t0; t < t1; ++t) {
+          ErTile T = full;
+          const int64_t r0 = t * wtile_rods;
+          T.r0 = (int32_t)r0;
+          T.nbase = r0 * (N + 1);
+          T.ebase = r0 * N;
+          T.boff = t * bsz;
+          if (t == nt - 1 && Rn - r0 < wtile_rods) {  // partial last tile
+            T.nr = (int32_t)(Rn - r0);
+            T.nslots = T.nr * (N + 1);
+            T.nel = T.nr * N;
+            std::memset(T.smask, 0, sizeof T.smask);
+            std::memset(T.pfx, 0, sizeof T.pfx);
+            for (int32_t q = 0, st = 0; q < T.nr; ++q, st += N + 1) T.smask[st >> 5] |= 1u << (st & 31);
+            for (int wd = 1; wd < 16; ++wd) T.pfx[wd] = (uint8_t)(T.pfx[wd - 1] + __builtin_popcount(T.smask[wd - 1]));
+          }
+          tiles[(size_t)t] = T;
+        }
+      };
+      const int nth = (int)std::max<unsigned>(1u, std::min<unsigned>(8u, std::thread::hardware_concurrency() / 2));
+      std::vector<std::thread> th;
+      for (int k = 0; k < nth; ++k) th.emplace_back(fill, nt * k / nth, nt * (k + 1) / nth);
+      for (auto &x : th) x.join();
+      b->n_tiles_norm = nt;
+      b->state_doubles = nt ? tiles.back().boff + tile_block_size(tiles.back(), b->has_kappa0) : 0;
+      return;
+    }
     tiles.reserve((size_t)(Rn / std::max(1, b->block / std::max<int32_t>(max_n + 1, 1))) + (size_t)(R - Rn) * 16 + 64);
     int64_t r = 0, boff = 0;
     while (r < Rn) {
@@ -911,7 +955,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
     if (std::getenv("ER_WARP_TMA") == nullptr && b->n_tiles_norm > 0 && wtile_rods == b->wR) {
       // per-warp streaming (default): uniform tiles (every rod N elements, identity order), a ring
       // of 2..4 slots of one warp chunk (wR rods: node, element, kappa0 planes, records) per warp
-      const int32_t N = b->wN, Rw = b->wR;
+      const int32_t Rw = b->wR;
       b->wrt = wtile_rods;
       b->wcs = tile_block_size(tiles[0], b->has_kappa0);
       b->wrods = Rn;

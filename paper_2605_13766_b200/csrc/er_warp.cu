@@ -512,11 +512,11 @@ template <int NT>
 __device__ __forceinline__ void issue_wtile_async(const ErStepParams &p, const WTile &g, double *S, int lane) {
   const double *G = p.state + g.boff;
   if (NT) {
+    constexpr int NTc = NT ? NT : 1;
+    constexpr int CS = (6 * (32 / NTc) * (NTc + 1) + ER_EPL * (32 / NTc) * NTc + 1) & ~1;  // state planes
 #pragma unroll
-    for (int x = 2 * lane; x < ((6 * (32 / NT) * (NT + 1) + ER_EPL * (32 / NT) * NT + 1) & ~1); x += 64)
-      cp_async16(S + x, G + x);
-    for (int x = 6 * (32 / NT) * (NT + 1) + ER_EPL * (32 / NT) * NT + 2 * lane; x < g.cs; x += 64)  // kappa0 planes
-      cp_async16(S + x, G + x);
+    for (int x = 2 * lane; x < CS; x += 64) cp_async16(S + x, G + x);
+    for (int x = CS + 2 * lane; x < g.cs; x += 64) cp_async16(S + x, G + x);  // kappa0 planes
   } else {
     for (int x = 2 * lane; x < g.cs; x += 64) cp_async16(S + x, G + x);
   }
