@@ -91,16 +91,18 @@ __device__ __forceinline__ void wstep(const ErStepParams &p, const double *__res
   const double t_half = t + hh;
   auto gp = [&](int plane, int64_t node) { return __ldg(p.gpar + plane * p.ng + node); };
 
-  // ---- A1-A3 drift-1
-  if (active && !(L.lb & WL_CL_NODE)) {
+  // ---- A1-A3 drift-1.  A clamped node / element moves by a zero step (r + 0 v = r; rot(0) Q = Q
+  // exactly), so the warp takes no branch for the rods' clamped ends.
+  const double hr = (L.lb & WL_CL_NODE) ? 0.0 : hh, hq = (L.lb & WL_CL_ELEM) ? 0.0 : hh;
+  if (active) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) r[c] = fma(hh, v[c], r[c]);
+    for (int c = 0; c < 3; ++c) r[c] = fma(hr, v[c], r[c]);
+    rotate_inplace(Q, hq * w[0], hq * w[1], hq * w[2]);
   }
   if (last && !(L.lb & WL_CL_NODEN)) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) xN.set_r(c, fma(hh, xN.v(c), xN.r(c)));
   }
-  if (active && !(L.lb & WL_CL_ELEM)) rotate_inplace(Q, hh * w[0], hh * w[1], hh * w[2]);
 
   // ---- exchange A: node i+1 from the next lane (the rod's last lane owns node N), element i-1
   double rn[3], vn[3], Qp[9];
@@ -110,7 +112,10 @@ __device__ __forceinline__ void wstep(const ErStepParams &p, const double *__res
     vn[c] = __shfl_down_sync(kFull, v[c], 1);
   }
 #pragma unroll
-  for (int c = 0; c < ER_QST; ++c) Qp[c] = __shfl_up_sync(kFull, Q[c], 1);
+  for (int c = 0; c < ER_QST; ++c) {  // a rod's first lane pairs its element with itself (kappa = 0)
+    const double q = __shfl_up_sync(kFull, Q[c], 1);
+    Qp[c] = has_v ? q : Q[c];
+  }
   if (last) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) { rn[c] = xN.r(c); vn[c] = xN.v(c); }
@@ -151,12 +156,14 @@ __device__ __forceinline__ void wstep(const ErStepParams &p, const double *__res
     for (int c = 0; c < 3; ++c) n[c] = fma(Q[c], nb[0], fma(Q[3 + c], nb[1], Q[6 + c] * nb[2]));  // Q^T nbar
   }
   // ---- A6 Voronoi i: curvature via inverse Rodrigues
-  double kap[3] = {0.0, 0.0, 0.0};
-  if (has_v) {
+  // (no branch: a rod's first lane computes kappa = 0 from its own frame and masks the moment below,
+  // so the curvature can be scheduled beside the edge block)
+  double kap[3];
+  {
     double cth, s2;
     complete_d3(Qp);  // the bits the neighbour holds in its registers
     logrot_pair(Q, Qp, kap, cth, s2);
-    if (cth < 0.0 && s2 <= 1e-12 * cth * cth) fbits |= 4u;  // ER_F_ANTIPODAL: theta >= pi - 1e-6
+    if (has_v && cth < 0.0 && s2 <= 1e-12 * cth * cth) fbits |= 4u;  // ER_F_ANTIPODAL: theta >= pi - 1e-6
   }
   // ---- exchange B: l_{i-1}, n_{i-1}
   const double lp = __shfl_up_sync(kFull, l, 1);
@@ -166,7 +173,7 @@ __device__ __forceinline__ void wstep(const ErStepParams &p, const double *__res
 
   // ---- A6 bending moment and its averaged cross term
   double mb[3] = {0.0, 0.0, 0.0}, be[3] = {0.0, 0.0, 0.0};
-  if (has_v) {
+  {
     const double Dh = general ? gp(GP_DH, L.node) : rec[REC_LHAT];
     const double iDh = general ? 1.0 / Dh : rec[REC_ILHAT];
 #pragma unroll
@@ -199,6 +206,11 @@ __device__ __forceinline__ void wstep(const ErStepParams &p, const double *__res
       mb[0] -= p.musc_comp == 0 ? tau : 0.0;
       mb[1] -= p.musc_comp == 1 ? tau : 0.0;
       mb[2] -= p.musc_comp == 2 ? tau : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {  // no Voronoi domain on a rod's first lane
+      mb[c] = has_v ? mb[c] : 0.0;
+      be[c] = has_v ? be[c] : 0.0;
     }
   }
   // ---- A7 + A9 node force, linear acceleration, kick: node i, and node N on the rod's last lane
@@ -290,15 +302,15 @@ __device__ __forceinline__ void wstep(const ErStepParams &p, const double *__res
   }
   // ---- A10 drift-2
   t = t_half + hh;
-  if (active && !(L.lb & WL_CL_NODE)) {
+  if (active) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) r[c] = fma(hh, v[c], r[c]);
+    for (int c = 0; c < 3; ++c) r[c] = fma(hr, v[c], r[c]);
+    rotate_inplace(Q, hq * w[0], hq * w[1], hq * w[2]);
   }
   if (last && !(L.lb & WL_CL_NODEN)) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) xN.set_r(c, fma(hh, xN.v(c), xN.r(c)));
   }
-  if (active && !(L.lb & WL_CL_ELEM)) rotate_inplace(Q, hh * w[0], hh * w[1], hh * w[2]);
   // fault checks: non-finite state, overspeed (as step_body; node N on the last lane)
   if (active) {
     const double acc = ((r[0] + r[1]) + (r[2] + v[0])) + ((v[1] + v[2]) + (w[0] + (w[1] + w[2])));
