@@ -715,24 +715,46 @@ __global__ void __launch_bounds__(kWarpBlock, 2) warp_bulk(const ErStepParams p)
   int64_t k = 0;
   for (int64_t t = gw; t < p.n_tiles; t += G, ++k) {
     const int j = (int)(k % NB);
+#if ER_TRACE  // measurement builds: per-warp timeline [global warp][64 tiles][4] (tools/warp_timeline.py)
+    unsigned long long *tr = (p.trace && lane == 0 && k < ER_TRACE_ITERS) ? p.trace + (gw * ER_TRACE_ITERS + k) * 8 : nullptr;
+    if (tr) tr[0] = (gtimer() & ((1ull << 48) - 1)) | ((unsigned long long)smid() << 56);
+#endif
     if (t + G >= p.n_tiles) griddep_launch_dependents();  // last tile of this warp
     mbar_wait(&bars[j], (uint32_t)((k / NB) & 1));
+#if ER_TRACE
+    if (tr) tr[1] = gtimer() & ((1ull << 48) - 1);
+#endif
     const WTile g = geom(t);
     double *S = ring + j * p.wch;
     if (NT && t < nfull) stream_tile<FEAT, NT, true>(p, g, S, lane, t0, fbits_all, frod);
     else stream_tile<FEAT, 0, true>(p, g, S, lane, t0, fbits_all, frod);
+#if ER_TRACE
+    if (tr) tr[2] = gtimer() & ((1ull << 48) - 1);
+#endif
     fence_proxy_async();  // this lane's generic smem writes -> visible to the async proxy
     __syncwarp();
+#if ER_TRACE
+    if (tr) tr[3] = gtimer() & ((1ull << 48) - 1);
+#endif
     if (lane == 0) {
       const uint32_t tot = (uint32_t)(6 * g.ns + ER_EPL * g.nel);
       bulk_s2g(p.state + g.boff, S, 8u * (tot & ~1u));
       bulk_commit();
       if (tot & 1u) p.state[g.boff + tot - 1] = S[tot - 1];
+#if ER_TRACE
+      if (tr) tr[4] = gtimer() & ((1ull << 48) - 1);
+#endif
       const int64_t tn = t + (NB - 1) * G;
       if (tn < p.n_tiles) {
         asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // the previous tile's store read its slot
+#if ER_TRACE
+        if (tr) tr[5] = gtimer() & ((1ull << 48) - 1);
+#endif
         issue(tn, (int)((k + NB - 1) % NB));
       }
+#if ER_TRACE
+      if (tr) tr[6] = gtimer() & ((1ull << 48) - 1);
+#endif
       // L2 prefetch further ahead (no shared memory needed): the slot loads then hit L2
       const int64_t tp = tn + (int64_t)p.wl2pf * G;
       if (p.wl2pf > 0 && tp < p.n_tiles) {
