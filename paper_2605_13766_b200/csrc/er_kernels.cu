@@ -128,12 +128,13 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
   const double t_half = t + hh;
   auto gp = [&](int plane) { return __ldg(p.gpar + plane * p.ng + si.node); };
 
+  // A clamped node / element (and a slot without an element) moves by a zero step: r + 0 v = r and
+  // rot(0) Q = Q exactly, so the drifts take no branch at the rods' ends.
+  const double hr = si.cl_node ? 0.0 : hh, hq = (si.has_e && !si.cl_elem) ? hh : 0.0;
   if (DRIFT1) {
-    if (!si.cl_node) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) r[c] = fma(hh, v[c], r[c]);
-    }
-    if (si.has_e && !si.cl_elem) rotate_inplace(Q, hh * w[0], hh * w[1], hh * w[2]);
+    for (int c = 0; c < 3; ++c) r[c] = fma(hr, v[c], r[c]);
+    rotate_inplace(Q, hq * w[0], hq * w[1], hq * w[2]);
   }
   if (DYN) {
     // ---- exchange A
@@ -181,14 +182,20 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
       for (int c = 0; c < 3; ++c) n[c] = fma(Q[c], nb[0], fma(Q[3 + c], nb[1], Q[6 + c] * nb[2]));  // Q^T nbar
     }
     // ---- A6 Voronoi i: curvature via inverse Rodrigues
-    double kap[3] = {0.0, 0.0, 0.0};
-    if (si.has_v) {
+    // (no branch: a slot without a Voronoi domain pairs its element with itself -- kappa = 0 -- and
+    // its moment is masked below)
+    double kap[3];
+    {
       double Qp[9], cth, s2;
+      const int sp = si.has_v ? s - 1 : s;  // (a long-rod segment's slot 0 reads its halo at -1)
 #pragma unroll
-      for (int c = 0; c < ER_QST; ++c) Qp[c] = X[(XQ + c) * XS + s - 1];
+      for (int c = 0; c < ER_QST; ++c) {
+        const double q = X[(XQ + c) * XS + sp];
+        Qp[c] = si.has_v ? q : Q[c];
+      }
       complete_d3(Qp);  // the bits the neighbour holds in its registers
       logrot_pair(Q, Qp, kap, cth, s2);
-      if (cth < 0.0 && s2 <= 1e-12 * cth * cth) fbits |= 4u;  // ER_F_ANTIPODAL: theta >= pi - 1e-6
+      if (si.has_v && cth < 0.0 && s2 <= 1e-12 * cth * cth) fbits |= 4u;  // ER_F_ANTIPODAL: theta >= pi - 1e-6
     }
     // ---- exchange B
     if (si.has_e) {
@@ -200,7 +207,7 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
 
     // ---- A6 bending moment and its averaged cross term
     double mb[3] = {0.0, 0.0, 0.0}, be[3] = {0.0, 0.0, 0.0};
-    if (si.has_v) {
+    {
       const double Dh = general ? gp(GP_DH) : rec[REC_LHAT];
       const double iDh = general ? 1.0 / Dh : rec[REC_ILHAT];
 #pragma unroll
@@ -237,6 +244,11 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
         mb[0] -= p.musc_comp == 0 ? tau : 0.0;
         mb[1] -= p.musc_comp == 1 ? tau : 0.0;
         mb[2] -= p.musc_comp == 2 ? tau : 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {  // no Voronoi domain at the slot
+        mb[c] = si.has_v ? mb[c] : 0.0;
+        be[c] = si.has_v ? be[c] : 0.0;
       }
     }
     // ---- A7 + A9 node force, linear acceleration, kick
@@ -312,11 +324,9 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
   }
   if (DRIFT2) {
     t = t_half + hh;
-    if (!si.cl_node) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) r[c] = fma(hh, v[c], r[c]);
-    }
-    if (si.has_e && !si.cl_elem) rotate_inplace(Q, hh * w[0], hh * w[1], hh * w[2]);
+    for (int c = 0; c < 3; ++c) r[c] = fma(hr, v[c], r[c]);
+    rotate_inplace(Q, hq * w[0], hq * w[1], hq * w[2]);
   }
   if ((DRIFT1 || DRIFT2) && si.active) {
     // fault checks: non-finite state, overspeed.  r, v and w suffice: Q changes only through
