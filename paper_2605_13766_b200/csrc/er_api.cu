@@ -683,13 +683,13 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   // that still run on them (staged ablations, contact mode, sweeps of small batches, diagnostics)
   // take the block size those tiles need.
   int32_t wtile_rods = 0;
-  if (!d->tile_slots && n_long == 0 && R > 0 && min_n == max_n && max_n >= ER_WARP_MIN_N && max_n <= 32 &&
-      std::getenv("ER_NO_WARP") == nullptr) {
+  if (!d->tile_slots && n_long == 0 && R > 0 && min_n == max_n && max_n >= ER_WARP_MIN_N &&
+      max_n <= (std::getenv("ER_NO_WARP_PAIR") ? 32 : 64) && std::getenv("ER_NO_WARP") == nullptr) {
     b->wN = max_n;
-    b->wR = 32 / max_n;
+    b->wR = max_n <= 32 ? 32 / max_n : 1;  // 33..64 elements: one rod per warp pair
     // default: warp-sized tiles (wR rods, one contiguous block per warp) for the per-warp streaming
     // kernel; ER_WARP_TMA=1: tiles of 8 warps for the tile-pipelined warp kernel
-    wtile_rods = std::getenv("ER_WARP_TMA") ? 8 * b->wR : b->wR;
+    wtile_rods = (std::getenv("ER_WARP_TMA") && max_n <= 32) ? 8 * b->wR : b->wR;
     if (const char *e = std::getenv("ER_WARP_TILE_RODS")) wtile_rods = std::max(1, std::min(8 * b->wR, std::atoi(e)));
     b->block = (int64_t)wtile_rods * (max_n + 1) <= 256 && wtile_rods <= 32 ? 256 : 512;
   }
@@ -952,15 +952,16 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
     const int64_t per_cta = 113 * 1024 - 64;
     b->wnb = (int32_t)std::max<int64_t>(2, std::min<int64_t>(4, per_cta / (8 * (int64_t)b->wbufd + 12)));
     if (const char *e = std::getenv("ER_WARP_BUFFERS")) b->wnb = std::max(1, std::min(8, std::atoi(e)));
-    if (std::getenv("ER_WARP_TMA") == nullptr && b->n_tiles_norm > 0 && wtile_rods == b->wR) {
+    if ((std::getenv("ER_WARP_TMA") == nullptr || b->wN > 32) && b->n_tiles_norm > 0 && wtile_rods == b->wR) {
       // per-warp streaming (default): uniform tiles (every rod N elements, identity order), a ring
       // of 2..4 slots of one warp chunk (wR rods: node, element, kappa0 planes, records) per warp
-      const int32_t Rw = b->wR;
+      const int32_t Rw = b->wR, N = b->wN;
       b->wrt = wtile_rods;
       b->wcs = tile_block_size(tiles[0], b->has_kappa0);
       b->wrods = Rn;
       b->wch = (int32_t)(b->wcs + Rw * ER_REC);  // block | records (both even: 16-byte copies)
-      b->wnb = (int32_t)std::max<int64_t>(2, std::min<int64_t>(4, (113 * 1024 - 64) / (8 * 8 * (int64_t)b->wch)));
+      const int64_t units = N > 32 ? 4 : 8;  // pipelines per CTA (warps, or warp pairs)
+      b->wnb = (int32_t)std::max<int64_t>(2, std::min<int64_t>(4, (113 * 1024 - 512) / (units * 8 * (int64_t)b->wch)));
       if (const char *e = std::getenv("ER_WARP_BUFFERS")) b->wnb = std::max(2, std::min(4, std::atoi(e)));
     }
   }

@@ -77,10 +77,72 @@ struct XReg {
   __device__ __forceinline__ void set_v(int c, double a) { vv[c] = a; }
 };
 
-template <int FEAT, class XN>
+// Neighbour exchange across a warp boundary.  NoCross: every rod lies in one warp.  PairCross: a rod
+// of 33..64 elements lies on two warps of a pair; element 31 (warp 0, lane 31) and element 32 (warp 1,
+// lane 0) swap their neighbour values through a mailbox in shared memory, one named barrier of the
+// pair's 64 threads per exchange (the three mailboxes are separate, so a mailbox is rewritten only
+// after both warps have passed the two later barriers of the step).
+struct NoCross {
+  __device__ __forceinline__ void a(const double *, const double *, const double *, double *, double *, double *) const {}
+  __device__ __forceinline__ void b(double, const double *, double &, double *) const {}
+  __device__ __forceinline__ void c(const double *, const double *, double *, double *) const {}
+};
+__device__ __forceinline__ void pair_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+struct PairCross {
+  double *mb;  // this pair's mailboxes: [0..5] r, v of element 32's node; [6..11] d1, d2 of element 31;
+               // [12..15] l, n of edge 31; [16..21] mbar, beta of Voronoi 32
+  int id;      // named barrier of the pair (1..4)
+  bool lo, hi; // this lane is warp 0 / lane 31, warp 1 / lane 0
+  __device__ __forceinline__ void a(const double *r, const double *v, const double *Q, double *rn, double *vn,
+                                    double *Qp) const {
+    if (hi) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) { mb[c] = r[c]; mb[3 + c] = v[c]; }
+    }
+    if (lo) {
+#pragma unroll
+      for (int c = 0; c < ER_QST; ++c) mb[6 + c] = Q[c];
+    }
+    pair_sync(id);
+    if (lo) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) { rn[c] = mb[c]; vn[c] = mb[3 + c]; }
+    }
+    if (hi) {
+#pragma unroll
+      for (int c = 0; c < ER_QST; ++c) Qp[c] = mb[6 + c];
+    }
+  }
+  __device__ __forceinline__ void b(double l, const double *n, double &lp, double *np) const {
+    if (lo) {
+      mb[12] = l;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) mb[13 + c] = n[c];
+    }
+    pair_sync(id);
+    if (hi) {
+      lp = mb[12];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) np[c] = mb[13 + c];
+    }
+  }
+  __device__ __forceinline__ void c(const double *m, const double *be, double *mbn, double *ben) const {
+    if (hi) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) { mb[16 + c] = m[c]; mb[19 + c] = be[c]; }
+    }
+    pair_sync(id);
+    if (lo) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) { mbn[c] = mb[16 + c]; ben[c] = mb[19 + c]; }
+    }
+  }
+};
+
+template <int FEAT, class XN, class CR = NoCross>
 __device__ __forceinline__ void wstep(const ErStepParams &p, const double *__restrict__ rec, const WLane &L,
                                       double r[3], double v[3], XN &xN, double Q[9], double w[3],
-                                      const double k0s[3], double &t, unsigned &fbits) {
+                                      const double k0s[3], double &t, unsigned &fbits, const CR &cr = CR()) {
   constexpr bool GEN = (FEAT & FEAT_GENERAL) != 0;
   constexpr bool EXTRA = (FEAT & FEAT_EXTRA) != 0;
   constexpr bool ACT = (FEAT & (FEAT_EXTRA | FEAT_ACT)) != 0;
@@ -116,6 +178,7 @@ __device__ __forceinline__ void wstep(const ErStepParams &p, const double *__res
     const double q = __shfl_up_sync(kFull, Q[c], 1);
     Qp[c] = has_v ? q : Q[c];
   }
+  cr.a(r, v, Q, rn, vn, Qp);
   if (last) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) { rn[c] = xN.r(c); vn[c] = xN.v(c); }
@@ -166,10 +229,11 @@ __device__ __forceinline__ void wstep(const ErStepParams &p, const double *__res
     if (has_v && cth < 0.0 && s2 <= 1e-12 * cth * cth) fbits |= 4u;  // ER_F_ANTIPODAL: theta >= pi - 1e-6
   }
   // ---- exchange B: l_{i-1}, n_{i-1}
-  const double lp = __shfl_up_sync(kFull, l, 1);
+  double lp = __shfl_up_sync(kFull, l, 1);
   double np[3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) np[c] = __shfl_up_sync(kFull, n[c], 1);
+  cr.b(l, n, lp, np);
 
   // ---- A6 bending moment and its averaged cross term
   double mb[3] = {0.0, 0.0, 0.0}, be[3] = {0.0, 0.0, 0.0};
@@ -261,6 +325,7 @@ __device__ __forceinline__ void wstep(const ErStepParams &p, const double *__res
     mbn[c] = __shfl_down_sync(kFull, mb[c], 1);
     ben[c] = __shfl_down_sync(kFull, be[c], 1);
   }
+  cr.c(mb, be, mbn, ben);
   if (last) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) { mbn[c] = 0.0; ben[c] = 0.0; }
@@ -540,9 +605,10 @@ __device__ __forceinline__ void issue_wtile_async(const ErStepParams &p, const W
 // One tile of one warp: stage slot -> registers, n_steps steps, results to HBM.
 // TO_SMEM: the results go back into the slot, in place (a bulk store moves the block); else straight
 // to HBM from registers.
-template <int FEAT, int NT, bool TO_SMEM = false>
+// lane: the lane's position in the tile's element range (a pair's second warp: 32 + lane).
+template <int FEAT, int NT, bool TO_SMEM = false, class CR = NoCross>
 __device__ __forceinline__ void stream_tile(const ErStepParams &p, const WTile &g, const double *S, int lane,
-                                            double t0, unsigned &fbits_all, int &frod) {
+                                            double t0, unsigned &fbits_all, int &frod, const CR &cr = CR()) {
   constexpr int NTc = NT ? NT : 1;
   const int N = NT ? NT : p.wN;
   const int gl = NT ? lane / NTc : lane / N;
@@ -586,7 +652,7 @@ __device__ __forceinline__ void stream_tile(const ErStepParams &p, const WTile &
   XSmem xN{const_cast<double *>(S) + sl + 1, ns};  // node N (last lanes), plane stride ns
   double tt = t0;
   unsigned fbits = 0;
-  for (int st = 0; st < p.n_steps; ++st) wstep<FEAT>(p, rec, L, r, v, xN, Q, w, k0s, tt, fbits);
+  for (int st = 0; st < p.n_steps; ++st) wstep<FEAT, XSmem, CR>(p, rec, L, r, v, xN, Q, w, k0s, tt, fbits, cr);
   if (fbits) {
     fbits_all |= fbits;
     frod = min(frod, (int)rec[REC_CANON]);
@@ -769,6 +835,73 @@ __global__ void __launch_bounds__(kWarpBlock, 2) warp_bulk(const ErStepParams p)
   report_fault(p, fbits_all, frod);
 }
 
+// pair_bulk: warp_bulk for rods of 33..64 elements (cfg4's 64): a rod is one tile and lies on the 64
+// lanes of a warp pair (element i on warp i / 32, lane i % 32); the pair shares a slot ring, its
+// lane 0 of warp 0 issues the TMA loads and stores, and the two warps meet at a named barrier in each
+// of the three exchanges and once per tile before the store.
+template <int FEAT, int NB>
+__global__ void __launch_bounds__(kWarpBlock, 2) pair_bulk(const ErStepParams p) {
+  constexpr int kPairs = kWarps / 2;
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int pw = warp >> 1, wp = warp & 1;
+  double *ring = sm + (size_t)pw * NB * p.wch;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sm + (size_t)kPairs * NB * p.wch) + pw * NB;
+  double *mbox = reinterpret_cast<double *>(reinterpret_cast<uint64_t *>(sm + (size_t)kPairs * NB * p.wch) + kPairs * NB) + pw * 24;
+  const bool kappa0 = (FEAT & FEAT_KAPPA0) && p.has_kappa0;
+  const bool issuer = wp == 0 && lane == 0;
+  const int barid = 1 + pw;
+  if (issuer) {
+    for (int j = 0; j < NB; ++j) mbar_init(&bars[j], 1);
+    fence_mbar_init();
+  }
+  pair_sync(barid);
+  griddep_wait();
+  const double t0 = launch_t0(p);
+  const int64_t G = (int64_t)gridDim.x * kPairs;
+  const int64_t gp = (int64_t)blockIdx.x * kPairs + pw;
+  auto issue = [&](int64_t t, int j) {
+    const WTile g = wtile_geom<0>(p, t, kappa0);
+    double *S = ring + j * p.wch;
+    mbar_expect_tx(&bars[j], 8u * (uint32_t)g.cs + (uint32_t)g.nr * ER_REC * 8u);
+    bulk_g2s(S, p.state + g.boff, 8u * (uint32_t)g.cs, &bars[j]);
+    bulk_g2s(S + p.wcs, p.rec + g.r0 * ER_REC, (uint32_t)g.nr * ER_REC * 8u, &bars[j]);
+  };
+  if (issuer) {
+#pragma unroll
+    for (int j = 0; j < NB - 1; ++j)
+      if (gp + j * G < p.n_tiles) issue(gp + j * G, j);
+  }
+  const PairCross cr{mbox, barid, wp == 0 && lane == 31, wp == 1 && lane == 0};
+  unsigned fbits_all = 0;
+  int frod = INT_MAX;
+  int64_t k = 0;
+  for (int64_t t = gp; t < p.n_tiles; t += G, ++k) {
+    const int j = (int)(k % NB);
+    if (t + G >= p.n_tiles) griddep_launch_dependents();
+    mbar_wait(&bars[j], (uint32_t)((k / NB) & 1));
+    const WTile g = wtile_geom<0>(p, t, kappa0);
+    double *S = ring + j * p.wch;
+    stream_tile<FEAT, 0, true, PairCross>(p, g, S, wp * 32 + lane, t0, fbits_all, frod, cr);
+    fence_proxy_async();
+    pair_sync(barid);  // both warps' results are in the slot
+    if (issuer) {
+      const uint32_t tot = (uint32_t)(6 * g.ns + ER_EPL * g.nel);
+      bulk_s2g(p.state + g.boff, S, 8u * (tot & ~1u));
+      bulk_commit();
+      if (tot & 1u) p.state[g.boff + tot - 1] = S[tot - 1];
+      const int64_t tn = t + (NB - 1) * G;
+      if (tn < p.n_tiles) {
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        issue(tn, (int)((k + NB - 1) % NB));
+      }
+    }
+  }
+  if (issuer) bulk_wait_all();
+  advance_tdev(p, t0);
+  report_fault(p, fbits_all, frod);
+}
+
 }  // namespace er
 
 namespace {
@@ -819,9 +952,12 @@ cudaError_t launch_stream_nb(const ErStepParams &p, cudaStream_t st) {
   // rods of 16 elements (BASELINE configs[2], 1024^2 filaments) get the specialised instantiation
   static const bool generic = std::getenv("ER_WARP_GENERIC") != nullptr;
   static const bool cpasync = std::getenv("ER_WARP_CPASYNC") != nullptr;  // A/B: per-lane cp.async + direct stores
-  auto k = cpasync ? ((p.wN == 16 && !generic) ? er::warp_stream<FEAT, NB, 16> : er::warp_stream<FEAT, NB, 0>)
+  const bool pair = p.wN > 32;  // rods of 33..64 elements: one rod per warp pair
+  auto k = pair ? er::pair_bulk<FEAT, NB>
+         : cpasync ? ((p.wN == 16 && !generic) ? er::warp_stream<FEAT, NB, 16> : er::warp_stream<FEAT, NB, 0>)
                    : ((p.wN == 16 && !generic) ? er::warp_bulk<FEAT, NB, 16> : er::warp_bulk<FEAT, NB, 0>);
-  const size_t sm = (size_t)er::kWarps * NB * p.wch * 8 + (size_t)er::kWarps * NB * 8;
+  const int units = pair ? er::kWarps / 2 : er::kWarps;  // pipelines per CTA
+  const size_t sm = (size_t)units * NB * p.wch * 8 + (size_t)units * NB * 8 + (pair ? (size_t)units * 24 * 8 : 0);
   static int cached_dev = -1, cached_per_sm = 0;
   static size_t cached_sm = 0, set_sm = 0;
   static const void *cached_k = nullptr;
@@ -841,7 +977,7 @@ cudaError_t launch_stream_nb(const ErStepParams &p, cudaStream_t st) {
   }
   int n_sm = 148;
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t g = std::min<int64_t>((p.n_tiles + er::kWarps - 1) / er::kWarps, (int64_t)n_sm * cached_per_sm);
+  const int64_t g = std::min<int64_t>((p.n_tiles + units - 1) / units, (int64_t)n_sm * cached_per_sm);
   static const bool pdl = std::getenv("ER_NO_PDL") == nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)g, 1, 1);

@@ -81,7 +81,8 @@ def same(a, b, rtol=0.0):
             assert np.max(np.abs(x - y), initial=0.0) <= rtol * max(1.0, np.max(np.abs(y), initial=0.0))
 
 
-@pytest.mark.parametrize("N,R", [(16, 600), (4, 300), (5, 333), (15, 250), (17, 200), (31, 100), (32, 90)])
+@pytest.mark.parametrize("N,R", [(16, 600), (4, 300), (5, 333), (15, 250), (17, 200), (31, 100), (32, 90),
+                                 (33, 90), (40, 80), (64, 70)])
 def test_warp_equals_tile_kernel(er, monkeypatch, N, R):
     w = uniform_batch(N, R, seed=N)
     a, da = run(er, w, 50)
@@ -91,7 +92,7 @@ def test_warp_equals_tile_kernel(er, monkeypatch, N, R):
     assert np.allclose(da, db, rtol=1e-12, atol=1e-300)
 
 
-@pytest.mark.parametrize("N", [16, 7])
+@pytest.mark.parametrize("N", [16, 7, 64, 45])
 def test_warp_parity_vs_oracle(er, orc, N):
     w = uniform_batch(N, 300, seed=100 + N)
     for n_steps, tol in ((1, TOL_1STEP), (1000, TOL_1000)):
@@ -198,6 +199,47 @@ def test_warp_fault_reports_rod(er):
             b.step(2, w.dt)
         rod_id, bits = b.fault()
         assert rod_id == 57 and bits & er.ER_F_NONFINITE
+
+
+def test_pair_features_equal_tile_kernel(er, monkeypatch):
+    """Rods of 33..64 elements on warp pairs (mailbox exchanges across the two warps) with actuation,
+    static rest curvature, per-element material, sigma0, magnetisation, muscle wave, external loads."""
+    w = uniform_batch(50, 60, seed=71)
+    rng = np.random.default_rng(72)
+    R, E = w.n_rods, w.n_elems_total
+    w.act_A, w.act_f, w.act_L = rng.uniform(0.5, 2, R), rng.uniform(0.5, 2, R), np.full(R, 0.1)
+    w.rest_kappa = rng.standard_normal((w.n_voronoi_total, 3)) * 0.5
+    same(run(er, w, 40)[0], run(er, w, 40, warp=False, monkeypatch=monkeypatch)[0])
+    rod_of = np.repeat(np.arange(R), w.n_elems)
+    for name in ("density", "area", "I1", "I2", "youngs", "shear_mod", "alpha_c"):
+        setattr(w, name, getattr(w, name)[rod_of] * rng.uniform(0.9, 1.1, E))
+    w.rest_sigma = rng.standard_normal((E, 3)) * 1e-4
+    w.magnetization = rng.standard_normal((E, 3)) * 1e-4
+    w.b_field, w.b_omega = np.array([1e-2, 0.0, 5e-3]), 30.0
+    w.musc_A, w.musc_T = rng.uniform(1e-9, 1e-8, R), rng.uniform(0.5, 2, R)
+    w.musc_lambda, w.musc_phi = rng.uniform(0.05, 0.1, R), rng.uniform(0, 6, R)
+    w.ext_force = rng.standard_normal((w.n_nodes_total, 3)) * 1e-7
+    w.ext_couple = rng.standard_normal((E, 3)) * 1e-10
+    same(run(er, w, 40)[0], run(er, w, 40, warp=False, monkeypatch=monkeypatch)[0])
+
+
+def test_pair_full_cfg4_sampled(er, orc):
+    """BASELINE configs[3] (65,536 rods of 64 elements, actuation) at full size on warp pairs,
+    1000 steps, 32 sampled rods re-run by the oracle."""
+    w = W.make("cfg4")
+    with er.RodBatch(w) as b:
+        assert b.info().warp_rod_elems == 64
+        b.step(1000, w.dt)
+        pos, vel, dirs, om, t = b.get_state()
+    rods = W.sample_rods(w, 32, seed=13)
+    ws = w.subset(rods)
+    no, eo = w.node_offsets(), w.elem_offsets()
+    nidx = np.concatenate([np.arange(no[r], no[r + 1]) for r in rods])
+    eidx = np.concatenate([np.arange(eo[r], eo[r + 1]) for r in rods])
+    st, s, _, _ = orc.step(ws, n_steps=1000)
+    assert s == 0 and t == st.t
+    assert_parity(ws, (pos[nidx], vel[nidx], dirs[eidx], om[eidx]), (st.positions, st.velocities, st.directors, st.omega),
+                  TOL_1000, raw=("r", "Q"), label="cfg4 full x1000, warp pairs")
 
 
 def test_warp_full_cfg3_sampled(er, orc):
