@@ -683,7 +683,11 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   // that still run on them (staged ablations, contact mode, sweeps of small batches, diagnostics)
   // take the block size those tiles need.
   int32_t wtile_rods = 0;
-  if (!d->tile_slots && n_long == 0 && R > 0 && min_n == max_n && max_n >= ER_WARP_MIN_N &&
+  // Small batches (the tile kernel would run them as sweeps: <= 4 tiles of 256 slots per CTA of the
+  // grid) stay in the tile layout: there the launch boundary, not the step, is the cost (cfg2: 11 vs
+  // 21 us per step).  ER_WARP=1 forces the warp layout (tests), ER_NO_WARP=1 forbids it.
+  const bool warp_size_ok = std::getenv("ER_WARP") != nullptr || R * (int64_t)(max_n + 1) > 4 * 296 * 256;
+  if (!d->tile_slots && n_long == 0 && R > 0 && min_n == max_n && max_n >= ER_WARP_MIN_N && warp_size_ok &&
       max_n <= (std::getenv("ER_NO_WARP_PAIR") ? 32 : 64) && std::getenv("ER_NO_WARP") == nullptr) {
     b->wN = max_n;
     b->wR = max_n <= 32 ? 32 / max_n : 1;  // 33..64 elements: one rod per warp pair

@@ -28,6 +28,12 @@ def er():
     return er
 
 
+@pytest.fixture(autouse=True)
+def force_warp_layout(monkeypatch):
+    """The warp layout is chosen for large batches only; these tests use small ones."""
+    monkeypatch.setenv("ER_WARP", "1")
+
+
 def run(er, w, n_steps, warp=True, monkeypatch=None, spl=1, dt=None, sweeps=1):
     if not warp:
         monkeypatch.setenv("ER_NO_WARP", "1")
