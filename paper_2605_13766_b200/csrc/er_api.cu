@@ -1775,7 +1775,12 @@ er_status er_diagnostics(er_batch *b, double out[ER_NDIAG]) {
   CK(cudaSetDevice(b->device), "cudaSetDevice");
   ErStepParams p = params_of(b);
   p.t = b->t;
-  CK(er_launch_diag(&p, b->block, b->d_diag_out, b->stream), "diag kernel");
+  int dblock = b->block;  // slots per tile at most (warp layouts: small tiles)
+  if (b->wN > 0 && b->wrt > 0) {
+    const int64_t slots = (int64_t)b->wrt * (b->wN + 1);
+    dblock = slots <= 64 ? 64 : slots <= 128 ? 128 : slots <= 256 ? 256 : 512;
+  }
+  CK(er_launch_diag(&p, dblock, b->d_diag_out, b->stream), "diag kernel");
   CK(cudaMemcpyAsync(out, b->d_diag_out, sizeof(double) * ER_NDIAG, cudaMemcpyDeviceToHost, b->stream), "D2H diag");
   CK(cudaStreamSynchronize(b->stream), "cudaStreamSynchronize");
   return ER_OK;

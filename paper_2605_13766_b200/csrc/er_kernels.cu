@@ -918,7 +918,11 @@ __global__ void __launch_bounds__(BLOCK) diag_kernel(const ErStepParams p) {
   double *xQ = xr + 3 * BLOCK;
   double *red = xQ + 9 * BLOCK;  // [16][BLOCK/32]
   int *rst = reinterpret_cast<int *>(red + 16 * (BLOCK / 32));
-  const ErTile T = p.tiles[blockIdx.x];
+  double acc[16];
+  for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+  // tiles tb = blockIdx.x, blockIdx.x + gridDim.x, ...: per-thread sums in a fixed order (deterministic)
+  for (int64_t tb = blockIdx.x; tb < p.n_tiles; tb += gridDim.x) {
+  const ErTile T = p.tiles[tb];
   SlotInfo si;
   decode_global<BLOCK>(p, T, si, rst);
   const int s = threadIdx.x;
@@ -940,26 +944,24 @@ __global__ void __launch_bounds__(BLOCK) diag_kernel(const ErStepParams p) {
     for (int c = 0; c < 9; ++c) xQ[c * BLOCK + s] = Q[c];
   }
   __syncthreads();
-  double acc[16];
-  for (int k = 0; k < 16; ++k) acc[k] = 0.0;
   if (si.active) {
     const double im = general ? gp(GP_IM) : rec[REC_IM] * ((i == 0 || i == N) ? 2.0 : 1.0);
     const double m = 1.0 / im;
     const double vv = dot3(v, v);
-    acc[0] = 0.5 * m * vv;
-    acc[4] = -m * (p.g[0] * r[0] + p.g[1] * r[1] + p.g[2] * r[2]);
+    acc[0] += 0.5 * m * vv;
+    acc[4] += -m * (p.g[0] * r[0] + p.g[1] * r[1] + p.g[2] * r[2]);
     if ((si.fl & FL_TIP) && i == ((si.fl & FL_CLAMP_MASK) == 2 ? 0 : N))
-      acc[5] = -(rec[REC_TIPX] * r[0] + rec[REC_TIPY] * r[1] + rec[REC_TIPZ] * r[2]);
-    acc[6] = m * v[0]; acc[7] = m * v[1]; acc[8] = m * v[2];
-    acc[9] = sqrt(vv);
-    acc[10] = m;
+      acc[5] += -(rec[REC_TIPX] * r[0] + rec[REC_TIPY] * r[1] + rec[REC_TIPZ] * r[2]);
+    acc[6] += m * v[0]; acc[7] += m * v[1]; acc[8] += m * v[2];
+    acc[9] = fmax(acc[9], sqrt(vv));
+    acc[10] += m;
   }
   if (si.has_e) {
     const double lh = general ? gp(GP_LHAT) : rec[REC_LHAT];
     const double ilh = general ? gp(GP_ILHAT) : rec[REC_ILHAT];
     double ell[3];
     if (s + 1 == T.nslots && T.seg + 1 < T.nseg) {  // long rod: next node is slot 0 of the next segment
-      const ErTile Tn = p.tiles[blockIdx.x + 1];
+      const ErTile Tn = p.tiles[tb + 1];
       for (int c = 0; c < 3; ++c) ell[c] = p.state[Tn.boff + c * Tn.nslots] - r[c];
     } else {
       for (int c = 0; c < 3; ++c) ell[c] = xr[c * BLOCK + s + 1] - r[c];
@@ -970,17 +972,17 @@ __global__ void __launch_bounds__(BLOCK) diag_kernel(const ErStepParams p) {
     if (p.sigma0) for (int c = 0; c < 3; ++c) sg[c] -= p.sigma0[c * p.ne + si.elem];
     const double S1 = general ? gp(GP_S1) : rec[REC_S1];
     const double S3 = general ? gp(GP_S3) : rec[REC_S3];
-    acc[2] = 0.5 * (S1 * sg[0] * sg[0] + S1 * sg[1] * sg[1] + S3 * sg[2] * sg[2]) * lh;
+    acc[2] += 0.5 * (S1 * sg[0] * sg[0] + S1 * sg[1] * sg[1] + S3 * sg[2] * sg[2]) * lh;
     for (int c = 0; c < 3; ++c) {
       const double iJ = general ? gp(GP_IJ1 + c) : rec[REC_IJ1 + c];
       acc[1] += 0.5 * w[c] * w[c] / (iJ * e);
     }
-    acc[11] = 1.0;
+    acc[11] += 1.0;
   }
   if (si.has_v) {
     double Qp[9], kap[3], cth, s2;
     if (s == 0) {  // long rod segment: previous element is the last of the previous segment
-      const ErTile Tp = p.tiles[blockIdx.x - 1];
+      const ErTile Tp = p.tiles[tb - 1];
       for (int c = 0; c < ER_QST; ++c) Qp[c] = p.state[Tp.boff + 6 * Tp.nslots + c * Tp.nel + Tp.nel - 1];
       complete_d3(Qp);
     } else {
@@ -1004,7 +1006,10 @@ __global__ void __launch_bounds__(BLOCK) diag_kernel(const ErStepParams p) {
       acc[3] += 0.5 * Bv * d * d * Dh;
     }
   }
+  __syncthreads();  // the exchange arrays and rod starts are refilled for the next tile
+  }
   // deterministic block reduction: warp shuffles, then warp partials in fixed order
+  const int s = threadIdx.x;
   const int lane = s & 31, wid = s >> 5;
   for (int k = 0; k < 12; ++k) {
     double x = acc[k];
@@ -1077,7 +1082,11 @@ __global__ void pack_planes(const double *__restrict__ src, double *__restrict__
 // Directors: the canonical rows hold all 9 components; the tiles store d1, d2 (er_layout.h), so
 // to_tiles drops d3 and the way back rebuilds it with complete_d3, the bits every kernel uses.
 __global__ void canon_tiles(const ErStepParams p, double *canon, int field, int to_tiles) {
-  const ErTile T = p.tiles[blockIdx.x];
+  // one warp per tile (warp-sized tiles of the warp kernel are small)
+  const int64_t tix = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (tix >= p.n_tiles) return;
+  const int lane = threadIdx.x & 31;
+  const ErTile T = p.tiles[tix];
   const int k = field == FIELD_DIR ? 9 : 3;
   int64_t count, off;
   int shift;  // rows per rod = N + shift
@@ -1102,7 +1111,7 @@ __global__ void canon_tiles(const ErStepParams p, double *canon, int field, int 
       can += shift < 0 ? (T.seg == 0 ? 0 : k0 - 1) : k0;
     }
     if (field == FIELD_DIR) {  // consecutive threads on consecutive canonical doubles (coalesced)
-      for (int64_t x = threadIdx.x; x < n * 9; x += blockDim.x) {
+      for (int64_t x = lane; x < n * 9; x += 32) {
         const int64_t u = x / 9;
         const int c = (int)(x - u * 9);
         const double *q = blk + loc + u;  // this element's stored components, plane stride count
@@ -1114,7 +1123,7 @@ __global__ void canon_tiles(const ErStepParams p, double *canon, int field, int 
       }
       continue;
     }
-    for (int64_t x = threadIdx.x; x < n * k; x += blockDim.x) {
+    for (int64_t x = lane; x < n * k; x += 32) {
       const int64_t u = x / k;
       const int c = (int)(x - u * k);
       if (to_tiles) blk[c * count + loc + u] = canon ? canon[can * k + x] : 0.0;
@@ -1347,22 +1356,22 @@ cudaError_t er_launch_long(const ErStepParams *p, int64_t tile0, int64_t n_rods,
 }
 
 cudaError_t er_launch_diag(const ErStepParams *p, int block, double *out, cudaStream_t st) {
+  // a grid of at most 148 x 8 CTAs walks the tiles (partials per CTA, summed in a fixed order)
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(p->n_tiles, 148 * 8));
   if (p->n_tiles > 0) {
     const size_t sm = diag_smem(block);
-    if (block == 128) {
-      cudaFuncSetAttribute(er::diag_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      er::diag_kernel<128><<<(unsigned)p->n_tiles, 128, sm, st>>>(*p);
-    } else if (block == 256) {
-      cudaFuncSetAttribute(er::diag_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      er::diag_kernel<256><<<(unsigned)p->n_tiles, 256, sm, st>>>(*p);
-    } else {
-      cudaFuncSetAttribute(er::diag_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      er::diag_kernel<512><<<(unsigned)p->n_tiles, 512, sm, st>>>(*p);
-    }
+    auto go = [&](auto kern, int b) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      kern<<<(unsigned)grid, b, sm, st>>>(*p);
+    };
+    if (block == 64) go(er::diag_kernel<64>, 64);
+    else if (block == 128) go(er::diag_kernel<128>, 128);
+    else if (block == 256) go(er::diag_kernel<256>, 256);
+    else go(er::diag_kernel<512>, 512);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  er::diag_finish_kernel<<<12, 32, 0, st>>>(p->diag_partial, p->n_tiles, out);
+  er::diag_finish_kernel<<<12, 32, 0, st>>>(p->diag_partial, p->n_tiles > 0 ? grid : 0, out);
   return cudaGetLastError();
 }
 
@@ -1379,7 +1388,7 @@ cudaError_t er_launch_pack_planes(const double *src, double *dst, int64_t stride
 }
 cudaError_t er_launch_canon_tiles(const ErStepParams *p, double *canon, int field, int to_tiles, cudaStream_t st) {
   if (p->n_tiles <= 0) return cudaSuccess;
-  er::canon_tiles<<<(unsigned)p->n_tiles, 256, 0, st>>>(*p, canon, field, to_tiles);
+  er::canon_tiles<<<(unsigned)((p->n_tiles + 7) / 8), 256, 0, st>>>(*p, canon, field, to_tiles);
   return cudaGetLastError();
 }
 cudaError_t er_launch_apply_forcing(double *rec, int64_t n_rods, const int32_t *flags, const double *damping,
