@@ -288,6 +288,40 @@ typedef struct {
 } er_contact;
 er_status er_set_contact(er_batch *b, const er_contact *c);
 
+/* ------------------------------------------------------------------------- contact across GPUs
+ * Rods sharded over ranks may touch rods of another rank (NEXT-4; the paper's
+ * collision engine with synchronisation after every stage).  Such rods enter this
+ * batch as GHOST rods: only their contact geometry is declared here, and their node records
+ * (r, v after drift-1: 6 doubles per node, lab frame) are supplied by the caller every step; this
+ * batch never advances them.  The broad and narrow phases then run over own + ghost elements; only
+ * the own nodes receive forces.  Pair forces are evaluated from both sides with bit-identical
+ * inputs (the ghost records are copies), so the owner of either rod applies exactly the opposite
+ * force of the other (momentum balance across ranks).
+ *
+ * er_set_contact_ghosts declares n_ghost ghost rods (HOST arrays [n_ghost]): elements per rod (>= 1),
+ * contact radius (> 0), stiffness scale E r (k_n <= 0 uses min(E_a r_a, E_b r_b)), shortest and
+ * longest rest element length (HHG levels).  n_ghost = 0 removes them.  If contact is enabled,
+ * it is re-initialised with the same parameters (candidate lists rebuilt).  Ghost node records
+ * start at zero: set them before the first step.
+ *
+ * With ghosts, a step is split so that the caller can exchange node records between the halves:
+ *   er_step_begin(b, dt)   drift-1 of one step (every own rod), own node records ready;
+ *   er_contact_records(b, ER_..., dst)           own node records [n_nodes][6] -> dst;
+ *   er_set_ghost_records(b, ER_..., src)         ghost node records [n_ghost_nodes][6] <- src
+ *                                                 (ghost rods in declaration order, N_g + 1 nodes each);
+ *   er_step_finish(b, dt)  contact evaluation over own + ghost elements, kick, drift-2.
+ * er_step_begin / er_step_finish also work without ghosts (a plain contact step in two calls; the
+ * trajectory is bitwise that of er_step).  er_step itself returns ER_EINVAL while ghosts are
+ * declared (their records would be stale).  Both calls are stream-ordered; er_step_finish reads
+ * the fault word like er_step (ER_EUNSTABLE).  Errors: ER_EINVAL (contact off, begin/finish out of
+ * order, a dt different from begin's), ER_ECUDA. */
+er_status er_set_contact_ghosts(er_batch *b, int64_t n_ghost, const int32_t *n_elems, const double *radius,
+                                const double *stiffness, const double *lhat_min, const double *lhat_max);
+er_status er_step_begin(er_batch *b, double dt);
+er_status er_step_finish(er_batch *b, double dt);
+er_status er_contact_records(er_batch *b, int32_t dst_mem, double *dst);
+er_status er_set_ghost_records(er_batch *b, int32_t src_mem, const double *src);
+
 /* Contact statistics (synchronises the stream): per step = of the last step of the last er_step
  * call; per build = of the last candidate-list build. */
 typedef struct {

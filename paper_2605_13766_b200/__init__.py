@@ -95,7 +95,8 @@ class er_phase_times(C.Structure):
 EXPORTS = ("er_create_batch", "er_set_bc", "er_set_forcing", "er_step", "er_get_state", "er_set_state",
            "er_diagnostics", "er_fault", "er_set_option", "er_set_trace", "er_query", "er_last_error",
            "er_abi_version", "er_destroy", "er_set_contact", "er_get_contact_stats", "er_get_phase_times",
-           "er_set_external_loads")
+           "er_set_external_loads", "er_set_contact_ghosts", "er_step_begin", "er_step_finish",
+           "er_contact_records", "er_set_ghost_records")
 
 
 def _load():
@@ -121,12 +122,19 @@ def _load():
     lib.er_get_contact_stats.argtypes = [h, C.POINTER(er_contact_stats)]
     lib.er_get_phase_times.argtypes = [h, C.POINTER(er_phase_times)]
     lib.er_set_external_loads.argtypes = [h, C.c_int32, C.c_void_p, C.c_void_p]
+    lib.er_set_contact_ghosts.argtypes = [h, C.c_int64, _ip, _dp, _dp, _dp, _dp]
+    lib.er_step_begin.argtypes = [h, C.c_double]
+    lib.er_step_finish.argtypes = [h, C.c_double]
+    lib.er_contact_records.argtypes = [h, C.c_int32, C.c_void_p]
+    lib.er_set_ghost_records.argtypes = [h, C.c_int32, C.c_void_p]
     lib.er_abi_version.restype = C.c_int32
     lib.er_destroy.argtypes = [h]
     lib.er_destroy.restype = None
     for name in ("er_create_batch", "er_set_bc", "er_set_forcing", "er_step", "er_get_state",
                  "er_set_state", "er_diagnostics", "er_fault", "er_set_option", "er_set_trace", "er_query",
-                 "er_set_contact", "er_get_contact_stats", "er_get_phase_times", "er_set_external_loads"):
+                 "er_set_contact", "er_get_contact_stats", "er_get_phase_times", "er_set_external_loads",
+                 "er_set_contact_ghosts", "er_step_begin", "er_step_finish", "er_contact_records",
+                 "er_set_ghost_records"):
         getattr(lib, name).restype = C.c_int
     return lib
 
@@ -205,6 +213,26 @@ def er_query(handle) -> er_info:
 
 def er_set_contact(handle, contact):
     _check(handle, lib.er_set_contact(handle, None if contact is None else C.byref(contact)))
+
+
+def er_set_contact_ghosts(handle, n, n_elems, radius, stiffness, lmin, lmax):
+    _check(handle, lib.er_set_contact_ghosts(handle, n, n_elems, radius, stiffness, lmin, lmax))
+
+
+def er_step_begin(handle, dt):
+    _check(handle, lib.er_step_begin(handle, dt))
+
+
+def er_step_finish(handle, dt):
+    _check(handle, lib.er_step_finish(handle, dt))
+
+
+def er_contact_records(handle, dst_mem, dst):
+    _check(handle, lib.er_contact_records(handle, dst_mem, dst))
+
+
+def er_set_ghost_records(handle, src_mem, src):
+    _check(handle, lib.er_set_ghost_records(handle, src_mem, src))
 
 
 def er_set_external_loads(handle, src_mem, node_force, elem_couple):
@@ -388,6 +416,35 @@ class RodBatch:
         s.pool_factor = float(pool_factor)
         s.skin = float(skin)
         er_set_contact(self.handle, s)
+
+    def set_contact_ghosts(self, n_elems, radius, stiffness, lhat_min, lhat_max):
+        """Declare the ghost rods of a contact shard (include/er.h er_set_contact_ghosts); empty
+        arrays remove them."""
+        k = _Keep()
+        n = int(len(n_elems))
+        er_set_contact_ghosts(self.handle, n, k.host(n_elems, np.int32, _ip), k.host(radius), k.host(stiffness),
+                              k.host(lhat_min), k.host(lhat_max))
+
+    def step_begin(self, dt: float):
+        er_step_begin(self.handle, dt)
+
+    def step_finish(self, dt: float):
+        er_step_finish(self.handle, dt)
+
+    def contact_records(self, out):
+        """Own node records after er_step_begin ([n_nodes][6]: r, v) into `out` (a torch CUDA
+        tensor -> device copy, numpy -> host)."""
+        dev = _is_torch(out) and out.is_cuda
+        er_contact_records(self.handle, ER_DEVICE if dev else ER_HOST, out.data_ptr() if _is_torch(out) else out.ctypes.data)
+
+    def set_ghost_records(self, src):
+        dev = _is_torch(src) and src.is_cuda
+        if dev:
+            import torch
+            torch.cuda.current_stream(self.device).synchronize()  # its producer ran on torch's stream
+        buf = src if _is_torch(src) else np.ascontiguousarray(src, dtype=np.float64)
+        er_set_ghost_records(self.handle, ER_DEVICE if dev else ER_HOST,
+                             buf.data_ptr() if _is_torch(buf) else buf.ctypes.data)
 
     def contact_stats(self) -> er_contact_stats:
         return er_get_contact_stats(self.handle)

@@ -26,6 +26,7 @@
 extern "C" {
 cudaError_t er_launch_step(const ErStepParams *p, int block, int kind, int feat, cudaStream_t st);
 cudaError_t er_launch_warp(const ErStepParams *p, int feat, cudaStream_t st);
+cudaError_t er_contact_ghost_check(const ErContactParams *pp, int64_t n0, double disp2, cudaStream_t st);
 cudaError_t er_launch_long(const ErStepParams *p, int64_t tile0, int64_t n_rods, int nseg, int feat, cudaStream_t st);
 cudaError_t er_launch_diag(const ErStepParams *p, int block, double *out, cudaStream_t st);
 cudaError_t er_launch_canon_tiles(const ErStepParams *p, double *canon, int field, int to_tiles, cudaStream_t st);
@@ -96,6 +97,18 @@ struct er_batch {
   // warp kernel (er_warp.cu): equal-length rods of ER_WARP_MIN_N..32 elements; 0 = not used
   int32_t wN = 0, wR = 0, wnb = 0, wbufd = 0, wrec = 0, wdesc = 0;
   int32_t wrt = 0, wch = 0;    // per-warp streaming variant (0: the tile-pipelined warp kernel)
+  // ghost rods (contact across GPUs, er_set_contact_ghosts): contact geometry only, packed after the
+  // own rods in the contact arrays; node records supplied by the caller every split step
+  int64_t g_rods = 0, g_elems = 0, g_nodes = 0;
+  std::vector<int32_t> g_nel;
+  std::vector<double> g_rad, g_kr, g_lmin, g_lmax;
+  int32_t *d_cord = nullptr;   // packed -> reported rod id for own + ghost rods (contact faults)
+  er_contact saved_contact{};  // the last er_set_contact parameters (ghost changes re-apply them)
+  std::vector<double> saved_radius;
+  bool have_saved_contact = false;
+  int split_mode = 0;          // er_step internals: 0 whole steps, 1 begin (drift-1), 2 finish
+  bool split_begun = false;
+  double split_dt = 0.0;
   int64_t wcs = 0, wrods = 0;
   int64_t n_tiles = 0;       // all tiles (layout conversion, diagnostics)
   int64_t n_tiles_norm = 0;  // tiles of rods with <= 511 elements (the step kernels); long rods'
@@ -254,6 +267,8 @@ void free_contact(er_batch *b) {
   if (b->cgraph) cudaGraphExecDestroy(b->cgraph);
   b->cgraph = nullptr;
   b->cp = ErContactParams{};
+  if (b->d_cord) cudaFree(b->d_cord);
+  b->d_cord = nullptr;
   b->sort_tmp = nullptr;
   b->sort_bytes = 0;
   b->contact_on = false;
@@ -1244,6 +1259,8 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
   Errors err;
   if (n_steps < 0) err.add("n_steps = %lld < 0", (long long)n_steps);
   if (!(std::isfinite(dt) && dt > 0.0)) err.add("dt = %g must be positive and finite", dt);
+  if (b->g_rods > 0 && b->split_mode == 0)
+    err.add("ghost rods are declared (er_set_contact_ghosts): step with er_step_begin / er_step_finish");
   if (err.count) { b->last_error = err.msg; return ER_EINVAL; }
   b->fault_rod = -1;
   b->fault_bits = 0;
@@ -1294,20 +1311,26 @@ er_status er_step(er_batch *b, int64_t n_steps, double dt) {
     p.disp2 = 0.25 * b->cp.skin * b->cp.skin;
     p.rebuild = b->cp.rebuild;
     int m0 = mark(b);
-    p.n_tiles = b->n_tiles;  // the drift kernel handles long-rod segment tiles too (no exchange)
-    CK(er_launch_step(&p, b->block, 1, 15, b->stream), "drift kernel");
-    p.n_tiles = b->n_tiles_norm;
-    b->launches += 1;
+    if (b->split_mode != 2) {  // (er_step_finish: the drift-1 ran in er_step_begin)
+      p.n_tiles = b->n_tiles;  // the drift kernel handles long-rod segment tiles too (no exchange)
+      CK(er_launch_step(&p, b->block, 1, 15, b->stream), "drift kernel");
+      p.n_tiles = b->n_tiles_norm;
+      b->launches += 1;
+    }
     int m1 = mark(b);
     interval(b, m0, m1, 0);
     p.cfc = b->cp.fc;
     p.cfs = b->cp.fs;
-    for (int64_t q = 0; q < n_steps; ++q) {
+    for (int64_t q = 0; q < n_steps && b->split_mode != 1; ++q) {
+      if (b->g_rods > 0) {  // ghost records (just supplied): their Verlet bound
+        CK(er_contact_ghost_check(&b->cp, b->n_nodes, p.disp2, b->stream), "ghost check");
+        b->launches += 1;
+      }
       CK(er_contact_eval(&b->cp, b->sort_tmp, b->sort_bytes, b->cgraph, b->stream, &b->launches, b->cgraph_kernels), "contact");
       const int m2 = mark(b);
       interval(b, m1, m2, 1);
       p.t = t;
-      p.cnode = q + 1 < n_steps ? b->cp.cnode : nullptr;
+      p.cnode = q + 1 < n_steps && b->split_mode == 0 ? b->cp.cnode : nullptr;
       CK(er_launch_step(&p, b->block, 0, feat | FEAT_CONTACT, b->stream), "step kernel");
       b->launches += 1;
       CK(launch_long(1, t, feat | FEAT_CONTACT), "long-rod kernel");
@@ -1611,8 +1634,16 @@ er_status er_set_contact(er_batch *b, const er_contact *c) {
   if (c->radius)
     for (int64_t r = 0; r < R; ++r)
       if (!pos_finite(c->radius[r])) { err.add("radius[%lld] = %g must be positive and finite", (long long)r, c->radius[r]); break; }
-  if (E >= (1ll << 30)) err.add("contact supports < 2^30 elements per batch (got %lld)", (long long)E);
+  if (E + b->g_elems >= (1ll << 30)) err.add("contact supports < 2^30 elements per batch incl. ghosts (got %lld)", (long long)(E + b->g_elems));
   if (err.count) { b->last_error = err.msg; return ER_EINVAL; }
+  if (c != &b->saved_contact) {  // kept for er_set_contact_ghosts, which re-applies them
+    b->saved_contact = *c;
+    if (c->radius) {
+      b->saved_radius.assign(c->radius, c->radius + R);
+      b->saved_contact.radius = b->saved_radius.data();
+    }
+    b->have_saved_contact = true;
+  }
   CK(cudaSetDevice(b->device), "cudaSetDevice");
   CK(cudaStreamSynchronize(b->stream), "sync");
   free_contact(b);
@@ -1627,19 +1658,31 @@ er_status er_set_contact(er_batch *b, const er_contact *c) {
   for (int q = 0; q < 3; ++q) L.pn[q] = c->plane_on ? c->plane_n[q] / nn : 0.0;
   L.pd = c->plane_d;
   L.exclude = c->exclude;
-  // per-rod contact radius (default sqrt(A/pi)) and stiffness scale E r; rest capsule extents
-  std::vector<double> rad((size_t)std::max<int64_t>(R, 1)), kr((size_t)std::max<int64_t>(R, 1));
+  // per-rod contact radius (default sqrt(A/pi)) and stiffness scale E r; rest capsule extents.
+  // Ghost rods (er_set_contact_ghosts) follow the own rods: RT rods, ET elements, NT nodes.
+  const int64_t RT = R + b->g_rods, ET = E + b->g_elems, NT = b->n_nodes + b->g_nodes;
+  std::vector<double> rad((size_t)std::max<int64_t>(RT, 1)), kr((size_t)std::max<int64_t>(RT, 1));
   double xmin = 0.0, xmax = 0.0;
-  for (int64_t r = 0; r < R; ++r) {
-    rad[r] = c->radius ? c->radius[b->ord[r]] : std::sqrt(b->rod_A0[r] / 3.14159265358979323846);  // r packed
-    kr[r] = b->rod_E0[r] * rad[r];
-    const double lo = b->rod_lmin[r] + 2.0 * rad[r], hi = b->rod_lmax[r] + 2.0 * rad[r];
+  for (int64_t r = 0; r < RT; ++r) {
+    double lmn, lmx;
+    if (r < R) {
+      rad[r] = c->radius ? c->radius[b->ord[r]] : std::sqrt(b->rod_A0[r] / 3.14159265358979323846);  // r packed
+      kr[r] = b->rod_E0[r] * rad[r];
+      lmn = b->rod_lmin[r];
+      lmx = b->rod_lmax[r];
+    } else {
+      rad[r] = b->g_rad[r - R];
+      kr[r] = b->g_kr[r - R];
+      lmn = b->g_lmin[r - R];
+      lmx = b->g_lmax[r - R];
+    }
+    const double lo = lmn + 2.0 * rad[r], hi = lmx + 2.0 * rad[r];
     xmin = r == 0 ? lo : std::min(xmin, lo);
     xmax = r == 0 ? hi : std::max(xmax, hi);
   }
   // Verlet skin (default: a quarter of the smallest contact radius)
   double rmin = 0.0;
-  for (int64_t r = 0; r < R; ++r) rmin = r == 0 ? rad[r] : std::min(rmin, rad[r]);
+  for (int64_t r = 0; r < RT; ++r) rmin = r == 0 ? rad[r] : std::min(rmin, rad[r]);
   cp.skin = c->skin > 0.0 ? c->skin : 0.25 * rmin;
   xmin += cp.skin;
   xmax += cp.skin;
@@ -1652,64 +1695,148 @@ er_status er_set_contact(er_batch *b, const er_contact *c) {
     if (c->cell0 == 0.0 && cell0 * std::ldexp(1.0, nlev - 1) < 1.25 * xmax) cell0 = 1.25 * xmax / std::ldexp(1.0, nlev - 1);
     nlev = std::min(nlev + 1, ER_HHG_MAXLEV);  // one level of headroom for stretched elements
   }
-  if (R > 0 && !(cell0 > 0.0)) { b->last_error = "HHG cell size must be positive"; return ER_EINVAL; }
+  if (RT > 0 && !(cell0 > 0.0)) { b->last_error = "HHG cell size must be positive"; return ER_EINVAL; }
   cp.nlev = nlev;
   for (int l = 0; l < ER_HHG_MAXLEV; ++l) {
     cp.cell[l] = cell0 * std::ldexp(1.0, l);
     cp.icell[l] = 1.0 / cp.cell[l];
   }
   int hb = 10;
-  while (hb < 29 && (1ll << hb) < 2 * E) ++hb;
+  while (hb < 29 && (1ll << hb) < 2 * ET) ++hb;
   cp.hbits = hb;
-  cp.n_elems = E; cp.n_nodes = b->n_nodes; cp.n_rods = R;
-  cp.fs = b->ne;
+  cp.n_elems = ET; cp.n_nodes = NT; cp.n_rods = RT;
+  cp.fs = pad_to(ET, 32);
   const double pf = c->pool_factor > 0.0 ? c->pool_factor : 4.0;
-  cp.pcap = std::max<int64_t>(1024, (int64_t)(pf * (double)E));
+  cp.pcap = std::max<int64_t>(1024, (int64_t)(pf * (double)ET));
 
-  std::vector<int32_t> erod((size_t)std::max<int64_t>(E, 1));
-  std::vector<double> nrad((size_t)std::max<int64_t>(b->n_nodes, 1)), nkr((size_t)std::max<int64_t>(b->n_nodes, 1));
-  for (int64_t r = 0; r < R; ++r) {
-    for (int64_t j = b->eoff[r]; j < b->eoff[r + 1]; ++j) erod[j] = (int32_t)r;
-    for (int64_t n = b->eoff[r] + r; n <= b->eoff[r + 1] + r; ++n) { nrad[n] = rad[r]; nkr[n] = kr[r]; }
+  std::vector<int32_t> erod((size_t)std::max<int64_t>(ET, 1)), cord((size_t)std::max<int64_t>(RT, 1));
+  std::vector<double> nrad((size_t)std::max<int64_t>(NT, 1)), nkr((size_t)std::max<int64_t>(NT, 1));
+  for (int64_t r = 0, e0 = 0; r < RT; ++r) {  // element e of rod r: nodes e + r and e + r + 1
+    const int64_t ne = r < R ? b->eoff[r + 1] - b->eoff[r] : b->g_nel[r - R];
+    for (int64_t j = e0; j < e0 + ne; ++j) erod[j] = (int32_t)r;
+    for (int64_t n = e0 + r; n <= e0 + ne + r; ++n) { nrad[n] = rad[r]; nkr[n] = kr[r]; }
+    cord[r] = r < R ? b->ord[r] : (int32_t)r;  // a ghost rod reports as n_rods + its index
+    e0 += ne;
   }
   double *d_nrad = nullptr, *d_nkr = nullptr;
   double *d_rad = nullptr, *d_kr = nullptr;
   int32_t *d_erod = nullptr;
   const int64_t T = 1ll << hb;
 #define CA(ptr, n) CK(dalloc(b, &(ptr), (n)), "cudaMalloc(contact)")
-  CA(d_rad, R); CA(d_kr, R); CA(d_erod, E);
-  CA(d_nrad, b->n_nodes); CA(d_nkr, b->n_nodes);
+  CA(d_rad, RT); CA(d_kr, RT); CA(d_erod, ET);
+  CA(d_nrad, NT); CA(d_nkr, NT);
+  CA(b->d_cord, RT);
   cp.rad = d_rad; cp.kr = d_kr; cp.erod = d_erod; cp.nrad = d_nrad; cp.nkr = d_nkr;
-  cp.ord = b->d_ord;
-  CA(cp.cnode, 6 * b->n_nodes); CA(cp.cbuild, 3 * b->n_nodes); CA(cp.rebuild, 1);
+  cp.ord = b->d_cord;
+  CA(cp.cnode, 6 * NT); CA(cp.cbuild, 3 * NT); CA(cp.rebuild, 1);
   CA(cp.gext, 3 * ER_HHG_MAXLEV); CA(cp.gdim, 4 * ER_HHG_MAXLEV);
-  CA(cp.key, E); CA(cp.key_s, E); CA(cp.val, E); CA(cp.val_s, E);
-  CA(cp.table, T); CA(cp.code_s, E);
-  CA(cp.boxa, E); CA(cp.boxb, E); CA(cp.qidx, E);
-  CA(cp.cnt, E); CA(cp.cand, ER_CAND_K * E);
-  CA(cp.fc, 6 * b->ne);
-  CA(cp.head, b->n_nodes); CA(cp.pnext, cp.pcap); CA(cp.psrc, cp.pcap); CA(cp.pf, 6 * cp.pcap);
+  CA(cp.key, ET); CA(cp.key_s, ET); CA(cp.val, ET); CA(cp.val_s, ET);
+  CA(cp.table, T); CA(cp.code_s, ET);
+  CA(cp.boxa, ET); CA(cp.boxb, ET); CA(cp.qidx, ET);
+  CA(cp.cnt, ET); CA(cp.cand, ER_CAND_K * ET);
+  CA(cp.fc, 6 * cp.fs);
+  CA(cp.head, NT); CA(cp.pnext, cp.pcap); CA(cp.psrc, cp.pcap); CA(cp.pf, 6 * cp.pcap);
   CA(cp.ctr, 8); CA(cp.bctr, 8);
 #undef CA
   cp.fault = b->d_fault;
-  CK(er_contact_tmp_bytes(E, hb, &b->sort_bytes), "cub temp size");
+  CK(er_contact_tmp_bytes(ET, hb, &b->sort_bytes), "cub temp size");
   CK(cudaMalloc(&b->sort_tmp, std::max<size_t>(b->sort_bytes, 16)), "cudaMalloc(sort)");
   b->device_bytes += (int64_t)b->sort_bytes;
-  if (R > 0) {
-    CK(cudaMemcpyAsync(d_rad, rad.data(), sizeof(double) * R, cudaMemcpyHostToDevice, b->stream), "H2D rad");
-    CK(cudaMemcpyAsync(d_kr, kr.data(), sizeof(double) * R, cudaMemcpyHostToDevice, b->stream), "H2D kr");
-    CK(cudaMemcpyAsync(d_erod, erod.data(), sizeof(int32_t) * E, cudaMemcpyHostToDevice, b->stream), "H2D erod");
-    CK(cudaMemcpyAsync(d_nrad, nrad.data(), sizeof(double) * b->n_nodes, cudaMemcpyHostToDevice, b->stream), "H2D nrad");
-    CK(cudaMemcpyAsync(d_nkr, nkr.data(), sizeof(double) * b->n_nodes, cudaMemcpyHostToDevice, b->stream), "H2D nkr");
+  if (RT > 0) {
+    CK(cudaMemcpyAsync(d_rad, rad.data(), sizeof(double) * RT, cudaMemcpyHostToDevice, b->stream), "H2D rad");
+    CK(cudaMemcpyAsync(d_kr, kr.data(), sizeof(double) * RT, cudaMemcpyHostToDevice, b->stream), "H2D kr");
+    CK(cudaMemcpyAsync(d_erod, erod.data(), sizeof(int32_t) * ET, cudaMemcpyHostToDevice, b->stream), "H2D erod");
+    CK(cudaMemcpyAsync(d_nrad, nrad.data(), sizeof(double) * NT, cudaMemcpyHostToDevice, b->stream), "H2D nrad");
+    CK(cudaMemcpyAsync(d_nkr, nkr.data(), sizeof(double) * NT, cudaMemcpyHostToDevice, b->stream), "H2D nkr");
+    CK(cudaMemcpyAsync(b->d_cord, cord.data(), sizeof(int32_t) * RT, cudaMemcpyHostToDevice, b->stream), "H2D cord");
   }
+  if (NT > 0) CK(cudaMemsetAsync(cp.cnode, 0, sizeof(double) * 6 * NT, b->stream), "memset");
   CK(cudaMemsetAsync(cp.ctr, 0, 8 * sizeof(unsigned long long), b->stream), "memset");
   CK(cudaMemsetAsync(cp.bctr, 0, 8 * sizeof(unsigned long long), b->stream), "memset");
   CK(cudaMemsetAsync(cp.rebuild, 1, sizeof(int32_t), b->stream), "memset");
-  CK(cudaMemsetAsync(cp.fc, 0, 6 * sizeof(double) * b->ne, b->stream), "memset");
+  CK(cudaMemsetAsync(cp.fc, 0, 6 * sizeof(double) * cp.fs, b->stream), "memset");
   CK(cudaStreamSynchronize(b->stream), "sync");
   if (!std::getenv("ER_NO_GRAPH"))
     CK(er_contact_graph(&cp, b->sort_tmp, b->sort_bytes, &b->cgraph, &b->cgraph_kernels), "contact graph");
   b->contact_on = true;
+  return ER_OK;
+}
+
+er_status er_set_contact_ghosts(er_batch *b, int64_t n_ghost, const int32_t *n_elems, const double *radius,
+                                const double *stiffness, const double *lhat_min, const double *lhat_max) {
+  if (!b) return ER_EINVAL;
+  Errors err;
+  if (n_ghost < 0) err.add("n_ghost = %lld < 0", (long long)n_ghost);
+  if (n_ghost > 0 && !(n_elems && radius && stiffness && lhat_min && lhat_max)) err.add("ghost arrays must be non-NULL");
+  if (b->split_begun) err.add("a split step is in progress (er_step_begin without er_step_finish)");
+  int64_t ge = 0;
+  for (int64_t g = 0; g < n_ghost && !err.count; ++g) {
+    if (n_elems[g] < 1) err.add("ghost n_elems[%lld] = %d < 1", (long long)g, n_elems[g]);
+    if (!pos_finite(radius[g])) err.add("ghost radius[%lld] = %g must be positive and finite", (long long)g, radius[g]);
+    if (!std::isfinite(stiffness[g])) err.add("ghost stiffness[%lld] not finite", (long long)g);
+    if (!(pos_finite(lhat_min[g]) && pos_finite(lhat_max[g]) && lhat_min[g] <= lhat_max[g]))
+      err.add("ghost rest lengths [%lld] must satisfy 0 < lhat_min <= lhat_max", (long long)g);
+    ge += n_elems[g];
+  }
+  if (err.count) { b->last_error = err.msg; return ER_EINVAL; }
+  b->g_rods = n_ghost;
+  b->g_elems = ge;
+  b->g_nodes = ge + n_ghost;
+  b->g_nel.assign(n_elems, n_elems + n_ghost);
+  b->g_rad.assign(radius, radius + n_ghost);
+  b->g_kr.assign(stiffness, stiffness + n_ghost);
+  b->g_lmin.assign(lhat_min, lhat_min + n_ghost);
+  b->g_lmax.assign(lhat_max, lhat_max + n_ghost);
+  if (b->contact_on && b->have_saved_contact) return er_set_contact(b, &b->saved_contact);
+  return ER_OK;
+}
+
+er_status er_step_begin(er_batch *b, double dt) {
+  if (!b) return ER_EINVAL;
+  if (!b->contact_on || b->kernel_mode == 1) { b->last_error = "er_step_begin needs contact (fused kernels)"; return ER_EINVAL; }
+  if (b->split_begun) { b->last_error = "er_step_begin twice without er_step_finish"; return ER_EINVAL; }
+  b->split_mode = 1;
+  const er_status st = er_step(b, 1, dt);
+  b->split_mode = 0;
+  if (st == ER_OK) {
+    b->split_begun = true;
+    b->split_dt = dt;
+  }
+  return st;
+}
+
+er_status er_step_finish(er_batch *b, double dt) {
+  if (!b) return ER_EINVAL;
+  if (!b->split_begun) { b->last_error = "er_step_finish without er_step_begin"; return ER_EINVAL; }
+  if (dt != b->split_dt) { b->last_error = "er_step_finish dt differs from er_step_begin's"; return ER_EINVAL; }
+  b->split_mode = 2;
+  const er_status st = er_step(b, 1, dt);
+  b->split_mode = 0;
+  b->split_begun = false;
+  return st;
+}
+
+er_status er_contact_records(er_batch *b, int32_t dst_mem, double *dst) {
+  if (!b || !dst) return ER_EINVAL;
+  if (!b->contact_on) { b->last_error = "contact is not enabled"; return ER_EINVAL; }
+  if (dst_mem != ER_HOST && dst_mem != ER_DEVICE) { b->last_error = "dst_mem must be ER_HOST or ER_DEVICE"; return ER_EINVAL; }
+  CK(cudaSetDevice(b->device), "cudaSetDevice");
+  const size_t bytes = sizeof(double) * 6 * (size_t)b->n_nodes;
+  CK(cudaMemcpyAsync(dst, b->cp.cnode, bytes, dst_mem == ER_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                     b->stream), "node records");
+  CK(cudaStreamSynchronize(b->stream), "sync");
+  return ER_OK;
+}
+
+er_status er_set_ghost_records(er_batch *b, int32_t src_mem, const double *src) {
+  if (!b || !src) return ER_EINVAL;
+  if (!b->contact_on || b->g_rods == 0) { b->last_error = "no ghost rods (er_set_contact_ghosts) or contact off"; return ER_EINVAL; }
+  if (src_mem != ER_HOST && src_mem != ER_DEVICE) { b->last_error = "src_mem must be ER_HOST or ER_DEVICE"; return ER_EINVAL; }
+  CK(cudaSetDevice(b->device), "cudaSetDevice");
+  const size_t bytes = sizeof(double) * 6 * (size_t)b->g_nodes;
+  CK(cudaMemcpyAsync(b->cp.cnode + 6 * b->n_nodes, src, bytes,
+                     src_mem == ER_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, b->stream), "ghost records");
+  if (src_mem == ER_HOST) CK(cudaStreamSynchronize(b->stream), "sync");  // the caller may reuse its buffer
   return ER_OK;
 }
 

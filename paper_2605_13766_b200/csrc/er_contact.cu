@@ -558,6 +558,23 @@ __global__ void hhg_finish(const ErContactParams p) {
   }
 }
 
+// Ghost rods (contact across GPUs): the caller supplied their node records; a node farther than
+// skin/2 from its position at the last list build raises the rebuild flag, as the drift kernel does
+// for the own nodes.
+__global__ void hhg_ghost_check(const ErContactParams p, int64_t n0, double disp2) {
+  bool moved = false;
+  for (int64_t n = n0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < p.n_nodes; n += (int64_t)gridDim.x * blockDim.x) {
+    double d2 = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double d = p.cnode[6 * n + c] - p.cbuild[3 * n + c];
+      d2 = fma(d, d, d2);
+    }
+    moved = moved || !(d2 <= disp2);  // also for NaN
+  }
+  if (__any_sync(0xffffffffu, moved) && (threadIdx.x & 31) == 0) atomicOr(p.rebuild, 1);
+}
+
 }  // namespace erc
 
 namespace {
@@ -613,6 +630,13 @@ cudaError_t capture_if(cudaStream_t st, cudaStream_t side, Cond &&cond, Body &&b
 }  // namespace
 
 extern "C" {
+
+cudaError_t er_contact_ghost_check(const ErContactParams *pp, int64_t n0, double disp2, cudaStream_t st) {
+  if (pp->n_nodes <= n0) return cudaSuccess;
+  const unsigned g = (unsigned)std::min<int64_t>((pp->n_nodes - n0 + 255) / 256, 148 * 8);
+  erc::hhg_ghost_check<<<g, 256, 0, st>>>(*pp, n0, disp2);
+  return cudaGetLastError();
+}
 
 // Temporary-storage bytes of the broad-phase sort (n keys of `bits` bits).
 cudaError_t er_contact_tmp_bytes(int64_t n, int bits, size_t *bytes) {
