@@ -117,7 +117,8 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
                                           const double *__restrict__ rec, const SlotInfo &si,
                                           double r[3], double v[3], double Q[9], double w[3],
                                           const double k0s[3], double &t, unsigned &fbits,
-                                          const double *fcon = nullptr, XSync xsync = XSync()) {
+                                          const double *fcon = nullptr, XSync xsync = XSync(),
+                                          bool final_step = false) {
   constexpr bool GEN = (FEAT & FEAT_GENERAL) != 0;
   constexpr bool EXTRA = (FEAT & FEAT_EXTRA) != 0;
   constexpr bool ACT = (FEAT & (FEAT_EXTRA | FEAT_ACT)) != 0;
@@ -326,7 +327,7 @@ __device__ __forceinline__ void step_body(const ErStepParams &p, double *__restr
     t = t_half + hh;
 #pragma unroll
     for (int c = 0; c < 3; ++c) r[c] = fma(hr, v[c], r[c]);
-    rotate_inplace(Q, hq * w[0], hq * w[1], hq * w[2]);
+    rotate_inplace(Q, hq * w[0], hq * w[1], hq * w[2], !final_step);  // (d3 of the last step is not stored)
   }
   if ((DRIFT1 || DRIFT2) && si.active) {
     // fault checks: non-finite state, overspeed.  r, v and w suffice: Q changes only through
@@ -528,7 +529,8 @@ __global__ void __launch_bounds__(BLOCK, MINB) fused_persistent(const ErStepPara
       }
     } else {
       for (int st = 0; st < p.n_steps; ++st) {
-        step_body<BLOCK, FEAT, true, true, true>(p, B, rec, si, r, v, Q, w, k0s, t, fbits);
+        step_body<BLOCK, FEAT, true, true, true>(p, B, rec, si, r, v, Q, w, k0s, t, fbits, nullptr, CtaSync(),
+                                                 st + 1 == p.n_steps);
         if (st + 1 < p.n_steps) __syncthreads();  // exchange C is re-used as A by the next step
       }
     }

@@ -85,7 +85,8 @@ __device__ __forceinline__ double d3_component(int j, const double *q, int64_t s
 // rotation of PAPER.md:30).  Rows of Q are the directors.  Rows d1, d2 are rotated, d3 is rebuilt
 // as d1 x d2 (equal in exact arithmetic for a proper rotation).  v = 0 leaves Q bit-identical
 // when it already holds d3 = complete_d3(d1, d2), which every kernel maintains.
-__device__ __forceinline__ void rotate_inplace(double Q[9], double vx, double vy, double vz) {
+// complete = false skips rebuilding d3 (the caller's last rotation before only d1, d2 are stored).
+__device__ __forceinline__ void rotate_inplace(double Q[9], double vx, double vy, double vz, bool complete = true) {
   const double x = fma(vx, vx, fma(vy, vy, vz * vz));
   double a, b;
   if (x < 0.25) {
@@ -112,7 +113,7 @@ __device__ __forceinline__ void rotate_inplace(double Q[9], double vx, double vy
     Q[c] = fma(R00, q0, fma(R01, q1, R02 * q2));
     Q[3 + c] = fma(R10, q0, fma(R11, q1, R12 * q2));
   }
-  complete_d3(Q);
+  if (complete) complete_d3(Q);
 }
 
 __device__ __forceinline__ double dot3(const double *a, const double *b) {

@@ -142,7 +142,8 @@ struct PairCross {
 template <int FEAT, class XN, class CR = NoCross>
 __device__ __forceinline__ void wstep(const ErStepParams &p, const double *__restrict__ rec, const WLane &L,
                                       double r[3], double v[3], XN &xN, double Q[9], double w[3],
-                                      const double k0s[3], double &t, unsigned &fbits, const CR &cr = CR()) {
+                                      const double k0s[3], double &t, unsigned &fbits, const CR &cr = CR(),
+                                      bool final_step = false) {
   constexpr bool GEN = (FEAT & FEAT_GENERAL) != 0;
   constexpr bool EXTRA = (FEAT & FEAT_EXTRA) != 0;
   constexpr bool ACT = (FEAT & (FEAT_EXTRA | FEAT_ACT)) != 0;
@@ -370,7 +371,7 @@ __device__ __forceinline__ void wstep(const ErStepParams &p, const double *__res
   if (active) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) r[c] = fma(hr, v[c], r[c]);
-    rotate_inplace(Q, hq * w[0], hq * w[1], hq * w[2]);
+    rotate_inplace(Q, hq * w[0], hq * w[1], hq * w[2], !final_step);  // (d3 of the last step is not stored)
   }
   if (last && !(L.lb & WL_CL_NODEN)) {
 #pragma unroll
@@ -652,7 +653,8 @@ __device__ __forceinline__ void stream_tile(const ErStepParams &p, const WTile &
   XSmem xN{const_cast<double *>(S) + sl + 1, ns};  // node N (last lanes), plane stride ns
   double tt = t0;
   unsigned fbits = 0;
-  for (int st = 0; st < p.n_steps; ++st) wstep<FEAT, XSmem, CR>(p, rec, L, r, v, xN, Q, w, k0s, tt, fbits, cr);
+  for (int st = 0; st < p.n_steps; ++st)
+    wstep<FEAT, XSmem, CR>(p, rec, L, r, v, xN, Q, w, k0s, tt, fbits, cr, st + 1 == p.n_steps);
   if (fbits) {
     fbits_all |= fbits;
     frod = min(frod, (int)rec[REC_CANON]);
