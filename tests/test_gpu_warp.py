@@ -293,3 +293,42 @@ def test_contact_relayouts_warp_batch(er):
     finally:
         del os.environ["ER_NO_WARP"]
     same(a, ref)
+
+
+def test_warp_faults_antipodal_degenerate_overspeed(er, orc):
+    """The warp kernel's fault word: an adjacent relative rotation near pi, a collapsed element and an
+    overspeeding node each report their rod (canonical id), like the tile kernel and the oracle."""
+    import scipy.linalg as sla
+    K = lambda v: np.array([[0, -v[2], v[1]], [v[2], 0, -v[0]], [-v[1], v[0], 0.0]])
+    base = uniform_batch(16, 40, seed=91, clamp_mix=False, tip=False)
+    base.velocities[:] = 0.0
+    base.omega[:] = 0.0
+    no, eo = base.node_offsets(), base.elem_offsets()
+    # antipodal: rod 23, elements 9.. turned by pi - 1e-8 about an axis
+    w = dataclasses.replace(base, directors=base.directors.copy())
+    a = np.array([0.2, -0.5, 1.0]) / np.linalg.norm([0.2, -0.5, 1.0])
+    w.directors[eo[23] + 9:eo[24]] = sla.expm((np.pi - 1e-8) * K(a)) @ w.directors[eo[23] + 8]  # relative turn = R
+    with er.RodBatch(w) as b:
+        assert b.info().warp_rod_elems == 16
+        with pytest.raises(er.ErError):
+            b.step(1, 1e-9)
+        rod_id, bits = b.fault()
+        assert rod_id == 23 and bits & er.ER_F_ANTIPODAL
+    st, s, bad, bits = orc.step(w, n_steps=1, dt=1e-9)
+    assert bad == 23 and bits & orc.F_ANTIPODAL
+    # degenerate: rod 31's element 15 (the lane that also owns node N) collapses
+    w = dataclasses.replace(base, positions=base.positions.copy())
+    w.positions[no[31] + 16] = w.positions[no[31] + 15]
+    with er.RodBatch(w) as b:
+        with pytest.raises(er.ErError):
+            b.step(1, 1e-9)
+        rod_id, bits = b.fault()
+        assert rod_id == 31 and bits & er.ER_F_DEGENERATE
+    # overspeed on node N of rod 7
+    w = dataclasses.replace(base, velocities=base.velocities.copy())
+    w.velocities[no[7] + 16, 0] = 1e12
+    with er.RodBatch(w) as b:
+        with pytest.raises(er.ErError):
+            b.step(1, 1e-12)
+        rod_id, bits = b.fault()
+        assert rod_id == 7 and bits & er.ER_F_OVERSPEED
