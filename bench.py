@@ -71,16 +71,19 @@ def peaks():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
-def b_min_per_el_step(w, q_planes: float = 9.0) -> float:
+def b_min_per_el_step(w, q_planes: float = 9.0, rec_bytes: float = 128.0) -> float:
     """SURVEY §8 D.3 with the stored director form (DESIGN §4 "Director storage"): the state is
     r, v per node and d1, d2, w per element (d3 = d1 x d2 is rebuilt on chip), so
     16 [6(N+1) + 9 N] + P + 24 (N-1) chi_kappa0 bytes per rod-step, / N (SURVEY's 12 N counts
     the full 3x3 Q; `b_min_survey_3x3` below keeps that figure for reference).
     Contact mode (NEXT-4) adds, for the step kernel: the contact force on each element's
     two nodes read (48 B per element), the node records for the next contact evaluation written
-    (48 B per node) and the build positions read for the Verlet check (24 B per node)."""
+    (48 B per node) and the build positions read for the Verlet check (24 B per node).
+    `rec_bytes` is SURVEY's P, the per-rod record (128 B); a shared-material batch (every rod has
+    the same material constants; er_info.shared_material) needs only its 48-byte rod
+    record (tip force, actuation, flags) per rod-step."""
     N = w.n_elems.astype(np.float64)
-    per_rod = 16.0 * (6.0 * (N + 1) + q_planes * N) + 128.0 + (24.0 * (N - 1) if w.rest_kappa is not None else 0.0)
+    per_rod = 16.0 * (6.0 * (N + 1) + q_planes * N) + rec_bytes + (24.0 * (N - 1) if w.rest_kappa is not None else 0.0)
     if getattr(w, "contact", None) is not None:
         per_rod = per_rod + 48.0 * N + 72.0 * (N + 1)
     return float(per_rod.sum() / N.sum())
@@ -388,7 +391,8 @@ def main():
     # roofline of the dominant kernel (the rod step kernel; in contact mode the step kernel beside
     # the contact graph): algorithmic bytes per launch / its mean launch duration from the CUDA
     # events er_step records around each launch on its stream (ER_OPT_PHASE_TIMING)
-    bmin = b_min_per_el_step(w)
+    shared = bool(b.info().shared_material)
+    bmin = b_min_per_el_step(w, rec_bytes=48.0 if shared else 128.0)
     per_launch_bytes = bmin * el_local * max(1, a.steps_per_launch)
     n_kl = max(int(ph.step_kernel_launches), 1)
     launch_ms = ph.step_kernel_ms / n_kl if ph.step_kernel_launches else ms / max(launches, 1)
@@ -406,9 +410,12 @@ def main():
             traffic = None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "peak_source": peak_src, "bytes_per_el_step": bmin,
-            "b_min_survey_3x3": b_min_per_el_step(w, 12.0),
-            "kernel": (f"er::warp_bulk<FEAT,{b.info().warp_buffers},{b.info().warp_rod_elems}> (warp-local step: lane = "
-                       "element, shuffle exchanges, per-warp TMA bulk load/store ring)" if b.info().warp_rod_elems
+            "b_min_survey_3x3": b_min_per_el_step(w, 12.0), "b_min_survey_P128": b_min_per_el_step(w),
+            "shared_material": shared,
+            "kernel": (f"er::pair_bulk<FEAT,{b.info().warp_buffers}> (warp-pair step: lane = element, a rod on "
+                       "the 64 lanes of two warps, per-pair TMA bulk load/store ring)" if b.info().warp_rod_elems > 32
+                       else f"er::warp_bulk<FEAT,{b.info().warp_buffers},{b.info().warp_rod_elems}> (warp-local step: "
+                       "lane = element, shuffle exchanges, per-warp TMA bulk load/store ring)" if b.info().warp_rod_elems
                        else f"er::fused_persistent<{b.info().tile_slots},MINB,FEAT> (tile step, CTA-level TMA bulk "
                             "load/store pipeline)"),
             "kernel_ms_per_launch": launch_ms, "kernel_share_of_step": ph.step_kernel_ms / ms if ms > 0 else None}

@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define ER_ABI_VERSION 2
+#define ER_ABI_VERSION 3
 
 typedef struct er_batch er_batch; /* opaque handle; owns device memory */
 
@@ -405,6 +405,10 @@ typedef struct {
                            /* (equal-length rods of this many elements, one   */
                            /* rod per <= 32 lanes); 0: tile kernel */
   int32_t warp_buffers;    /* its stage buffers per CTA (0 if not used)       */
+  int32_t shared_material; /* 1: every rod has the same material constants and */
+                           /* the warp kernel reads them from its parameters, */
+                           /* with a 48-byte record per rod       */
+  int32_t reserved_;
 } er_info;
 er_status er_query(const er_batch *b, er_info *info);
 

@@ -65,6 +65,7 @@ class er_info(C.Structure):
         ("device", C.c_int32), ("stream", C.c_void_p), ("launches", C.c_int64),
         ("device_bytes", C.c_int64), ("t", C.c_double), ("bytes_per_step", C.c_double),
         ("warp_rod_elems", C.c_int32), ("warp_buffers", C.c_int32),
+        ("shared_material", C.c_int32), ("reserved_", C.c_int32),
     ]
 
 

@@ -13,7 +13,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "lib", "libelasticarod.so")
+# ER_BUILD_OUT: build a variant library elsewhere (A/B measurements; lib_ab/ is git-ignored)
+OUT = os.path.abspath(os.environ.get("ER_BUILD_OUT", os.path.join(HERE, "lib", "libelasticarod.so")))
 SOURCES = ["er_api.cu", "er_kernels.cu", "er_warp.cu", "er_contact.cu"]
 # per-file flags: the contact narrow phase takes its branch decisions on IEEE-rounded products
 # and sums in the order written (no FMA contraction; DESIGN §3 #27)

@@ -34,6 +34,7 @@ cudaError_t er_launch_aos_to_soa(const double *src, double *dst, int64_t n, int 
 cudaError_t er_launch_pack_planes(const double *src, double *dst, int64_t stride, const int64_t *eoffp,
                                   const int32_t *ord, const int64_t *eoffc, int64_t n_rods, int nodes, cudaStream_t st);
 cudaError_t er_launch_validate(const double *aos, int64_t n, int k, int orth, double *out, cudaStream_t st);
+cudaError_t er_launch_compact_records(const double *rec, int64_t n_rods, double *wrec, int *differ, cudaStream_t st);
 cudaError_t er_launch_apply_forcing(double *rec, int64_t n_rods, const int32_t *flags, const double *damping,
                                     double damping_all, const double *tip, const double *actA, const double *actF,
                                     const double *actL, int forcing, cudaStream_t st);
@@ -125,6 +126,10 @@ struct er_batch {
   int64_t state_doubles = 0;
   int64_t ng = 0, ne = 0;     // canonical plane strides of gpar (nodes) and sigma0/mag (elements)
   double *d_rec = nullptr;
+  double *d_wrecu = nullptr;  // shared-material warp batches: [n_rods][ER_WREC] compact records
+  bool wuni = false;          // ... valid (every rod has the same material constants, umat)
+  double umat[ER_UMAT] = {};
+  int *d_uni_flag = nullptr;
   int64_t *d_eoff = nullptr;
   ErTile *d_tiles = nullptr;
   double *d_gpar = nullptr, *d_sigma0 = nullptr, *d_mag = nullptr, *d_musc = nullptr;
@@ -323,7 +328,7 @@ void free_all(er_batch *b) {
   b->upload_stage = nullptr;
   for (cudaEvent_t e : b->ev_pool) cudaEventDestroy(e);
   b->ev_pool.clear();
-  void *ptrs[] = {b->d_state, b->d_rec, b->d_eoff, b->d_ord, b->d_eoffc, b->d_tiles, b->d_gpar, b->d_sigma0, b->d_mag, b->d_musc,
+  void *ptrs[] = {b->d_state, b->d_rec, b->d_wrecu, b->d_uni_flag, b->d_eoff, b->d_ord, b->d_eoffc, b->d_tiles, b->d_gpar, b->d_sigma0, b->d_mag, b->d_musc,
                   b->d_fext, b->d_cext,
                   b->d_fault, b->d_diag_partial, b->d_diag_out, b->d_valid};
   for (void *p : ptrs)
@@ -372,6 +377,9 @@ ErStepParams params_of(const er_batch *b) {
   p.trace = b->trace;
   p.wN = b->wN; p.wR = b->wR; p.wnb = b->wnb; p.wbufd = b->wbufd; p.wrec = b->wrec; p.wdesc = b->wdesc;
   p.wrt = b->wrt; p.wch = b->wch; p.wcs = b->wcs; p.wrods = b->wrods;
+  p.wuni = b->wuni ? 1 : 0;
+  p.wrecu = b->d_wrecu;
+  for (int k = 0; k < ER_UMAT; ++k) p.umat[k] = b->umat[k];
   {
     static const int l2pf = std::getenv("ER_WARP_L2PF") ? std::atoi(std::getenv("ER_WARP_L2PF")) : 0;
     p.wl2pf = l2pf;
@@ -506,6 +514,37 @@ er_status upload_records(er_batch *b) {
   return ER_OK;
 }
 
+// Shared-material form of the records (DESIGN §4 "Shared material"), after every record change: for a
+// warp-layout batch without per-slot parameters, a kernel writes the 48-byte compact records and
+// tests whether every rod has rod 0's material constants; if so the warp kernels take those from
+// the kernel parameters.  Captured step graphs hold the parameters by value: they are re-captured.
+er_status refresh_shared_material(er_batch *b) {
+  const int64_t R = b->n_rods;
+  const bool want = b->wN > 0 && b->wrt > 0 && !b->any_general && R > 0 && std::getenv("ER_NO_UNI") == nullptr;
+  bool uni = false;
+  if (want) {
+    if (!b->d_wrecu) CK(dalloc(b, &b->d_wrecu, R * ER_WREC + 2), "cudaMalloc(wrecu)");
+    if (!b->d_uni_flag) CK(cudaMalloc((void **)&b->d_uni_flag, sizeof(int)), "cudaMalloc(uni flag)");
+    CK(cudaMemsetAsync(b->d_uni_flag, 0, sizeof(int), b->stream), "memset");
+    CK(er_launch_compact_records(b->d_rec, R, b->d_wrecu, b->d_uni_flag, b->stream), "compact records");
+    int differ = 1;
+    double r0[ER_REC];
+    CK(cudaMemcpyAsync(&differ, b->d_uni_flag, sizeof(int), cudaMemcpyDeviceToHost, b->stream), "D2H");
+    CK(cudaMemcpyAsync(r0, b->d_rec, sizeof r0, cudaMemcpyDeviceToHost, b->stream), "D2H");
+    CK(cudaStreamSynchronize(b->stream), "sync");
+    uni = differ == 0;
+    if (uni) {
+      for (int k = 0; k <= REC_VMAX2; ++k) b->umat[k] = r0[k];
+      b->umat[16] = r0[REC_ACTIL];
+    }
+  } else {
+    CK(cudaStreamSynchronize(b->stream), "sync");
+  }
+  if (uni != b->wuni || uni) free_step_graph(b);  // graphs hold umat by value
+  b->wuni = uni;
+  return ER_OK;
+}
+
 // Upload the per-rod flags (and, with `forcing`, the caller's damping / tip / actuation arrays as
 // given) and let a kernel write those record fields -- no 192-byte records cross PCIe again.
 er_status apply_forcing(er_batch *b, const er_forcing *f, bool forcing) {
@@ -538,8 +577,7 @@ er_status apply_forcing(er_batch *b, const er_forcing *f, bool forcing) {
   CK(er_launch_apply_forcing(b->d_rec, R, dflags, ddamp, forcing ? f->damping_all : 0.0, dtip, dA, dF, dL,
                              forcing ? 1 : 0, b->stream), "apply forcing");
   CK(cudaFreeAsync(d, b->stream), "cudaFreeAsync");
-  CK(cudaStreamSynchronize(b->stream), "sync");
-  return ER_OK;
+  return refresh_shared_material(b);
 }
 
 }  // namespace
@@ -979,8 +1017,9 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
       b->wcs = tile_block_size(tiles[0], b->has_kappa0);
       b->wrods = Rn;
       b->wch = (int32_t)(b->wcs + Rw * ER_REC);  // block | records (both even: 16-byte copies)
-      const int64_t units = N > 32 ? 4 : 8;  // pipelines per CTA (warps, or warp pairs)
-      b->wnb = (int32_t)std::max<int64_t>(2, std::min<int64_t>(4, (113 * 1024 - 512) / (units * 8 * (int64_t)b->wch)));
+      const int64_t units = N > 32 ? 4 : ER_WB_WARPS;  // pipelines per CTA (warps, or warp pairs)
+      const int64_t budget = N > 32 ? 113 * 1024 - 512 : 227 * 1024 / ER_WB_MINB - 1024;  // smem per CTA
+      b->wnb = (int32_t)std::max<int64_t>(2, std::min<int64_t>(4, budget / (units * 8 * (int64_t)b->wch)));
       if (const char *e = std::getenv("ER_WARP_BUFFERS")) b->wnb = std::max(2, std::min(4, std::atoi(e)));
     }
   }
@@ -1592,6 +1631,7 @@ er_status relayout_to_tiles(er_batch *b) {
   if (!tiles.empty())
     CK(cudaMemcpyAsync(b->d_tiles, tiles.data(), sizeof(ErTile) * tiles.size(), cudaMemcpyHostToDevice, b->stream), "H2D tiles");
   b->wN = b->wR = b->wnb = b->wbufd = b->wrec = b->wdesc = b->wrt = b->wch = 0;
+  b->wuni = false;
   b->wcs = b->wrods = 0;
   for (int f = 0; f < nf; ++f) {
     er_status st = upload_field(b, tmp[f], ER_DEVICE, fields[f], false);
@@ -1939,14 +1979,17 @@ er_status er_query(const er_batch *b, er_info *info) {
   info->tile_slots = b->block;
   info->warp_rod_elems = b->wN;
   info->warp_buffers = b->wnb;
+  info->shared_material = b->wuni ? 1 : 0;
+  info->reserved_ = 0;
   info->device = b->device;
   info->stream = (void *)b->stream;
   info->launches = b->launches;
   info->device_bytes = b->device_bytes;
   info->t = b->t;
   // bytes one fused step moves: state read + written once (r, v: 6 per node; d1, d2, w: ER_EPL
-  // per element), the 192-byte rod record read once, static kappa0 read once
-  double bytes = 16.0 * (6.0 * b->n_nodes + (double)ER_EPL * b->n_elems) + 8.0 * ER_REC * b->n_rods;
+  // per element), the 192-byte rod record (48 bytes in a shared-material batch) read once, static
+  // kappa0 read once
+  double bytes = 16.0 * (6.0 * b->n_nodes + (double)ER_EPL * b->n_elems) + 8.0 * (b->wuni ? ER_WREC : ER_REC) * b->n_rods;
   if (b->has_kappa0) bytes += 24.0 * b->n_vor;
   info->bytes_per_step = bytes;
   return ER_OK;

@@ -1178,6 +1178,25 @@ __global__ void apply_forcing(double *rec, int64_t n_rods, const int32_t *flags,
   }
 }
 
+// Shared-material records (er_layout.h ER_WREC): the compact record of every rod, and whether any
+// rod's material constants (REC_LHAT..REC_VMAX2, REC_ACTIL) differ bitwise from rod 0's.
+__global__ void compact_records(const double *rec, int64_t n_rods, double *wrec, int *differ) {
+  bool d = false;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rods; r += (int64_t)gridDim.x * blockDim.x) {
+    const double *x = rec + r * ER_REC;
+    double *y = wrec + r * ER_WREC;
+    for (int c = 0; c < 3; ++c) y[WREC_TIPX + c] = x[REC_TIPX + c];
+    y[WREC_ACTA] = x[REC_ACTA];
+    y[WREC_ACTF] = x[REC_ACTF];
+    const long long fl = __double_as_longlong(x[REC_FLAGS]) & 0xffffffffll;
+    const long long cn = (long long)x[REC_CANON];
+    y[WREC_FC] = __longlong_as_double(fl | (cn << 32));
+    for (int k = 0; k <= REC_VMAX2; ++k) d |= __double_as_longlong(x[k]) != __double_as_longlong(rec[k]);
+    d |= __double_as_longlong(x[REC_ACTIL]) != __double_as_longlong(rec[REC_ACTIL]);
+  }
+  if (d) atomicOr(differ, 1);
+}
+
 }  // namespace er
 
 // --------------------------------------------------------------------------- launch wrappers
@@ -1398,6 +1417,11 @@ cudaError_t er_launch_apply_forcing(double *rec, int64_t n_rods, const int32_t *
                                     const double *actL, int forcing, cudaStream_t st) {
   if (n_rods <= 0) return cudaSuccess;
   er::apply_forcing<<<148 * 4, 256, 0, st>>>(rec, n_rods, flags, damping, damping_all, tip, actA, actF, actL, forcing);
+  return cudaGetLastError();
+}
+cudaError_t er_launch_compact_records(const double *rec, int64_t n_rods, double *wrec, int *differ, cudaStream_t st) {
+  if (n_rods <= 0) return cudaSuccess;
+  er::compact_records<<<148 * 4, 256, 0, st>>>(rec, n_rods, wrec, differ);
   return cudaGetLastError();
 }
 cudaError_t er_launch_validate(const double *aos, int64_t n, int k, int orth, double *out, cudaStream_t st) {

@@ -84,7 +84,17 @@ enum {
 enum { FEAT_GENERAL = 1, FEAT_KAPPA0 = 2,
        FEAT_EXTRA = 4   /* sigma0 / magnetization / muscle wave (and actuation) */,
        FEAT_CONTACT = 8 /* contact forces from ErStepParams.cfc; launch = kick + drift-2 [+ next drift-1] */,
-       FEAT_ACT = 16    /* rest-curvature actuation only (a lighter kernel than FEAT_EXTRA) */ };
+       FEAT_ACT = 16    /* rest-curvature actuation only (a lighter kernel than FEAT_EXTRA) */,
+       FEAT_UNI = 32    /* warp kernels: shared material constants (ErStepParams.umat), 48-byte rod records */ };
+
+// Shared-material batches (warp kernels; DESIGN §4 "Shared material"): when every rod of a batch has
+// the same REC_LHAT..REC_VMAX2 and REC_ACTIL, those 17 constants travel in the kernel parameters
+// (constant bank: FP64 instructions take them as operands, no shared-memory load) and each rod keeps
+// a 48-byte record of what differs per rod -- 144 fewer bytes per rod and step than ER_REC's 192.
+enum { WREC_TIPX = 0, WREC_TIPY, WREC_TIPZ, WREC_ACTA, WREC_ACTF,
+       WREC_FC,  // flag word (low 32 bits) | canonical rod id (high 32 bits)
+       ER_WREC };
+#define ER_UMAT 17  // umat[0..15] = REC_LHAT..REC_VMAX2, umat[16] = REC_ACTIL
 
 // canonical fields (er_get_state / er_set_state order)
 enum { FIELD_POS = 0, FIELD_VEL = 1, FIELD_DIR = 2, FIELD_OMEGA = 3, FIELD_KAPPA0 = 4 };
@@ -230,8 +240,16 @@ struct ErStepParams {
   int64_t wcs;            // doubles per full tile block (tile t starts at t * wcs)
   int64_t wrods;          // rods in the tile part of the batch
   int32_t wl2pf;          // warp_bulk: L2 prefetch distance in tiles beyond the slot ring (0 = none)
-  int32_t pad4_;
+  int32_t wuni;           // shared-material batch: wrecu / umat are valid (FEAT_UNI kernels)
+  const double *wrecu;    // [n_rods][ER_WREC] compact rod records (packed order)
+  double umat[ER_UMAT];   // the shared material constants
 };
+#ifndef ER_WB_WARPS
+#define ER_WB_WARPS 8  // warp_bulk: warps per CTA (measurement builds may change it with ER_WB_MINB)
+#endif
+#ifndef ER_WB_MINB
+#define ER_WB_MINB 2   // warp_bulk: CTAs per SM its register budget is compiled for
+#endif
 #define ER_WARP_MIN_N 4     // warp kernel: <= 8 rods per warp, <= 64 per tile (the record staging)
 #define ER_TRACE_ITERS 64
 #ifndef ER_TRACE

@@ -23,6 +23,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -139,8 +140,28 @@ struct PairCross {
   }
 };
 
-template <int FEAT, class XN, class CR = NoCross>
-__device__ __forceinline__ void wstep(const ErStepParams &p, const double *__restrict__ rec, const WLane &L,
+// Rod-record access.  RecFull: the rod's ER_REC-double record, staged in the slot.  RecUni
+// (FEAT_UNI, a shared-material batch): the 17 shared constants from the kernel parameters (constant
+// bank operands), tip force / actuation / flags from the rod's ER_WREC-double record in the slot.
+// Both hand wstep the same values, so the trajectory is bitwise the same.
+struct RecFull {
+  const double *r;
+  __device__ __forceinline__ double operator[](int k) const { return r[k]; }
+  __device__ __forceinline__ int flags() const { return rec_flags(r); }
+  __device__ __forceinline__ int canon() const { return (int)r[REC_CANON]; }
+};
+struct RecUni {
+  const double *r;
+  const ErStepParams &p;
+  __device__ __forceinline__ double operator[](int k) const {
+    return (k >= REC_TIPX && k <= REC_ACTF) ? r[WREC_TIPX + (k - REC_TIPX)] : k == REC_ACTIL ? p.umat[16] : p.umat[k];
+  }
+  __device__ __forceinline__ int flags() const { return (int)(__double_as_longlong(r[WREC_FC]) & 0xffffffffll); }
+  __device__ __forceinline__ int canon() const { return (int)(__double_as_longlong(r[WREC_FC]) >> 32); }
+};
+
+template <int FEAT, class XN, class CR = NoCross, class RC = RecFull>
+__device__ __forceinline__ void wstep(const ErStepParams &p, const RC &rec, const WLane &L,
                                       double r[3], double v[3], XN &xN, double Q[9], double w[3],
                                       const double k0s[3], double &t, unsigned &fbits, const CR &cr = CR(),
                                       bool final_step = false) {
@@ -467,8 +488,8 @@ __global__ void __launch_bounds__(kWarpBlock, 2) warp_persistent(const ErStepPar
     L.i = i;
     L.N = N;
     const bool active = g < R && q < T.nr;
-    const double *rec = B + p.wrec + (active ? q : 0) * ER_REC;
-    L.fl = active ? rec_flags(rec) : 0;
+    const RecFull rec{B + p.wrec + (active ? q : 0) * ER_REC};
+    L.fl = active ? rec.flags() : 0;
     const int clamp = L.fl & FL_CLAMP_MASK;
     const bool last = active && i == N - 1;
     L.lb = (active ? WL_ACTIVE : 0u) | (active && i >= 1 ? WL_HAS_V : 0u) | (last ? WL_LAST : 0u) |
@@ -505,10 +526,10 @@ __global__ void __launch_bounds__(kWarpBlock, 2) warp_persistent(const ErStepPar
     // ---- the steps, in registers
     double t = t0;
     unsigned fbits = 0;
-    for (int st = 0; st < p.n_steps; ++st) wstep<FEAT>(p, rec, L, r, v, xN, Q, w, k0s, t, fbits);
+    for (int st = 0; st < p.n_steps; ++st) wstep<FEAT, XSmem, NoCross, RecFull>(p, rec, L, r, v, xN, Q, w, k0s, t, fbits);
     if (fbits) {
       fbits_all |= fbits;
-      frod = min(frod, (int)rec[REC_CANON]);  // canonical rod id
+      frod = min(frod, rec.canon());  // canonical rod id
     }
 
     // ---- registers -> stage, in place (only this lane ever touches these entries; node N is there already)
@@ -603,6 +624,22 @@ __device__ __forceinline__ void issue_wtile_async(const ErStepParams &p, const W
   for (int x = 2 * lane; x < g.nr * ER_REC; x += 64) cp_async16(SR + x, Rc + x);
 }
 
+template <bool UNI>
+__device__ __forceinline__ typename std::conditional<UNI, RecUni, RecFull>::type make_rc(const ErStepParams &p,
+                                                                                     const double *r);
+template <>
+__device__ __forceinline__ RecFull make_rc<false>(const ErStepParams &, const double *r) { return RecFull{r}; }
+template <>
+__device__ __forceinline__ RecUni make_rc<true>(const ErStepParams &p, const double *r) { return RecUni{r, p}; }
+
+// Size and source of a tile's rod records (full or shared-material form).
+template <int FEAT>
+__device__ __forceinline__ uint32_t rec_bytes(int nr) { return (uint32_t)nr * ((FEAT & FEAT_UNI) ? ER_WREC : ER_REC) * 8u; }
+template <int FEAT>
+__device__ __forceinline__ const double *rec_src(const ErStepParams &p, int64_t r0) {
+  return (FEAT & FEAT_UNI) ? p.wrecu + r0 * ER_WREC : p.rec + r0 * ER_REC;
+}
+
 // One tile of one warp: stage slot -> registers, n_steps steps, results to HBM.
 // TO_SMEM: the results go back into the slot, in place (a bulk store moves the block); else straight
 // to HBM from registers.
@@ -619,8 +656,10 @@ __device__ __forceinline__ void stream_tile(const ErStepParams &p, const WTile &
   L.i = i;
   L.N = N;
   const bool active = NT ? true : gl < g.nr;
-  const double *rec = S + p.wcs + (active ? gl : 0) * ER_REC;
-  L.fl = active ? rec_flags(rec) : 0;
+  constexpr bool UNI = (FEAT & FEAT_UNI) != 0;
+  using RC = typename std::conditional<UNI, RecUni, RecFull>::type;
+  const RC rec = make_rc<UNI>(p, S + p.wcs + (active ? gl : 0) * (UNI ? ER_WREC : ER_REC));
+  L.fl = active ? rec.flags() : 0;
   const int clamp = L.fl & FL_CLAMP_MASK;
   const bool last = active && i == N - 1;
   L.lb = (active ? WL_ACTIVE : 0u) | (active && i >= 1 ? WL_HAS_V : 0u) | (last ? WL_LAST : 0u) |
@@ -654,10 +693,10 @@ __device__ __forceinline__ void stream_tile(const ErStepParams &p, const WTile &
   double tt = t0;
   unsigned fbits = 0;
   for (int st = 0; st < p.n_steps; ++st)
-    wstep<FEAT, XSmem, CR>(p, rec, L, r, v, xN, Q, w, k0s, tt, fbits, cr, st + 1 == p.n_steps);
+    wstep<FEAT, XSmem, CR, RC>(p, rec, L, r, v, xN, Q, w, k0s, tt, fbits, cr, st + 1 == p.n_steps);
   if (fbits) {
     fbits_all |= fbits;
-    frod = min(frod, (int)rec[REC_CANON]);
+    frod = min(frod, rec.canon());
   }
   if (TO_SMEM) {  // in place: only this lane touches these entries (node N is there already)
     double *O = const_cast<double *>(S);
@@ -748,8 +787,10 @@ __global__ void __launch_bounds__(kWarpBlock, 2) warp_stream(const ErStepParams 
 // block and records into a slot with two cp.async.bulk copies completing the slot's mbarrier, the warp
 // computes, writes its results back into the slot, and lane 0 bulk-stores the block.  The slot of the
 // previous tile is refilled (NB - 1 tiles ahead) once its store has read it.
+constexpr int kBulkWarps = ER_WB_WARPS;
 template <int FEAT, int NB, int NT>
-__global__ void __launch_bounds__(kWarpBlock, 2) warp_bulk(const ErStepParams p) {
+__global__ void __launch_bounds__(32 * kBulkWarps, ER_WB_MINB) warp_bulk(const ErStepParams p) {
+  constexpr int kWarps = kBulkWarps;
   extern __shared__ __align__(16) double sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double *ring = sm + (size_t)warp * NB * p.wch;  // this warp's NB slots
@@ -769,9 +810,9 @@ __global__ void __launch_bounds__(kWarpBlock, 2) warp_bulk(const ErStepParams p)
   auto issue = [&](int64_t t, int j) {  // lane 0
     const WTile g = geom(t);
     double *S = ring + j * p.wch;
-    mbar_expect_tx(&bars[j], 8u * (uint32_t)g.cs + (uint32_t)g.nr * ER_REC * 8u);
+    mbar_expect_tx(&bars[j], 8u * (uint32_t)g.cs + rec_bytes<FEAT>(g.nr));
     bulk_g2s(S, p.state + g.boff, 8u * (uint32_t)g.cs, &bars[j]);
-    bulk_g2s(S + p.wcs, p.rec + g.r0 * ER_REC, (uint32_t)g.nr * ER_REC * 8u, &bars[j]);
+    bulk_g2s(S + p.wcs, rec_src<FEAT>(p, g.r0), rec_bytes<FEAT>(g.nr), &bars[j]);
   };
   if (lane == 0) {
 #pragma unroll
@@ -865,9 +906,9 @@ __global__ void __launch_bounds__(kWarpBlock, 2) pair_bulk(const ErStepParams p)
   auto issue = [&](int64_t t, int j) {
     const WTile g = wtile_geom<0>(p, t, kappa0);
     double *S = ring + j * p.wch;
-    mbar_expect_tx(&bars[j], 8u * (uint32_t)g.cs + (uint32_t)g.nr * ER_REC * 8u);
+    mbar_expect_tx(&bars[j], 8u * (uint32_t)g.cs + rec_bytes<FEAT>(g.nr));
     bulk_g2s(S, p.state + g.boff, 8u * (uint32_t)g.cs, &bars[j]);
-    bulk_g2s(S + p.wcs, p.rec + g.r0 * ER_REC, (uint32_t)g.nr * ER_REC * 8u, &bars[j]);
+    bulk_g2s(S + p.wcs, rec_src<FEAT>(p, g.r0), rec_bytes<FEAT>(g.nr), &bars[j]);
   };
   if (issuer) {
 #pragma unroll
@@ -955,10 +996,16 @@ cudaError_t launch_stream_nb(const ErStepParams &p, cudaStream_t st) {
   static const bool generic = std::getenv("ER_WARP_GENERIC") != nullptr;
   static const bool cpasync = std::getenv("ER_WARP_CPASYNC") != nullptr;  // A/B: per-lane cp.async + direct stores
   const bool pair = p.wN > 32;  // rods of 33..64 elements: one rod per warp pair
-  auto k = pair ? er::pair_bulk<FEAT, NB>
-         : cpasync ? ((p.wN == 16 && !generic) ? er::warp_stream<FEAT, NB, 16> : er::warp_stream<FEAT, NB, 0>)
-                   : ((p.wN == 16 && !generic) ? er::warp_bulk<FEAT, NB, 16> : er::warp_bulk<FEAT, NB, 0>);
-  const int units = pair ? er::kWarps / 2 : er::kWarps;  // pipelines per CTA
+  void (*k)(ErStepParams);
+  if constexpr ((FEAT & FEAT_UNI) != 0) {  // (er_launch_warp never combines FEAT_UNI with ER_WARP_CPASYNC)
+    k = pair ? er::pair_bulk<FEAT, NB> : (p.wN == 16 && !generic) ? er::warp_bulk<FEAT, NB, 16> : er::warp_bulk<FEAT, NB, 0>;
+  } else {
+    k = pair ? er::pair_bulk<FEAT, NB>
+        : cpasync ? ((p.wN == 16 && !generic) ? er::warp_stream<FEAT, NB, 16> : er::warp_stream<FEAT, NB, 0>)
+                  : ((p.wN == 16 && !generic) ? er::warp_bulk<FEAT, NB, 16> : er::warp_bulk<FEAT, NB, 0>);
+  }
+  const int units = pair ? er::kWarps / 2 : er::kBulkWarps;  // pipelines per CTA
+  const int block = pair ? er::kWarpBlock : 32 * er::kBulkWarps;
   const size_t sm = (size_t)units * NB * p.wch * 8 + (size_t)units * NB * 8 + (pair ? (size_t)units * 24 * 8 : 0);
   static int cached_dev = -1, cached_per_sm = 0;
   static size_t cached_sm = 0, set_sm = 0;
@@ -970,7 +1017,7 @@ cudaError_t launch_stream_nb(const ErStepParams &p, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     set_sm = std::max(sm, set_sm);
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, er::kWarpBlock, sm);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, block, sm);
     if (e != cudaSuccess) return e;
     cached_dev = dev;
     cached_sm = sm;
@@ -983,7 +1030,7 @@ cudaError_t launch_stream_nb(const ErStepParams &p, cudaStream_t st) {
   static const bool pdl = std::getenv("ER_NO_PDL") == nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)g, 1, 1);
-  cfg.blockDim = dim3(er::kWarpBlock, 1, 1);
+  cfg.blockDim = dim3((unsigned)block, 1, 1);
   cfg.dynamicSmemBytes = sm;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1011,6 +1058,15 @@ cudaError_t er_launch_warp(const ErStepParams *p, int feat, cudaStream_t st) {
   const int base = feat & (FEAT_GENERAL | FEAT_KAPPA0);
   const int x = (feat & FEAT_EXTRA) ? FEAT_EXTRA : (feat & FEAT_ACT) ? FEAT_ACT : 0;
   if (p->wrt > 0) {  // per-warp streaming pipeline (default)
+    static const bool cpasync = std::getenv("ER_WARP_CPASYNC") != nullptr;
+    if (p->wuni && p->wrecu && !cpasync && !(base & FEAT_GENERAL) && x != FEAT_EXTRA) {  // shared material
+      switch (x | base) {
+        case 0: return launch_stream<FEAT_UNI>(*p, st);
+        case FEAT_KAPPA0: return launch_stream<FEAT_UNI | FEAT_KAPPA0>(*p, st);
+        case FEAT_ACT: return launch_stream<FEAT_UNI | FEAT_ACT>(*p, st);
+        default: return launch_stream<FEAT_UNI | FEAT_ACT | FEAT_KAPPA0>(*p, st);
+      }
+    }
     switch (x | base) {
       case 0: return launch_stream<0>(*p, st);
       case 1: return launch_stream<1>(*p, st);

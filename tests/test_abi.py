@@ -39,7 +39,7 @@ def test_library_exports_every_declared_symbol(er):
 
 
 def test_abi_version(er):
-    assert er.lib.er_abi_version() == 2
+    assert er.lib.er_abi_version() == 3
 
 
 def test_struct_layouts_match_header(er):

@@ -5,7 +5,7 @@ import collections, csv, io, re, subprocess, sys, os
 rep, fn, units = sys.argv[1], sys.argv[2], float(sys.argv[3])
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 30
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-lib = os.path.join(ROOT, "paper_2605_13766_b200", "lib", "libelasticarod.so")
+lib = os.environ.get("ER_LIB", os.path.join(ROOT, "paper_2605_13766_b200", "lib", "libelasticarod.so"))
 tmp = "/tmp/_cubins"
 os.makedirs(tmp, exist_ok=True)
 subprocess.run(["cuobjdump", "-xelf", "all", lib], cwd=tmp, capture_output=True)
