@@ -5,6 +5,7 @@
 // stepping with one fault-word read per er_step, state read-back and the diagnostics
 // reduction.  Nothing here does per-element physics on the host: every step of the path runs
 // in er_kernels.cu.
+#include <nvtx3/nvToolsExt.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -49,6 +50,16 @@ cudaError_t er_contact_graph(const ErContactParams *p, void *tmp, size_t tmp_byt
 #define ER_GRAPH_LAUNCHES 32  // step launches per CUDA-graph launch (even: the time ping-pong)
 
 namespace {
+
+// NVTX range around each public call (SURVEY §5 tracing): visible to ncu --nvtx / nsys; the calls
+// cost nothing measurable when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
+
 
 thread_local std::string g_create_error;
 
@@ -589,6 +600,7 @@ int32_t er_abi_version(void) { return ER_ABI_VERSION; }
 const char *er_last_error(const er_batch *b) { return b ? b->last_error.c_str() : g_create_error.c_str(); }
 
 er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
+  NvtxRange nvtx_("er_create_batch");
   g_create_error.clear();
   if (out) *out = nullptr;
   if (!d || !out) { g_create_error = "desc and out must be non-NULL"; return ER_EINVAL; }
@@ -1094,6 +1106,7 @@ er_status er_create_batch(const er_batch_desc *d, er_batch **out) {
   } while (0)
 
 er_status er_set_bc(er_batch *b, const int8_t *clamp_end) {
+  NvtxRange nvtx_("er_set_bc");
   if (!b) return ER_EINVAL;
   Errors err;
   if (clamp_end)
@@ -1111,6 +1124,7 @@ er_status er_set_bc(er_batch *b, const int8_t *clamp_end) {
 }
 
 er_status er_set_forcing(er_batch *b, const er_forcing *f) {
+  NvtxRange nvtx_("er_set_forcing");
   if (!b || !f) { if (b) b->last_error = "forcing is NULL"; return ER_EINVAL; }
   b->forcing_version += 1;  // step-graph parameters (gravity, field, features) may change
   Errors err;
@@ -1294,6 +1308,7 @@ er_status er_set_trace(er_batch *b, void *trace) {
 }
 
 er_status er_step(er_batch *b, int64_t n_steps, double dt) {
+  NvtxRange nvtx_("er_step");
   if (!b) return ER_EINVAL;
   Errors err;
   if (n_steps < 0) err.add("n_steps = %lld < 0", (long long)n_steps);
@@ -1907,6 +1922,7 @@ er_status er_get_contact_stats(er_batch *b, er_contact_stats *out) {
 
 er_status er_get_state(er_batch *b, int32_t dst_mem, double *positions, double *velocities, double *directors,
                        double *omega, double *t) {
+  NvtxRange nvtx_("er_get_state");
   if (!b) return ER_EINVAL;
   if (dst_mem != ER_HOST && dst_mem != ER_DEVICE) { b->last_error = "dst_mem must be ER_HOST or ER_DEVICE"; return ER_EINVAL; }
   CK(cudaSetDevice(b->device), "cudaSetDevice");
@@ -1922,6 +1938,7 @@ er_status er_get_state(er_batch *b, int32_t dst_mem, double *positions, double *
 
 er_status er_set_state(er_batch *b, int32_t src_mem, const double *positions, const double *velocities,
                        const double *directors, const double *omega, const double *t) {
+  NvtxRange nvtx_("er_set_state");
   if (!b) return ER_EINVAL;
   if (src_mem != ER_HOST && src_mem != ER_DEVICE) { b->last_error = "src_mem must be ER_HOST or ER_DEVICE"; return ER_EINVAL; }
   if (t && !std::isfinite(*t)) { b->last_error = "t is not finite"; return ER_EINVAL; }
@@ -1938,6 +1955,7 @@ er_status er_set_state(er_batch *b, int32_t src_mem, const double *positions, co
 }
 
 er_status er_diagnostics(er_batch *b, double out[ER_NDIAG]) {
+  NvtxRange nvtx_("er_diagnostics");
   if (!b || !out) return ER_EINVAL;
   CK(cudaSetDevice(b->device), "cudaSetDevice");
   ErStepParams p = params_of(b);
