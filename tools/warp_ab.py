@@ -17,6 +17,7 @@ for rep in range(3):
     for v in variants:
         env = dict(kv.split("=", 1) for kv in v.split())
         spl = int(env.pop("SPL", "1"))
+        sweeps = int(env.pop("SWEEPS", "0"))  # ER_OPT_SWEEPS_PER_LAUNCH (0 = the library's default)
         old = {k: os.environ.get(k) for k in env}
         os.environ.update(env)
         b = er.RodBatch(w, stream=stream)
@@ -27,6 +28,8 @@ for rep in range(3):
                 os.environ[k] = x
         if spl > 1:
             b.set_option(er.ER_OPT_STEPS_PER_LAUNCH, spl)
+        if sweeps:
+            b.set_option(er.ER_OPT_SWEEPS_PER_LAUNCH, sweeps)
         def stepq(n):  # ER_AB_IGNORE_FAULTS=1: timing experiments whose physics is knowingly wrong
             try:
                 b.step(n, w.dt)
