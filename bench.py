@@ -126,13 +126,13 @@ class ClockSampler:
                 N.nvmlInit()
                 self.stop = threading.Event()
                 self.th = threading.Thread(target=self._nvml_loop,
-                                           args=(float(os.environ.get("ER_BENCH_CLOCK_MS", "100")) / 1e3,), daemon=True)
+                                           args=(float(os.environ.get("ER_BENCH_CLOCK_MS", "200")) / 1e3,), daemon=True)
                 self.th.start()
                 self.nvml = True
                 return self
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms",
-                                          os.environ.get("ER_BENCH_CLOCK_MS", "100")],
+                                          os.environ.get("ER_BENCH_CLOCK_MS", "200")],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()

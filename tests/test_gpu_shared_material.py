@@ -99,3 +99,13 @@ def test_baseline_workloads_are_shared(er):
         with er.RodBatch(w) as b:
             info = b.info()
             assert info.warp_rod_elems > 0 and info.shared_material == 1, (name, info.warp_rod_elems)
+
+
+def test_pair_walk_direction_bitwise(er, monkeypatch):
+    """pair_bulk walks the tiles in alternating directions across step-graph launches (L2 reuse); the
+    trajectory equals plain launches in one direction bitwise."""
+    w = shared_batch(64, 300, seed=77, act=True)
+    a, fa = run(er, w, 96, monkeypatch)                                   # 3 graph chunks of 32 launches
+    b, fb = run(er, w, 96, monkeypatch, env={"ER_NO_STEP_GRAPH": "1"})   # plain launches
+    assert fa == fb == [1]
+    same(a, b)
