@@ -835,8 +835,10 @@ __global__ void __launch_bounds__(32 * kBulkWarps, ER_WB_MINB) warp_bulk(const E
 #endif
     const WTile g = geom(t);
     double *S = ring + j * p.wch;
+#ifndef ER_EXP_PROBE  // (measurement builds, -DER_EXP_PROBE: the memory stream alone, tiles stored back unchanged)
     if (NT && t < nfull) stream_tile<FEAT, NT, true>(p, g, S, lane, t0, fbits_all, frod);
     else stream_tile<FEAT, 0, true>(p, g, S, lane, t0, fbits_all, frod);
+#endif
 #if ER_TRACE
     if (tr) tr[2] = gtimer() & ((1ull << 48) - 1);
 #endif
