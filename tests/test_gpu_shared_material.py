@@ -54,8 +54,9 @@ def run(er, w, n_steps, monkeypatch, env=None, forcing_seq=()):
     return out, flags
 
 
-@pytest.mark.parametrize("N,R,act,kappa0", [(16, 700, False, False), (16, 300, True, True), (7, 333, True, False),
-                                            (32, 90, False, True), (64, 70, True, False), (45, 60, False, False)])
+@pytest.mark.parametrize("N,R,act,kappa0", [(16, 700, False, False), (16, 301, True, True), (7, 333, True, False),
+                                            (4, 301, True, False), (32, 90, False, True), (33, 41, True, True),
+                                            (64, 70, True, False), (45, 60, False, False)])
 def test_shared_material_bitwise(er, monkeypatch, N, R, act, kappa0):
     w = shared_batch(N, R, seed=300 + N, act=act, kappa0=kappa0)
     a, fa = run(er, w, 64, monkeypatch)
