@@ -545,13 +545,18 @@ er_status refresh_shared_material(er_batch *b) {
     CK(cudaStreamSynchronize(b->stream), "sync");
     uni = differ == 0;
     if (uni) {
-      for (int k = 0; k <= REC_VMAX2; ++k) b->umat[k] = r0[k];
-      b->umat[16] = r0[REC_ACTIL];
+      double u[ER_UMAT];
+      for (int k = 0; k <= REC_VMAX2; ++k) u[k] = r0[k];
+      u[16] = r0[REC_ACTIL];
+      if (std::memcmp(u, b->umat, sizeof u) != 0) {
+        std::memcpy(b->umat, u, sizeof u);
+        free_step_graph(b);  // captured step graphs hold umat by value
+      }
     }
   } else {
     CK(cudaStreamSynchronize(b->stream), "sync");
   }
-  if (uni != b->wuni || uni) free_step_graph(b);  // graphs hold umat by value
+  if (uni != b->wuni) free_step_graph(b);
   b->wuni = uni;
   return ER_OK;
 }
