@@ -183,11 +183,6 @@ __device__ __forceinline__ void wstep(const ErStepParams &p, const RC &rec, cons
     for (int c = 0; c < 3; ++c) r[c] = fma(hr, v[c], r[c]);
     rotate_inplace(Q, hq * w[0], hq * w[1], hq * w[2]);
   }
-  if (last && !(L.lb & WL_CL_NODEN)) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) xN.set_r(c, fma(hh, xN.v(c), xN.r(c)));
-  }
-
   // ---- exchange A: node i+1 from the next lane (the rod's last lane owns node N), element i-1
   double rn[3], vn[3], Qp[9];
 #pragma unroll
@@ -201,9 +196,14 @@ __device__ __forceinline__ void wstep(const ErStepParams &p, const RC &rec, cons
     Qp[c] = has_v ? q : Q[c];
   }
   cr.a(r, v, Q, rn, vn, Qp);
-  if (last) {
+  if (last) {  // node N: drift-1 (one divergent block with its use as node i+1)
+    const double hN = (L.lb & WL_CL_NODEN) ? 0.0 : hh;  // (a clamped node moves by a zero step: r + 0 v = r)
 #pragma unroll
-    for (int c = 0; c < 3; ++c) { rn[c] = xN.r(c); vn[c] = xN.v(c); }
+    for (int c = 0; c < 3; ++c) {
+      vn[c] = xN.v(c);
+      rn[c] = fma(hN, vn[c], xN.r(c));
+      xN.set_r(c, rn[c]);
+    }
   }
   // ---- A4-A5 edge i: kinematics, shear/stretch strain, stress
   double Ql[3] = {0.0, 0.0, 0.0}, nb[3] = {0.0, 0.0, 0.0}, n[3] = {0.0, 0.0, 0.0};
@@ -320,26 +320,6 @@ __device__ __forceinline__ void wstep(const ErStepParams &p, const RC &rec, cons
       v[c] = (L.lb & WL_CL_NODE) ? 0.0 : fma(h, a, v[c]);
     }
   }
-  if (last) {
-    double F[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) F[c] = 0.0 - n[c];  // n_N = 0 (zero-padded difference operator)
-    if (L.lb & WL_TIP_N) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) F[c] += rec[REC_TIPX + c];
-    }
-    if (EXTRA && p.fext) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) F[c] += __ldg(p.fext + c * p.ng + L.node + 1);
-    }
-    const double im = general ? gp(GP_IM, L.node + 1) : rec[REC_IM] * 2.0;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const double vc = xN.v(c);
-      const double a = fma(F[c], im, fma(-nu, vc, p.g[c]));
-      xN.set_v(c, (L.lb & WL_CL_NODEN) ? 0.0 : fma(h, a, vc));
-    }
-  }
   // ---- exchange C: mbar_{i+1}, beta_{i+1} (zero past the rod's last Voronoi domain)
   double mbn[3], ben[3];
 #pragma unroll
@@ -394,18 +374,36 @@ __device__ __forceinline__ void wstep(const ErStepParams &p, const RC &rec, cons
     for (int c = 0; c < 3; ++c) r[c] = fma(hr, v[c], r[c]);
     rotate_inplace(Q, hq * w[0], hq * w[1], hq * w[2], !final_step);  // (d3 of the last step is not stored)
   }
-  if (last && !(L.lb & WL_CL_NODEN)) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) xN.set_r(c, fma(hh, xN.v(c), xN.r(c)));
-  }
-  // fault checks: non-finite state, overspeed (as step_body; node N on the last lane)
+  // fault checks: non-finite state, overspeed (as step_body)
   if (active) {
     const double acc = ((r[0] + r[1]) + (r[2] + v[0])) + ((v[1] + v[2]) + (w[0] + (w[1] + w[2])));
     if (!isfinite(acc)) fbits |= 1u;
     if (dot3(v, v) > rec[REC_VMAX2]) fbits |= 8u;
   }
-  if (last) {
-    const double rN[3] = {xN.r(0), xN.r(1), xN.r(2)}, vN[3] = {xN.v(0), xN.v(1), xN.v(2)};
+  if (last) {  // node N: force, kick (A7, A9), drift-2 and its fault checks in one divergent block
+    double F[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) F[c] = 0.0 - n[c];  // n_N = 0 (zero-padded difference operator)
+    if (L.lb & WL_TIP_N) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) F[c] += rec[REC_TIPX + c];
+    }
+    if (EXTRA && p.fext) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) F[c] += __ldg(p.fext + c * p.ng + L.node + 1);
+    }
+    const double im = general ? gp(GP_IM, L.node + 1) : rec[REC_IM] * 2.0;
+    const bool cl = (L.lb & WL_CL_NODEN) != 0;
+    double rN[3], vN[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double vc = xN.v(c);
+      const double a = fma(F[c], im, fma(-nu, vc, p.g[c]));
+      vN[c] = cl ? 0.0 : fma(h, a, vc);
+      rN[c] = fma(cl ? 0.0 : hh, vN[c], xN.r(c));
+      xN.set_v(c, vN[c]);
+      xN.set_r(c, rN[c]);
+    }
     const double acc = ((rN[0] + rN[1]) + (rN[2] + vN[0])) + (vN[1] + vN[2]);
     if (!isfinite(acc)) fbits |= 1u;
     if (dot3(vN, vN) > rec[REC_VMAX2]) fbits |= 8u;
