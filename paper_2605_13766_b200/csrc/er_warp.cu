@@ -820,14 +820,17 @@ __global__ void __launch_bounds__(32 * kBulkWarps, ER_WB_MINB) warp_bulk(const E
   unsigned fbits_all = 0;
   int frod = INT_MAX;
   int64_t k = 0;
+  // slot of tile k, its load parity, and the slot the refill goes to (k + NB - 1): counters instead of
+  // 64-bit k % NB, k / NB per tile
+  int j = 0, jn = NB - 1;
+  uint32_t par = 0;
   for (int64_t t = gw; t < p.n_tiles; t += G, ++k) {
-    const int j = (int)(k % NB);
 #if ER_TRACE  // measurement builds: per-warp timeline [global warp][64 tiles][4] (tools/warp_timeline.py)
     unsigned long long *tr = (p.trace && lane == 0 && k < ER_TRACE_ITERS) ? p.trace + (gw * ER_TRACE_ITERS + k) * 8 : nullptr;
     if (tr) tr[0] = (gtimer() & ((1ull << 48) - 1)) | ((unsigned long long)smid() << 56);
 #endif
     if (t + G >= p.n_tiles) griddep_launch_dependents();  // last tile of this warp
-    mbar_wait(&bars[j], (uint32_t)((k / NB) & 1));
+    mbar_wait(&bars[j], par);
 #if ER_TRACE
     if (tr) tr[1] = gtimer() & ((1ull << 48) - 1);
 #endif
@@ -859,19 +862,26 @@ __global__ void __launch_bounds__(32 * kBulkWarps, ER_WB_MINB) warp_bulk(const E
 #if ER_TRACE
         if (tr) tr[5] = gtimer() & ((1ull << 48) - 1);
 #endif
-        issue(tn, (int)((k + NB - 1) % NB));
+        issue(tn, jn);
       }
 #if ER_TRACE
       if (tr) tr[6] = gtimer() & ((1ull << 48) - 1);
 #endif
-      // L2 prefetch further ahead (no shared memory needed): the slot loads then hit L2
-      const int64_t tp = tn + (int64_t)p.wl2pf * G;
-      if (p.wl2pf > 0 && tp < p.n_tiles) {
-        const WTile gp = geom(tp);
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.state + gp.boff), "r"(8u * (uint32_t)gp.cs) : "memory");
+      // L2 prefetch further ahead (measurement option ER_WARP_L2PF; no shared memory needed)
+      if (p.wl2pf > 0) {
+        const int64_t tp = tn + (int64_t)p.wl2pf * G;
+        if (tp < p.n_tiles) {
+          const WTile gp = geom(tp);
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.state + gp.boff), "r"(8u * (uint32_t)gp.cs) : "memory");
+        }
       }
     }
     __syncwarp();
+    jn = j;
+    if (++j == NB) {
+      j = 0;
+      par ^= 1u;
+    }
   }
   if (lane == 0) bulk_wait_all();  // stores complete before the kernel retires
   advance_tdev(p, t0);
@@ -923,11 +933,11 @@ __global__ void __launch_bounds__(kWarpBlock, 2) pair_bulk(const ErStepParams p)
   const PairCross cr{mbox, barid, wp == 0 && lane == 31, wp == 1 && lane == 0};
   unsigned fbits_all = 0;
   int frod = INT_MAX;
-  int64_t k = 0;
-  for (int64_t t = gp; t < p.n_tiles; t += G, ++k) {
-    const int j = (int)(k % NB);
+  int j = 0, jn = NB - 1;  // slot of this tile, slot of the refill (k + NB - 1), load parity
+  uint32_t par = 0;
+  for (int64_t t = gp; t < p.n_tiles; t += G) {
     if (t + G >= p.n_tiles) griddep_launch_dependents();
-    mbar_wait(&bars[j], (uint32_t)((k / NB) & 1));
+    mbar_wait(&bars[j], par);
     const WTile g = wtile_geom<0>(p, rev ? p.n_tiles - 1 - t : t, kappa0);
     double *S = ring + j * p.wch;
     stream_tile<FEAT, 0, true, PairCross>(p, g, S, wp * 32 + lane, t0, fbits_all, frod, cr);
@@ -941,8 +951,13 @@ __global__ void __launch_bounds__(kWarpBlock, 2) pair_bulk(const ErStepParams p)
       const int64_t tn = t + (NB - 1) * G;
       if (tn < p.n_tiles) {
         asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        issue(tn, (int)((k + NB - 1) % NB));
+        issue(tn, jn);
       }
+    }
+    jn = j;
+    if (++j == NB) {
+      j = 0;
+      par ^= 1u;
     }
   }
   if (issuer) bulk_wait_all();
