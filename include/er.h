@@ -198,8 +198,13 @@ er_status er_set_external_loads(er_batch *b, int32_t src_mem, const double *node
 er_status er_step(er_batch *b, int64_t n_steps, double dt);
 
 /* ------------------------------------------------------------------------- er_get_state
- * Copy the current state out in canonical order.  dst_mem says where the (caller-owned)
- * buffers live.  Any pointer may be NULL to skip that quantity.  *t receives the time.
+ * Copy the current state out in canonical order (north_star "er_get_state"): the rod's
+ * dynamic unknowns of Eqs. (1a)-(1b), i.e. the centerline r and its velocity at the nodes, the
+ * frame Q (rows d1, d2, d3) and the local angular velocity w = ax(Q dQ^T/dt)
+ * on the elements, at the end of the last completed step.  dst_mem says
+ * where the (caller-owned) buffers live.  Any pointer may be NULL to skip that quantity.
+ * *t receives the time.  Synchronises the batch's stream.  d3 is rebuilt as d1 x d2 from the
+ * stored pair (DESIGN §4 "Director storage").  Errors: ER_EINVAL (bad dst_mem), ER_ECUDA.
  */
 er_status er_get_state(er_batch *b, int32_t dst_mem, double *positions, double *velocities,
                        double *directors, double *omega, double *t);
