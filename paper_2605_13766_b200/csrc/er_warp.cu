@@ -842,8 +842,8 @@ __global__ void __launch_bounds__(32 * kBulkWarps, ER_WB_MINB) warp_bulk(const E
 #if ER_TRACE
     if (tr) tr[1] = gtimer() & ((1ull << 48) - 1);
 #endif
-    const WTile g = geom(t);
     double *S = ring + j * p.wch;
+    const WTile g = geom(t);
 #ifndef ER_EXP_PROBE  // (measurement builds, -DER_EXP_PROBE: the memory stream alone, tiles stored back unchanged)
     if (NT && t < nfull) stream_tile<FEAT, NT, true>(p, g, S, lane, t0, fbits_all, frod);
     else stream_tile<FEAT, 0, true>(p, g, S, lane, t0, fbits_all, frod);
